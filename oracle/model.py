@@ -1,0 +1,103 @@
+"""Transducer model pieces in float64 (TEST INFRASTRUCTURE, see oracle/__init__.py).
+
+Fig. 1: encoder -> joiner <- predictor.  The encoder itself is
+out of scope: its outputs `enc[t]` are the inputs.  Two linear projections map
+encoder and predictor outputs into the joint space (§3.4):
+    f[t] = W_enc enc[t] + b_enc          (precomputed once, Alg. 3 line 2)
+    g    = W_pred dec + b_pred           (once per predictor call, Alg. 3 line 6)
+Joiner (reading A11, north_star): logits = W_out ReLU(f[t] + g) + b_out,
+TDT duration head sharing z (A12): dur_logits = W_dur ReLU(f[t] + g) + b_dur.
+Predictor (Alg. 1 lines 6-8, `dec, new_state = predictor(state, label)`):
+  LSTM (A9): PyTorch nn.LSTM convention, gate rows i,f,g,o, two biases,
+      x = Emb[label]; c' = s(f) c + s(i) tanh(g); h' = s(o) tanh(c'); dec = h'.
+  stateless (A10): state = last c labels (most recent first),
+      dec = concat_k Emb_k[state'[k]], no nonlinearity.
+Initial state (A8): h = c = 0, stateless context = [blank]*c; SOS = blank (A7).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def argmax_lowest(v: np.ndarray) -> int:
+    """argmax with the lowest index among ties (PAPER.md:141 `argmax`; tie rule A16)."""
+    v = np.asarray(v)
+    m = v.max()
+    return int(np.flatnonzero(v == m)[0])
+
+
+def _sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+class Transducer:
+    """A Transducer with weights given in the C-ABI layout (synth.make_weights).
+
+    All arrays are converted to float64; the values are the exact bf16 (or
+    f32) values the GPU receives (reading A24)."""
+
+    def __init__(self, weights: dict, blank_id: int = 0, pred_kind: str = "lstm",
+                 context: int = 1, durations=None):
+        self.w = {k: np.asarray(v, dtype=np.float64) for k, v in weights.items()}
+        self.blank = int(blank_id)
+        self.kind = pred_kind
+        self.context = int(context)
+        self.durations = None if durations is None else [int(d) for d in durations]
+        self.num_tokens = self.w["w_out"].shape[0]
+        self.H = self.w["w_out"].shape[1]
+        if pred_kind == "lstm":
+            self.P = self.w["w_hh"].shape[1]
+        else:
+            self.P = self.context * self.w["embedding"].shape[2]
+
+    @classmethod
+    def from_spec(cls, spec, weights):
+        return cls(weights, spec.blank_id, spec.pred_kind, spec.context, spec.durations)
+
+    # -- encoder projection, PAPER.md:219 / Alg. 3 line 2 (:134) -----------------
+    def enc_proj(self, enc_rows: np.ndarray) -> np.ndarray:
+        """f[t] = W_enc enc[t] + b_enc for every given frame ([T, D_e] -> [T, H])."""
+        enc_rows = np.asarray(enc_rows, dtype=np.float64)
+        return enc_rows @ self.w["w_enc"].T + self.w["b_enc"]
+
+    # -- predictor, Alg. 1 lines 62-68 (:62-68) ----------------------------------
+    def pred_init(self):
+        """predictor.init_state() (Alg. 1 line 3): zeros / context of blanks (A8)."""
+        if self.kind == "lstm":
+            return (np.zeros(self.P), np.zeros(self.P))
+        return tuple([self.blank] * self.context)
+
+    def pred_step(self, state, label: int):
+        """dec, new_state = predictor(state, label) (Alg. 1 line 65/67)."""
+        if self.kind == "lstm":
+            h, c = state
+            x = self.w["embedding"][label]
+            gates = (self.w["w_ih"] @ x + self.w["b_ih"]) + (self.w["w_hh"] @ h + self.w["b_hh"])
+            P = self.P
+            i = _sigmoid(gates[0:P])
+            f = _sigmoid(gates[P:2 * P])
+            g = np.tanh(gates[2 * P:3 * P])
+            o = _sigmoid(gates[3 * P:4 * P])
+            c2 = f * c + i * g
+            h2 = o * np.tanh(c2)
+            return h2, (h2, c2)
+        new_state = (int(label),) + tuple(state[:-1])
+        dec = np.concatenate([self.w["embedding"][k][new_state[k]] for k in range(self.context)])
+        return dec, new_state
+
+    def pred_proj(self, dec: np.ndarray) -> np.ndarray:
+        """g = W_pred dec + b_pred."""
+        return self.w["w_pred"] @ dec + self.w["b_pred"]
+
+    # -- joiner, PAPER.md:41 / Alg. 3 lines 7, 13 --------------------------------
+    def joint_z(self, f_t: np.ndarray, g: np.ndarray) -> np.ndarray:
+        return np.maximum(f_t + g, 0.0)
+
+    def joint(self, f_t: np.ndarray, g: np.ndarray):
+        """Token logits [V+1] (and TDT duration logits [|D|], else None)."""
+        z = self.joint_z(f_t, g)
+        logits = self.w["w_out"] @ z + self.w["b_out"]
+        dur = None
+        if self.durations is not None:
+            dur = self.w["w_dur"] @ z + self.w["b_dur"]
+        return logits, dur

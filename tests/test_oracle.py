@@ -1,0 +1,423 @@
+"""Pins of the float64 oracle against what the paper and the mathematics fix.
+
+Nothing here touches the CUDA path.  Each test names the passage it pins.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+import synth
+from oracle import Transducer, decode_sequential, decode_frame_looping, decode_label_looping
+from oracle.brute import brute_force_rnnt, brute_force_tdt, rnnt_alignments, tdt_alignments
+from oracle.model import argmax_lowest
+from oracle.verify import verify_rnnt, verify_tdt
+
+
+def tiny_model(seed, V1=5, De=8, P=8, H=8, kind="lstm", ctx=1, durations=None, blank_bias=0.0,
+               m=3):
+    spec = synth.ModelSpec(V1, De, P, H, kind, ctx, durations, 0, m)
+    w = synth.make_weights(spec, seed, blank_bias=blank_bias)
+    return spec, Transducer.from_spec(spec, w), w
+
+
+# ---------------------------------------------------------------- worked example
+def test_cat_dog_fig2():
+    """Fig. 2 encoded as real weights: tokens, timestamps,
+    and the batched predictor / joint call counts of Alg. 2 vs Alg. 3."""
+    gold = golden("cat_dog.txt")
+    spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
+    model = Transducer.from_spec(spec, w)
+    for u, key in enumerate(["utt0", "utt1"]):
+        want = gold[key]
+        at = want.index("@")
+        toks, stamps = want[:at], [int(x) for x in want[at + 1:]]
+        r = decode_sequential(model, enc[u], int(lengths[u]), spec.max_symbols)
+        assert [vocab[y] for y in r.tokens] == toks
+        assert r.timestamps == stamps
+    lab, cl = decode_label_looping(model, enc, lengths, spec.max_symbols)
+    frm, cf = decode_frame_looping(model, enc, lengths, spec.max_symbols)
+    for u in range(2):
+        assert lab[u].tokens == frm[u].tokens == decode_sequential(model, enc[u], 4, 10).tokens
+        assert lab[u].timestamps == frm[u].timestamps
+    assert cl["predictor_calls"] == int(gold["label_looping_predictor_calls"][0])
+    assert cl["joint_rounds"] == int(gold["label_looping_joint_rounds"][0])
+    assert cf["predictor_calls"] == int(gold["frame_looping_predictor_calls"][0])
+
+
+def test_tdt_forced_alignment():
+    """SPEC.md:311 forced TDT alignment -> D,O,G @ [0,1,3] (PAPER.md:212-213 time rule)."""
+    gold = golden("tdt_forced.txt")
+    spec, w, enc, lengths, vocab = synth.tdt_forced_fixture()
+    model = Transducer.from_spec(spec, w)
+    r = decode_sequential(model, enc[0], int(lengths[0]), spec.max_symbols)
+    assert [vocab[y] for y in r.tokens] == gold["tokens"]
+    assert r.timestamps == [int(x) for x in gold["timestamps"]]
+    assert r.durations == [int(x) for x in gold["durations"]]
+    assert r.joint_evals == int(gold["joint_evals"][0])
+    lab, _ = decode_label_looping(model, enc, lengths, spec.max_symbols)
+    assert (lab[0].tokens, lab[0].timestamps, lab[0].durations) == (r.tokens, r.timestamps, r.durations)
+
+
+# ---------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("kind", ["lstm", "stateless"])
+def test_always_blank(kind):
+    """always-blank -> empty output, L joint evals, 1 predictor call."""
+    spec, model, _ = tiny_model(1, kind=kind, blank_bias=1e4)
+    enc, lengths = synth.make_inputs(2, 3, 7, spec.enc_dim, 7, 7)
+    for b in range(3):
+        r = decode_sequential(model, enc[b], 7, 3)
+        assert r.tokens == [] and r.joint_evals == 7 and r.predictor_calls == 1
+    lab, cnt = decode_label_looping(model, enc, lengths, 3)
+    assert cnt["predictor_calls"] == 1 and cnt["joint_rounds"] == 7
+    assert all(x.tokens == [] for x in lab)
+
+
+@pytest.mark.parametrize("m", [1, 3, 10])
+def test_never_blank_guard(m):
+    """never-blank -> exactly L*m labels stamped 0 x m, 1 x m, ...
+    (max-symbols guard, PAPER.md:24 / reading A6)."""
+    spec, model, _ = tiny_model(3, blank_bias=-1e4, m=m)
+    L = 4
+    enc, _ = synth.make_inputs(4, 1, L, spec.enc_dim, L, L)
+    r = decode_sequential(model, enc[0], L, m)
+    assert len(r.tokens) == L * m
+    assert r.timestamps == [t for t in range(L) for _ in range(m)]
+    assert r.joint_evals == L * m  # no blank evaluation after the m-th label
+    lab, _ = decode_label_looping(model, enc, [L], m)
+    frm, _ = decode_frame_looping(model, enc, [L], m)
+    assert lab[0].tokens == frm[0].tokens == r.tokens
+
+
+def test_tdt_always_blank_duration_2():
+    """always (blank, d=2), T=4 -> no labels, 2 joint evals (t: 0->2->4)."""
+    spec, model, w = tiny_model(5, durations=[0, 1, 2, 3, 4], blank_bias=1e4)
+    w = dict(w)
+    w["b_dur"] = w["b_dur"].copy()
+    w["b_dur"][2] += 1e4
+    model = Transducer.from_spec(spec, w)
+    enc, _ = synth.make_inputs(6, 1, 4, spec.enc_dim, 4, 4)
+    r = decode_sequential(model, enc[0], 4, 3)
+    assert r.tokens == [] and r.joint_evals == 2
+
+
+def test_tdt_blank_duration_0_anti_stall():
+    """blank with d=0 advances by 1 (reading A13) -> L evals, terminates."""
+    spec, model, w = tiny_model(7, durations=[0, 1, 2], blank_bias=1e4)
+    w = dict(w)
+    w["b_dur"] = w["b_dur"].copy()
+    w["b_dur"][0] += 1e4
+    model = Transducer.from_spec(spec, w)
+    enc, _ = synth.make_inputs(8, 1, 6, spec.enc_dim, 6, 6)
+    r = decode_sequential(model, enc[0], 6, 3)
+    assert r.tokens == [] and r.joint_evals == 6
+
+
+def test_tdt_label_duration_0_guard():
+    """Zero-duration labels count toward the guard (A14): never-blank with d=0
+    -> m labels per frame, like RNN-T."""
+    spec, model, w = tiny_model(9, durations=[0, 1, 2], blank_bias=-1e4, m=2)
+    w = dict(w)
+    w["b_dur"] = w["b_dur"].copy()
+    w["b_dur"][0] += 1e4
+    model = Transducer.from_spec(spec, w)
+    enc, _ = synth.make_inputs(10, 1, 3, spec.enc_dim, 3, 3)
+    r = decode_sequential(model, enc[0], 3, 2)
+    assert r.timestamps == [0, 0, 1, 1, 2, 2] and r.durations == [0] * 6
+
+
+def test_zero_length_and_empty_batch():
+    """SPEC.md:299 (len 0 -> empty output), SPEC.md:463 (B=0)."""
+    spec, model, _ = tiny_model(11)
+    enc, _ = synth.make_inputs(12, 2, 5, spec.enc_dim, 0, 0)
+    r = decode_sequential(model, enc[0], 0, 3)
+    assert r.tokens == [] and r.joint_evals == 0
+    lab, cnt = decode_label_looping(model, enc, [0, 0], 3)
+    assert cnt["outer_steps"] == 0 and all(x.tokens == [] for x in lab)
+    lab, cnt = decode_label_looping(model, enc[:0], [], 3)
+    assert lab == [] and cnt["predictor_calls"] == 0
+
+
+# ---------------------------------------------------------------- library routines
+def test_lstm_step_matches_torch_lstmcell():
+    """Reading A9: the LSTM predictor step equals torch.nn.LSTMCell (float64)."""
+    spec, model, w = tiny_model(13, V1=7, P=16, kind="lstm")
+    cell = torch.nn.LSTMCell(16, 16).double()
+    with torch.no_grad():
+        cell.weight_ih.copy_(torch.from_numpy(w["w_ih"].astype(np.float64)))
+        cell.weight_hh.copy_(torch.from_numpy(w["w_hh"].astype(np.float64)))
+        cell.bias_ih.copy_(torch.from_numpy(w["b_ih"].astype(np.float64)))
+        cell.bias_hh.copy_(torch.from_numpy(w["b_hh"].astype(np.float64)))
+    st = model.pred_init()
+    h = torch.zeros(1, 16, dtype=torch.float64)
+    c = torch.zeros(1, 16, dtype=torch.float64)
+    for y in [0, 3, 5, 1, 6]:
+        dec, st = model.pred_step(st, y)
+        x = torch.from_numpy(w["embedding"][y].astype(np.float64))[None]
+        with torch.no_grad():
+            h, c = cell(x, (h, c))
+        np.testing.assert_allclose(dec, h[0].numpy(), rtol=0, atol=1e-14)
+        np.testing.assert_allclose(st[1], c[0].numpy(), rtol=0, atol=1e-14)
+
+
+def test_projections_and_joint_match_torch_linear():
+    """f = W_enc enc + b_enc, g = W_pred dec + b_pred and the joint
+    W_out ReLU(f+g) + b_out (A11) equal torch.nn.functional.linear in float64."""
+    spec, model, w = tiny_model(14, V1=11, De=12, P=10, H=9, kind="stateless", ctx=2,
+                                durations=[0, 1, 2])
+    F = torch.nn.functional
+    t64 = lambda a: torch.from_numpy(np.asarray(a, np.float64))
+    enc, _ = synth.make_inputs(15, 1, 6, 12, 6, 6)
+    f = model.enc_proj(enc[0])
+    np.testing.assert_allclose(f, F.linear(t64(enc[0]), t64(w["w_enc"]), t64(w["b_enc"])).numpy(),
+                               atol=1e-13)
+    dec, _ = model.pred_step(model.pred_init(), 4)
+    g = model.pred_proj(dec)
+    np.testing.assert_allclose(g, F.linear(t64(dec), t64(w["w_pred"]), t64(w["b_pred"])).numpy(),
+                               atol=1e-13)
+    logits, dl = model.joint(f[2], g)
+    z = F.relu(t64(f[2]) + t64(g))
+    np.testing.assert_allclose(logits, F.linear(z, t64(w["w_out"]), t64(w["b_out"])).numpy(), atol=1e-13)
+    np.testing.assert_allclose(dl, F.linear(z, t64(w["w_dur"]), t64(w["b_dur"])).numpy(), atol=1e-13)
+
+
+def test_stateless_context_order():
+    """Reading A10: dec = concat_k Emb_k[y_{-1-k}] (slot 0 = most recent label),
+    initial context = [blank]*c (A8)."""
+    spec, model, w = tiny_model(16, V1=6, P=8, kind="stateless", ctx=2)
+    dec, st = model.pred_step(model.pred_init(), 0)
+    np.testing.assert_array_equal(dec, np.concatenate([w["embedding"][0][0], w["embedding"][1][0]]))
+    dec, st = model.pred_step(st, 3)
+    dec, st = model.pred_step(st, 5)
+    np.testing.assert_array_equal(dec, np.concatenate([w["embedding"][0][5], w["embedding"][1][3]]))
+
+
+def test_argmax_lowest_ties():
+    """SPEC.md:56-58 tie-break examples."""
+    assert argmax_lowest([0.1, 0.9, 0.9]) == 1
+    assert argmax_lowest([5.0]) == 0
+    assert argmax_lowest([-1, -3, -0.5]) == 2
+
+
+# ---------------------------------------------------------------- brute force
+@pytest.mark.parametrize("case", [("rnnt", 3, 4, 2, 2401), ("rnnt", 3, 3, 3, 3375)])
+def test_brute_force_rnnt(case):
+    """Unique greedy-consistent alignment == Alg. 1 output."""
+    _, V1, L, m, n_align = case
+    seeds_done = 0
+    for seed in range(20):
+        for kind in ["lstm", "stateless"]:
+            spec, model, _ = tiny_model(100 + seed, V1=V1, De=4, P=4, H=4, kind=kind,
+                                        blank_bias=float(seed % 3) - 0.5, m=m)
+            enc, _ = synth.make_inputs(200 + seed, 1, L, 4, L, L)
+            surv, n = brute_force_rnnt(model, enc[0], L, m)
+            assert n == n_align
+            assert len(surv) == 1
+            r = decode_sequential(model, enc[0], L, m)
+            assert surv[0] == (r.tokens, r.timestamps)
+            seeds_done += 1
+    assert seeds_done == 40
+
+
+@pytest.mark.parametrize("case", [(3, 3, 2, (0, 1, 2), 6769), (2, 4, 2, (0, 1, 2), 4601)])
+def test_brute_force_tdt(case):
+    V1, L, m, D, n_align = case
+    for seed in range(15):
+        spec, model, _ = tiny_model(300 + seed, V1=V1, De=4, P=4, H=4, kind="lstm",
+                                    durations=list(D), blank_bias=float(seed % 3) - 0.5, m=m)
+        enc, _ = synth.make_inputs(400 + seed, 1, L, 4, L, L)
+        surv, n = brute_force_tdt(model, enc[0], L, m)
+        assert n == n_align
+        assert len(surv) == 1
+        r = decode_sequential(model, enc[0], L, m)
+        assert surv[0] == (r.tokens, r.timestamps, r.durations)
+
+
+# ---------------------------------------------------------------- algorithm equivalence
+def _random_case(rng, tdt):
+    V1 = int(rng.integers(2, 12))
+    dims = [int(rng.integers(2, 10)) for _ in range(3)]
+    kind = "lstm" if rng.random() < 0.5 else "stateless"
+    ctx = int(rng.integers(1, 3)) if kind == "stateless" else 1
+    P = dims[1] * ctx
+    dur = sorted(set([0] + list(rng.choice(5, size=int(rng.integers(1, 4)), replace=False)))) if tdt else None
+    m = int(rng.integers(1, 4))
+    bias = float(rng.normal(0.5, 1.0))
+    spec = synth.ModelSpec(V1, dims[0], P, dims[2], kind, ctx, dur, int(rng.integers(0, V1)), m)
+    w = synth.make_weights(spec, int(rng.integers(1 << 30)), blank_bias=bias)
+    B = int(rng.integers(1, 9))
+    enc, lengths = synth.make_inputs(int(rng.integers(1 << 30)), B, 20, dims[0], 0, 20)
+    return spec, Transducer.from_spec(spec, w), enc, lengths
+
+
+@pytest.mark.parametrize("tdt", [False, True])
+def test_label_looping_equals_sequential(tdt):
+    """Alg. 3 == Alg. 1 bit-exactly (same hypotheses, fewer predictor
+    calls, acceptance :502-503) on 500 seeded tiny configs; for RNN-T
+    also Alg. 2 frame-looping.  Label-looping predictor calls never exceed
+    frame-looping's."""
+    rng = np.random.default_rng(2024 + tdt)
+    stats = {"guard": 0, "blank_d0": 0, "label_d0": 0, "labels": 0}
+    for _ in range(500):
+        spec, model, enc, lengths = _random_case(rng, tdt)
+        m = spec.max_symbols
+        lab, cl = decode_label_looping(model, enc, lengths, m)
+        if not tdt:
+            frm, cf = decode_frame_looping(model, enc, lengths, m)
+            assert cl["predictor_calls"] <= cf["predictor_calls"]
+        for b in range(enc.shape[0]):
+            r = decode_sequential(model, enc[b], int(lengths[b]), m, keep_trace=True)
+            assert (lab[b].tokens, lab[b].timestamps, lab[b].durations) == \
+                   (r.tokens, r.timestamps, r.durations)
+            if not tdt:
+                assert (frm[b].tokens, frm[b].timestamps) == (r.tokens, r.timestamps)
+            stats["labels"] += len(r.tokens)
+            ts = r.timestamps
+            stats["guard"] += sum(1 for i in range(len(ts)) if i >= m - 1 and ts[i - m + 1] == ts[i])
+            if tdt:
+                stats["blank_d0"] += sum(1 for e in r.trace if e[1] == model.blank and e[2] == 0)
+                stats["label_d0"] += sum(1 for e in r.trace if e[1] != model.blank and e[2] == 0)
+    assert stats["labels"] > 1000 and stats["guard"] > 10
+    if tdt:
+        assert stats["blank_d0"] > 0 and stats["label_d0"] > 0
+
+
+def test_predictor_call_count_A21():
+    """Reading A21: label-looping batched predictor calls = max_b(1 + U_b - e_b),
+    e_b = 1 iff row b's last label pushed t >= L_b (guard or TDT d)."""
+    rng = np.random.default_rng(77)
+    for _ in range(200):
+        tdt = bool(rng.random() < 0.5)
+        spec, model, enc, lengths = _random_case(rng, tdt)
+        lab, cl = decode_label_looping(model, enc, lengths, spec.max_symbols)
+        want = 0
+        for b in range(enc.shape[0]):
+            L = int(lengths[b])
+            if L == 0:
+                continue
+            r = lab[b]
+            U = len(r.tokens)
+            e = 0
+            if U:
+                t, d = r.timestamps[-1], (r.durations[-1] if tdt else 0)
+                m = spec.max_symbols
+                k_last = sum(1 for x in r.timestamps if x == t)
+                if tdt and d > 0:
+                    e = int(t + d >= L)
+                else:
+                    # zero-duration (or RNN-T) label: advanced only by the guard
+                    run = 0
+                    for x, dd in zip(reversed(r.timestamps), reversed(r.durations or [0] * U)):
+                        if x != t or (tdt and dd > 0):
+                            break
+                        run += 1
+                    e = int(run % m == 0 and t + 1 >= L)
+            want = max(want, 1 + U - e)
+        assert cl["predictor_calls"] == want
+
+
+def test_batch_composition_and_permutation():
+    """an utterance decodes identically alone and inside any
+    batch; permuting the batch permutes the outputs."""
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        spec, model, enc, lengths = _random_case(rng, bool(rng.random() < 0.5))
+        full, _ = decode_label_looping(model, enc, lengths, spec.max_symbols)
+        perm = rng.permutation(enc.shape[0])
+        pr, _ = decode_label_looping(model, enc[perm], lengths[perm], spec.max_symbols)
+        for i, b in enumerate(perm):
+            alone, _ = decode_label_looping(model, enc[b:b + 1], lengths[b:b + 1], spec.max_symbols)
+            assert (alone[0].tokens, alone[0].timestamps) == (full[b].tokens, full[b].timestamps)
+            assert (pr[i].tokens, pr[i].timestamps) == (full[b].tokens, full[b].timestamps)
+
+
+def test_output_invariants():
+    """timestamps non-decreasing and < L, at most m labels per
+    frame (RNN-T / zero-duration TDT labels), |hyp| <= L*m (reading A18)."""
+    rng = np.random.default_rng(6)
+    for _ in range(100):
+        tdt = bool(rng.random() < 0.5)
+        spec, model, enc, lengths = _random_case(rng, tdt)
+        lab, _ = decode_label_looping(model, enc, lengths, spec.max_symbols)
+        for b, r in enumerate(lab):
+            L = int(lengths[b])
+            assert all(0 <= t < L for t in r.timestamps)
+            assert r.timestamps == sorted(r.timestamps)
+            assert len(r.tokens) <= L * spec.max_symbols
+            assert all(y != spec.blank_id for y in r.tokens)
+            if not tdt:
+                for t in set(r.timestamps):
+                    assert r.timestamps.count(t) <= spec.max_symbols
+
+
+# ---------------------------------------------------------------- verifier
+def test_verifier_accepts_oracle_and_rejects_corruption():
+    """Negative control: a corrupted decode must fail verification."""
+    rng = np.random.default_rng(8)
+    checked = 0
+    for _ in range(60):
+        tdt = bool(rng.random() < 0.5)
+        spec, model, enc, lengths = _random_case(rng, tdt)
+        m = spec.max_symbols
+        for b in range(enc.shape[0]):
+            L = int(lengths[b])
+            r = decode_sequential(model, enc[b], L, m)
+            if tdt:
+                assert verify_tdt(model, enc[b], L, m, r.tokens, r.timestamps, r.durations, tol=0).ok
+            else:
+                assert verify_rnnt(model, enc[b], L, m, r.tokens, r.timestamps, tol=0).ok
+            if not r.tokens:
+                continue
+            bad = list(r.tokens)
+            bad[0] = (bad[0] + 1) % spec.num_tokens
+            if bad[0] == spec.blank_id:
+                bad[0] = (bad[0] + 1) % spec.num_tokens
+            if spec.num_tokens <= 2:
+                continue
+            if tdt:
+                v = verify_tdt(model, enc[b], L, m, bad, r.timestamps, r.durations, tol=0)
+            else:
+                v = verify_rnnt(model, enc[b], L, m, bad, r.timestamps, tol=0)
+            assert not v.ok
+            checked += 1
+    assert checked > 20
+
+
+def test_verifier_rejects_disabled_guard():
+    """Negative control: a decoder without the max-symbols guard emits more than m
+    labels per frame on a never-blank model; verification fails."""
+    spec, model, _ = tiny_model(21, blank_bias=-1e4, m=2)
+    enc, _ = synth.make_inputs(22, 1, 3, spec.enc_dim, 3, 3)
+    r = decode_sequential(model, enc[0], 3, 3)   # wrong m on purpose
+    assert not verify_rnnt(model, enc[0], 3, 2, r.tokens, r.timestamps).ok
+
+
+# ---------------------------------------------------------------- planted (closed form at scale)
+@pytest.mark.parametrize("kind", ["lstm", "stateless"])
+def test_planted_rnnt_full_shapes(kind):
+    """Planted-alignment workload at FastConformer shapes (V+1=1025, H=640): the
+    oracle decode equals the planted alignment (closed form)."""
+    ctx = 2 if kind == "stateless" else 1
+    spec = synth.ModelSpec(1025, 512, 640, 640, kind, ctx, None, 0, 10)
+    w, enc, lengths, planted = synth.make_planted_rnnt(spec, 31, 2, 60, 40, 60)
+    model = Transducer.from_spec(spec, w)
+    for b in range(2):
+        r = decode_sequential(model, enc[b], int(lengths[b]), 10)
+        assert (r.tokens, r.timestamps) == (planted[b][0], planted[b][1])
+
+
+def test_planted_tdt_full_shapes():
+    spec = synth.ModelSpec(1025, 512, 640, 640, "lstm", 1, (0, 1, 2, 3, 4), 0, 10)
+    w, enc, lengths, planted = synth.make_planted_tdt(spec, 32, 2, 60, 40, 60)
+    model = Transducer.from_spec(spec, w)
+    for b in range(2):
+        r = decode_sequential(model, enc[b], int(lengths[b]), 10)
+        assert (r.tokens, r.timestamps, r.durations) == planted[b]
+
+
+def test_enumeration_counts_closed_form():
+    """RNN-T per-frame choices sum_{j<m} V^j + V^m (guard) -> 7^4 for V=2,m=2,L=4."""
+    assert sum(1 for _ in rnnt_alignments(4, [1, 2], 2)) == 7 ** 4
+    assert sum(1 for _ in rnnt_alignments(3, [1, 2], 3)) == 15 ** 3
+    # TDT: small case counted by hand: L=1, one token + blank, D={1}: (b,1) or (y,1)
+    assert sum(1 for _ in tdt_alignments(1, [0, 1], 0, [1], 1)) == 2
