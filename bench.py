@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Throughput of batched label-looping greedy decoding on B200 (arXiv 2406.06220).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config fc-rnnt] [--impl ours|reference]
+
+One STEP decodes one batch of synthetic encoder outputs through the whole hot
+path (encoder projection, model tables, the persistent label-looping kernel)
+via the C ABI.  Default workload: BASELINE config (2) "fc-rnnt": B=32
+utterances, T in U{225..275} frames (80 ms), D_e=512, LSTM predictor P=640,
+joint H=640, V+1=1025, max_symbols=10, bf16, planted-alignment family
+(DESIGN.md "Input recipe").  Metric: decoded audio-seconds per second (RTFx,
+PAPER.md:234 footnote; 0.08 s per frame) -- plus utterances/s.
+
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events on
+the decode stream with a 512 MiB L2 flush between steps (outside the events);
+a barrier + synchronize on both sides; the max over ranks.  Multi-GPU (torchrun):
+each rank decodes its own batches (utterances are independent, no data-path
+collective; weak scaling).
+
+`--impl reference` times the float64 CPU oracle (oracle/, the conventional
+sequential greedy decoder, Alg. 1) as it stands on the host cores, on a bounded
+sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "decoded audio-sec/sec (RTFx) and utterances/sec at B=32, 1/2/4/8 B200"
+UNIT = "audio-s/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="fc-rnnt", choices=list(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--family", default="planted", choices=["planted", "random"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0: auto)")
+    return ap.parse_args()
+
+
+def workload(cfg_name, seed, family="planted"):
+    c = synth.CONFIGS[cfg_name]
+    spec = c["spec"]
+    if family == "planted" and spec.joint_dim >= 70:
+        if spec.is_tdt:
+            w, enc, lengths, _ = synth.make_planted_tdt(spec, seed, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+        else:
+            w, enc, lengths, _ = synth.make_planted_rnnt(spec, seed, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+    else:
+        w = synth.make_weights(spec, seed, blank_bias=3.0 if spec.joint_dim > 64 else 0.5)
+        enc, lengths = synth.make_inputs(seed + 1, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
+    return spec, w, enc, lengths
+
+
+def algorithmic_flops(spec, stats, total_frames):
+    """a1 L*2*D_e*H; a3 E*2*H*(V+1+|D|); a2 S*(2*(P+P)*4P [LSTM] + 2*P*H)."""
+    H, P, De = spec.joint_dim, spec.pred_dim, spec.enc_dim
+    V = spec.num_tokens + (len(spec.durations) if spec.is_tdt else 0)
+    E, S = stats["joint_row_evals"], stats["predictor_rows"]
+    a1 = total_frames * 2 * De * H
+    a3 = E * 2 * H * V
+    a2 = S * ((2 * (P + P) * 4 * P) if spec.pred_kind == "lstm" else 0) + S * 2 * P * H
+    return a1, a2, a3
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_worker(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    spec, w, enc_row, L = args
+    from oracle import Transducer, decode_sequential
+    model = Transducer.from_spec(spec, w)
+    r = decode_sequential(model, enc_row, L, spec.max_symbols)
+    return len(r.tokens)
+
+
+def cpu_oracle_time(spec, w, enc, lengths, n_utt):
+    """Time the float64 oracle (as it stands) on the host cores: one utterance per task."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    idx = list(range(min(n_utt, enc.shape[0])))
+    tasks = [(spec, w, enc[b], int(lengths[b])) for b in idx]
+    ctx = mp.get_context("fork")
+    procs = min(cores, len(tasks))
+    with ctx.Pool(procs, initializer=_limit_threads) as pool:
+        pool.map(oracle_worker, tasks[:procs])  # warm the workers (imports)
+        t0 = time.perf_counter()
+        pool.map(oracle_worker, tasks, chunksize=1)
+        dt = time.perf_counter() - t0
+    audio = float(sum(int(lengths[b]) for b in idx)) * synth.frame_seconds
+    return audio / dt, dt, procs, len(idx), audio
+
+
+def _limit_threads():
+    """One BLAS thread per worker process (the pool supplies the parallelism)."""
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return
+    spec, w, enc, lengths = workload(a.config, 1000, a.family)
+    n = a.cpu_sample or enc.shape[0]
+    times = []
+    for i in range(a.warmup + a.steps):
+        v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc, lengths, n)
+        if i >= a.warmup:
+            times.append((v, dt))
+    value = statistics.mean(v for v, _ in times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(d for _, d in times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": a.config, "family": a.family, "sample_utts": nutt},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle",
+                         "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2406_06220_b200 import build as llbuild
+    from paper_2406_06220_b200 import ll
+    from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
+
+    llbuild.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    spec, w, enc_np, len_np = workload(a.config, 1000 + rank, a.family)
+    B, T = enc_np.shape[0], enc_np.shape[1]
+    model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16", device=f"cuda:{local}")
+    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T)
+    enc = torch.from_numpy(enc_np).to(dev, torch.bfloat16)
+    lengths = torch.from_numpy(len_np).to(dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ev_s0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ev_s1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+
+    def step():
+        s = dec.launch(enc, lengths)
+        if s != ll.LL_OK:
+            raise ll.LLError(s, "decode")
+
+    for _ in range(a.warmup):
+        step()
+    if dec.sync() != ll.LL_OK:
+        raise RuntimeError("warm-up decode failed")
+    stats = dec.stats()
+    ref_out = dec.tokens.clone(), dec.lengths_out.clone()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            flush.zero_()
+            ev_s0[i].record(stream)
+            ll.ll_set_timing_events(ev_k0[i].cuda_event, ev_k1[i].cuda_event)
+            step()
+            ll.ll_set_timing_events(None, None)
+            ev_s1[i].record(stream)
+        torch.cuda.synchronize()
+    if dec.sync() != ll.LL_OK:
+        raise RuntimeError("timed decode failed")
+    step_ms = [ev_s0[i].elapsed_time(ev_s1[i]) for i in range(a.steps)]
+    kern_ms = [ev_k0[i].elapsed_time(ev_k1[i]) for i in range(a.steps)]
+    assert torch.equal(dec.tokens, ref_out[0]) and torch.equal(dec.lengths_out, ref_out[1]), "non-deterministic"
+    tot_ms = sum(step_ms)
+
+    # end to end through the public API with host buffers: H2D of the step's
+    # inputs from pinned memory, decode, D2H of the results, all timed.
+    enc_h = torch.from_numpy(enc_np).to(torch.bfloat16).pin_memory()
+    len_h = torch.from_numpy(len_np).pin_memory()
+    out_tok = torch.empty_like(dec.tokens, device="cpu").pin_memory()
+    out_ts = torch.empty_like(dec.timestamps, device="cpu").pin_memory()
+    out_len = torch.empty_like(dec.lengths_out, device="cpu").pin_memory()
+    enc_d2 = torch.empty_like(enc)
+    len_d2 = torch.empty_like(lengths)
+
+    def e2e_step():
+        enc_d2.copy_(enc_h, non_blocking=True)
+        len_d2.copy_(len_h, non_blocking=True)
+        s = dec.launch(enc_d2, len_d2)
+        if s != ll.LL_OK:
+            raise ll.LLError(s, "decode")
+        out_tok.copy_(dec.tokens, non_blocking=True)
+        out_ts.copy_(dec.timestamps, non_blocking=True)
+        out_len.copy_(dec.lengths_out, non_blocking=True)
+
+    for _ in range(a.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for i in range(a.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    h2d = enc_h.numel() * enc_h.element_size() + len_h.numel() * 4
+    d2h = (out_tok.numel() + out_ts.numel() + out_len.numel()) * 4
+
+    audio_s = float(len_np.sum()) * synth.frame_seconds
+    t_all = torch.tensor([tot_ms, sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    tot_ms_max, e2e_ms_max = float(t_all[0]), float(t_all[1])
+    value = world * a.steps * audio_s / (tot_ms_max / 1e3)
+    utt_s = world * a.steps * B / (tot_ms_max / 1e3)
+    e2e_value = world * a.steps * audio_s / (e2e_ms_max / 1e3)
+
+    # roofline of the dominant kernel (the persistent decode kernel)
+    a1, a2, a3 = algorithmic_flops(spec, stats, int(len_np.sum()))
+    kern_mean = statistics.mean(kern_ms)
+    peaks = {}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
+        peaks = json.load(open(pk_path))
+    peak = peaks.get("bf16_tflops", 1590.0)
+    achieved = (a2 + a3) / (kern_mean / 1e3) / 1e12
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get(a.config)
+
+    rows = stats["joint_row_evals"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": tot_ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": a.config, "family": a.family, "B": B, "T_max": T,
+                   "frames": int(len_np.sum()), "audio_s_per_step": audio_s, "l2": "flushed (512 MiB) between steps",
+                   "parallelism": f"utterance-sharded x{world}"},
+        "utterances_per_s": utt_s,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms_max / a.steps},
+        "gpu_launches": a.steps * (3 if spec.pred_kind == "lstm" else 2 + spec.context),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "decode_kernel",
+                     "kernel_ms": kern_mean, "kernel_share_of_step": kern_mean / (tot_ms_max / a.steps),
+                     "flops_per_launch": a2 + a3,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF"},
+        "decode_stats": {"labels": stats["labels"], "tokens_per_frame": stats["labels"] / max(1, int(len_np.sum())),
+                         "outer_steps": stats["outer_steps"], "joint_rounds": stats["joint_rounds"],
+                         "mean_active_rows": rows / max(1, stats["joint_rounds"]),
+                         "predictor_steps": stats["predictor_steps"], "groups": stats["groups"],
+                         "cluster_size": stats["cluster_size"]},
+        "context": "paper: 5197.2 non-encoder RTFx RNNT-L B=32 with CUDA graphs on one RTX A6000, bf16 (PAPER.md:354)",
+    }
+    if rank == 0 and not a.no_cpu_baseline:
+        n = a.cpu_sample or B
+        v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc_np, len_np, n)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
+                                "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch, "
+                                          f"{dt:.1f} s wall"}
+    clocks = clk.summary()
+    if clocks:
+        line["clocks"] = clocks
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

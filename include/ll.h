@@ -1,0 +1,188 @@
+/*
+ * ll.h -- C ABI of the B200-native label-looping greedy Transducer decoder.
+ *
+ * Method: batched label-looping greedy decoding for RNN-T and TDT models,
+ * arXiv 2406.06220 (the paper's text is PAPER.md; citations are PAPER.md line
+ * numbers).  The outer loop runs over labels, the inner loop over frames:
+ * Alg. 3 "Label-looping Algorithm", TDT variant
+ * (PAPER.md:211-213), precomputed projections, batched
+ * hypotheses.  The problem statement follows Alg. 3 line 1
+ * (PAPER.md:133): "acoustic input x_1..x_B, input_length".
+ *
+ * Conventions (all entry points):
+ *  - Tensor pointers are DEVICE pointers unless marked HOST, row-major,
+ *    contiguous, caller-owned (e.g. allocated with PyTorch).  The library
+ *    allocates nothing on the decode path; all scratch lives in the caller's
+ *    `workspace`.
+ *  - Calls are stream-ordered and asynchronous: they enqueue work on `stream`
+ *    and return.  Weights, inputs, outputs and workspace must stay valid until
+ *    that work completes.  Calls on different streams with distinct
+ *    workspaces are independent.
+ *  - Host-side validation errors are returned synchronously and nothing is
+ *    enqueued.  Errors found on the device (a length > T_max, a hypothesis
+ *    overflowing `out_capacity`) are returned by ll_sync().
+ *  - No C++ exception crosses this boundary.
+ *  - There is no CPU fallback: every step of decoding runs in the library's
+ *    CUDA kernels for sm_100a.
+ */
+#ifndef LL_H_
+#define LL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ll_status;
+enum {
+  LL_OK = 0,
+  LL_ERR_INVALID_ARGUMENT = 1, /* null pointer, negative size, bad id, inconsistent dims */
+  LL_ERR_UNSUPPORTED = 2,      /* valid but not implemented (dims not multiple of 16, ...) */
+  LL_ERR_WORKSPACE = 3,        /* workspace_bytes < ll_workspace_size(...) */
+  LL_ERR_CUDA = 4,             /* a CUDA launch / runtime call failed */
+  LL_ERR_CAPACITY = 5          /* (ll_sync) a hypothesis exceeded out_capacity */
+};
+
+/* Element type of `enc` and of every weight and bias tensor. */
+typedef enum { LL_BF16 = 0, LL_F32 = 1 } ll_dtype;
+
+/* LL_PREC_FAST: bf16 tensor-core contractions with fp32 accumulation; the
+ * projected encoder rows f are stored in bf16.  (LL_F32 inputs are always
+ * computed in fp32.)  LL_PREC_EXACT is reserved (returns LL_ERR_UNSUPPORTED). */
+typedef enum { LL_PREC_FAST = 0, LL_PREC_EXACT = 1 } ll_prec;
+
+typedef enum { LL_PRED_LSTM = 0, LL_PRED_STATELESS = 1 } ll_pred_kind;
+
+/* An opaque CUDA stream (binary-compatible with cudaStream_t; NULL = legacy default stream). */
+typedef struct CUstream_st *ll_stream;
+
+/*
+ * Prediction network (Fig. 1; "stateful (LSTM) and stateless", :33).
+ *  LSTM (PyTorch nn.LSTM convention, one layer, gate rows i,f,g,o):
+ *    x = embedding[y];  gates = w_ih x + b_ih + w_hh h + b_hh
+ *    c' = sigmoid(f) c + sigmoid(i) tanh(g);  h' = sigmoid(o) tanh(c');  dec = h'
+ *    embedding [num_tokens, hidden], w_ih/w_hh [4*hidden, hidden], b_ih/b_hh [4*hidden].
+ *  Stateless: dec = concat_k embedding[k][y_{-1-k}], k < context,
+ *    embedding [context][num_tokens][hidden/context]; w_ih..b_hh unused (may be NULL).
+ *  Initial state: h = c = 0, context = [blank]*context.  The first predictor
+ *  input (SOS / "BOS") is the blank id, i.e. embedding row blank_id.
+ */
+typedef struct {
+  int32_t kind;        /* ll_pred_kind */
+  int32_t num_tokens;  /* V+1 (blank included); must equal ll_joint.num_outputs */
+  int32_t hidden;      /* P; must equal ll_joint.pred_dim */
+  int32_t context;     /* stateless only: 1..4, hidden % context == 0 */
+  const void *embedding;
+  const void *w_ih, *w_hh, *b_ih, *b_hh;
+} ll_predictor;
+
+/*
+ * Joint network with its two projections (§3.4):
+ *   f[t] = w_enc enc[t] + b_enc           [H]   (precomputed once per call, Alg. 3 line 2)
+ *   g    = w_pred dec + b_pred            [H]   (once per predictor call, Alg. 3 line 6)
+ *   z    = ReLU(f[t] + g)
+ *   logits     = w_out z + b_out          [V+1] (Alg. 3 lines 7, 13)
+ *   dur_logits = w_dur z + b_dur          [|D|] (TDT only)
+ * w_enc [H, D_e], b_enc [H], w_pred [H, P], b_pred [H], w_out [V+1, H], b_out [V+1],
+ * w_dur [|D|, H], b_dur [|D|] (NULL for RNN-T).
+ */
+typedef struct {
+  int32_t enc_dim, pred_dim, joint_dim, num_outputs; /* D_e, P, H, V+1 */
+  const void *w_enc, *b_enc, *w_pred, *b_pred;
+  const void *w_out, *b_out;
+  const void *w_dur, *b_dur;
+} ll_joint;
+
+/* Bytes of device workspace needed by a decode (or ll_debug_joint) call with
+ * these shapes.  num_durations = 0 for RNN-T.  Returns 0 if the arguments are
+ * invalid. */
+size_t ll_workspace_size(int32_t B, int32_t T_max, const ll_predictor *pred, const ll_joint *joint,
+                         ll_dtype dtype, ll_prec prec, int32_t num_durations);
+
+/*
+ * Greedy RNN-T decoding of B utterances by label looping (Alg. 3).
+ *  enc          [B, T_max, D_e] encoder outputs (frames t >= lengths[b] are never read)
+ *  lengths      [B] int32, 0 <= lengths[b] <= T_max (checked on the device -> ll_sync)
+ *  blank_id     in [0, V]; also the SOS input of the predictor
+ *  max_symbols  >= 1: after max_symbols labels at one frame, decoding moves to the
+ *               next frame without evaluating a blank (termination guard)
+ *  out_tokens, out_timestamps  [B, out_capacity] int32: label ids and the frame index
+ *               each label was emitted at; entries >= out_lengths[b] are untouched
+ *  out_lengths  [B] int32: number of labels of each hypothesis (true count, even if it
+ *               exceeded out_capacity -- then ll_sync returns LL_ERR_CAPACITY and only
+ *               the first out_capacity labels are written).  out_capacity >=
+ *               T_max*max_symbols can never overflow.
+ *  workspace    >= ll_workspace_size(...) bytes, 256-byte aligned.
+ * Results are identical to per-utterance greedy decoding (Alg. 1)
+ * up to floating-point near-ties of the joint logits.
+ */
+ll_status ll_decode_rnnt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                         const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                         int32_t blank_id, int32_t max_symbols,
+                         int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_lengths,
+                         int32_t out_capacity, void *workspace, size_t workspace_bytes,
+                         ll_stream stream);
+
+/*
+ * Greedy TDT decoding.  As ll_decode_rnnt, plus:
+ *  durations      HOST int32 [num_durations], each >= 0, 1 <= num_durations <= 16: the
+ *                 duration set D; dur_logits index i means "advance by durations[i]".
+ *  out_durations  [B, out_capacity] int32 or NULL: predicted duration of each label.
+ * Time rule: blank -> t += max(d, 1); label -> append (timestamp = t), then
+ * d > 0 ? t += d : (count toward max_symbols at frame t).
+ */
+ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                        const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                        int32_t blank_id, int32_t max_symbols,
+                        const int32_t *durations, int32_t num_durations,
+                        int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_durations,
+                        int32_t *out_lengths, int32_t out_capacity,
+                        void *workspace, size_t workspace_bytes, ll_stream stream);
+
+/* Waits for the work enqueued on `stream` and returns the device-side status of
+ * the last decode that used `workspace`: LL_OK, LL_ERR_INVALID_ARGUMENT (some
+ * lengths[b] > T_max; that row decodes as empty), LL_ERR_CAPACITY, or
+ * LL_ERR_CUDA. */
+ll_status ll_sync(void *workspace, ll_stream stream);
+
+/* Static description of a status code (never NULL). */
+const char *ll_status_string(ll_status status);
+
+/* Decode statistics of the last call that used `workspace`, copied to HOST
+ * `out[8]` after synchronising `stream`: [0] outer steps (summed over groups),
+ * [1] joint rounds, [2] joint row evaluations, [3] batched predictor steps,
+ * [4] predictor row evaluations, [5] labels emitted, [6] groups decoded,
+ * [7] cluster size used. */
+ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream);
+
+/*
+ * Test/debug: the joint of the decode kernel on n given rows, with the
+ * encoder projection of Alg. 3 line 2 applied first:
+ *   f_i = w_enc enc_rows[i] + b_enc;  logits_i = w_out ReLU(f_i + g_rows[i]) + b_out
+ *  enc_rows        [n, D_e] (dtype);  g_rows [n, H] fp32 (predictor projection outputs)
+ *  out_logits      [n, V+1+num_durations] fp32 or NULL (token logits then duration logits)
+ *  out_argmax      [n] int32 (lowest index among ties)
+ *  out_dur_argmax  [n] int32 or NULL (TDT)
+ * Uses the same cluster kernel code path (weights slicing, tensor-core joint,
+ * fused argmax, cross-CTA reduction) as the decoders.
+ */
+ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, const ll_joint *joint,
+                         ll_dtype dtype, ll_prec prec, int32_t num_durations,
+                         float *out_logits, int32_t *out_argmax, int32_t *out_dur_argmax,
+                         void *workspace, size_t workspace_bytes, ll_stream stream);
+
+/* Test/debug: CUDA events (cudaEvent_t handles created by the caller) that the
+ * following decode calls made from this host thread record on their stream
+ * immediately before and after the persistent decode kernel, so a caller can
+ * time that kernel alone with CUDA events.  Pass NULL, NULL to disable. */
+ll_status ll_set_timing_events(void *ev_before_decode, void *ev_after_decode);
+
+/* Library version string. */
+const char *ll_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LL_H_ */

@@ -1,0 +1,49 @@
+"""Build the C-ABI shared library `libll.so` in-tree for sm_100a.
+
+    python -m paper_2406_06220_b200.build          # nvcc, a few tens of seconds
+
+The library is plain CUDA C++ (no torch headers); the Python binding loads it
+with ctypes.  Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libll.so")
+SOURCES = [os.path.join(HERE, "csrc", "ll_api.cu")]
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "linear.cuh", "decode.cuh")] + \
+    [os.path.join(ROOT, "include", "ll.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return LIB
+    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + SOURCES
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libll.so")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+        fh.write(r.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,398 @@
+// ll_api.cu -- host side of the C ABI declared in include/ll.h.
+//
+// Validation (synchronous, nothing enqueued on error), workspace carving,
+// cluster-size selection and the launches:
+//   1. encoder projection f = W_enc enc + b_enc over all B*T_max frames
+//      (Alg. 3 line 2; precompute)
+//   2. model tables (LSTM E' = W_ih Emb + b_ih + b_hh; stateless G_k)
+//   3. the persistent cluster decode kernel (decode.cuh)
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "../../include/ll.h"
+#include "decode.cuh"
+#include "linear.cuh"
+
+using namespace ll;
+
+namespace {
+
+constexpr size_t HDR_BYTES = 4096;  // [0] status, [1] group counter, [16..] stats (u64 x 8 at byte 64)
+constexpr size_t SMEM_LIMIT = 232448;
+
+struct Ws {
+  size_t f, tab, h, g, total;
+};
+
+size_t esize(ll_dtype d) { return d == LL_BF16 ? 2 : 4; }
+
+Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype dt) {
+  Ws w;
+  const size_t H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs;
+  size_t o = HDR_BYTES;
+  w.f = o;
+  o = align_up(o + (size_t)B * T * H * esize(dt), 256);
+  w.tab = o;
+  if (pr->kind == LL_PRED_LSTM)
+    o = align_up(o + V1 * 4 * P * 4, 256);
+  else
+    o = align_up(o + (size_t)pr->context * V1 * H * 4, 256);
+  w.h = o;
+  if (pr->kind == LL_PRED_LSTM) o = align_up(o + 2 * (size_t)B * P * esize(dt), 256);
+  w.g = o;
+  if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
+  w.total = o;
+  return w;
+}
+
+thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+ll_status check_model(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, ll_prec prec,
+                      int nD, bool need_pred) {
+  if (!jn) return LL_ERR_INVALID_ARGUMENT;
+  if (dt != LL_BF16 && dt != LL_F32) return LL_ERR_INVALID_ARGUMENT;
+  if (prec != LL_PREC_FAST && prec != LL_PREC_EXACT) return LL_ERR_INVALID_ARGUMENT;
+  if (jn->enc_dim <= 0 || jn->pred_dim <= 0 || jn->joint_dim <= 0 || jn->num_outputs < 1)
+    return LL_ERR_INVALID_ARGUMENT;
+  if (!jn->w_enc || !jn->b_enc || !jn->w_out || !jn->b_out) return LL_ERR_INVALID_ARGUMENT;
+  if (nD < 0 || nD > MAX_DUR) return LL_ERR_INVALID_ARGUMENT;
+  if (nD > 0 && (!jn->w_dur || !jn->b_dur)) return LL_ERR_INVALID_ARGUMENT;
+  if (need_pred) {
+    if (!pr) return LL_ERR_INVALID_ARGUMENT;
+    if (!jn->w_pred || !jn->b_pred || !pr->embedding) return LL_ERR_INVALID_ARGUMENT;
+    if (pr->num_tokens != jn->num_outputs || pr->hidden != jn->pred_dim) return LL_ERR_INVALID_ARGUMENT;
+    if (pr->kind == LL_PRED_LSTM) {
+      if (!pr->w_ih || !pr->w_hh || !pr->b_ih || !pr->b_hh) return LL_ERR_INVALID_ARGUMENT;
+    } else if (pr->kind == LL_PRED_STATELESS) {
+      if (pr->context < 1) return LL_ERR_INVALID_ARGUMENT;
+      if (pr->context > MAX_CTX || pr->hidden % pr->context) return LL_ERR_UNSUPPORTED;
+    } else {
+      return LL_ERR_INVALID_ARGUMENT;
+    }
+  }
+  if (prec == LL_PREC_EXACT) return LL_ERR_UNSUPPORTED;
+  if (jn->enc_dim % 16 || jn->pred_dim % 16 || jn->joint_dim % 16) return LL_ERR_UNSUPPORTED;
+  if (need_pred && pr->kind == LL_PRED_STATELESS && (jn->pred_dim / pr->context) % 8)
+    return LL_ERR_UNSUPPORTED;
+  return LL_OK;
+}
+
+// Choose the cluster size C and rows per group R; returns false if none fits.
+bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int &C, int &R, Layout &L) {
+  const int forceC = env_int("LL_CLUSTER", 0);
+  const int wantR = env_int("LL_GROUP_ROWS", 16);
+  const int Rs[2] = {wantR == 32 ? 32 : 16, 16};
+  for (int pass = 0; pass < 2; ++pass) {      // pass 0: one vocab tile per warp; pass 1: any
+    for (int ri = 0; ri < 2; ++ri) {
+      R = Rs[ri];
+      for (C = 1; C <= 16; C *= 2) {
+        if (forceC && C != forceC) continue;
+        const int NT = (V1 + nD + 7) / 8;
+        if (bf && pass == 0 && (NT + C - 1) / C > MAX_NW) continue;
+        if (bf) {
+          if (H % (8 * C)) continue;
+          if (lstm && P % (2 * C)) continue;
+        } else {
+          if (H % C) continue;
+          if (lstm && P % C) continue;
+        }
+        L = make_layout(bf, H, P, V1, nD, R, C, lstm);
+        if (L.total + sizeof(RowState) + 1024 > SMEM_LIMIT) continue;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+template <typename T, int PRED>
+ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
+                        int &used_clusters) {
+  auto kern = decode_kernel<T, PRED>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
+    return LL_ERR_CUDA;
+  if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return LL_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(L.NW * 32);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int max_clusters = 0;
+  cfg.gridDim = dim3(C);
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)kern, &cfg) != cudaSuccess || max_clusters < 1) {
+    cudaGetLastError();
+    return LL_ERR_UNSUPPORTED;
+  }
+  const int cap = env_int("LL_MAX_CLUSTERS", 0);
+  if (cap > 0) max_clusters = std::min(max_clusters, cap);
+  used_clusters = std::min(n_groups, max_clusters);
+  cfg.gridDim = dim3(used_clusters * C);
+  if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return LL_ERR_CUDA;
+  return LL_OK;
+}
+
+template <typename T>
+ll_status launch_debug(const DecodeParams &p, int C, const Layout &L, int n_chunks, cudaStream_t st) {
+  auto kern = debug_joint_kernel<T>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
+    return LL_ERR_CUDA;
+  if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return LL_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(L.NW * 32);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int max_clusters = 0;
+  cfg.gridDim = dim3(C);
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)kern, &cfg) != cudaSuccess || max_clusters < 1) {
+    cudaGetLastError();
+    return LL_ERR_UNSUPPORTED;
+  }
+  cfg.gridDim = dim3(std::min(n_chunks, max_clusters) * C);
+  if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return LL_ERR_CUDA;
+  return LL_OK;
+}
+
+ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw, const void *bias,
+                 const void *bias2, void *Y, int64_t ldy, int M, int N, int K, bool out_bf16,
+                 cudaStream_t st) {
+  if (M <= 0 || N <= 0) return LL_OK;
+  LinearArgs a{X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K};
+  if (bf) {
+    dim3 grid((N + LB_N - 1) / LB_N, (M + LB_M - 1) / LB_M);
+    if (out_bf16)
+      linear_bf16_kernel<bf16><<<grid, 256, 0, st>>>(a);
+    else
+      linear_bf16_kernel<float><<<grid, 256, 0, st>>>(a);
+  } else {
+    dim3 grid((N + 63) / 64, (M + 63) / 64);
+    linear_f32_kernel<<<grid, 256, 0, st>>>(a);
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
+}
+
+ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int32_t B, int32_t T_max,
+                      const int32_t *lengths, const ll_predictor *pr, const ll_joint *jn,
+                      int32_t blank_id, int32_t max_symbols, const int32_t *durations, int32_t nD,
+                      int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_durations,
+                      int32_t *out_lengths, int32_t cap, void *workspace, size_t workspace_bytes,
+                      ll_stream stream) {
+  if (B < 0 || T_max < 0 || cap < 0) return LL_ERR_INVALID_ARGUMENT;
+  if (!workspace || ((uintptr_t)workspace & 255)) return LL_ERR_INVALID_ARGUMENT;
+  if (B > 0 && (!enc || !lengths || !out_tokens || !out_timestamps || !out_lengths))
+    return LL_ERR_INVALID_ARGUMENT;
+  if (tdt) {
+    if (nD < 1 || !durations) return LL_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < nD; ++i)
+      if (durations[i] < 0) return LL_ERR_INVALID_ARGUMENT;
+  } else {
+    nD = 0;
+  }
+  ll_status s = check_model(pr, jn, dt, prec, nD, true);
+  if (s != LL_OK) return s;
+  if (blank_id < 0 || blank_id >= jn->num_outputs) return LL_ERR_INVALID_ARGUMENT;
+  if (max_symbols < 1) return LL_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < ll_workspace_size(B, T_max, pr, jn, dt, prec, nD)) return LL_ERR_WORKSPACE;
+  const bool bf = dt == LL_BF16;
+  const bool lstm = pr->kind == LL_PRED_LSTM;
+  const int H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs, De = jn->enc_dim;
+  int C = 0, R = 0;
+  Layout L;
+  if (!choose_config(bf, lstm, H, P, V1, nD, C, R, L)) return LL_ERR_UNSUPPORTED;
+
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t *ws = (uint8_t *)workspace;
+  const Ws w = ws_layout(B, T_max, pr, jn, dt);
+  if (cudaMemsetAsync(ws, 0, HDR_BYTES, st) != cudaSuccess) return LL_ERR_CUDA;
+  if (B == 0) return LL_OK;
+
+  // (1) encoder projection for all frames: f [B*T_max, H]
+  s = linear(bf, enc, De, jn->w_enc, De, jn->b_enc, nullptr, ws + w.f, H, B * T_max, H, De, bf, st);
+  if (s != LL_OK) return s;
+  // (2) model tables
+  float *tab = (float *)(ws + w.tab);
+  if (lstm) {
+    s = linear(bf, pr->embedding, P, pr->w_ih, P, pr->b_ih, pr->b_hh, tab, 4 * P, V1, 4 * P, P, false, st);
+  } else {
+    const int c = pr->context, Pc = P / c;
+    for (int k = 0; k < c && s == LL_OK; ++k) {
+      const uint8_t *emb = (const uint8_t *)pr->embedding + (size_t)k * V1 * Pc * esize(dt);
+      const uint8_t *wp = (const uint8_t *)jn->w_pred + (size_t)k * Pc * esize(dt);
+      s = linear(bf, emb, Pc, wp, P, k == 0 ? jn->b_pred : nullptr, nullptr, tab + (size_t)k * V1 * H, H,
+                 V1, H, Pc, false, st);
+    }
+  }
+  if (s != LL_OK) return s;
+  // (3) decode
+  DecodeParams p;
+  memset(&p, 0, sizeof(p));
+  p.B = B; p.T_max = T_max; p.H = H; p.P = P; p.V1 = V1; p.nD = nD;
+  p.blank = blank_id; p.max_sym = max_symbols; p.tdt = tdt ? 1 : 0;
+  for (int i = 0; i < nD; ++i) p.durations[i] = durations[i];
+  p.context = lstm ? 1 : pr->context;
+  p.R = R;
+  p.n_groups = (B + R - 1) / R;
+  p.cap = cap;
+  p.spec_prefetch = env_int("LL_SPEC_PREFETCH", 1);
+  p.lengths = lengths;
+  p.f = ws + w.f;
+  p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
+  p.w_pred = jn->w_pred; p.b_pred = jn->b_pred; p.w_hh = lstm ? pr->w_hh : nullptr;
+  p.tab = tab;
+  p.h = lstm ? (void *)(ws + w.h) : nullptr;
+  p.gglob = lstm ? (float *)(ws + w.g) : nullptr;
+  p.out_tokens = out_tokens; p.out_timestamps = out_timestamps;
+  p.out_durations = tdt ? out_durations : nullptr;
+  p.out_lengths = out_lengths;
+  p.status = (int *)ws;
+  p.group_counter = (int *)ws + 1;
+  p.stats = (unsigned long long *)(ws + 64);
+  int used = 0;
+  if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
+  if (bf)
+    s = lstm ? launch_decode<bf16, 0>(p, C, L, p.n_groups, st, used)
+             : launch_decode<bf16, 1>(p, C, L, p.n_groups, st, used);
+  else
+    s = lstm ? launch_decode<float, 0>(p, C, L, p.n_groups, st, used)
+             : launch_decode<float, 1>(p, C, L, p.n_groups, st, used);
+  if (s == LL_OK && g_ev_after && cudaEventRecord(g_ev_after, st) != cudaSuccess) return LL_ERR_CUDA;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+ll_status ll_set_timing_events(void *ev_before_decode, void *ev_after_decode) {
+  if ((ev_before_decode == nullptr) != (ev_after_decode == nullptr)) return LL_ERR_INVALID_ARGUMENT;
+  g_ev_before = (cudaEvent_t)ev_before_decode;
+  g_ev_after = (cudaEvent_t)ev_after_decode;
+  return LL_OK;
+}
+
+const char *ll_version(void) { return "ll 0.1 (sm_100a, label-looping arXiv 2406.06220)"; }
+
+const char *ll_status_string(ll_status s) {
+  switch (s) {
+    case LL_OK: return "LL_OK";
+    case LL_ERR_INVALID_ARGUMENT: return "LL_ERR_INVALID_ARGUMENT";
+    case LL_ERR_UNSUPPORTED: return "LL_ERR_UNSUPPORTED";
+    case LL_ERR_WORKSPACE: return "LL_ERR_WORKSPACE";
+    case LL_ERR_CUDA: return "LL_ERR_CUDA";
+    case LL_ERR_CAPACITY: return "LL_ERR_CAPACITY";
+    default: return "LL_ERR_UNKNOWN";
+  }
+}
+
+size_t ll_workspace_size(int32_t B, int32_t T_max, const ll_predictor *pred, const ll_joint *joint,
+                         ll_dtype dtype, ll_prec prec, int32_t num_durations) {
+  if (B < 0 || T_max < 0 || !pred || !joint) return 0;
+  if (check_model(pred, joint, dtype, prec, num_durations, false) == LL_ERR_INVALID_ARGUMENT) return 0;
+  if (pred->kind != LL_PRED_LSTM && pred->kind != LL_PRED_STATELESS) return 0;
+  if (pred->kind == LL_PRED_STATELESS && pred->context < 1) return 0;
+  return ws_layout(B, T_max, pred, joint, dtype).total;
+}
+
+ll_status ll_decode_rnnt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                         const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                         int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
+                         int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
+                         void *workspace, size_t workspace_bytes, ll_stream stream) {
+  return decode_impl(false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+                     nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
+                     workspace_bytes, stream);
+}
+
+ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                        const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                        int32_t blank_id, int32_t max_symbols, const int32_t *durations,
+                        int32_t num_durations, int32_t *out_tokens, int32_t *out_timestamps,
+                        int32_t *out_durations, int32_t *out_lengths, int32_t out_capacity,
+                        void *workspace, size_t workspace_bytes, ll_stream stream) {
+  return decode_impl(true, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+                     durations, num_durations, out_tokens, out_timestamps, out_durations, out_lengths,
+                     out_capacity, workspace, workspace_bytes, stream);
+}
+
+ll_status ll_sync(void *workspace, ll_stream stream) {
+  if (!workspace) return LL_ERR_INVALID_ARGUMENT;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return LL_ERR_CUDA;
+  int status = 0;
+  if (cudaMemcpy(&status, workspace, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return LL_ERR_CUDA;
+  if (status & 2) return LL_ERR_CAPACITY;
+  if (status & 1) return LL_ERR_INVALID_ARGUMENT;
+  return LL_OK;
+}
+
+ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream) {
+  if (!workspace || !out) return LL_ERR_INVALID_ARGUMENT;
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return LL_ERR_CUDA;
+  if (cudaMemcpy(out, (const uint8_t *)workspace + 64, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return LL_ERR_CUDA;
+  return LL_OK;
+}
+
+ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, const ll_joint *joint,
+                         ll_dtype dtype, ll_prec prec, int32_t num_durations, float *out_logits,
+                         int32_t *out_argmax, int32_t *out_dur_argmax, void *workspace,
+                         size_t workspace_bytes, ll_stream stream) {
+  if (n < 0) return LL_ERR_INVALID_ARGUMENT;
+  if (!workspace || ((uintptr_t)workspace & 255)) return LL_ERR_INVALID_ARGUMENT;
+  ll_status s = check_model(nullptr, joint, dtype, prec, num_durations, false);
+  if (s != LL_OK) return s;
+  if (n > 0 && (!enc_rows || !g_rows || !out_argmax)) return LL_ERR_INVALID_ARGUMENT;
+  ll_predictor dummy = {};
+  dummy.kind = LL_PRED_STATELESS;
+  dummy.context = 1;
+  dummy.num_tokens = joint->num_outputs;
+  dummy.hidden = joint->pred_dim;
+  if (workspace_bytes < ll_workspace_size(n, 1, &dummy, joint, dtype, prec, num_durations))
+    return LL_ERR_WORKSPACE;
+  const bool bf = dtype == LL_BF16;
+  const int H = joint->joint_dim, V1 = joint->num_outputs, De = joint->enc_dim;
+  int C = 0, R = 0;
+  Layout L;
+  if (!choose_config(bf, false, H, joint->pred_dim, V1, num_durations, C, R, L)) return LL_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t *ws = (uint8_t *)workspace;
+  const Ws w = ws_layout(n, 1, &dummy, joint, dtype);
+  if (n == 0) return LL_OK;
+  s = linear(bf, enc_rows, De, joint->w_enc, De, joint->b_enc, nullptr, ws + w.f, H, n, H, De, bf, st);
+  if (s != LL_OK) return s;
+  DecodeParams p;
+  memset(&p, 0, sizeof(p));
+  p.B = n; p.T_max = 1; p.H = H; p.P = joint->pred_dim; p.V1 = V1; p.nD = num_durations;
+  p.R = R;
+  p.f = ws + w.f;
+  p.w_out = joint->w_out; p.b_out = joint->b_out; p.w_dur = joint->w_dur; p.b_dur = joint->b_dur;
+  p.dbg_g = g_rows; p.dbg_logits = out_logits; p.dbg_argmax = out_argmax; p.dbg_dargmax = out_dur_argmax;
+  p.dbg_n = n;
+  const int chunks = (n + R - 1) / R;
+  return bf ? launch_debug<bf16>(p, C, L, chunks, st) : launch_debug<float>(p, C, L, chunks, st);
+}
+
+}  // extern "C"

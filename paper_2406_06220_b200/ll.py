@@ -1,0 +1,137 @@
+"""Thin ctypes binding of the C ABI in include/ll.h (argument marshalling only).
+
+Every function here has the name of the C entry point it forwards to and takes
+plain integers (device pointers, sizes) and the ctypes structs below; every
+step of decoding runs in the library's CUDA kernels.  The library is built
+in-tree (`python -m paper_2406_06220_b200.build`); if it is missing or cannot
+be loaded, importing the binding raises -- there is no fallback path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_int32, c_size_t, c_uint64, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libll.so")
+
+LL_OK, LL_ERR_INVALID_ARGUMENT, LL_ERR_UNSUPPORTED, LL_ERR_WORKSPACE, LL_ERR_CUDA, LL_ERR_CAPACITY = range(6)
+LL_BF16, LL_F32 = 0, 1
+LL_PREC_FAST, LL_PREC_EXACT = 0, 1
+LL_PRED_LSTM, LL_PRED_STATELESS = 0, 1
+
+# Every symbol include/ll.h declares (checked by tests/test_abi.py).
+EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_tdt", "ll_sync", "ll_status_string",
+            "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version"]
+
+
+class ll_predictor(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("num_tokens", c_int32), ("hidden", c_int32), ("context", c_int32),
+                ("embedding", c_void_p), ("w_ih", c_void_p), ("w_hh", c_void_p), ("b_ih", c_void_p),
+                ("b_hh", c_void_p)]
+
+
+class ll_joint(ctypes.Structure):
+    _fields_ = [("enc_dim", c_int32), ("pred_dim", c_int32), ("joint_dim", c_int32),
+                ("num_outputs", c_int32), ("w_enc", c_void_p), ("b_enc", c_void_p), ("w_pred", c_void_p),
+                ("b_pred", c_void_p), ("w_out", c_void_p), ("b_out", c_void_p), ("w_dur", c_void_p),
+                ("b_dur", c_void_p)]
+
+
+class LLError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {ll_status_string(status)} ({status})")
+        self.status = status
+
+
+_lib = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libll.so (raises if it is missing: no CPU fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing; build it with `python -m paper_2406_06220_b200.build`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, J = POINTER(ll_predictor), POINTER(ll_joint)
+    lib.ll_workspace_size.argtypes = [c_int32, c_int32, P, J, c_int32, c_int32, c_int32]
+    lib.ll_workspace_size.restype = c_size_t
+    lib.ll_decode_rnnt.argtypes = [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, P, J, c_int32,
+                                   c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_void_p, c_size_t,
+                                   c_void_p]
+    lib.ll_decode_rnnt.restype = c_int32
+    lib.ll_decode_tdt.argtypes = [c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, P, J, c_int32,
+                                  c_int32, POINTER(c_int32), c_int32, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_int32, c_void_p, c_size_t, c_void_p]
+    lib.ll_decode_tdt.restype = c_int32
+    lib.ll_sync.argtypes = [c_void_p, c_void_p]
+    lib.ll_sync.restype = c_int32
+    lib.ll_status_string.argtypes = [c_int32]
+    lib.ll_status_string.restype = c_char_p
+    lib.ll_stats.argtypes = [c_void_p, POINTER(c_uint64), c_void_p]
+    lib.ll_stats.restype = c_int32
+    lib.ll_debug_joint.argtypes = [c_void_p, c_void_p, c_int32, J, c_int32, c_int32, c_int32, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+    lib.ll_debug_joint.restype = c_int32
+    lib.ll_set_timing_events.argtypes = [c_void_p, c_void_p]
+    lib.ll_set_timing_events.restype = c_int32
+    lib.ll_version.argtypes = []
+    lib.ll_version.restype = c_char_p
+    _lib = lib
+    return lib
+
+
+def ll_status_string(status: int) -> str:
+    return load_library().ll_status_string(int(status)).decode()
+
+
+def ll_version() -> str:
+    return load_library().ll_version().decode()
+
+
+def ll_workspace_size(B, T_max, pred: ll_predictor, joint: ll_joint, dtype, prec, num_durations) -> int:
+    return int(load_library().ll_workspace_size(B, T_max, ctypes.byref(pred), ctypes.byref(joint), dtype,
+                                                prec, num_durations))
+
+
+def ll_decode_rnnt(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols, out_tokens,
+                   out_timestamps, out_lengths, out_capacity, workspace, workspace_bytes, stream) -> int:
+    return int(load_library().ll_decode_rnnt(enc, dtype, prec, B, T_max, lengths, ctypes.byref(pred),
+                                             ctypes.byref(joint), blank_id, max_symbols, out_tokens,
+                                             out_timestamps, out_lengths, out_capacity, workspace,
+                                             workspace_bytes, stream))
+
+
+def ll_decode_tdt(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols, durations,
+                  num_durations, out_tokens, out_timestamps, out_durations, out_lengths, out_capacity,
+                  workspace, workspace_bytes, stream) -> int:
+    dur = None
+    if durations is not None:
+        dur = (c_int32 * max(1, len(durations)))(*[int(d) for d in durations])
+    return int(load_library().ll_decode_tdt(enc, dtype, prec, B, T_max, lengths, ctypes.byref(pred),
+                                            ctypes.byref(joint), blank_id, max_symbols, dur, num_durations,
+                                            out_tokens, out_timestamps, out_durations, out_lengths,
+                                            out_capacity, workspace, workspace_bytes, stream))
+
+
+def ll_sync(workspace, stream) -> int:
+    return int(load_library().ll_sync(workspace, stream))
+
+
+def ll_stats(workspace, stream):
+    out = (c_uint64 * 8)()
+    st = int(load_library().ll_stats(workspace, out, stream))
+    return st, list(out)
+
+
+def ll_debug_joint(enc_rows, g_rows, n, joint, dtype, prec, num_durations, out_logits, out_argmax,
+                   out_dur_argmax, workspace, workspace_bytes, stream) -> int:
+    return int(load_library().ll_debug_joint(enc_rows, g_rows, n, ctypes.byref(joint), dtype, prec,
+                                             num_durations, out_logits, out_argmax, out_dur_argmax,
+                                             workspace, workspace_bytes, stream))
+
+
+def ll_set_timing_events(ev_before_decode, ev_after_decode) -> int:
+    return int(load_library().ll_set_timing_events(ev_before_decode, ev_after_decode))

@@ -200,14 +200,19 @@ def _planted_base(spec: ModelSpec, seed: int, n_extra: int):
     return rng, w, codes, nd
 
 
-def _planted_tokens(rng, n, V1, blank_id, prev=None):
-    """Draw n non-blank tokens, never equal to the previous planted token."""
+def _planted_tokens(rng, n, V1, blank_id, codes, prev=None, max_overlap=4):
+    """Draw n non-blank tokens; each differs from the previous planted token and
+    shares at most `max_overlap` code bits with it, so that z = ReLU(code(y) -
+    code(last)) keeps >= 12 active code dims and y wins by a wide margin."""
     out = []
     for _ in range(n):
         while True:
             y = int(rng.integers(0, V1))
-            if y != blank_id and y != prev:
-                break
+            if y == blank_id or y == prev:
+                continue
+            if prev is not None and float(codes[y] @ codes[prev]) > max_overlap:
+                continue
+            break
         out.append(y)
         prev = y
     return out
@@ -228,7 +233,7 @@ def make_planted_rnnt(spec: ModelSpec, seed: int, B: int, T_max: int, len_lo: in
     for b in range(B):
         L = int(lengths[b])
         frames = [t for t in range(L) if rng.random() < rho]
-        toks = _planted_tokens(rng, len(frames), spec.num_tokens, spec.blank_id)
+        toks = _planted_tokens(rng, len(frames), spec.num_tokens, spec.blank_id, codes)
         for t, y in zip(frames, toks):
             enc[b, t, 0] = -1.0
             enc[b, t, 1:1 + _CODE_DIMS] = codes[y]
@@ -267,7 +272,7 @@ def make_planted_tdt(spec: ModelSpec, seed: int, B: int, T_max: int, len_lo: int
             di = D.index(d)
             enc[b, t, dur0 + di] = 1.0
             if is_tok:
-                y = _planted_tokens(rng, 1, spec.num_tokens, spec.blank_id, prev)[0]
+                y = _planted_tokens(rng, 1, spec.num_tokens, spec.blank_id, codes, prev)[0]
                 prev = y
                 enc[b, t, 0] = -1.0
                 enc[b, t, 1:1 + _CODE_DIMS] = codes[y]

@@ -1,0 +1,135 @@
+"""The C-ABI library loads, exports every symbol include/ll.h declares, and
+validates its arguments on the host (nothing enqueued, no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2406_06220_b200 import ll
+from paper_2406_06220_b200 import build as llbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    llbuild.build()
+    return ll.load_library()
+
+
+def test_exports_every_declared_symbol(lib):
+    header = open(os.path.join(ROOT, "include", "ll.h")).read()
+    declared = set(re.findall(r"\b(ll_[a-z_]+)\s*\(", header))
+    assert declared == set(ll.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_status_strings_and_version(lib):
+    assert ll.ll_status_string(ll.LL_OK) == "LL_OK"
+    assert ll.ll_status_string(ll.LL_ERR_CAPACITY) == "LL_ERR_CAPACITY"
+    assert ll.ll_status_string(99) == "LL_ERR_UNKNOWN"
+    assert "sm_100a" in ll.ll_version()
+
+
+FAKE = 0x10000  # never dereferenced: validation fails first
+
+
+def _model(kind=ll.LL_PRED_LSTM, V1=1025, P=640, H=640, De=512, ctx=1, tdt=False):
+    pred = ll.ll_predictor(kind, V1, P, ctx, FAKE, FAKE, FAKE, FAKE, FAKE)
+    joint = ll.ll_joint(De, P, H, V1, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE,
+                        FAKE if tdt else None, FAKE if tdt else None)
+    return pred, joint
+
+
+def _rnnt(pred, joint, **kw):
+    a = dict(enc=FAKE, dtype=ll.LL_BF16, prec=ll.LL_PREC_FAST, B=32, T_max=275, lengths=FAKE, blank=0, m=10,
+             tok=FAKE, ts=FAKE, lens=FAKE, cap=2750, ws=0x100000, ws_bytes=1 << 40)
+    a.update(kw)
+    return ll.ll_decode_rnnt(a["enc"], a["dtype"], a["prec"], a["B"], a["T_max"], a["lengths"], pred, joint,
+                             a["blank"], a["m"], a["tok"], a["ts"], a["lens"], a["cap"], a["ws"],
+                             a["ws_bytes"], None)
+
+
+def test_workspace_size(lib):
+    pred, joint = _model()
+    n = ll.ll_workspace_size(32, 275, pred, joint, ll.LL_BF16, ll.LL_PREC_FAST, 0)
+    # f [B*T*H] bf16 + E' [V1*4P] f32 + h [2*B*P] bf16 + g [B*H] f32 + header
+    assert n >= 32 * 275 * 640 * 2 + 1025 * 2560 * 4 + 2 * 32 * 640 * 2 + 32 * 640 * 4
+    assert ll.ll_workspace_size(-1, 275, pred, joint, ll.LL_BF16, ll.LL_PREC_FAST, 0) == 0
+    assert ll.ll_workspace_size(32, 275, pred, joint, 7, ll.LL_PREC_FAST, 0) == 0
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(B=-1), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(T_max=-1), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(enc=None), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(lengths=None), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(tok=None), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(lens=None), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(blank=1025), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(blank=-1), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(m=0), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(cap=-1), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(ws=None), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(ws=0x100010), ll.LL_ERR_INVALID_ARGUMENT),      # not 256-byte aligned
+    (dict(ws_bytes=1024), ll.LL_ERR_WORKSPACE),
+    (dict(dtype=5), ll.LL_ERR_INVALID_ARGUMENT),
+    (dict(prec=ll.LL_PREC_EXACT), ll.LL_ERR_UNSUPPORTED),
+])
+def test_rnnt_validation(lib, kw, status):
+    pred, joint = _model()
+    assert _rnnt(pred, joint, **kw) == status
+
+
+def test_model_validation(lib):
+    pred, joint = _model()
+    pred.hidden = 320                      # predictor / joint dims inconsistent
+    assert _rnnt(pred, joint) == ll.LL_ERR_INVALID_ARGUMENT
+    pred, joint = _model(H=632, P=640)     # joint dim not a multiple of 16
+    assert _rnnt(pred, joint) == ll.LL_ERR_UNSUPPORTED
+    pred, joint = _model()
+    pred.w_hh = None
+    assert _rnnt(pred, joint) == ll.LL_ERR_INVALID_ARGUMENT
+    pred, joint = _model(kind=ll.LL_PRED_STATELESS, ctx=0)
+    assert _rnnt(pred, joint) == ll.LL_ERR_INVALID_ARGUMENT
+    pred, joint = _model(kind=ll.LL_PRED_STATELESS, ctx=5)
+    assert _rnnt(pred, joint) == ll.LL_ERR_UNSUPPORTED
+    pred, joint = _model(kind=7)
+    assert _rnnt(pred, joint) == ll.LL_ERR_INVALID_ARGUMENT
+
+
+def test_tdt_validation(lib):
+    pred, joint = _model(tdt=True)
+    call = lambda durs, n, **kw: ll.ll_decode_tdt(FAKE, ll.LL_BF16, ll.LL_PREC_FAST, 32, 275, FAKE, pred, joint,
+                                                  0, 10, durs, n, FAKE, FAKE, None, FAKE, 2750, 0x100000,
+                                                  kw.get("ws_bytes", 1 << 40), None)
+    assert call([0, 1, 2], 0) == ll.LL_ERR_INVALID_ARGUMENT      # empty duration set
+    assert call(None, 3) == ll.LL_ERR_INVALID_ARGUMENT
+    assert call([0, -1, 2], 3) == ll.LL_ERR_INVALID_ARGUMENT     # negative duration
+    assert call(list(range(17)), 17) == ll.LL_ERR_INVALID_ARGUMENT
+    joint.w_dur = None
+    assert call([0, 1, 2], 3) == ll.LL_ERR_INVALID_ARGUMENT      # TDT needs the duration head
+    joint.w_dur = FAKE
+    assert call([0, 1, 2], 3, ws_bytes=100) == ll.LL_ERR_WORKSPACE
+
+
+def test_debug_joint_validation(lib):
+    _, joint = _model()
+    assert ll.ll_debug_joint(FAKE, FAKE, -1, joint, ll.LL_BF16, 0, 0, None, FAKE, None, 0x100000, 1 << 40,
+                             None) == ll.LL_ERR_INVALID_ARGUMENT
+    assert ll.ll_debug_joint(FAKE, FAKE, 4, joint, ll.LL_BF16, 0, 0, None, None, None, 0x100000, 1 << 40,
+                             None) == ll.LL_ERR_INVALID_ARGUMENT
+    assert ll.ll_debug_joint(FAKE, FAKE, 4, joint, ll.LL_BF16, 0, 0, None, FAKE, None, 0x100000, 10,
+                             None) == ll.LL_ERR_WORKSPACE
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports or loads the oracle (test infrastructure only)."""
+    pkg = os.path.join(ROOT, "paper_2406_06220_b200")
+    pat = re.compile(r"^\s*(from\s+oracle|import\s+oracle)|oracle/", re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                assert not pat.search(open(os.path.join(dirpath, f)).read()), f

@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle.
+
+Tolerances (north_star): joint logits within 2e-3 absolute in bf16 and 1e-5
+in fp32; token / timestamp / length sequences bit-exact except at decisions
+whose float64 top-2 gap is below 1e-3 (teacher-forced verifier, oracle/verify.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from gpu_helpers import TOL, gpu_decode, gpu_model, oracle_hyps, verify_all
+from oracle import Transducer
+from paper_2406_06220_b200 import ll
+from paper_2406_06220_b200.decoder import LabelLoopingDecoder, debug_joint
+
+pytestmark = pytest.mark.gpu
+
+
+def _joint_case(spec, seed, n, dtype):
+    w = synth.make_weights(spec, seed, blank_bias=0.3)
+    rng = np.random.default_rng(seed)
+    enc = synth.bf16_round(rng.normal(0, 1, size=(n, spec.enc_dim)))
+    g = rng.normal(0, 0.5, size=(n, spec.joint_dim)).astype(np.float32)
+    model = gpu_model(spec, w, dtype)
+    logits, am, dam = debug_joint(model, torch.from_numpy(enc).to("cuda", model.tdtype),
+                                  torch.from_numpy(g).cuda())
+    o = Transducer.from_spec(spec, w)
+    f = o.enc_proj(enc)
+    ref, dref = [], []
+    for i in range(n):
+        l, dl = o.joint(f[i], g[i].astype(np.float64))
+        ref.append(l)
+        dref.append(dl)
+    ref = np.array(ref)
+    full = np.concatenate([ref, np.array(dref)], 1) if spec.is_tdt else ref
+    return logits.cpu().numpy().astype(np.float64), am.cpu().numpy(), \
+        None if dam is None else dam.cpu().numpy(), full, ref, (np.array(dref) if spec.is_tdt else None)
+
+
+@pytest.mark.parametrize("dtype,tol", [("bf16", 2e-3), ("f32", 1e-5)])
+@pytest.mark.parametrize("shape", ["fc", "tiny"])
+@pytest.mark.parametrize("tdt", [False, True])
+def test_debug_joint_logits(dtype, tol, shape, tdt):
+    """Joint (+ encoder projection) logits vs float64 (north_star tolerances);
+    argmax equal except at float64 near-ties.  n spans several R=16 chunks and a
+    ragged tail."""
+    durs = (0, 1, 2, 3, 4) if tdt else None
+    if shape == "fc":
+        spec = synth.ModelSpec(1025, 512, 640, 640, "lstm", 1, durs, 0, 10)
+    else:
+        spec = synth.ModelSpec(9, 16, 16, 16, "stateless", 1, durs, 0, 3)
+    logits, am, dam, full, ref, dref = _joint_case(spec, 11, 45, dtype)
+    err = np.abs(logits - full).max()
+    assert err < tol, err
+    for i in range(len(am)):
+        gap = ref[i].max() - ref[i][am[i]]
+        assert am[i] == int(np.argmax(ref[i])) or gap < TOL
+        if tdt:
+            gap = dref[i].max() - dref[i][dam[i]]
+            assert dam[i] == int(np.argmax(dref[i])) or gap < TOL
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_cat_dog_through_abi(dtype):
+    """Fig. 2 worked example through ll_decode_rnnt."""
+    spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
+    hyps, dec = gpu_decode(spec, w, enc, lengths, dtype)
+    assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
+    assert [h[1] for h in hyps] == [[0, 2, 2], [1, 3, 3]]
+    st = dec.stats()
+    assert st["predictor_steps"] == 4      # label-looping: BOS + longest hypothesis
+    assert st["joint_rounds"] == 8         # tests/golden/cat_dog.txt
+
+
+def test_tdt_forced_through_abi():
+    spec, w, enc, lengths, vocab = synth.tdt_forced_fixture()
+    hyps, _ = gpu_decode(spec, w, enc, lengths, "bf16")
+    assert [vocab[y] for y in hyps[0][0]] == list("DOG")
+    assert hyps[0][1] == [0, 1, 3] and hyps[0][2] == [1, 2, 1]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("cfg", ["tiny", "tiny-tdt"])
+def test_tiny_random_family(dtype, cfg):
+    """BASELINE configs (1) and (3)-tiny on many seeds (random family, guard and
+    zero-duration paths exercised), teacher-forced against float64."""
+    c = synth.CONFIGS[cfg]
+    spec = c["spec"]
+    ties = decs = 0
+    for seed in range(12):
+        for kind, ctx in [("stateless", 1), ("stateless", 2), ("lstm", 1)]:
+            sp = synth.ModelSpec(spec.num_tokens, spec.enc_dim, spec.pred_dim, spec.joint_dim, kind, ctx,
+                                 spec.durations, spec.blank_id, spec.max_symbols)
+            w = synth.make_weights(sp, 1000 + seed, blank_bias=0.5)
+            enc, lengths = synth.make_inputs(2000 + seed, c["B"], c["T_max"], sp.enc_dim, c["len_lo"], c["len_hi"])
+            hyps, _ = gpu_decode(sp, w, enc, lengths, dtype)
+            t, d = verify_all(sp, w, enc, lengths, hyps)
+            ties += t
+            decs += d
+            if dtype == "f32":
+                ref = oracle_hyps(sp, w, enc, lengths)
+                mism = sum(1 for b in ref if tuple(map(list, ref[b])) != tuple(map(list, hyps[b])))
+                assert mism == 0 or ties > 0
+    assert decs > 1000
+
+
+@pytest.mark.parametrize("kind", ["lstm", "stateless"])
+def test_fc_rnnt_planted_full_batch(kind):
+    """Config (2) at full size (B=32, T in 225..275, V+1=1025, H=P=640, D_e=512),
+    planted family: the decode equals the planted alignment exactly (closed
+    form), and 4 sampled rows pass the float64 teacher-forced verifier."""
+    c = synth.CONFIGS["fc-rnnt"]
+    spec = c["spec"]
+    if kind == "stateless":
+        spec = synth.ModelSpec(1025, 512, 640, 640, "stateless", 2, None, 0, 10)
+    w, enc, lengths, planted = synth.make_planted_rnnt(spec, 5, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+    hyps, dec = gpu_decode(spec, w, enc, lengths, "bf16")
+    for b in range(c["B"]):
+        assert (hyps[b][0], hyps[b][1]) == (planted[b][0], planted[b][1]), b
+    verify_all(spec, w, enc, lengths, hyps, rows=[0, 7, 19, 31])
+    st = dec.stats()
+    assert st["labels"] == sum(len(p[0]) for p in planted)
+
+
+def test_fc_tdt_planted_full_batch():
+    c = synth.CONFIGS["fc-tdt"]
+    spec = c["spec"]
+    w, enc, lengths, planted = synth.make_planted_tdt(spec, 6, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+    hyps, _ = gpu_decode(spec, w, enc, lengths, "bf16")
+    for b in range(c["B"]):
+        assert hyps[b] == planted[b], b
+    verify_all(spec, w, enc, lengths, hyps, rows=[0, 13, 31])
+
+
+@pytest.mark.parametrize("tdt", [False, True])
+def test_fc_random_family_full_batch(tdt):
+    """Config (2)/(3) shapes, random family (near-ties present): all 32 rows pass
+    the teacher-forced float64 verifier with the 1e-3 near-tie tolerance."""
+    c = synth.CONFIGS["fc-tdt" if tdt else "fc-rnnt"]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 21, blank_bias=3.0 if not tdt else 1.0)
+    enc, lengths = synth.make_inputs(22, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
+    hyps, _ = gpu_decode(spec, w, enc, lengths, "bf16")
+    ties, decs = verify_all(spec, w, enc, lengths, hyps)
+    assert decs > 32 * (60 if tdt else 200)
+    assert ties <= decs * 0.01
+
+
+def test_stateless_large_batch_config4_sampled():
+    """Config (4): B=512, lengths 50..1500, D_e=1024, stateless context 2, in the
+    launch configuration bench.py uses; sampled rows verified in float64 and
+    properties (lengths, monotone timestamps, <= m per frame) on all rows."""
+    c = synth.CONFIGS["stateless-b512"]
+    spec = c["spec"]
+    w, enc, lengths, planted = synth.make_planted_rnnt(spec, 9, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+    hyps, _ = gpu_decode(spec, w, enc, lengths, "bf16")
+    for b in range(c["B"]):
+        assert (hyps[b][0], hyps[b][1]) == (planted[b][0], planted[b][1]), b
+    verify_all(spec, w, enc, lengths, hyps, rows=[3, 200, 511])
+
+
+def test_edge_cases():
+    """Empty batch, zero lengths, length > T_max (reported by ll_sync), NaN
+    padding never read (A17), capacity overflow (bounded writes, true count)."""
+    spec = synth.ModelSpec(9, 16, 16, 16, "lstm", 1, None, 0, 3)
+    w = synth.make_weights(spec, 3, blank_bias=-2.0)
+    model = gpu_model(spec, w)
+    # B = 0
+    dec = LabelLoopingDecoder(model, 3, 4, 10)
+    enc = torch.zeros(0, 10, 16, dtype=torch.bfloat16, device="cuda")
+    out = dec.decode(enc, torch.zeros(0, dtype=torch.int32, device="cuda"))
+    assert out.lengths.numel() == 0
+    # zero lengths + NaN padding
+    encn, lengths = synth.make_inputs(4, 4, 10, 16, 0, 10, pad_value=float("nan"))
+    lengths[:2] = 0
+    hyps, _ = gpu_decode(spec, w, encn, lengths)
+    assert hyps[0][0] == [] and hyps[1][0] == []
+    verify_all(spec, w, np.nan_to_num(encn), lengths, hyps)
+    # length > T_max -> LL_ERR_INVALID_ARGUMENT from ll_sync, row decodes empty
+    enc_d = torch.from_numpy(np.nan_to_num(encn)).to("cuda", torch.bfloat16)
+    bad = torch.tensor([3, 11, 5, 2], dtype=torch.int32, device="cuda")
+    assert dec.launch(enc_d, bad) == ll.LL_OK
+    assert dec.sync() == ll.LL_ERR_INVALID_ARGUMENT
+    assert dec.lengths_out[1].item() == 0
+    # capacity overflow: never-blank model emits L*m labels, cap smaller
+    w2 = synth.make_weights(spec, 3, blank_bias=-1e4)
+    m2 = gpu_model(spec, w2)
+    dec2 = LabelLoopingDecoder(m2, 3, 4, 10, cap=7)
+    enc2, len2 = synth.make_inputs(5, 4, 10, 16, 10, 10)
+    dec2.tokens.fill_(-7)
+    assert dec2.launch(torch.from_numpy(enc2).to("cuda", torch.bfloat16), torch.from_numpy(len2).cuda()) == 0
+    assert dec2.sync() == ll.LL_ERR_CAPACITY
+    assert dec2.lengths_out.cpu().tolist() == [30, 30, 30, 30]
+    assert (dec2.tokens[:, :7] >= 1).all()
+
+
+def test_determinism_and_batch_composition():
+    """SPEC.md:354/:356/:395: repeat runs are bitwise identical; an utterance
+    decodes identically alone and inside a permuted batch."""
+    c = synth.CONFIGS["fc-rnnt"]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 31, blank_bias=3.0)
+    enc, lengths = synth.make_inputs(32, 20, 120, spec.enc_dim, 60, 120)
+    model = gpu_model(spec, w)
+    h1, _ = gpu_decode(spec, w, enc, lengths, model=model)
+    h2, _ = gpu_decode(spec, w, enc, lengths, model=model)
+    assert h1 == h2
+    perm = np.random.default_rng(0).permutation(20)
+    hp, _ = gpu_decode(spec, w, enc[perm], lengths[perm], model=model)
+    for i, b in enumerate(perm):
+        assert hp[i] == h1[b]
+    for b in [0, 5, 19]:
+        ha, _ = gpu_decode(spec, w, enc[b:b + 1], lengths[b:b + 1], model=model)
+        assert ha[0] == h1[b]
