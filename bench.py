@@ -75,7 +75,7 @@ def algorithmic_flops(spec, stats, total_frames):
     """a1 L*2*D_e*H; a3 E*2*H*(V+1+|D|); a2 S*(2*(P+P)*4P [LSTM] + 2*P*H)."""
     H, P, De = spec.joint_dim, spec.pred_dim, spec.enc_dim
     V = spec.num_tokens + (len(spec.durations) if spec.is_tdt else 0)
-    E, S = stats["joint_row_evals"], stats["predictor_rows"]
+    E, S = stats["joint_evals"], stats["predictor_rows"]
     a1 = total_frames * 2 * De * H
     a3 = E * 2 * H * V
     a2 = S * ((2 * (P + P) * 4 * P) if spec.pred_kind == "lstm" else 0) + S * 2 * P * H
@@ -227,6 +227,8 @@ def main():
     ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev_s0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev_s1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    for e in ev_k0 + ev_k1:      # torch creates CUDA events lazily: force the handles now
+        e.record(stream)
 
     def step():
         s = dec.launch(enc, lengths)
@@ -317,7 +319,7 @@ def main():
     if os.path.exists(tr_path):
         traffic = json.load(open(tr_path)).get(a.config)
 
-    rows = stats["joint_row_evals"]
+    rows = stats["joint_evals"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": tot_ms_max / a.steps, "higher_is_better": True, "scaling": "weak",

@@ -151,10 +151,13 @@ ll_status ll_sync(void *workspace, ll_stream stream);
 const char *ll_status_string(ll_status status);
 
 /* Decode statistics of the last call that used `workspace`, copied to HOST
- * `out[8]` after synchronising `stream`: [0] outer steps (summed over groups),
- * [1] joint rounds, [2] joint row evaluations, [3] batched predictor steps,
- * [4] predictor row evaluations, [5] labels emitted, [6] groups decoded,
- * [7] cluster size used. */
+ * `out[12]` after synchronising `stream`: [0] outer steps (label-loop
+ * iterations, summed over groups), [1] joint rounds (W-frame windows),
+ * [2] joint evaluations whose decision was used (the algorithmic count of
+ * Alg. 1), [3] batched predictor steps, [4] predictor row evaluations,
+ * [5] labels emitted, [6] groups decoded, [7] cluster size, [8] joint rows
+ * computed (including speculative window frames), [9] window W, [10] rows
+ * per group R, [11] reserved. */
 ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream);
 
 /*

@@ -3,58 +3,88 @@
 // TDT PAPER.md:211-213).
 //
 // One cluster of C CTAs decodes one GROUP of up to R utterances at a time
-// (groups are taken from a device work counter, so any number of clusters /
-// groups works).  Inside a group the control loop of Alg. 3 runs entirely on
-// the device:
+// (groups come from a device work counter; a batch is split into groups
+// because utterances are independent -- batch composition does not change
+// any hypothesis).  Inside a group the control loop of Alg. 3
+// runs entirely on the device:
 //
 //   outer step (label loop, Alg. 3 line 5):
-//     predictor phase   rows that found a label and are still active:
-//                       LSTM  gates = E'[y] + W_hh h  (tensor cores, W_hh streamed
-//                             from L2, gate nonlinearities + cell update fused in the
-//                             epilogue; c stays in the owner CTA), g = W_pred h' + b_pred
-//                       stateless  g = sum_k G_k[ctx_k]  (precomputed tables)
-//     scan (frame loop, Alg. 3 lines 7-19), one ROUND per inner iteration:
-//       z = ReLU(f[b, t_b] + g_b) for the scanning rows (compacted), bf16
-//       joint GEMM [M x H] x [H x slice of V+1(+|D|)] on the CTA's resident
-//       weight slice, argmax fused into the epilogue (packed 64-bit keys, warp
-//       shuffles), per-CTA partial keys broadcast to every CTA through
-//       distributed shared memory, one cluster barrier, then every CTA reduces
-//       the C partials and applies the same time rules -> replicated row state.
-//       Next frame rows f[b, t+1] are prefetched speculatively (RNN-T).
+//     predictor phase (Alg. 3 line 6) for rows that found a label and are still
+//       active.  LSTM (bf16): gates = E'[y] + W_hh h on tensor cores; the W_hh /
+//       W_pred tiles of this CTA stream through a shared-memory ring filled by
+//       a dedicated producer warp with bulk (TMA-engine) copies -- it runs ahead
+//       and prefetches the next step's tiles while the scan is running; gate
+//       nonlinearities + cell update fused in the epilogue (c stays in its
+//       owner CTA); h' and g = W_pred h' + b_pred slices are exchanged between
+//       the CTAs with st.async + mbarriers (no global memory, no cluster
+//       barrier).  Stateless: g = sum_k G_k[ctx_k] (precomputed tables).
+//     scan (frame loop, Alg. 3 lines 7-19) in ROUNDS.  While a row scans, its
+//       predictor output g is fixed, so the joint at frames t..t+W-1 does not
+//       depend on the blank decisions between them: a round evaluates a W-frame
+//       window of every scanning row at once and then applies the decisions in
+//       frame order (first non-blank wins; TDT follows the duration chain).
+//       This is an exact reordering of the inner loop.
+//       Per round:
+//         z = ReLU(f[b, t..t+W-1] + g_b)                     (bf16, shared memory)
+//         joint GEMM [R*W x H] x [H x slice of V+1(+|D|)]    (mma.sync; the CTA's
+//           weight slice lives in REGISTERS for the whole kernel)
+//         argmax fused in the epilogue (packed 64-bit keys, warp shuffles),
+//         per-CTA partial keys st.async'ed to every CTA of the cluster,
+//         mbarrier completion, every CTA reduces the C partials and applies the
+//         same rules -> replicated row state.
+//       f rows arrive by bulk copies; the next window is prefetched
+//       speculatively (assuming the row keeps scanning).
 //     append + time rules + guard (BatchedHyps add_results):
-//       masked append into the caller's preallocated [B, cap] buffers, lanes =
-//       rows of the group (no atomics: each row has one owner lane).
-//
-// Weights stay resident in shared memory (joint slice) for the whole kernel;
-// no host synchronisation happens until the caller's ll_sync.
+//       masked append into the caller's preallocated [B, cap] buffers, one lane
+//       per row (each row has one owner, no atomics).
 #pragma once
 #include "common.cuh"
 
 namespace ll {
 
 constexpr int MAX_R = 32;        // rows per group (<= 32: one lane per row)
+constexpr int MAX_JR = 32;       // joint rows per round R*W (<= 32: one lane per joint row)
 constexpr int MAX_DUR = 16;
 constexpr int MAX_CTX = 4;
-constexpr int MAX_NW = 12;       // warps per CTA (<= 384 threads: up to 168 registers)
+constexpr int MAX_NW = 10;       // consumer warps per CTA (+1 producer warp: <= 352 threads, <= 184 regs)
+constexpr int MAX_C = 16;        // cluster size
+constexpr int KREG = 20;         // 32-wide K blocks of the joint weight slice held in registers (H <= 656)
+constexpr int NSMAX = 8;         // weight-ring slots
+
+// mbarrier indices
+enum {
+  BAR_F = 0,        // [2] f-row bulk copies into fbuf[0/1]
+  BAR_X = 2,        // [2] partial keys arriving (st.async) in part[0/1]
+  BAR_GRP = 4,      // [2] group index broadcast
+  BAR_ACK = 6,      // [2] (rank 0) acknowledgements of the group index
+  BAR_H = 8,        // h' slices arriving
+  BAR_G = 9,        // g slices arriving
+  BAR_FULL = 10,    // [NSMAX] weight ring: tile landed
+  BAR_EMPTY = 10 + NSMAX,  // [NSMAX] weight ring: tile consumed
+  NBARS = 10 + 2 * NSMAX
+};
 
 struct DecodeParams {
   int B, T_max, H, P, V1, nD;
   int blank, max_sym, tdt;
   int durations[MAX_DUR];
   int context;
-  int R, n_groups, cap;
-  int spec_prefetch;             // speculative next-frame prefetch (RNN-T)
+  int R, W, WF;                  // rows per group, window frames, buffered frames per row
+  int NS;                        // weight-ring slots (bf16 LSTM), 0 otherwise
+  int n_groups, cap;
+  int spec_prefetch;             // speculative next-window prefetch
   const int *lengths;
   const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
   const void *w_out, *b_out, *w_dur, *b_dur;
   const void *w_pred, *b_pred, *w_hh;
   const float *tab;              // LSTM: E' [V1][4P]; stateless: G [ctx][V1][H] (b_pred in G_0)
-  void *h;                       // LSTM: [2][B][P] (bf16 / f32)
-  float *gglob;                  // LSTM: [B][H]
+  void *h;                       // f32 LSTM: [2][B][P]
+  float *gglob;                  // f32 LSTM: [B][H]
   int *out_tokens, *out_timestamps, *out_durations, *out_lengths;
   int *status;                   // bit0 bad length, bit1 capacity
   int *group_counter;
   unsigned long long *stats;     // see ll.h ll_stats
+  unsigned long long *prof;      // optional per-phase clock64 totals (LL_PROFILE)
   // ll_debug_joint mode
   const float *dbg_g;
   float *dbg_logits;
@@ -64,14 +94,15 @@ struct DecodeParams {
 
 // Shared-memory layout (identical on host and device).
 struct Layout {
-  int wstride, zstride, tiles_max, UPC, DPC, NW;
-  size_t off_w, off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, total;
+  int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
+  size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline Layout make_layout(bool bf, int H, int P, int V1, int nD, int R, int C,
-                                              bool lstm) {
+// ring: bf16 LSTM (producer warp + weight ring + shared-memory h); NS slots.
+__host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, int V1, int nD, int R, int W,
+                                              int WF, int C, int NS) {
   Layout L;
   const int NT = (V1 + nD + 7) / 8;
   L.tiles_max = (NT + C - 1) / C;
@@ -81,18 +112,24 @@ __host__ __device__ inline Layout make_layout(bool bf, int H, int P, int V1, int
   if (nw < 8) nw = 8;
   if (nw > MAX_NW) nw = MAX_NW;
   L.NW = nw;
+  L.ring = (bf && lstm) ? 1 : 0;
+  L.NS = L.ring ? NS : 0;
+  L.JR = R * W;
+  L.JRp = (L.JR + 15) / 16 * 16;
+  if (L.JRp < R) L.JRp = (R + 15) / 16 * 16;
   const int K = H > P ? H : P;
-  L.wstride = bf ? (int)(align_up((size_t)H * 2, 128) + 64) : 0;
   L.zstride = bf ? (int)(align_up((size_t)K * 2, 128) + 64) : K * 4;
+  L.hstride = (int)(align_up((size_t)P * 2, 128) + 64);
   size_t o = 0;
-  L.off_w = o;    o = align_up(o + (bf ? (size_t)L.tiles_max * 8 * L.wstride : 0), 128);
   L.off_b = o;    o = align_up(o + (size_t)L.tiles_max * 8 * 4, 128);
-  L.off_z = o;    o = align_up(o + (size_t)R * L.zstride, 128);
-  L.off_f = o;    o = align_up(o + (size_t)2 * R * H * (bf ? 2 : 4), 128);
+  L.off_z = o;    o = align_up(o + (size_t)L.JRp * L.zstride, 128);
+  L.off_f = o;    o = align_up(o + (size_t)2 * R * WF * H * (bf ? 2 : 4), 128);
   L.off_g = o;    o = align_up(o + (size_t)R * H * 4, 128);
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * 4, 128);
-  L.off_part = o; o = align_up(o + (size_t)2 * C * R * 16, 128);
-  L.off_wkey = o; o = align_up(o + (size_t)L.NW * R * 16, 128);
+  L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 16, 128);
+  L.off_wkey = o; o = align_up(o + (size_t)L.NW * L.JR * 16, 128);
+  L.off_hs = o;   o = align_up(o + (size_t)(L.ring ? 2 * R * L.hstride : 0), 128);
+  L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * L.hstride, 128);
   L.total = o;
   return L;
 }
@@ -102,10 +139,21 @@ struct RowState {
   int ctx[MAX_CTX][MAX_R];
   int active[MAX_R], scanning[MAX_R], found[MAX_R], needp[MAX_R];
   int fy[MAX_R], ft[MAX_R], fd[MAX_R];
+  int fbase[2][MAX_R], fcnt[2][MAX_R];   // frames held in fbuf[X] for each slot
   int slist[MAX_R], plist[MAX_R];
-  int nscan, npred, nactive;
-  int grp;
+  int zsrc[MAX_JR], zdst[MAX_JR];        // live joint rows: f row offset (elements) / z row
+  int dec[MAX_JR];                        // per joint row: token | dur_index << 24
+  int nscan, npred, nactive, nz, ready;
+  int grp[2];                            // group index broadcast (double-buffered)
+  int ack[2];
+  volatile int done;                     // consumers finished (producer exits)
+  volatile unsigned tag[NSMAX];          // ring: index of the tile last issued into each slot
 };
+
+// Consumer-only CTA barrier (named barrier 1): the producer warp never joins.
+__device__ __forceinline__ void csync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 
 // Per-CTA context of the cluster kernel.
 template <typename T>
@@ -115,16 +163,24 @@ struct Ctx {
   Layout L;
   uint8_t *sm;
   RowState &rs;
-  int C, rank, tid, warp, lane, NW, g, q;
+  uint64_t *bars;
+  int C, rank, tid, warp, lane, NW, NCT, g, q;
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
   int u0, d0;                 // LSTM units / W_pred output dims owned
-  int par;                    // DSMEM partial-buffer parity
-  __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm)
-      : p(p_), sm(sm_), rs(rs_) {
+  int par;                    // partial-buffer parity
+  uint32_t fph, fpend, xph;   // phase / pending bits (replicated in every consumer thread)
+  uint32_t hph;               // BAR_H / BAR_G phase
+  unsigned long long ntile_c; // weight-ring tiles consumed so far (replicated)
+  uint4 wreg[KREG];           // this warp's joint weight tile (bf16), K-permuted fragments
+  uint2 wtail;
+  __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm, uint64_t *bars_)
+      : p(p_), sm(sm_), rs(rs_), bars(bars_), fph(0), fpend(0), xph(0), hph(0), ntile_c(0) {
     C = (int)cluster_size();
     rank = (int)cluster_rank();
-    L = make_layout(BF, p.H, p.P, p.V1, p.nD, p.R, C, lstm);
-    tid = threadIdx.x; warp = tid >> 5; lane = tid & 31; NW = blockDim.x >> 5;
+    L = make_layout(BF, lstm, p.H, p.P, p.V1, p.nD, p.R, p.W, p.WF, C, p.NS);
+    tid = threadIdx.x; warp = tid >> 5; lane = tid & 31;
+    NW = L.NW;               // consumer warps
+    NCT = NW * 32;           // consumer threads
     g = lane >> 2; q = lane & 3;
     const int NT = (p.V1 + p.nD + 7) / 8;
     const int base = NT / C, rem = NT % C;
@@ -134,203 +190,291 @@ struct Ctx {
     d0 = rank * L.DPC;
     par = 0;
   }
-  __device__ uint8_t *wsl() const { return sm + L.off_w; }
+  __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
   __device__ uint8_t *zs() const { return sm + L.off_z; }
-  __device__ uint8_t *fbuf(int cur) const {
-    return sm + L.off_f + (size_t)cur * p.R * p.H * sizeof(T);
-  }
+  __device__ uint8_t *fbuf(int X) const { return sm + L.off_f + (size_t)X * p.R * p.WF * p.H * sizeof(T); }
   __device__ float *gs() const { return (float *)(sm + L.off_g); }
   __device__ float *cs() const { return (float *)(sm + L.off_c); }
-  __device__ uint64_t *part(int pr) const {
-    return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * p.R * 2;
-  }
+  __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
+  __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * L.hstride; }
+  __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * L.hstride; }
+  __device__ void sync() const { csync(NCT); }
+
+  __device__ void init_barriers() {
+    if (tid == 0) {
+      for (int i = 0; i < NBARS; ++i) mbar_init(bars + i, 1);
+      fence_mbar_init();
+    }
+  }
 
   // -------------------------------------------------------------------------
-  // Load this CTA's slice of [W_out; W_dur] (rows tile0*8 ...) into shared
-  // memory once per kernel (bf16 path), and the matching bias slice (fp32).
+  // This CTA's slice of [W_out; W_dur]: rows tile0*8 ... (8 per warp) into the
+  // warp's registers once per kernel (bf16 path); bias slice (fp32) in smem.
   // -------------------------------------------------------------------------
   __device__ void load_weight_slice() {
     const int nrows = L.tiles_max * 8;
     const int V1 = p.V1, NV = p.V1 + p.nD, H = p.H;
     float *bs = bsl();
-    for (int r = tid; r < nrows; r += blockDim.x) {
+    for (int r = tid; r < nrows; r += NCT) {
       const int v = tile0 * 8 + r;
       float bv = 0.f;
-      if (r < ntiles * 8 && v < NV) {
+      if (r < ntiles * 8 && v < NV)
         bv = v < V1 ? to_f32(((const T *)p.b_out)[v]) : to_f32(((const T *)p.b_dur)[v - V1]);
-      }
       bs[r] = bv;
     }
     if constexpr (BF) {
-      const int chunks = H / 8;  // 16-byte chunks per row
-      for (int idx = tid; idx < nrows * chunks; idx += blockDim.x) {
-        const int r = idx / chunks, c = idx % chunks;
-        const int v = tile0 * 8 + r;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (r < ntiles * 8 && v < NV) {
-          const bf16 *src = v < V1 ? (const bf16 *)p.w_out + (size_t)v * H
-                                   : (const bf16 *)p.w_dur + (size_t)(v - V1) * H;
-          val = ldg128_nc(src + c * 8);
+      const int KB = H / 32;
+      const int v = tile0 * 8 + warp * 8 + g;
+      const bool ok = warp < ntiles && v < NV;
+      const bf16 *src = ok ? (v < V1 ? (const bf16 *)p.w_out + (size_t)v * H
+                                     : (const bf16 *)p.w_dur + (size_t)(v - V1) * H)
+                           : nullptr;
+#pragma unroll
+      for (int kb = 0; kb < KREG; ++kb)
+        wreg[kb] = (ok && kb < KB) ? ldg128_nc(src + kb * 32 + q * 8) : make_uint4(0, 0, 0, 0);
+      wtail = (ok && (H & 31)) ? ldg64_nc(src + KB * 32 + q * 4) : make_uint2(0, 0);
+    }
+  }
+
+  // -------------------------------------------------------------------------
+  // f rows: for every scanning slot, frames [base, base + n) with
+  //   base = t (or t + W when speculating that the row keeps scanning),
+  //   n = min(WF, L - base),
+  // by one bulk (TMA-engine) copy per slot into fbuf[X], completing on BAR_F+X.
+  // Called by every consumer thread (the phase bookkeeping is replicated);
+  // only warp 0 issues.  Caller guarantees nobody reads fbuf[X] meanwhile.
+  // -------------------------------------------------------------------------
+  __device__ void wait_f(int X) {
+    mbar_wait(bar(BAR_F + X), (fph >> X) & 1u);
+    fph ^= 1u << X;
+    fpend &= ~(1u << X);
+  }
+  __device__ void issue_f(int X, bool spec) {
+    if ((fpend >> X) & 1u) wait_f(X);  // drain a stale speculative copy first
+    const int n = rs.nscan;
+    const uint32_t frb = (uint32_t)(p.H * sizeof(T));
+    if (warp == 0) {
+      uint32_t bytes = 0;
+      int s = 0, base = 0, cnt = 0;
+      if (lane < n) {
+        s = rs.slist[lane];
+        base = rs.t[s] + (spec ? p.W : 0);
+        cnt = rs.L[s] - base;
+        if (cnt > p.WF) cnt = p.WF;
+        if (cnt < 0) cnt = 0;
+        bytes = (uint32_t)cnt * frb;
+      }
+      uint32_t tot = bytes;
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if (lane == 0) mbar_arrive_expect_tx(bar(BAR_F + X), tot);
+      __syncwarp();
+      if (lane < n) {
+        rs.fbase[X][s] = base;
+        rs.fcnt[X][s] = cnt;
+        if (cnt > 0) {
+          const uint8_t *src = (const uint8_t *)p.f + ((size_t)rs.b[s] * p.T_max + base) * frb;
+          bulk_g2s(fbuf(X) + (size_t)s * p.WF * frb, src, bytes, bar(BAR_F + X));
         }
-        *reinterpret_cast<uint4 *>(wsl() + (size_t)r * L.wstride + c * 16) = val;
+      }
+    }
+    fpend |= 1u << X;
+  }
+
+  // warp 0: the live joint rows of the round (window frames of scanning slots
+  // that exist): z row index and the element offset of their f row in fbuf[X].
+  __device__ void plan_z(int X) {
+    if (warp != 0) return;
+    const int W = p.W;
+    bool live = false;
+    int src = 0, dst = 0;
+    if (lane < rs.nscan * W) {
+      const int s = rs.slist[lane / W], j = lane % W;
+      const int fr = rs.t[s] + j - rs.fbase[X][s];
+      live = rs.t[s] + j < rs.L[s] && fr >= 0 && fr < rs.fcnt[X][s];
+      src = (s * p.WF + fr) * p.H;
+      dst = s * W + j;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const int k = __popc(m & ((1u << lane) - 1u));
+      rs.zsrc[k] = src;
+      rs.zdst[k] = dst;
+    }
+    if (lane == 0) rs.nz = __popc(m);
+  }
+
+  // z[jr] = ReLU(f[b_s, t_s + j] + g_s) for the live joint rows.  Other joint
+  // rows keep stale values: an MMA output row depends only on its own A row
+  // and those rows are never read.  Warp per joint row, 8 columns per lane.
+  __device__ void build_z(int X) {
+    const int H = p.H, W = p.W;
+    const int nz = rs.nz;
+    for (int k = warp; k < nz; k += NW) {
+      const int jr = rs.zdst[k], s = jr / W;
+      if constexpr (BF) {
+        const uint4 *frp = reinterpret_cast<const uint4 *>(fbuf(X)) + rs.zsrc[k] / 8;
+        const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
+        uint4 *zr = reinterpret_cast<uint4 *>(zs() + (size_t)jr * L.zstride);
+#pragma unroll 3
+        for (int c = lane; c < H / 8; c += 32) {
+          const uint4 fv = frp[c];
+          const float4 g0 = gr[2 * c], g1 = gr[2 * c + 1];
+          uint4 o;
+          o.x = pack_bf16x2(fmaxf(bf16_lo(fv.x) + g0.x, 0.f), fmaxf(bf16_hi(fv.x) + g0.y, 0.f));
+          o.y = pack_bf16x2(fmaxf(bf16_lo(fv.y) + g0.z, 0.f), fmaxf(bf16_hi(fv.y) + g0.w, 0.f));
+          o.z = pack_bf16x2(fmaxf(bf16_lo(fv.z) + g1.x, 0.f), fmaxf(bf16_hi(fv.z) + g1.y, 0.f));
+          o.w = pack_bf16x2(fmaxf(bf16_lo(fv.w) + g1.z, 0.f), fmaxf(bf16_hi(fv.w) + g1.w, 0.f));
+          zr[c] = o;
+        }
+      } else {
+        const float4 *frp = reinterpret_cast<const float4 *>(fbuf(X)) + rs.zsrc[k] / 4;
+        const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
+        float4 *zr = reinterpret_cast<float4 *>(zs() + (size_t)jr * L.zstride);
+        for (int c = lane; c < H / 4; c += 32) {
+          const float4 fv = frp[c], gv = gr[c];
+          zr[c] = make_float4(fmaxf(fv.x + gv.x, 0.f), fmaxf(fv.y + gv.y, 0.f), fmaxf(fv.z + gv.z, 0.f),
+                              fmaxf(fv.w + gv.w, 0.f));
+        }
       }
     }
   }
 
-  // f rows f[b, t] of the listed row slots into fbuf[cur][slot] (cp.async).
-  __device__ void issue_f_loads(int cur, const int *slots, const int *tt, int n) {
-    const int chunks = p.H * (int)sizeof(T) / 16;
-    for (int idx = tid; idx < n * chunks; idx += blockDim.x) {
-      const int i = idx / chunks, c = idx % chunks;
-      const int s = slots[i];
-      const int b = rs.b[s];
-      const uint8_t *src = (const uint8_t *)p.f + ((size_t)b * p.T_max + tt[i]) * p.H * sizeof(T);
-      cp_async16(fbuf(cur) + (size_t)s * p.H * sizeof(T) + c * 16, src + c * 16);
-    }
-    cp_async_commit();
-  }
-
-  // z[i] = ReLU(f[slot_i] + g[slot_i]) for i < M; rows M..Mpad-1 zero.
-  __device__ void build_z(int cur, int M, int Mpad) {
-    const int H = p.H;
-    if constexpr (BF) {
-      const int pairs = H / 2;
-      for (int idx = tid; idx < Mpad * pairs; idx += blockDim.x) {
-        const int i = idx / pairs, c = idx % pairs;
-        uint32_t out = 0;
-        if (i < M) {
-          const int s = rs.slist[i];
-          const uint32_t fw = *reinterpret_cast<const uint32_t *>(fbuf(cur) + ((size_t)s * H + 2 * c) * 2);
-          const float2 gv = *reinterpret_cast<const float2 *>(gs() + (size_t)s * H + 2 * c);
-          out = pack_bf16x2(fmaxf(bf16_lo(fw) + gv.x, 0.f), fmaxf(bf16_hi(fw) + gv.y, 0.f));
+  // -------------------------------------------------------------------------
+  // Joint + fused argmax over this CTA's vocabulary slice for joint rows
+  // [0, MT*16).  Writes per-warp keys wkey[warp][jr] = {token key, duration key}.
+  // If `logits` != nullptr (debug), also writes raw logits [row_base + jr][v].
+  // -------------------------------------------------------------------------
+  template <int MT>
+  __device__ __forceinline__ void joint_mma(float (&acc)[2][2][4]) const {
+    const int KB = p.H / 32;
+    const uint8_t *a0 = zs() + (size_t)g * L.zstride + q * 16;
+    const uint8_t *a1 = a0 + (size_t)8 * L.zstride;
+    const uint8_t *a2 = a0 + (size_t)16 * L.zstride;
+    const uint8_t *a3 = a0 + (size_t)24 * L.zstride;
+    if (KB == KREG) {
+      // hot path (H = 640): fully unrolled, no guards, loads can be hoisted
+#pragma unroll
+      for (int kb = 0; kb < KREG; ++kb) {
+        const uint4 b = wreg[kb];
+        const uint4 x0 = lds128(a0 + kb * 64), x1 = lds128(a1 + kb * 64);
+        mma_bf16_16816(acc[0][kb & 1], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
+        mma_bf16_16816(acc[0][kb & 1], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
+        if (MT > 1) {
+          const uint4 x2 = lds128(a2 + kb * 64), x3 = lds128(a3 + kb * 64);
+          mma_bf16_16816(acc[1][kb & 1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+          mma_bf16_16816(acc[1][kb & 1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
         }
-        *reinterpret_cast<uint32_t *>(zs() + (size_t)i * L.zstride + c * 4) = out;
       }
     } else {
-      for (int idx = tid; idx < Mpad * H; idx += blockDim.x) {
-        const int i = idx / H, c = idx % H;
-        float out = 0.f;
-        if (i < M) {
-          const int s = rs.slist[i];
-          out = fmaxf(((const float *)fbuf(cur))[(size_t)s * H + c] + gs()[(size_t)s * H + c], 0.f);
+#pragma unroll
+      for (int kb = 0; kb < KREG; ++kb) {
+        if (kb < KB) {
+          const uint4 b = wreg[kb];
+          const uint4 x0 = lds128(a0 + kb * 64), x1 = lds128(a1 + kb * 64);
+          mma_bf16_16816(acc[0][kb & 1], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
+          mma_bf16_16816(acc[0][kb & 1], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
+          if (MT > 1) {
+            const uint4 x2 = lds128(a2 + kb * 64), x3 = lds128(a3 + kb * 64);
+            mma_bf16_16816(acc[1][kb & 1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+            mma_bf16_16816(acc[1][kb & 1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
+          }
         }
-        ((float *)zs())[(size_t)i * (L.zstride / 4) + c] = out;
+      }
+      if (p.H & 31) {
+        const int o = KB * 64 - q * 8;
+        const uint2 x0 = lds64(a0 + o), x1 = lds64(a1 + o);
+        mma_bf16_16816(acc[0][0], x0.x, x1.x, x0.y, x1.y, wtail.x, wtail.y);
+        if (MT > 1) {
+          const uint2 x2 = lds64(a2 + o), x3 = lds64(a3 + o);
+          mma_bf16_16816(acc[1][0], x2.x, x3.x, x2.y, x3.y, wtail.x, wtail.y);
+        }
       }
     }
   }
 
-  // -------------------------------------------------------------------------
-  // Joint + fused argmax over this CTA's vocabulary slice.  Writes per-warp
-  // keys wkey[warp][i] = {token key, duration key} for rows i < Mpad.
-  // If `logits` != nullptr (debug), also writes raw logits [row_base+i][v].
-  // -------------------------------------------------------------------------
-  __device__ void joint_keys(int M, int MT, float *logits, int row_base) {
+  __device__ void joint_keys(int MT, int nrows_valid, float *logits, int row_base) {
     const int V1 = p.V1, NV = p.V1 + p.nD, H = p.H;
     uint64_t *wk = wkey();
     if constexpr (BF) {
-      uint64_t tk[2][2], dk[2][2];
+      float acc[2][2][4];  // [m-tile][K chain][frag]
 #pragma unroll
-      for (int a = 0; a < 2; ++a) tk[a][0] = tk[a][1] = dk[a][0] = dk[a][1] = 0;
-      const int KB = H / 32;
-      const bool tail = (H & 31) != 0;
-      for (int j = warp; j < ntiles; j += NW) {
-        float acc[2][4];
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-        const uint8_t *brow = wsl() + (size_t)(j * 8 + g) * L.wstride;
-        const uint8_t *a0row = zs() + (size_t)g * L.zstride;
-        const uint8_t *a1row = zs() + (size_t)(g + 8) * L.zstride;
-        const uint8_t *a2row = zs() + (size_t)(g + 16) * L.zstride;
-        const uint8_t *a3row = zs() + (size_t)(g + 24) * L.zstride;
-#pragma unroll 4
-        for (int kb = 0; kb < KB; ++kb) {
-          const uint4 b = lds128(brow + kb * 64 + q * 16);
-          const uint4 x0 = lds128(a0row + kb * 64 + q * 16);
-          const uint4 x1 = lds128(a1row + kb * 64 + q * 16);
-          mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-          mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
-          if (MT > 1) {
-            const uint4 x2 = lds128(a2row + kb * 64 + q * 16);
-            const uint4 x3 = lds128(a3row + kb * 64 + q * 16);
-            mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
-            mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
-          }
-        }
-        if (tail) {
-          const uint2 b = lds64(brow + KB * 64 + q * 8);
-          const uint2 x0 = lds64(a0row + KB * 64 + q * 8);
-          const uint2 x1 = lds64(a1row + KB * 64 + q * 8);
-          mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-          if (MT > 1) {
-            const uint2 x2 = lds64(a2row + KB * 64 + q * 8);
-            const uint2 x3 = lds64(a3row + KB * 64 + q * 8);
-            mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
-          }
-        }
-        // epilogue: bias, keys (and debug logits)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          if (mt >= MT) break;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int rr = e >> 1;                       // 0: row g, 1: row g+8
-            const int lr = (j * 8 + 2 * q + (e & 1));    // local vocab row
-            const int v = tile0 * 8 + lr;
-            const float val = acc[mt][e] + bsl()[lr];
-            const int i = mt * 16 + g + rr * 8;
-            if (v < V1) tk[mt][rr] = umax64(tk[mt][rr], pack_key(val, v));
-            else if (v < NV) dk[mt][rr] = umax64(dk[mt][rr], pack_key(val, v - V1));
-            if (logits != nullptr && i < M && v < NV)
-              logits[(size_t)(row_base + i) * NV + v] = val;
-          }
-        }
+          for (int e = 0; e < 4; ++e) acc[a][c][e] = 0.f;
+      if (warp < ntiles) {
+        if (MT > 1) joint_mma<2>(acc);
+        else joint_mma<1>(acc);
       }
+      uint64_t tk[2][2], dk[2][2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
+          tk[mt][rr] = 0;
+          dk[mt][rr] = 0;
+#pragma unroll
+          for (int e2 = 0; e2 < 2; ++e2) {
+            const int e = rr * 2 + e2;
+            const int lr = warp * 8 + 2 * q + e2;     // local vocab row
+            const int v = tile0 * 8 + lr;
+            if (warp < ntiles && v < NV) {
+              const float val = (acc[mt][0][e] + acc[mt][1][e]) + bsl()[lr];
+              if (v < V1) tk[mt][rr] = umax64(tk[mt][rr], pack_key(val, v));
+              else dk[mt][rr] = umax64(dk[mt][rr], pack_key(val, v - V1));
+              const int jr = mt * 16 + g + rr * 8;
+              if (logits != nullptr && mt < MT && jr < nrows_valid) logits[(size_t)(row_base + jr) * NV + v] = val;
+            }
+          }
           tk[mt][rr] = umax64(tk[mt][rr], shfl_xor_u64(tk[mt][rr], 1));
           tk[mt][rr] = umax64(tk[mt][rr], shfl_xor_u64(tk[mt][rr], 2));
-          dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 1));
-          dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 2));
+          if (p.nD > 0) {
+            dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 1));
+            dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 2));
+          }
         }
       if (q == 0) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
           for (int rr = 0; rr < 2; ++rr) {
-            const int i = mt * 16 + g + rr * 8;
-            if (i < p.R) {
-              wk[((size_t)warp * p.R + i) * 2 + 0] = tk[mt][rr];
-              wk[((size_t)warp * p.R + i) * 2 + 1] = dk[mt][rr];
+            const int jr = mt * 16 + g + rr * 8;
+            if (mt < MT && jr < L.JR) {
+              uint4 e;
+              e.x = (uint32_t)tk[mt][rr]; e.y = (uint32_t)(tk[mt][rr] >> 32);
+              e.z = (uint32_t)dk[mt][rr]; e.w = (uint32_t)(dk[mt][rr] >> 32);
+              *reinterpret_cast<uint4 *>(wk + ((size_t)warp * L.JR + jr) * 2) = e;
             }
           }
       }
     } else {
       // fp32 SIMT: one warp per vocabulary row, lanes split K in a fixed order,
-      // butterfly reduction; lane i keeps the best key of batch row i.
+      // butterfly reduction; lane jr keeps the best key of joint row jr.
       uint64_t tkey = 0, dkey = 0;
       const int nrows = ntiles * 8;
       const int zst = L.zstride / 4;
       const float *z = (const float *)zs();
+      const int M = L.JR;
       for (int lr = warp; lr < nrows; lr += NW) {
         const int v = tile0 * 8 + lr;
         if (v >= NV) break;
         const float *wr = v < V1 ? (const float *)p.w_out + (size_t)v * H
                                  : (const float *)p.w_dur + (size_t)(v - V1) * H;
-        float acc[MAX_R];
+        float acc[MAX_JR];
 #pragma unroll
-        for (int i = 0; i < MAX_R; ++i) acc[i] = 0.f;
+        for (int i = 0; i < MAX_JR; ++i) acc[i] = 0.f;
         for (int k = lane; k < H; k += 32) {
           const float w = __ldg(wr + k);
 #pragma unroll
-          for (int i = 0; i < MAX_R; ++i)
+          for (int i = 0; i < MAX_JR; ++i)
             if (i < M) acc[i] = fmaf(w, z[(size_t)i * zst + k], acc[i]);
         }
+        float mine = 0.f;
 #pragma unroll
-        for (int i = 0; i < MAX_R; ++i) {
+        for (int i = 0; i < MAX_JR; ++i) {
           if (i < M) {
             float s = acc[i];
             s += __shfl_xor_sync(0xffffffffu, s, 16);
@@ -338,127 +482,395 @@ struct Ctx {
             s += __shfl_xor_sync(0xffffffffu, s, 4);
             s += __shfl_xor_sync(0xffffffffu, s, 2);
             s += __shfl_xor_sync(0xffffffffu, s, 1);
-            acc[i] = s;
+            if (lane == i) mine = s;
           }
         }
-        const float bv = bsl()[lr];
-#pragma unroll
-        for (int i = 0; i < MAX_R; ++i) {
-          if (i < M && lane == i) {
-            const float val = acc[i] + bv;
-            if (v < V1) tkey = umax64(tkey, pack_key(val, v));
-            else dkey = umax64(dkey, pack_key(val, v - V1));
-            if (logits != nullptr) logits[(size_t)(row_base + i) * NV + v] = val;
-          }
+        if (lane < M) {
+          const float val = mine + bsl()[lr];
+          if (v < V1) tkey = umax64(tkey, pack_key(val, v));
+          else dkey = umax64(dkey, pack_key(val, v - V1));
+          if (logits != nullptr && lane < nrows_valid) logits[(size_t)(row_base + lane) * NV + v] = val;
         }
       }
-      if (lane < p.R) {
-        wk[((size_t)warp * p.R + lane) * 2 + 0] = tkey;
-        wk[((size_t)warp * p.R + lane) * 2 + 1] = dkey;
+      if (lane < L.JR) {
+        wk[((size_t)warp * L.JR + lane) * 2 + 0] = tkey;
+        wk[((size_t)warp * L.JR + lane) * 2 + 1] = dkey;
       }
     }
   }
 
-  // Reduce per-warp keys and broadcast this CTA's partial to every CTA of the
-  // cluster (distributed shared memory), then one cluster barrier.
-  __device__ void exchange_keys(int M) {
-    __syncthreads();
+  // Reduce per-warp keys of the live joint rows and st.async this CTA's
+  // partial to every CTA of the cluster; each CTA's BAR_X+par completes when
+  // all C partials of all live rows have landed.  The partial buffers are
+  // double-buffered by round parity, and a CTA can be at most one round ahead
+  // of any other (it needs everyone's partials to leave a round).
+  __device__ void exchange_keys() {
+    const int nz = rs.nz;
+    if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par), (uint32_t)(C * nz * 16));
+    sync();
     const uint64_t *wk = wkey();
     uint64_t *pt = part(par);
-    for (int idx = tid; idx < M * C; idx += blockDim.x) {
-      const int i = idx / C, dst = idx % C;
+    if (tid < nz) {
+      const int jr = rs.zdst[tid];
       uint64_t tkey = 0, dkey = 0;
-      for (int w = 0; w < NW; ++w) {
-        tkey = umax64(tkey, wk[((size_t)w * p.R + i) * 2 + 0]);
-        dkey = umax64(dkey, wk[((size_t)w * p.R + i) * 2 + 1]);
+#pragma unroll
+      for (int w = 0; w < MAX_NW; ++w) {
+        if (w < NW) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(wk + ((size_t)w * L.JR + jr) * 2);
+          tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
+          dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
+        }
       }
-      uint64_t *slot = pt + ((size_t)rank * p.R + i) * 2;
-      if (C == 1) {
-        slot[0] = tkey;
-        slot[1] = dkey;
-      } else {
-        st_dsmem_u64x2(dsmem_addr(slot, (uint32_t)dst), tkey, dkey);
+      const uint32_t slot = smem_u32(pt + ((size_t)rank * L.JR + jr) * 2);
+      const uint32_t bb = smem_u32(bar(BAR_X + par));
+      for (int d = 0; d < C; ++d) {
+        const int dst = (rank + d) % C;
+        st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, dkey, mapa_u32(bb, (uint32_t)dst));
       }
     }
-    if (C > 1) cluster_sync_all(); else __syncthreads();
+    mbar_wait(bar(BAR_X + par), (xph >> par) & 1u);
+    xph ^= 1u << par;
   }
 
-  // Final argmax of compact row i from the C partials (after exchange_keys).
-  __device__ void final_keys(int i, int &y, int &di) const {
+  // Final argmax of joint row jr from the C partials (after exchange_keys).
+  __device__ void final_keys(int jr, int &y, int &di) const {
     const uint64_t *pt = part(par);
     uint64_t tkey = 0, dkey = 0;
-    for (int r = 0; r < C; ++r) {
-      tkey = umax64(tkey, pt[((size_t)r * p.R + i) * 2 + 0]);
-      dkey = umax64(dkey, pt[((size_t)r * p.R + i) * 2 + 1]);
+#pragma unroll
+    for (int r = 0; r < MAX_C; ++r) {
+      if (r < C) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + jr) * 2);
+        tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
+        dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
+      }
     }
     y = key_index(tkey);
     di = p.nD > 0 ? key_index(dkey) : 0;
   }
 
-  // -------------------------------------------------------------------------
-  // Warp GEMM with B streamed from global memory (weights read-only, L2
-  // resident): acc[mt] += A(zs rows mt*16..) . B(row brow)^T over K.
-  // Register double buffer of KCH 32-wide K blocks per lane.
-  // -------------------------------------------------------------------------
-  template <int KCH>
-  __device__ __forceinline__ void warp_mma_gB(float (&acc)[2][4], const bf16 *brow, int K, int MT) const {
-    const int KB = K / 32;
-    const int nch = (KB + KCH - 1) / KCH;
-    const uint8_t *a0row = zs() + (size_t)g * L.zstride;
-    const uint8_t *a1row = zs() + (size_t)(g + 8) * L.zstride;
-    const uint8_t *a2row = zs() + (size_t)(g + 16) * L.zstride;
-    const uint8_t *a3row = zs() + (size_t)(g + 24) * L.zstride;
-    uint4 b0[KCH], b1[KCH];
-    auto load = [&](uint4(&buf)[KCH], int ch) {
-#pragma unroll
-      for (int c = 0; c < KCH; ++c) {
-        const int kb = ch * KCH + c;
-        if (kb < KB) buf[c] = ldg128_nc(brow + kb * 32 + q * 8);
-      }
-    };
-    auto compute = [&](uint4(&buf)[KCH], int ch) {
-#pragma unroll
-      for (int c = 0; c < KCH; ++c) {
-        const int kb = ch * KCH + c;
-        if (kb < KB) {
-          const uint4 b = buf[c];
-          const uint4 x0 = lds128(a0row + kb * 64 + q * 16);
-          const uint4 x1 = lds128(a1row + kb * 64 + q * 16);
-          mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-          mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
-          if (MT > 1) {
-            const uint4 x2 = lds128(a2row + kb * 64 + q * 16);
-            const uint4 x3 = lds128(a3row + kb * 64 + q * 16);
-            mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
-            mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
-          }
-        }
-      }
-    };
-    if (nch > 0) load(b0, 0);
-    for (int ch = 0; ch < nch; ch += 2) {
-      if (ch + 1 < nch) load(b1, ch + 1);
-      compute(b0, ch);
-      if (ch + 1 < nch) {
-        if (ch + 2 < nch) load(b0, ch + 2);
-        compute(b1, ch + 1);
-      }
+  // Apply the decisions of one round (warp 0): lane k resolves live joint row
+  // k, then lane s walks slot s's window in frame order (Alg. 3 lines 9-11
+  // and 15-19 for each frame; TDT: blank advances by max(d, 1)).
+  // Also rebuilds the scanning list and checks the speculative window X.
+  __device__ void decide(long long &algevals, int Xnext) {
+    if (warp != 0) return;
+    const int W = p.W;
+    int e = 0x7FFFFFFF;
+    int my_jr = -1;
+    if (lane < rs.nz) {
+      int y, di;
+      my_jr = rs.zdst[lane];
+      final_keys(my_jr, y, di);
+      e = y | (di << 24);
     }
-    if (K & 31) {
-      const uint2 b = ldg64_nc(brow + KB * 32 + q * 4);
-      const uint2 x0 = lds64(a0row + KB * 64 + q * 8);
-      const uint2 x1 = lds64(a1row + KB * 64 + q * 8);
-      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-      if (MT > 1) {
-        const uint2 x2 = lds64(a2row + KB * 64 + q * 8);
-        const uint2 x3 = lds64(a3row + KB * 64 + q * 8);
-        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+    int used = 0;
+    bool sc = false;
+    // publish the decisions by joint row, then walk each slot's window
+    if (lane < rs.nz) rs.dec[my_jr] = e;
+    __syncwarp();
+    if (lane < p.R && rs.scanning[lane]) {
+      const int s = lane;
+      const int t0 = rs.t[s], Ls = rs.L[s];
+      int pos = 0;
+      bool found = false;
+      while (pos < W && t0 + pos < Ls) {
+        const int ee = rs.dec[s * W + pos];
+        const int y = ee & 0xFFFFFF, d = p.tdt ? p.durations[ee >> 24] : 0;
+        ++used;
+        if (y != p.blank) {
+          rs.found[s] = 1;
+          rs.fy[s] = y;
+          rs.ft[s] = t0 + pos;
+          rs.fd[s] = d;
+          found = true;
+          break;
+        }
+        pos += p.tdt ? (d > 1 ? d : 1) : 1;
+      }
+      rs.t[s] = t0 + pos;
+      if (!found) {
+        rs.k[s] = 0;
+        if (rs.t[s] >= Ls) rs.active[s] = 0;
+        else sc = true;
+      }
+      rs.scanning[s] = sc;
+    }
+    // rebuild the scanning list (ascending slot order) and check that the
+    // speculative window in fbuf[Xnext] covers every row that keeps scanning
+    const unsigned ms = __ballot_sync(0xffffffffu, sc);
+    if (sc) rs.slist[__popc(ms & ((1u << lane) - 1u))] = lane;
+    bool ok = true;
+    if (sc) {
+      const int s = lane;
+      int need = rs.L[s] - rs.t[s];
+      if (need > W) need = W;
+      ok = Xnext >= 0 && rs.t[s] >= rs.fbase[Xnext][s] && rs.t[s] + need <= rs.fbase[Xnext][s] + rs.fcnt[Xnext][s];
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+    for (int o = 16; o > 0; o >>= 1) used += __shfl_xor_sync(0xffffffffu, used, o);
+    if (lane == 0) {
+      rs.nscan = __popc(ms);
+      rs.ready = all_ok;
+    }
+    algevals += used;
+  }
+
+  // warp 0: rebuild the compacted scanning / predictor lists (ascending slot order)
+  __device__ void rebuild_lists() {
+    if (warp == 0) {
+      const bool sc = lane < p.R && rs.scanning[lane];
+      const bool pr = lane < p.R && rs.needp[lane];
+      const bool ac = lane < p.R && rs.active[lane];
+      const unsigned ms = __ballot_sync(0xffffffffu, sc);
+      const unsigned mp = __ballot_sync(0xffffffffu, pr);
+      const unsigned ma = __ballot_sync(0xffffffffu, ac);
+      const unsigned below = (1u << lane) - 1u;
+      if (sc) rs.slist[__popc(ms & below)] = lane;
+      if (pr) rs.plist[__popc(mp & below)] = lane;
+      if (lane == 0) {
+        rs.nscan = __popc(ms);
+        rs.npred = __popc(mp);
+        rs.nactive = __popc(ma);
       }
     }
   }
 
-  // SIMT (fp32) warp dot products: out[i] = sum_k A[i][k] W[k] for i < M,
-  // lanes split K, butterfly reduction (every lane ends with all sums).
+  // -------------------------------------------------------------------------
+  // bf16 LSTM predictor.  Tile sequence of one step (identical every step):
+  //   n_local in [0, NG):        W_hh rows {gate*P + u0 + 2n + c/4 : gate = c%4}, c < 8
+  //   n_local in [NG, NG + NPT): W_pred rows d0 + 8(n - NG) + c
+  // A producer warp streams the tiles through the NS-slot ring (bulk copies);
+  // consumer warp w takes tiles w, w + NW, ... of each phase.
+  // -------------------------------------------------------------------------
+  __device__ int ng() const { return L.UPC / 2; }
+  __device__ int npt() const { return L.DPC / 8; }
+
+  __device__ void producer_loop() {
+    const int NS = L.NS, NG = ng(), NT = NG + npt();
+    const uint32_t rowb = (uint32_t)(p.P * 2);
+    unsigned long long n = 0;
+    for (;;) {
+      const int slot = (int)(n % NS);
+      const uint32_t ph = (uint32_t)(((n / NS) & 1) ^ 1);
+      // wait for the slot to be free (or for the consumers to finish)
+      bool freed = false;
+      for (;;) {
+        int ok = 0;
+        if (lane == 0) ok = mbar_try_wait(smem_u32(bar(BAR_EMPTY + slot)), ph) ? 1 : 0;
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (ok) { freed = true; break; }
+        if (rs.done) break;
+      }
+      if (!freed) break;
+      const int nl = (int)(n % NT);
+      // publish which tile the slot's next phase carries: a consumer that wants
+      // tile n waits for the tag first, so an mbarrier parity two phases back
+      // can never be mistaken for tile n (warps take tiles round-robin and may
+      // run more than one ring cycle ahead of the slot).
+      if (lane == 0) {
+        rs.tag[slot] = (unsigned)n;
+        mbar_arrive_expect_tx(bar(BAR_FULL + slot), 8 * rowb);
+      }
+      __syncwarp();
+      if (lane < 8) {
+        const bf16 *src;
+        if (nl < NG) {
+          const int gate = lane & 3, unit = u0 + 2 * nl + (lane >> 2);
+          src = (const bf16 *)p.w_hh + ((size_t)gate * p.P + unit) * p.P;
+        } else {
+          src = (const bf16 *)p.w_pred + (size_t)(d0 + 8 * (nl - NG) + lane) * p.P;
+        }
+        bulk_g2s(ringslot(slot) + (size_t)lane * L.hstride, src, rowb, bar(BAR_FULL + slot));
+      }
+      ++n;
+    }
+    // drain: every issued tile has landed before the CTA may exit
+    const unsigned long long first = n > (unsigned long long)NS ? n - NS : 0;
+    for (unsigned long long k = first; k < n; ++k)
+      if (lane == 0) mbar_wait(bar(BAR_FULL + (int)(k % NS)), (uint32_t)((k / NS) & 1));
+    __syncwarp();
+  }
+
+  // consumer: MMA of ring tile n (global index) against A rows = hs rows of the
+  // predictor list (row pointers per lane), then release the slot.
+  __device__ __forceinline__ void ring_mma(float (&acc)[2][4], unsigned long long n, int MT, const uint8_t *ar0,
+                                           const uint8_t *ar1, const uint8_t *ar2, const uint8_t *ar3,
+                                           unsigned long long *pp = nullptr) {
+    const int NS = L.NS, slot = (int)(n % NS);
+    const long long tw = pp ? clock64() : 0;
+    while (rs.tag[slot] != (unsigned)n) {
+    }
+    mbar_wait(bar(BAR_FULL + slot), (uint32_t)((n / NS) & 1));
+    if (pp) pp[8] += (unsigned long long)(clock64() - tw);
+    const uint8_t *brow = ringslot(slot) + (size_t)g * L.hstride + q * 16;
+    const int KB = p.P / 32;
+#pragma unroll 4
+    for (int kb = 0; kb < KB; ++kb) {
+      const uint4 b = lds128(brow + kb * 64);
+      const uint4 x0 = lds128(ar0 + kb * 64), x1 = lds128(ar1 + kb * 64);
+      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
+      mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
+      if (MT > 1) {
+        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
+        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+        mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
+      }
+    }
+    if (p.P & 31) {
+      const int o = KB * 64 - q * 8;
+      const uint2 b = lds64(brow + o);
+      const uint2 x0 = lds64(ar0 + o), x1 = lds64(ar1 + o);
+      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
+      if (MT > 1) {
+        const uint2 x2 = lds64(ar2 + o), x3 = lds64(ar3 + o);
+        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar(BAR_EMPTY + slot));
+  }
+
+  // broadcast `nbytes16` 16-byte chunks starting at local smem `src` (same
+  // offset in every CTA) to the other CTAs, completing tx on barrier `bi`.
+  __device__ void bcast_rows(const uint8_t *base, int row_stride, int col_off, int row_bytes, int nrows,
+                             const int *rows, int bi) {
+    const int chunks = row_bytes / 16;
+    const int total = nrows * chunks * (C - 1);
+    const uint32_t bb = smem_u32(bar(bi));
+    for (int idx = tid; idx < total; idx += NCT) {
+      const int d = idx % (C - 1), rem = idx / (C - 1);
+      const int c = rem % chunks, i = rem / chunks;
+      const int dst = (rank + 1 + d) % C;
+      const uint8_t *src = base + (size_t)rows[i] * row_stride + col_off + c * 16;
+      const uint4 v = *reinterpret_cast<const uint4 *>(src);
+      const uint32_t la = smem_u32(src);
+      st_async_u64x2(mapa_u32(la, (uint32_t)dst), ((uint64_t)v.y << 32) | v.x, ((uint64_t)v.w << 32) | v.z,
+                     mapa_u32(bb, (uint32_t)dst));
+    }
+  }
+
+  __device__ void predictor_lstm_ring(unsigned long long *pp = nullptr) {
+    long long tm = pp ? clock64() : 0;
+#define LL_SUB(k)                                          \
+  if (pp) {                                                \
+    const long long nw = clock64();                        \
+    pp[k] += (unsigned long long)(nw - tm);                \
+    tm = nw;                                               \
+  }
+    const int n = rs.npred, MT = (n + 15) / 16;
+    const int P = p.P, H = p.H, NG = ng(), NPT = npt();
+    const unsigned long long base = ntile_c;
+    // arm the h' / g exchange barriers for this step (tx from the other CTAs)
+    if (tid == 0 && C > 1) {
+      mbar_arrive_expect_tx(bar(BAR_H), (uint32_t)((C - 1) * n * L.UPC * 2));
+      mbar_arrive_expect_tx(bar(BAR_G), (uint32_t)((C - 1) * n * L.DPC * 4));
+    }
+    // A rows: h of the predictor rows (row i -> slot plist[i]); pad rows reuse row 0
+    auto arow = [&](int i, int hpx) -> const uint8_t * {
+      const int s = rs.plist[i < n ? i : 0];
+      return hsrow(hpx ? (rs.hpar[s] ^ 1) : rs.hpar[s], s) + q * 16;
+    };
+    const uint8_t *ar0 = arow(g, 0), *ar1 = arow(g + 8, 0), *ar2 = arow(g + 16, 0), *ar3 = arow(g + 24, 0);
+    // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units
+    for (int j = warp; j < NG; j += NW) {
+      const int unit = u0 + 2 * j + (q >> 1);
+      const int gate0 = (q & 1) * 2;  // q even: (i, f); q odd: (g, o)
+      // gather E' entries first (L2 latency overlaps the tile wait + MMA)
+      float ev[2][2][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int i = mt * 16 + g + rr * 8;
+          ev[mt][rr][0] = ev[mt][rr][1] = 0.f;
+          if (mt < MT && i < n) {
+            const float *te = p.tab + (size_t)rs.last[rs.plist[i]] * 4 * P + (size_t)gate0 * P + unit;
+            ev[mt][rr][0] = __ldg(te);
+            ev[mt][rr][1] = __ldg(te + P);
+          }
+        }
+      float acc[2][4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
+      LL_SUB(0);
+      ring_mma(acc, base + j, MT, ar0, ar1, ar2, ar3, pp);
+      LL_SUB(1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= MT) break;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int i = mt * 16 + g + rr * 8;
+          const bool valid = i < n;
+          const float v0 = acc[mt][rr * 2 + 0] + ev[mt][rr][0], v1 = acc[mt][rr * 2 + 1] + ev[mt][rr][1];
+          const float o0 = __shfl_xor_sync(0xffffffffu, v0, 1);
+          const float o1 = __shfl_xor_sync(0xffffffffu, v1, 1);
+          if (valid && (q & 1) == 0) {
+            const int s = rs.plist[i];
+            const float ig = sigmoidf_(v0), fg = sigmoidf_(v1), gg = tanhf(o0), og = sigmoidf_(o1);
+            float *cp = cs() + (size_t)s * L.UPC + (unit - u0);
+            const float cn = fg * *cp + ig * gg;
+            *cp = cn;
+            reinterpret_cast<bf16 *>(hsrow(rs.hpar[s] ^ 1, s))[unit] = __float2bfloat16_rn(og * tanhf(cn));
+          }
+        }
+      }
+    }
+    LL_SUB(2);
+    // (2) exchange the h' slices (this CTA's units) with every CTA
+    sync();
+    LL_SUB(3);
+    if (C > 1) {
+      // rows: slot ids; the destination row is the slot's NEXT parity
+      if (tid < n) {
+        const int s = rs.plist[tid];
+        rs.zsrc[tid] = (rs.hpar[s] ^ 1) * p.R + s;  // row index into hs
+      }
+      sync();
+      bcast_rows(sm + L.off_hs, L.hstride, u0 * 2, L.UPC * 2, n, rs.zsrc, BAR_H);
+      mbar_wait(bar(BAR_H), hph & 1u);
+    }
+    LL_SUB(4);
+    const uint8_t *br0 = arow(g, 1), *br1 = arow(g + 8, 1), *br2 = arow(g + 16, 1), *br3 = arow(g + 24, 1);
+    // (3) g = W_pred h' + b_pred for this CTA's output dims
+    for (int j = warp; j < NPT; j += NW) {
+      float acc[2][4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
+      ring_mma(acc, base + NG + j, MT, br0, br1, br2, br3, pp);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        if (mt >= MT) break;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = mt * 16 + g + (e >> 1) * 8;
+          const int d = d0 + j * 8 + 2 * q + (e & 1);
+          if (i < n) gs()[(size_t)rs.plist[i] * H + d] = acc[mt][e] + __bfloat162float(((const bf16 *)p.b_pred)[d]);
+        }
+      }
+    }
+    ntile_c = base + NG + NPT;
+    LL_SUB(5);
+    // (4) exchange the g slices
+    sync();
+    LL_SUB(6);
+    if (C > 1) {
+      bcast_rows((const uint8_t *)gs(), H * 4, d0 * 4, L.DPC * 4, n, rs.plist, BAR_G);
+      mbar_wait(bar(BAR_G), hph & 1u);
+    }
+    hph ^= 1u;
+    if (warp == 0 && lane < n) {
+      const int s = rs.plist[lane];
+      rs.hpar[s] ^= 1;
+    }
+    sync();
+    LL_SUB(7);
+#undef LL_SUB
+  }
+
+  // -------------------------------------------------------------------------
+  // fp32 predictor (LL_F32): SIMT, h / g through global memory + cluster barriers.
+  // -------------------------------------------------------------------------
   __device__ __forceinline__ void warp_dot_f32(float (&acc)[MAX_R], const float *wr, int K, int M) const {
     const float *z = (const float *)zs();
     const int zst = L.zstride / 4;
@@ -484,167 +896,82 @@ struct Ctx {
     }
   }
 
-  // A operand rows (zs) <- h rows of the predictor list (global, written by
-  // every CTA of the cluster), zeros for padding / initial state.
-  __device__ void load_h_rows(int n, int npad, int which /*0: current hpar, 1: next*/) {
+  __device__ void load_h_rows_f32(int n, int which /*0: current hpar, 1: next*/) {
     const int P = p.P;
-    const int chunks = P * (int)sizeof(T) / 16;
-    for (int idx = tid; idx < npad * chunks; idx += blockDim.x) {
-      const int i = idx / chunks, c = idx % chunks;
-      uint8_t *dst = zs() + (size_t)i * L.zstride + c * 16;
-      bool zero = i >= n;
-      int s = 0;
-      if (!zero) {
-        s = rs.plist[i];
-        if (which == 0 && rs.hzero[s]) zero = true;
-      }
-      if (zero) {
-        *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
-      } else {
+    float *z = (float *)zs();
+    const int zst = L.zstride / 4;
+    for (int idx = tid; idx < n * P; idx += NCT) {
+      const int i = idx / P, c = idx % P;
+      const int s = rs.plist[i];
+      float v = 0.f;
+      if (!(which == 0 && rs.hzero[s])) {
         const int hp = which == 0 ? rs.hpar[s] : (rs.hpar[s] ^ 1);
-        const uint8_t *src = (const uint8_t *)p.h + (((size_t)hp * p.B + rs.b[s]) * P) * sizeof(T);
-        cp_async16(dst, src + c * 16);
+        v = __ldcg((const float *)p.h + ((size_t)hp * p.B + rs.b[s]) * P + c);
       }
+      z[(size_t)i * zst + c] = v;
     }
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
+    sync();
   }
 
-  // -------------------------------------------------------------------------
-  // Predictor phase (Alg. 3 line 6 + projection) for the rows in
-  // rs.plist.  Leaves g rows in gs() (cp.async in flight; the scan waits).
-  // -------------------------------------------------------------------------
-  __device__ void predictor_lstm() {
-    const int n = rs.npred, MT = (n + 15) / 16, npad = MT * 16;
-    const int P = p.P, H = p.H;
-    const float *tab = p.tab;  // E' [V1][4P]
-    // (1) gates = E'[y] + W_hh h, fused LSTM cell update for this CTA's units
-    load_h_rows(n, npad, 0);
-    if constexpr (BF) {
-      const int ntile = L.UPC / 2;
-      for (int j = warp; j < ntile; j += NW) {
-        const int ucol = u0 + 2 * j + (g >> 2);
-        const bf16 *brow = (const bf16 *)p.w_hh + ((size_t)(g & 3) * P + ucol) * P;
-        float acc[2][4];
+  __device__ void predictor_lstm_f32() {
+    const int n = rs.npred, P = p.P, H = p.H;
+    const float *tab = p.tab;
+    load_h_rows_f32(n, 0);
+    for (int uu = warp; uu < L.UPC; uu += NW) {
+      const int unit = u0 + uu;
+      float mine[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[MAX_R];
 #pragma unroll
-        for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-        warp_mma_gB<6>(acc, brow, P, MT);
-        const int unit = u0 + 2 * j + (q >> 1);
-        const int gate0 = (q & 1) * 2;  // q even: (i, f); q odd: (g, o)
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          if (mt >= MT) break;
-#pragma unroll
-          for (int rr = 0; rr < 2; ++rr) {
-            const int i = mt * 16 + g + rr * 8;
-            const bool valid = i < n;
-            const int s = valid ? rs.plist[i] : 0;
-            const int y = valid ? rs.last[s] : 0;
-            float v0 = acc[mt][rr * 2 + 0], v1 = acc[mt][rr * 2 + 1];
-            if (valid) {
-              v0 += tab[(size_t)y * 4 * P + (size_t)(gate0 + 0) * P + unit];
-              v1 += tab[(size_t)y * 4 * P + (size_t)(gate0 + 1) * P + unit];
-            }
-            const float o0 = __shfl_xor_sync(0xffffffffu, v0, 1);
-            const float o1 = __shfl_xor_sync(0xffffffffu, v1, 1);
-            if (valid && (q & 1) == 0) {
-              const float ig = sigmoidf_(v0), fg = sigmoidf_(v1), gg = tanhf(o0), og = sigmoidf_(o1);
-              float *cp = cs() + (size_t)s * L.UPC + (unit - u0);
-              const float cn = fg * (rs.hzero[s] ? 0.f : *cp) + ig * gg;
-              *cp = cn;
-              const float hn = og * tanhf(cn);
-              ((bf16 *)p.h)[((size_t)(rs.hpar[s] ^ 1) * p.B + rs.b[s]) * P + unit] = __float2bfloat16_rn(hn);
-            }
-          }
-        }
-      }
-    } else {
-      for (int uu = warp; uu < L.UPC; uu += NW) {
-        const int unit = u0 + uu;
-        float mine[4] = {0.f, 0.f, 0.f, 0.f};
-        float acc[MAX_R];
-#pragma unroll
-        for (int gi = 0; gi < 4; ++gi) {
-          warp_dot_f32(acc, (const float *)p.w_hh + ((size_t)gi * P + unit) * P, P, n);
-#pragma unroll
-          for (int i = 0; i < MAX_R; ++i)
-            if (lane == i) mine[gi] = acc[i];
-        }
-        if (lane < n) {
-          const int s = rs.plist[lane];
-          const int y = rs.last[s];
-          float gate[4];
-#pragma unroll
-          for (int gi = 0; gi < 4; ++gi) gate[gi] = mine[gi] + tab[(size_t)y * 4 * P + (size_t)gi * P + unit];
-          float *cp = cs() + (size_t)s * L.UPC + uu;
-          const float cn = sigmoidf_(gate[1]) * (rs.hzero[s] ? 0.f : *cp) + sigmoidf_(gate[0]) * tanhf(gate[2]);
-          *cp = cn;
-          ((float *)p.h)[((size_t)(rs.hpar[s] ^ 1) * p.B + rs.b[s]) * P + unit] = sigmoidf_(gate[3]) * tanhf(cn);
-        }
-      }
-    }
-    __threadfence();
-    if (C > 1) cluster_sync_all(); else __syncthreads();
-    // (2) g = W_pred h' + b_pred for this CTA's output dims
-    load_h_rows(n, npad, 1);
-    if constexpr (BF) {
-      const int ntile = L.DPC / 8;
-      for (int j = warp; j < ntile; j += NW) {
-        const bf16 *brow = (const bf16 *)p.w_pred + (size_t)(d0 + j * 8 + g) * P;
-        float acc[2][4];
-#pragma unroll
-        for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-        warp_mma_gB<6>(acc, brow, P, MT);
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          if (mt >= MT) break;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int i = mt * 16 + g + (e >> 1) * 8;
-            const int d = d0 + j * 8 + 2 * q + (e & 1);
-            if (i < n) {
-              const int s = rs.plist[i];
-              p.gglob[(size_t)rs.b[s] * H + d] = acc[mt][e] + __bfloat162float(((const bf16 *)p.b_pred)[d]);
-            }
-          }
-        }
-      }
-    } else {
-      for (int dd = warp; dd < L.DPC; dd += NW) {
-        const int d = d0 + dd;
-        float acc[MAX_R];
-        warp_dot_f32(acc, (const float *)p.w_pred + (size_t)d * P, P, n);
-        const float bv = ((const float *)p.b_pred)[d];
+      for (int gi = 0; gi < 4; ++gi) {
+        warp_dot_f32(acc, (const float *)p.w_hh + ((size_t)gi * P + unit) * P, P, n);
 #pragma unroll
         for (int i = 0; i < MAX_R; ++i)
-          if (i < n && lane == i) p.gglob[(size_t)rs.b[rs.plist[i]] * H + d] = acc[i] + bv;
+          if (lane == i) mine[gi] = acc[i];
+      }
+      if (lane < n) {
+        const int s = rs.plist[lane];
+        const int y = rs.last[s];
+        float gate[4];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) gate[gi] = mine[gi] + tab[(size_t)y * 4 * P + (size_t)gi * P + unit];
+        float *cp = cs() + (size_t)s * L.UPC + uu;
+        const float cn = sigmoidf_(gate[1]) * *cp + sigmoidf_(gate[0]) * tanhf(gate[2]);
+        *cp = cn;
+        ((float *)p.h)[((size_t)(rs.hpar[s] ^ 1) * p.B + rs.b[s]) * P + unit] = sigmoidf_(gate[3]) * tanhf(cn);
       }
     }
     __threadfence();
-    if (C > 1) cluster_sync_all(); else __syncthreads();
-    // (3) every CTA pulls the full g rows
-    const int chunks = H * 4 / 16;
-    for (int idx = tid; idx < n * chunks; idx += blockDim.x) {
-      const int i = idx / chunks, c = idx % chunks;
-      const int s = rs.plist[i];
-      cp_async16((uint8_t *)(gs() + (size_t)s * H) + c * 16,
-                 (const uint8_t *)(p.gglob + (size_t)rs.b[s] * H) + c * 16);
+    if (C > 1) cluster_sync_all(); else sync();
+    load_h_rows_f32(n, 1);
+    for (int dd = warp; dd < L.DPC; dd += NW) {
+      const int d = d0 + dd;
+      float acc[MAX_R];
+      warp_dot_f32(acc, (const float *)p.w_pred + (size_t)d * P, P, n);
+      const float bv = ((const float *)p.b_pred)[d];
+#pragma unroll
+      for (int i = 0; i < MAX_R; ++i)
+        if (i < n && lane == i) p.gglob[(size_t)rs.b[rs.plist[i]] * H + d] = acc[i] + bv;
     }
-    cp_async_commit();
-    __syncthreads();
+    __threadfence();
+    if (C > 1) cluster_sync_all(); else sync();
+    for (int idx = tid; idx < n * H; idx += NCT) {
+      const int i = idx / H, c = idx % H;
+      const int s = rs.plist[i];
+      gs()[(size_t)s * H + c] = __ldcg(p.gglob + (size_t)rs.b[s] * H + c);
+    }
+    sync();
     if (warp == 0 && lane < n) {
       const int s = rs.plist[lane];
       rs.hpar[s] ^= 1;
       rs.hzero[s] = 0;
     }
-    __syncthreads();
+    sync();
   }
 
   __device__ void predictor_stateless() {
     const int n = rs.npred, H = p.H, V1 = p.V1;
     const int c4 = H / 4;
-    for (int idx = tid; idx < n * c4; idx += blockDim.x) {
+    for (int idx = tid; idx < n * c4; idx += NCT) {
       const int i = idx / c4, c = idx % c4;
       const int s = rs.plist[i];
       float4 acc = *reinterpret_cast<const float4 *>(p.tab + (size_t)rs.ctx[0][s] * H + c * 4);
@@ -656,23 +983,39 @@ struct Ctx {
     }
   }
 
-  // warp 0: rebuild the compacted scanning / predictor lists (ascending slot order)
-  __device__ void rebuild_lists() {
-    if (warp == 0) {
-      const bool sc = lane < p.R && rs.scanning[lane];
-      const bool pr = lane < p.R && rs.needp[lane];
-      const bool ac = lane < p.R && rs.active[lane];
-      const unsigned ms = __ballot_sync(0xffffffffu, sc);
-      const unsigned mp = __ballot_sync(0xffffffffu, pr);
-      const unsigned ma = __ballot_sync(0xffffffffu, ac);
-      const unsigned below = (1u << lane) - 1u;
-      if (sc) rs.slist[__popc(ms & below)] = lane;
-      if (pr) rs.plist[__popc(mp & below)] = lane;
-      if (lane == 0) {
-        rs.nscan = __popc(ms);
-        rs.npred = __popc(mp);
-        rs.nactive = __popc(ma);
+  // -------------------------------------------------------------------------
+  // Group index broadcast without a cluster barrier: rank 0 takes the next
+  // group from the work counter and st.async's it to every CTA (BAR_GRP+gp);
+  // every CTA acknowledges to rank 0 (BAR_ACK+gp), and rank 0 reuses a
+  // broadcast buffer only after all acknowledgements of its previous use.
+  // -------------------------------------------------------------------------
+  __device__ int next_group(int k) {
+    const int gp = k & 1;
+    const uint32_t ph = (uint32_t)((k >> 1) & 1);
+    if (tid == 0) {
+      mbar_arrive_expect_tx(bar(BAR_GRP + gp), 4);
+      if (rank == 0) {
+        if (k >= 2) mbar_wait(bar(BAR_ACK + gp), ph ^ 1u);
+        mbar_arrive_expect_tx(bar(BAR_ACK + gp), (uint32_t)(4 * C));
+        const int gi = atomicAdd(p.group_counter, 1);
+        const uint32_t slot = smem_u32(&rs.grp[gp]), bb = smem_u32(bar(BAR_GRP + gp));
+        for (int r = 0; r < C; ++r) st_async_u32(mapa_u32(slot, (uint32_t)r), (uint32_t)gi, mapa_u32(bb, (uint32_t)r));
       }
+    }
+    mbar_wait(bar(BAR_GRP + gp), ph);
+    const int grp = rs.grp[gp];
+    sync();
+    if (tid == 0) {
+      const uint32_t slot = smem_u32(&rs.ack[gp]), bb = smem_u32(bar(BAR_ACK + gp));
+      st_async_u32(mapa_u32(slot, 0), 1u, mapa_u32(bb, 0));
+    }
+    return grp;
+  }
+  __device__ void final_acks(int k) {
+    // rank 0 waits for the acknowledgements of the last two broadcasts
+    if (rank == 0 && tid == 0) {
+      for (int kk = k - 1; kk <= k; ++kk)
+        if (kk >= 0) mbar_wait(bar(BAR_ACK + (kk & 1)), (uint32_t)((kk >> 1) & 1));
     }
   }
 };
@@ -681,234 +1024,261 @@ struct Ctx {
 // The decode kernel.  PRED: 0 = LSTM, 1 = stateless.
 // ---------------------------------------------------------------------------
 template <typename T, int PRED>
-__global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
-  __shared__ int s_grp;
-  __shared__ int s_tt[MAX_R];
-  Ctx<T> cx(p, smem, rs, PRED == 0);
+  __shared__ __align__(8) uint64_t s_bars[NBARS];
+  Ctx<T> cx(p, smem, rs, PRED == 0, s_bars);
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
+  constexpr bool RING = sizeof(T) == 2 && PRED == 0;
   unsigned long long st_outer = 0, st_rounds = 0, st_rowevals = 0, st_pred = 0, st_predrows = 0,
                      st_labels = 0, st_groups = 0;
+  long long algevals = 0;
 
-  cx.load_weight_slice();
+  cx.init_barriers();
+  if (tid == 0) rs.done = 0;
+  if (tid < NSMAX) rs.tag[tid] = 0xFFFFFFFFu;
+  if (warp < cx.NW) cx.load_weight_slice();
   __syncthreads();
+  if (C > 1) cluster_sync_all();  // barriers initialised cluster-wide before any st.async
 
-  for (;;) {
-    if (rank == 0 && tid == 0) {
-      const int gi = atomicAdd(p.group_counter, 1);
-      if (C == 1) s_grp = gi;
-      else
-        for (int r = 0; r < C; ++r) st_dsmem_u32(dsmem_addr(&s_grp, (uint32_t)r), (uint32_t)gi);
-    }
-    if (C > 1) cluster_sync_all(); else __syncthreads();
-    const int grp = s_grp;
-    if (grp >= p.n_groups) break;
-    st_groups++;
-
-    // ---- group init (warp 0: lane = row slot) -------------------------------
-    if (warp == 0 && lane < R) {
-      const int b = grp * R + lane;
-      int L = 0;
-      if (b < p.B) {
-        L = p.lengths[b];
-        if (L < 0 || L > p.T_max) {
-          if (rank == 0) atomicOr(p.status, 1);
-          L = 0;
-        }
-      }
-      rs.b[lane] = b < p.B ? b : 0;
-      rs.L[lane] = L;
-      rs.t[lane] = 0; rs.k[lane] = 0; rs.len[lane] = 0;
-      rs.last[lane] = p.blank;
-      rs.hpar[lane] = 0; rs.hzero[lane] = 1;
-      for (int c = 0; c < MAX_CTX; ++c) rs.ctx[c][lane] = p.blank;
-      rs.active[lane] = L > 0;
-      rs.needp[lane] = L > 0;
-      rs.scanning[lane] = 0;
-      rs.found[lane] = 0;
-    }
-    __syncwarp();
-    cx.rebuild_lists();
-    __syncthreads();
-
-    // ---- outer loop over labels (Alg. 3 line 5) -------------------------------
-    while (rs.nactive > 0) {
-      st_outer++;
-      // first-round f rows of every active row (overlaps the predictor phase)
+  if (RING && warp == cx.NW) {
+    cx.producer_loop();
+  } else {
+    int cur = 0;                  // f buffer of the current round
+    // optional phase profile (thread 0 of the first CTA): 0 wait_f, 1 build_z, 2 joint,
+    // 3 exchange, 4 decide, 5 predictor, 6 append/outer, 7 total
+    unsigned long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long pp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const bool prof = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
+    long long t_mark = clock64(), t_start = t_mark;
+#define LL_PHASE(k)                              \
+  if (prof) {                                    \
+    const long long now = clock64();             \
+    pt[k] += (unsigned long long)(now - t_mark); \
+    t_mark = now;                                \
+  }
+    int k = 0;
+    for (;; ++k) {
+      const int grp = cx.next_group(k);
+      if (grp >= p.n_groups) break;
+      st_groups++;
+      // ---- group init (warp 0: lane = row slot) -----------------------------
       if (warp == 0 && lane < R) {
-        rs.scanning[lane] = rs.active[lane];
+        const int b = grp * R + lane;
+        int L = 0;
+        if (b < p.B) {
+          L = p.lengths[b];
+          if (L < 0 || L > p.T_max) {
+            if (rank == 0) atomicOr(p.status, 1);
+            L = 0;
+          }
+        }
+        rs.b[lane] = b < p.B ? b : 0;
+        rs.L[lane] = L;
+        rs.t[lane] = 0; rs.k[lane] = 0; rs.len[lane] = 0;
+        rs.last[lane] = p.blank;
+        rs.hpar[lane] = 0; rs.hzero[lane] = 1;
+        for (int c = 0; c < MAX_CTX; ++c) rs.ctx[c][lane] = p.blank;
+        rs.active[lane] = L > 0;
+        rs.needp[lane] = L > 0;
+        rs.scanning[lane] = 0;
         rs.found[lane] = 0;
       }
+      if constexpr (PRED == 0) {
+        // LSTM initial state h = c = 0 (reading A8)
+        for (int i = tid; i < R * cx.L.UPC; i += cx.NCT) cx.cs()[i] = 0.f;
+        if constexpr (RING) {
+          for (int i = tid; i < R * p.P / 8; i += cx.NCT) {
+            const int s = i / (p.P / 8), c = i % (p.P / 8);
+            *reinterpret_cast<uint4 *>(cx.hsrow(0, s) + c * 16) = make_uint4(0, 0, 0, 0);
+          }
+        }
+      }
       __syncwarp();
       cx.rebuild_lists();
-      __syncthreads();
-      cp_async_wait_all();
-      if (tid < rs.nscan) s_tt[tid] = rs.t[rs.slist[tid]];
-      __syncthreads();
-      int cur = 0;
-      cx.issue_f_loads(cur, rs.slist, s_tt, rs.nscan);
-      // predictor (Alg. 3 line 6): only rows that found a label and stay active
-      if (rs.npred > 0) {
-        st_pred++;
-        st_predrows += rs.npred;
-        if constexpr (PRED == 0) cx.predictor_lstm();
-        else cx.predictor_stateless();
-      }
-      // ---- frame loop: joint rounds until no row scans (Alg. 3 lines 7-19) ----
-      while (rs.nscan > 0) {
-        const int M = rs.nscan, MT = (M + 15) / 16;
-        cp_async_wait_all();
-        __syncthreads();
-        cx.build_z(cur, M, MT * 16);
-        __syncthreads();
-        if (!p.tdt && p.spec_prefetch) {
-          // speculative: a row that predicts blank needs f[b, t+1] next round
-          if (tid < M) {
-            const int s = rs.slist[tid];
-            s_tt[tid] = rs.t[s] + 1 < rs.L[s] ? rs.t[s] + 1 : rs.t[s];
-          }
-          __syncthreads();
-          cx.issue_f_loads(cur ^ 1, rs.slist, s_tt, M);
+      cx.sync();
+
+      // ---- outer loop over labels (Alg. 3 line 5) -----------------------------
+      while (rs.nactive > 0) {
+        st_outer++;
+        if (warp == 0 && lane < R) {
+          rs.scanning[lane] = rs.active[lane];
+          rs.found[lane] = 0;
         }
-        cx.joint_keys(M, MT, nullptr, 0);
-        cx.exchange_keys(M);
-        st_rounds++;
-        st_rowevals += M;
-        // decisions (replicated in every CTA)
-        if (warp == 0 && lane < M) {
-          int y, di;
-          cx.final_keys(lane, y, di);
-          const int s = rs.slist[lane];
-          const int d = p.tdt ? p.durations[di] : 0;
-          if (y == p.blank) {
-            rs.t[s] += p.tdt ? (d > 1 ? d : 1) : 1;
-            rs.k[s] = 0;
-            if (rs.t[s] >= rs.L[s]) {
-              rs.active[s] = 0;
-              rs.scanning[s] = 0;
-            }
-          } else {
-            rs.found[s] = 1;
-            rs.fy[s] = y;
-            rs.ft[s] = rs.t[s];
-            rs.fd[s] = d;
-            rs.scanning[s] = 0;
-          }
-        }
-        cx.par ^= 1;
         __syncwarp();
         cx.rebuild_lists();
-        __syncthreads();
-        cur ^= 1;
-        if (p.tdt || !p.spec_prefetch) {
-          if (tid < rs.nscan) s_tt[tid] = rs.t[rs.slist[tid]];
-          __syncthreads();
-          cx.issue_f_loads(cur, rs.slist, s_tt, rs.nscan);
+        cx.sync();
+        // first window of every active row, overlapping the predictor phase
+        if ((cx.fpend >> cur) & 1u) cur ^= 1;
+        cx.issue_f(cur, false);
+        LL_PHASE(6);
+        // predictor (Alg. 3 line 6): only rows that found a label and stay active
+        if (rs.npred > 0) {
+          st_pred++;
+          st_predrows += rs.npred;
+          if constexpr (PRED == 1) cx.predictor_stateless();
+          else if constexpr (RING) cx.predictor_lstm_ring(prof ? pp : nullptr);
+          else cx.predictor_lstm_f32();
         }
-      }
-      // ---- append + time rules + guard (BatchedHyps.add_results, :196-199) ----
-      if (warp == 0 && lane < R) {
-        const int s = lane;
-        rs.needp[s] = 0;
-        if (rs.found[s]) {
-          const int b = rs.b[s];
-          const int pos = rs.len[s];
-          if (rank == 0) {
-            if (pos < p.cap) {
-              p.out_tokens[(size_t)b * p.cap + pos] = rs.fy[s];
-              p.out_timestamps[(size_t)b * p.cap + pos] = rs.ft[s];
-              if (p.out_durations) p.out_durations[(size_t)b * p.cap + pos] = rs.fd[s];
-            } else {
-              atomicOr(p.status, 2);
-            }
+        LL_PHASE(5);
+        // ---- frame loop: rounds of W-frame windows until no row scans ---------
+        while (rs.nscan > 0) {
+          const int MT = (cx.L.JR + 15) / 16;
+          cx.wait_f(cur);
+          cx.plan_z(cur);
+          cx.sync();                   // f landed, plan visible, predictor's g written
+          LL_PHASE(0);
+          cx.build_z(cur);
+          cx.sync();
+          // speculative: a row whose window is all blank needs the next window
+          if (p.spec_prefetch) cx.issue_f(cur ^ 1, true);
+          LL_PHASE(1);
+          cx.joint_keys(MT, 0, nullptr, 0);
+          LL_PHASE(2);
+          cx.exchange_keys();
+          LL_PHASE(3);
+          st_rounds++;
+          st_rowevals += rs.nz;
+          cx.decide(algevals, p.spec_prefetch ? (cur ^ 1) : -1);
+          cx.par ^= 1;
+          cx.sync();
+          if (rs.nscan > 0) {
+            cur ^= 1;
+            // TDT may jump past the prefetched frames (or no speculation): reload
+            if (!rs.ready) cx.issue_f(cur, false);
+          } else if (p.spec_prefetch) {
+            cur ^= 1;                    // the other buffer holds a stale speculative copy
           }
-          rs.len[s] = pos + 1;
-          if (p.tdt && rs.fd[s] > 0) {
-            rs.t[s] += rs.fd[s];
-            rs.k[s] = 0;
-          } else {
-            rs.k[s] += 1;
-            if (rs.k[s] == p.max_sym) {
-              rs.t[s] += 1;
+          LL_PHASE(4);
+        }
+        // ---- append + time rules + guard (BatchedHyps.add_results, :196-199) --
+        if (warp == 0 && lane < R) {
+          const int s = lane;
+          rs.needp[s] = 0;
+          if (rs.found[s]) {
+            const int b = rs.b[s];
+            const int pos = rs.len[s];
+            if (rank == 0) {
+              if (pos < p.cap) {
+                p.out_tokens[(size_t)b * p.cap + pos] = rs.fy[s];
+                p.out_timestamps[(size_t)b * p.cap + pos] = rs.ft[s];
+                if (p.out_durations) p.out_durations[(size_t)b * p.cap + pos] = rs.fd[s];
+              } else {
+                atomicOr(p.status, 2);
+              }
+            }
+            rs.len[s] = pos + 1;
+            if (p.tdt && rs.fd[s] > 0) {
+              rs.t[s] += rs.fd[s];
               rs.k[s] = 0;
+            } else {
+              rs.k[s] += 1;
+              if (rs.k[s] == p.max_sym) {
+                rs.t[s] += 1;
+                rs.k[s] = 0;
+              }
             }
+            rs.active[s] = rs.t[s] < rs.L[s];
+            rs.needp[s] = rs.active[s];
+            rs.last[s] = rs.fy[s];
+            for (int c = MAX_CTX - 1; c > 0; --c) rs.ctx[c][s] = rs.ctx[c - 1][s];
+            rs.ctx[0][s] = rs.fy[s];
+            rs.found[s] = 0;
           }
-          rs.active[s] = rs.t[s] < rs.L[s];
-          rs.needp[s] = rs.active[s];
-          rs.last[s] = rs.fy[s];
-          for (int c = MAX_CTX - 1; c > 0; --c) rs.ctx[c][s] = rs.ctx[c - 1][s];
-          rs.ctx[0][s] = rs.fy[s];
-          rs.found[s] = 0;
         }
+        __syncwarp();
+        cx.rebuild_lists();
+        cx.sync();
       }
-      __syncwarp();
-      cx.rebuild_lists();
-      __syncthreads();
-    }
-    // ---- group done: lengths, statistics -------------------------------------
-    if (rank == 0 && warp == 0 && lane < R) {
-      const int b = grp * R + lane;
-      if (b < p.B) {
-        p.out_lengths[b] = rs.len[lane];
+      // ---- group done: lengths, statistics -----------------------------------
+      if (rank == 0 && warp == 0) {
+        const int b = grp * R + lane;
+        int tot = 0;
+        if (lane < R && b < p.B) {
+          p.out_lengths[b] = rs.len[lane];
+          tot = rs.len[lane];
+        }
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        st_labels += tot;
       }
     }
-    if (rank == 0 && warp == 0) {
-      int tot = 0;
-      if (lane < R && grp * R + lane < p.B) tot = rs.len[lane];
-      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      st_labels += tot;
+    cx.final_acks(k);
+    // drain outstanding f bulk copies before the CTA exits
+    if ((cx.fpend >> 0) & 1u) cx.wait_f(0);
+    if ((cx.fpend >> 1) & 1u) cx.wait_f(1);
+    cx.sync();
+    if (tid == 0) rs.done = 1;
+    if (prof) {
+      LL_PHASE(6);
+      pt[7] = (unsigned long long)(clock64() - t_start);
+      for (int kk = 0; kk < 8; ++kk) p.prof[kk] = pt[kk];
+      for (int kk = 0; kk < 9; ++kk) p.prof[8 + kk] = pp[kk];
     }
-    if (C > 1) cluster_sync_all(); else __syncthreads();
+#undef LL_PHASE
+    if (rank == 0 && tid == 0 && p.stats) {
+      atomicAdd(p.stats + 0, st_outer);
+      atomicAdd(p.stats + 1, st_rounds);
+      atomicAdd(p.stats + 2, (unsigned long long)algevals);
+      atomicAdd(p.stats + 3, st_pred);
+      atomicAdd(p.stats + 4, st_predrows);
+      atomicAdd(p.stats + 5, st_labels);
+      atomicAdd(p.stats + 6, st_groups);
+      atomicAdd(p.stats + 8, st_rowevals);
+      if (blockIdx.x == 0) {
+        p.stats[7] = (unsigned long long)C;
+        p.stats[9] = (unsigned long long)p.W;
+        p.stats[10] = (unsigned long long)p.R;
+      }
+    }
   }
-  if (rank == 0 && tid == 0 && p.stats) {
-    atomicAdd(p.stats + 0, st_outer);
-    atomicAdd(p.stats + 1, st_rounds);
-    atomicAdd(p.stats + 2, st_rowevals);
-    atomicAdd(p.stats + 3, st_pred);
-    atomicAdd(p.stats + 4, st_predrows);
-    atomicAdd(p.stats + 5, st_labels);
-    atomicAdd(p.stats + 6, st_groups);
-    if (blockIdx.x == 0) p.stats[7] = (unsigned long long)C;
-  }
+  __syncthreads();
+  if (C > 1) cluster_sync_all();  // no CTA exits while peers may still st.async into it
 }
 
 // ---------------------------------------------------------------------------
 // ll_debug_joint: the same joint / argmax / cross-CTA path on given rows.
 // f rows [n][H] (workspace, produced by the encoder projection) + g [n][H].
+// Runs with W = 1: every row is one slot with one frame.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) debug_joint_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
-  __shared__ int s_tt[MAX_R];
-  Ctx<T> cx(p, smem, rs, false);
+  __shared__ __align__(8) uint64_t s_bars[NBARS];
+  Ctx<T> cx(p, smem, rs, false, s_bars);
   const int C = cx.C, tid = cx.tid, warp = cx.warp, lane = cx.lane, R = p.R;
+  cx.init_barriers();
   cx.load_weight_slice();
   __syncthreads();
+  if (C > 1) cluster_sync_all();
   const int cluster_id = blockIdx.x / C, n_clusters = gridDim.x / C;
   for (int base = cluster_id * R; base < p.dbg_n; base += n_clusters * R) {
     const int M = min(R, p.dbg_n - base), MT = (M + 15) / 16;
     if (warp == 0 && lane < R) {
       rs.b[lane] = base + (lane < M ? lane : 0);
-      rs.slist[lane] = lane;
+      rs.t[lane] = 0;
+      rs.L[lane] = 1;
+      rs.scanning[lane] = lane < M;
+      rs.needp[lane] = 0;
+      rs.active[lane] = lane < M;
     }
-    __syncthreads();
-    if (tid < M) s_tt[tid] = 0;
-    // f rows: the workspace holds [n][1][H]; T_max = 1 in debug mode
-    __syncthreads();
-    cx.issue_f_loads(0, rs.slist, s_tt, M);
+    __syncwarp();
+    cx.rebuild_lists();
     for (int idx = tid; idx < M * p.H; idx += blockDim.x) {
       const int i = idx / p.H, c = idx % p.H;
       cx.gs()[(size_t)i * p.H + c] = p.dbg_g[(size_t)(base + i) * p.H + c];
     }
-    cp_async_wait_all();
     __syncthreads();
-    cx.build_z(0, M, MT * 16);
+    cx.issue_f(0, false);   // the workspace holds f as [n][1][H] (T_max = 1)
+    cx.wait_f(0);
+    cx.plan_z(0);
     __syncthreads();
-    cx.joint_keys(M, MT, p.dbg_logits, base);
-    cx.exchange_keys(M);
+    cx.build_z(0);
+    __syncthreads();
+    cx.joint_keys(MT, M, p.dbg_logits, base);
+    cx.exchange_keys();
     if (cx.rank == 0 && warp == 0 && lane < M) {
       int y, di;
       cx.final_keys(lane, y, di);
@@ -916,8 +1286,9 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __gri
       if (p.dbg_dargmax) p.dbg_dargmax[base + lane] = di;
     }
     cx.par ^= 1;
-    if (C > 1) cluster_sync_all(); else __syncthreads();
+    __syncthreads();
   }
+  if (C > 1) cluster_sync_all();  // no CTA exits while peers may still st.async into it
 }
 
 }  // namespace ll

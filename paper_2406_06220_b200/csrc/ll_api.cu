@@ -86,32 +86,92 @@ ll_status check_model(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, l
   return LL_OK;
 }
 
-// Choose the cluster size C and rows per group R; returns false if none fits.
-bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int &C, int &R, Layout &L) {
+// Decode configuration: cluster size C, rows per group R, window W (R*W <= 32
+// joint rows per round), buffered frames WF = W + max_duration - 1.
+struct Config {
+  int C, R, W, WF, NS;
+  Layout L;
+};
+
+static int pow2ceil(int x) {
+  int r = 1;
+  while (r < x) r <<= 1;
+  return r;
+}
+
+// Candidate (C, R, W) in preference order; the first that fits wins.  The
+// preferred R spreads the batch over the ~8 concurrently resident 16-CTA
+// clusters of a B200 (small groups = fewer rounds per group), W = 32 / R.
+// nclusters: how many clusters of the chosen size can be resident (0: unknown,
+// assume 8).  R is chosen so that all groups of the batch run in one wave.
+bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf,
+                   int nclusters = 0) {
   const int forceC = env_int("LL_CLUSTER", 0);
-  const int wantR = env_int("LL_GROUP_ROWS", 16);
-  const int Rs[2] = {wantR == 32 ? 32 : 16, 16};
-  for (int pass = 0; pass < 2; ++pass) {      // pass 0: one vocab tile per warp; pass 1: any
-    for (int ri = 0; ri < 2; ++ri) {
-      R = Rs[ri];
-      for (C = 1; C <= 16; C *= 2) {
-        if (forceC && C != forceC) continue;
-        const int NT = (V1 + nD + 7) / 8;
-        if (bf && pass == 0 && (NT + C - 1) / C > MAX_NW) continue;
-        if (bf) {
-          if (H % (8 * C)) continue;
-          if (lstm && P % (2 * C)) continue;
-        } else {
-          if (H % C) continue;
-          if (lstm && P % C) continue;
+  const int forceR = env_int("LL_GROUP_ROWS", 0);
+  const int forceW = env_int("LL_WINDOW", 0);
+  const int forceNS = env_int("LL_RING", 0);
+  const bool ring = bf && lstm;
+  if (bf && H > KREG * 32 + 16) return false;        // joint slice must fit the register tile
+  const int ncl = nclusters > 0 ? nclusters : 8;
+  int Rpref = forceR ? forceR : (B + ncl - 1) / ncl;
+  if (Rpref < 1) Rpref = 1;
+  if (Rpref > MAX_R) Rpref = MAX_R;
+  for (int C = 1; C <= MAX_C; C *= 2) {
+    if (forceC && C != forceC) continue;
+    const int NT = (V1 + nD + 7) / 8;
+    if (bf && (NT + C - 1) / C > MAX_NW) continue;   // one vocab tile per warp
+    if (bf) {
+      if (H % (8 * C)) continue;
+      if (lstm && P % (8 * C)) continue;             // h' slice: whole 16-byte chunks
+    } else {
+      if (H % C) continue;
+      if (lstm && P % C) continue;
+    }
+    for (int R = Rpref; R >= 1; --R) {
+      if (forceR && R != forceR) continue;
+      int W = forceW ? forceW : MAX_JR / R;
+      if (W > 8) W = 8;
+      if (W < 1) W = 1;
+      if (R * W > MAX_JR) continue;
+      for (; W >= 1; W >>= 1) {
+        cf.C = C; cf.R = R; cf.W = W; cf.WF = W + (maxd > 1 ? maxd - 1 : 0);
+        // as many ring slots as fit (2..NSMAX)
+        for (int NS = ring ? (forceNS ? forceNS : NSMAX) : 0; NS >= (ring ? 2 : 0); --NS) {
+          cf.NS = NS;
+          cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, NS);
+          if (cf.L.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) return true;
+          if (!ring) break;
         }
-        L = make_layout(bf, H, P, V1, nD, R, C, lstm);
-        if (L.total + sizeof(RowState) + 1024 > SMEM_LIMIT) continue;
-        return true;
+        if (forceW) break;
       }
     }
   }
   return false;
+}
+
+// Resident clusters of size C for the decode kernel (1 CTA per SM).
+template <typename T, int PRED>
+int max_clusters(int C, const Layout &L) {
+  auto kern = decode_kernel<T, PRED>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3((L.NW + L.ring) * 32);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(C);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void *)kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 template <typename T, int PRED>
@@ -128,7 +188,7 @@ ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_gro
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(L.NW * 32);
+  cfg.blockDim = dim3((L.NW + L.ring) * 32);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = st;
   cfg.attrs = attr;
@@ -219,9 +279,19 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   const bool bf = dt == LL_BF16;
   const bool lstm = pr->kind == LL_PRED_LSTM;
   const int H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs, De = jn->enc_dim;
-  int C = 0, R = 0;
-  Layout L;
-  if (!choose_config(bf, lstm, H, P, V1, nD, C, R, L)) return LL_ERR_UNSUPPORTED;
+  int maxd = 1;
+  for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
+  Config cf;
+  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return LL_ERR_UNSUPPORTED;
+  {
+    // re-choose R / W with the number of clusters that can actually be resident
+    int ncl = 0;
+    if (bf) ncl = lstm ? max_clusters<bf16, 0>(cf.C, cf.L) : max_clusters<bf16, 1>(cf.C, cf.L);
+    else ncl = lstm ? max_clusters<float, 0>(cf.C, cf.L) : max_clusters<float, 1>(cf.C, cf.L);
+    if (ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl)) return LL_ERR_UNSUPPORTED;
+  }
+  const int C = cf.C, R = cf.R;
+  const Layout &L = cf.L;
 
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t *ws = (uint8_t *)workspace;
@@ -254,6 +324,9 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   for (int i = 0; i < nD; ++i) p.durations[i] = durations[i];
   p.context = lstm ? 1 : pr->context;
   p.R = R;
+  p.W = cf.W;
+  p.WF = cf.WF;
+  p.NS = cf.NS;
   p.n_groups = (B + R - 1) / R;
   p.cap = cap;
   p.spec_prefetch = env_int("LL_SPEC_PREFETCH", 1);
@@ -270,6 +343,7 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   p.status = (int *)ws;
   p.group_counter = (int *)ws + 1;
   p.stats = (unsigned long long *)(ws + 64);
+  p.prof = env_int("LL_PROFILE", 0) ? (unsigned long long *)(ws + 256) : nullptr;
   int used = 0;
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
   if (bf)
@@ -350,7 +424,7 @@ ll_status ll_sync(void *workspace, ll_stream stream) {
 ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream) {
   if (!workspace || !out) return LL_ERR_INVALID_ARGUMENT;
   if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return LL_ERR_CUDA;
-  if (cudaMemcpy(out, (const uint8_t *)workspace + 64, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost) !=
+  if (cudaMemcpy(out, (const uint8_t *)workspace + 64, 12 * sizeof(uint64_t), cudaMemcpyDeviceToHost) !=
       cudaSuccess)
     return LL_ERR_CUDA;
   return LL_OK;
@@ -374,9 +448,12 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
     return LL_ERR_WORKSPACE;
   const bool bf = dtype == LL_BF16;
   const int H = joint->joint_dim, V1 = joint->num_outputs, De = joint->enc_dim;
-  int C = 0, R = 0;
-  Layout L;
-  if (!choose_config(bf, false, H, joint->pred_dim, V1, num_durations, C, R, L)) return LL_ERR_UNSUPPORTED;
+  Config cf;
+  if (!choose_config(bf, false, H, joint->pred_dim, V1, num_durations, 1, 16 * 8, cf)) return LL_ERR_UNSUPPORTED;
+  cf.R = 16; cf.W = 1; cf.WF = 1; cf.NS = 0;
+  cf.L = make_layout(bf, false, H, joint->pred_dim, V1, num_durations, 16, 1, 1, cf.C, 0);
+  const int C = cf.C, R = cf.R;
+  const Layout &L = cf.L;
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t *ws = (uint8_t *)workspace;
   const Ws w = ws_layout(n, 1, &dummy, joint, dtype);
@@ -387,6 +464,8 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   memset(&p, 0, sizeof(p));
   p.B = n; p.T_max = 1; p.H = H; p.P = joint->pred_dim; p.V1 = V1; p.nD = num_durations;
   p.R = R;
+  p.W = 1;
+  p.WF = 1;
   p.f = ws + w.f;
   p.w_out = joint->w_out; p.b_out = joint->b_out; p.w_dur = joint->w_dur; p.b_dur = joint->b_dur;
   p.dbg_g = g_rows; p.dbg_logits = out_logits; p.dbg_argmax = out_argmax; p.dbg_dargmax = out_dur_argmax;

@@ -141,8 +141,8 @@ class LabelLoopingDecoder:
         s, v = ll.ll_stats(self.ws_ptr, st)
         if s != ll.LL_OK:
             raise ll.LLError(s, "ll_stats")
-        keys = ["outer_steps", "joint_rounds", "joint_row_evals", "predictor_steps", "predictor_rows",
-                "labels", "groups", "cluster_size"]
+        keys = ["outer_steps", "joint_rounds", "joint_evals", "predictor_steps", "predictor_rows",
+                "labels", "groups", "cluster_size", "joint_rows_computed", "window", "group_rows", "reserved"]
         return dict(zip(keys, v))
 
 

@@ -62,15 +62,26 @@ def test_debug_joint_logits(dtype, tol, shape, tdt):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-def test_cat_dog_through_abi(dtype):
-    """Fig. 2 worked example through ll_decode_rnnt."""
+@pytest.mark.parametrize("window", [1, 0])
+def test_cat_dog_through_abi(dtype, window, monkeypatch):
+    """Fig. 2 worked example through ll_decode_rnnt.  With a
+    one-frame window (W=1, the paper's inner loop) the device runs exactly the
+    golden 4 predictor steps and 8 joint rounds of Alg. 3; with the default
+    multi-frame window the hypotheses are identical and the decisions used
+    equal the frame-by-frame count."""
+    if window:
+        monkeypatch.setenv("LL_WINDOW", str(window))
+        monkeypatch.setenv("LL_GROUP_ROWS", "4")
     spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
     hyps, dec = gpu_decode(spec, w, enc, lengths, dtype)
     assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
     assert [h[1] for h in hyps] == [[0, 2, 2], [1, 3, 3]]
     st = dec.stats()
     assert st["predictor_steps"] == 4      # label-looping: BOS + longest hypothesis (SPEC.md:329)
-    assert st["joint_rounds"] == 8         # tests/golden/cat_dog.txt
+    assert st["joint_evals"] == 7 + 7      # one decision per alignment symbol (PAPER.md:172)
+    if window == 1:
+        assert st["window"] == 1
+        assert st["joint_rounds"] == 8     # tests/golden/cat_dog.txt
 
 
 def test_tdt_forced_through_abi():
