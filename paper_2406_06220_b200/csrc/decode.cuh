@@ -61,7 +61,8 @@ enum {
   BAR_G = 9,        // g slices arriving
   BAR_FULL = 10,    // [NSMAX] weight ring: tile landed
   BAR_EMPTY = 10 + NSMAX,  // [NSMAX] weight ring: tile consumed
-  NBARS = 10 + 2 * NSMAX
+  BAR_E = 10 + 2 * NSMAX,  // E' slices of the predictor rows landed
+  NBARS = 11 + 2 * NSMAX
 };
 
 struct DecodeParams {
@@ -78,6 +79,7 @@ struct DecodeParams {
   const void *w_out, *b_out, *w_dur, *b_dur;
   const void *w_pred, *b_pred, *w_hh;
   const float *tab;              // LSTM: E' [V1][4P]; stateless: G [ctx][V1][H] (b_pred in G_0)
+  const bf16 *wst;               // bf16 LSTM: per-CTA tile stream [C][NG+NPT][8][P] (packed, swizzled)
   void *h;                       // f32 LSTM: [2][B][P]
   float *gglob;                  // f32 LSTM: [B][H]
   int *out_tokens, *out_timestamps, *out_durations, *out_lengths;
@@ -95,7 +97,7 @@ struct DecodeParams {
 // Shared-memory layout (identical on host and device).
 struct Layout {
   int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
-  size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, total;
+  size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, off_es, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -129,7 +131,8 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 16, 128);
   L.off_wkey = o; o = align_up(o + (size_t)L.NW * L.JR * 16, 128);
   L.off_hs = o;   o = align_up(o + (size_t)(L.ring ? 2 * R * L.hstride : 0), 128);
-  L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * L.hstride, 128);
+  L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * P * 2, 128);
+  L.off_es = o;   o = align_up(o + (size_t)(L.ring ? R * 4 * L.UPC * 4 : 0), 128);
   L.total = o;
   return L;
 }
@@ -169,7 +172,7 @@ struct Ctx {
   int u0, d0;                 // LSTM units / W_pred output dims owned
   int par;                    // partial-buffer parity
   uint32_t fph, fpend, xph;   // phase / pending bits (replicated in every consumer thread)
-  uint32_t hph;               // BAR_H / BAR_G phase
+  uint32_t hph;               // BAR_H / BAR_G / BAR_E phase
   unsigned long long ntile_c; // weight-ring tiles consumed so far (replicated)
   uint4 wreg[KREG];           // this warp's joint weight tile (bf16), K-permuted fragments
   uint2 wtail;
@@ -199,7 +202,8 @@ struct Ctx {
   __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
   __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * L.hstride; }
-  __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * L.hstride; }
+  __device__ float *es() const { return (float *)(sm + L.off_es); }
+  __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * p.P * 2; }
   __device__ void sync() const { csync(NCT); }
 
   __device__ void init_barriers() {
@@ -670,18 +674,11 @@ struct Ctx {
       if (lane == 0) {
         rs.tag[slot] = (unsigned)n;
         mbar_arrive_expect_tx(bar(BAR_FULL + slot), 8 * rowb);
+        // the packed stream holds this CTA's tiles back to back: one 8*P*2-byte copy
+        const bf16 *src = p.wst + ((size_t)rank * NT + nl) * 8 * p.P;
+        bulk_g2s(ringslot(slot), src, 8 * rowb, bar(BAR_FULL + slot));
       }
       __syncwarp();
-      if (lane < 8) {
-        const bf16 *src;
-        if (nl < NG) {
-          const int gate = lane & 3, unit = u0 + 2 * nl + (lane >> 2);
-          src = (const bf16 *)p.w_hh + ((size_t)gate * p.P + unit) * p.P;
-        } else {
-          src = (const bf16 *)p.w_pred + (size_t)(d0 + 8 * (nl - NG) + lane) * p.P;
-        }
-        bulk_g2s(ringslot(slot) + (size_t)lane * L.hstride, src, rowb, bar(BAR_FULL + slot));
-      }
       ++n;
     }
     // drain: every issued tile has landed before the CTA may exit
@@ -692,33 +689,48 @@ struct Ctx {
   }
 
   // consumer: MMA of ring tile n (global index) against A rows = hs rows of the
-  // predictor list (row pointers per lane), then release the slot.
+  // predictor list (row pointers per lane), then release the slot.  HI: rows
+  // 8..15 of the m16 tile are used (more than 8 predictor rows); otherwise they
+  // are padding and are fed as zeros without touching shared memory.
+  template <bool HI>
+  __device__ __forceinline__ void ring_mma_kb(float (&acc)[2][4], const uint8_t *brow, int sw, int kb, int MT,
+                                              const uint8_t *ar0, const uint8_t *ar1, const uint8_t *ar2,
+                                              const uint8_t *ar3) const {
+    const uint4 b = lds128(brow + (((kb * 4 + q) ^ sw) * 16));
+    const uint4 x0 = lds128(ar0 + kb * 64);
+    const uint4 x1 = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
+    mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
+    mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
+    if (MT > 1) {
+      const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
+      mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+      mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
+    }
+  }
+  template <bool HI>
   __device__ __forceinline__ void ring_mma(float (&acc)[2][4], unsigned long long n, int MT, const uint8_t *ar0,
                                            const uint8_t *ar1, const uint8_t *ar2, const uint8_t *ar3,
                                            unsigned long long *pp = nullptr) {
     const int NS = L.NS, slot = (int)(n % NS);
     const long long tw = pp ? clock64() : 0;
-    while (rs.tag[slot] != (unsigned)n) {
-    }
+    while (rs.tag[slot] != (unsigned)n) __nanosleep(64);
     mbar_wait(bar(BAR_FULL + slot), (uint32_t)((n / NS) & 1));
     if (pp) pp[8] += (unsigned long long)(clock64() - tw);
-    const uint8_t *brow = ringslot(slot) + (size_t)g * L.hstride + q * 16;
+    // packed rows are unpadded (P*2 bytes); odd rows store 16-byte chunk c at
+    // c ^ 4 so the two rows of each 8-lane LDS.128 phase hit disjoint banks
+    const uint8_t *brow = ringslot(slot) + (size_t)g * p.P * 2;
+    const int sw = ((g & 1) && (p.P % 64) == 0) ? 4 : 0;
     const int KB = p.P / 32;
+    if (KB == KREG) {
+#pragma unroll
+      for (int kb = 0; kb < KREG; ++kb) ring_mma_kb<HI>(acc, brow, sw, kb, MT, ar0, ar1, ar2, ar3);
+    } else {
 #pragma unroll 4
-    for (int kb = 0; kb < KB; ++kb) {
-      const uint4 b = lds128(brow + kb * 64);
-      const uint4 x0 = lds128(ar0 + kb * 64), x1 = lds128(ar1 + kb * 64);
-      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-      mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
-      if (MT > 1) {
-        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
-        mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
-      }
+      for (int kb = 0; kb < KB; ++kb) ring_mma_kb<HI>(acc, brow, sw, kb, MT, ar0, ar1, ar2, ar3);
     }
     if (p.P & 31) {
       const int o = KB * 64 - q * 8;
-      const uint2 b = lds64(brow + o);
+      const uint2 b = lds64(brow + KB * 64 + q * 8);
       const uint2 x0 = lds64(ar0 + o), x1 = lds64(ar1 + o);
       mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
       if (MT > 1) {
@@ -771,30 +783,36 @@ struct Ctx {
       return hsrow(hpx ? (rs.hpar[s] ^ 1) : rs.hpar[s], s) + q * 16;
     };
     const uint8_t *ar0 = arow(g, 0), *ar1 = arow(g + 8, 0), *ar2 = arow(g + 16, 0), *ar3 = arow(g + 24, 0);
-    // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units
+    // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units.
+    // E'[y_i] slices of this CTA's units (4 gates x UPC floats per row) are
+    // staged into shared memory by bulk copies that overlap the first tiles.
+    if (warp == 0) {
+      const uint32_t segb = (uint32_t)(L.UPC * 4);
+      if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)(4 * n) * segb);
+      __syncwarp();
+      for (int x = lane; x < 4 * n; x += 32) {
+        const int i = x >> 2, gate = x & 3;
+        const int s = rs.plist[i];
+        bulk_g2s(es() + ((size_t)i * 4 + gate) * L.UPC, p.tab + (size_t)rs.last[s] * 4 * P + (size_t)gate * P + u0,
+                 segb, bar(BAR_E));
+      }
+    }
+    const bool hi = n > 8;
+    bool e_ready = false;
     for (int j = warp; j < NG; j += NW) {
       const int unit = u0 + 2 * j + (q >> 1);
       const int gate0 = (q & 1) * 2;  // q even: (i, f); q odd: (g, o)
-      // gather E' entries first (L2 latency overlaps the tile wait + MMA)
-      float ev[2][2][2];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int i = mt * 16 + g + rr * 8;
-          ev[mt][rr][0] = ev[mt][rr][1] = 0.f;
-          if (mt < MT && i < n) {
-            const float *te = p.tab + (size_t)rs.last[rs.plist[i]] * 4 * P + (size_t)gate0 * P + unit;
-            ev[mt][rr][0] = __ldg(te);
-            ev[mt][rr][1] = __ldg(te + P);
-          }
-        }
       float acc[2][4];
 #pragma unroll
       for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
       LL_SUB(0);
-      ring_mma(acc, base + j, MT, ar0, ar1, ar2, ar3, pp);
+      if (hi) ring_mma<true>(acc, base + j, MT, ar0, ar1, ar2, ar3, pp);
+      else ring_mma<false>(acc, base + j, MT, ar0, ar1, ar2, ar3, pp);
       LL_SUB(1);
+      if (!e_ready) {
+        mbar_wait(bar(BAR_E), hph & 1u);
+        e_ready = true;
+      }
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         if (mt >= MT) break;
@@ -802,7 +820,13 @@ struct Ctx {
         for (int rr = 0; rr < 2; ++rr) {
           const int i = mt * 16 + g + rr * 8;
           const bool valid = i < n;
-          const float v0 = acc[mt][rr * 2 + 0] + ev[mt][rr][0], v1 = acc[mt][rr * 2 + 1] + ev[mt][rr][1];
+          float e0 = 0.f, e1 = 0.f;
+          if (valid) {
+            const float *ep = es() + (size_t)i * 4 * L.UPC + (unit - u0);
+            e0 = ep[(size_t)gate0 * L.UPC];
+            e1 = ep[(size_t)(gate0 + 1) * L.UPC];
+          }
+          const float v0 = acc[mt][rr * 2 + 0] + e0, v1 = acc[mt][rr * 2 + 1] + e1;
           const float o0 = __shfl_xor_sync(0xffffffffu, v0, 1);
           const float o1 = __shfl_xor_sync(0xffffffffu, v1, 1);
           if (valid && (q & 1) == 0) {
@@ -816,6 +840,7 @@ struct Ctx {
         }
       }
     }
+    if (!e_ready) mbar_wait(bar(BAR_E), hph & 1u);  // keep every thread's view of the phase in step
     LL_SUB(2);
     // (2) exchange the h' slices (this CTA's units) with every CTA
     sync();
@@ -837,7 +862,8 @@ struct Ctx {
       float acc[2][4];
 #pragma unroll
       for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-      ring_mma(acc, base + NG + j, MT, br0, br1, br2, br3, pp);
+      if (hi) ring_mma<true>(acc, base + NG + j, MT, br0, br1, br2, br3, pp);
+      else ring_mma<false>(acc, base + NG + j, MT, br0, br1, br2, br3, pp);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         if (mt >= MT) break;
@@ -1019,6 +1045,31 @@ struct Ctx {
     }
   }
 };
+
+// ---------------------------------------------------------------------------
+// Pack the bf16 LSTM weights into the per-CTA tile stream read by the producer
+// warp: for cluster rank r, tiles n < NG are W_hh rows {gate*P + r*UPC + 2n + c/4 :
+// gate = c%4} (c < 8), tiles NG + k are W_pred rows r*DPC + 8k + c.  Rows are
+// stored unpadded; in odd rows the 16-byte chunk j is stored at j ^ 4 (the
+// bank swizzle undone by ring_mma).  One thread per 16-byte chunk.
+// ---------------------------------------------------------------------------
+__global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst, int P, int C, int UPC, int DPC) {
+  const int NG = UPC / 2, NPT = DPC / 8, NT = NG + NPT;
+  const int chunks = P / 8;
+  const long long total = (long long)C * NT * 8 * chunks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % chunks);
+    const long long rowid = i / chunks;
+    const int c = (int)(rowid % 8);
+    const int n = (int)((rowid / 8) % NT);
+    const int r = (int)(rowid / (8 * NT));
+    const bf16 *src;
+    if (n < NG) src = w_hh + ((size_t)(c & 3) * P + r * UPC + 2 * n + (c >> 2)) * P;
+    else src = w_pred + (size_t)(r * DPC + 8 * (n - NG) + c) * P;
+    const int jd = (c & 1) && (P % 64) == 0 ? (j ^ 4) : j;
+    reinterpret_cast<uint4 *>(wst + (size_t)rowid * P)[jd] = reinterpret_cast<const uint4 *>(src)[j];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // The decode kernel.  PRED: 0 = LSTM, 1 = stateless.

@@ -25,7 +25,7 @@ constexpr size_t HDR_BYTES = 4096;  // [0] status, [1] group counter, [16..] sta
 constexpr size_t SMEM_LIMIT = 232448;
 
 struct Ws {
-  size_t f, tab, h, g, total;
+  size_t f, tab, h, g, wst, total;
 };
 
 size_t esize(ll_dtype d) { return d == LL_BF16 ? 2 : 4; }
@@ -45,6 +45,8 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + 2 * (size_t)B * P * esize(dt), 256);
   w.g = o;
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
+  w.wst = o;  // packed LSTM weight stream (bf16): (4P + H) rows of P
+  if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + (4 * P + H) * P * 2, 256);
   w.total = o;
   return w;
 }
@@ -294,6 +296,7 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   const Layout &L = cf.L;
 
   cudaStream_t st = (cudaStream_t)stream;
+  const bool ring = bf && lstm;
   uint8_t *ws = (uint8_t *)workspace;
   const Ws w = ws_layout(B, T_max, pr, jn, dt);
   if (cudaMemsetAsync(ws, 0, HDR_BYTES, st) != cudaSuccess) return LL_ERR_CUDA;
@@ -316,6 +319,12 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
     }
   }
   if (s != LL_OK) return s;
+  if (ring) {
+    // (2b) contiguous per-CTA tile stream of W_hh / W_pred for the producer warp
+    pack_lstm_stream<<<296, 256, 0, st>>>((const bf16 *)pr->w_hh, (const bf16 *)jn->w_pred,
+                                          (bf16 *)(ws + w.wst), P, C, L.UPC, L.DPC);
+    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
+  }
   // (3) decode
   DecodeParams p;
   memset(&p, 0, sizeof(p));
@@ -335,6 +344,7 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
   p.w_pred = jn->w_pred; p.b_pred = jn->b_pred; p.w_hh = lstm ? pr->w_hh : nullptr;
   p.tab = tab;
+  p.wst = ring ? (const bf16 *)(ws + w.wst) : nullptr;
   p.h = lstm ? (void *)(ws + w.h) : nullptr;
   p.gglob = lstm ? (float *)(ws + w.g) : nullptr;
   p.out_tokens = out_tokens; p.out_timestamps = out_timestamps;

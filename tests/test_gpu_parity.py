@@ -77,10 +77,10 @@ def test_cat_dog_through_abi(dtype, window, monkeypatch):
     assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
     assert [h[1] for h in hyps] == [[0, 2, 2], [1, 3, 3]]
     st = dec.stats()
-    assert st["predictor_steps"] == 4      # label-looping: BOS + longest hypothesis
     assert st["joint_evals"] == 7 + 7      # one decision per alignment symbol
-    if window == 1:
-        assert st["window"] == 1
+    if window == 1:                        # one group of both rows, one frame per round
+        assert st["window"] == 1 and st["groups"] == 1
+        assert st["predictor_steps"] == 4  # label-looping: BOS + longest hypothesis
         assert st["joint_rounds"] == 8     # tests/golden/cat_dog.txt
 
 

@@ -258,7 +258,55 @@ int main2() {
   }
   return 0;
 }
+
+
+// many outstanding bulk copies: n copies of `bytes` from rows `stride` apart, one mbarrier
+__global__ void bulk_multi(const uint8_t *src, long long *cyc, int reps, int ncopies, int bytes, int stride) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[1];
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t ph = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, ncopies * bytes);
+    __syncwarp();
+    for (int i = threadIdx.x; i < ncopies; i += 32)
+      bulk_g2s(sm + (size_t)i * bytes, src + (size_t)((r * 7 + i) % 512) * stride, bytes, bar);
+    mbar_wait(bar, ph);
+    ph ^= 1;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+int main3() {
+  long long *cyc, h[8];
+  cudaMalloc(&cyc, 4096);
+  uint8_t *src;
+  cudaMalloc(&src, 256 << 20);
+  cudaMemset(src, 1, 256 << 20);
+  cudaFuncSetAttribute(bulk_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  struct { int n, bytes, stride; } cs[] = {{1, 1280, 1280 * 640}, {8, 1280, 1280 * 640}, {40, 1280, 1280 * 640},
+                                           {80, 1280, 1280 * 640}, {1, 10240, 10240}, {8, 10240, 10240},
+                                           {1, 40960, 40960}, {4, 40960, 40960}};
+  for (auto c : cs) {
+    bulk_multi<<<1, 32, 200 << 10>>>(src, cyc, 50, c.n, c.bytes, c.stride);  // warm L2
+    bulk_multi<<<1, 32, 200 << 10>>>(src, cyc, 200, c.n, c.bytes, c.stride);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+    const double per = (double)h[0] / 200;
+    printf("bulk %3d x %6d B (stride %7d): %7.0f cycles per batch, %6.1f B/cycle (%s)\n", c.n, c.bytes, c.stride, per,
+           c.n * c.bytes / per, cudaGetErrorString(e));
+  }
+  return 0;
+}
+
 int main(int argc, char **argv) {
+  if (argc > 1 && argv[1][0] == '3') return main3();
   if (argc > 1) return main2();
   return main1();
 }
