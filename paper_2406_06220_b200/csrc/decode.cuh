@@ -114,8 +114,10 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   if (nw < 8) nw = 8;
   if (nw > MAX_NW) nw = MAX_NW;
   L.NW = nw;
-  L.ring = (bf && lstm) ? 1 : 0;
-  L.NS = L.ring ? NS : 0;
+  L.ring = (bf && lstm) ? 1 : 0;   // bf16 LSTM: W_hh in TMEM, W_pred tiles resident in smem
+  L.NS = L.ring ? L.DPC / 8 : 0;   // W_pred tiles of this CTA
+  (void)NS;
+  if (L.ring) L.NW = MAX_NW;       // one extra warp for the predictor phases
   L.JR = R * W;
   L.JRp = (L.JR + 15) / 16 * 16;
   if (L.JRp < R) L.JRp = (R + 15) / 16 * 16;
@@ -167,6 +169,7 @@ struct Ctx {
   uint8_t *sm;
   RowState &rs;
   uint64_t *bars;
+  uint32_t tmem;              // TMEM base address (bf16 LSTM: W_hh tiles)
   int C, rank, tid, warp, lane, NW, NCT, g, q;
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
   int u0, d0;                 // LSTM units / W_pred output dims owned
@@ -649,84 +652,135 @@ struct Ctx {
   __device__ int ng() const { return L.UPC / 2; }
   __device__ int npt() const { return L.DPC / 8; }
 
-  __device__ void producer_loop() {
-    const int NS = L.NS, NG = ng(), NT = NG + npt();
-    const uint32_t rowb = (uint32_t)(p.P * 2);
-    unsigned long long n = 0;
-    for (;;) {
-      const int slot = (int)(n % NS);
-      const uint32_t ph = (uint32_t)(((n / NS) & 1) ^ 1);
-      // wait for the slot to be free (or for the consumers to finish)
-      bool freed = false;
-      for (;;) {
-        int ok = 0;
-        if (lane == 0) ok = mbar_try_wait(smem_u32(bar(BAR_EMPTY + slot)), ph) ? 1 : 0;
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (ok) { freed = true; break; }
-        if (rs.done) break;
+  // TMEM geometry of the W_hh tiles: gate tile n lives in lane quarter n % 4,
+  // columns [tcol(n), tcol(n) + tcols): thread (g, q) of a warp in that quarter
+  // holds, for every 32-wide K block kb, the 16-byte B fragment of row g,
+  // chunk 4kb + q in columns 4kb..4kb+3 (plus 2 columns for a 16-wide tail).
+  __device__ int tcols() const { return 4 * (p.P / 32) + ((p.P & 31) ? 2 : 0); }
+  __device__ uint32_t tile_taddr(int n) const {
+    return tmem + ((uint32_t)(32 * (n & 3)) << 16) + (uint32_t)((n >> 2) * tcols());
+  }
+  // warps of lane quarter qd = warp & 3 take that quarter's tiles round-robin
+  __device__ int quarter_warps() const { return (NW - (warp & 3) + 3) / 4; }
+
+  // Kernel start: W_hh tiles of this CTA from the packed stream into TMEM,
+  // W_pred tiles into shared memory (one bulk copy).
+  __device__ void load_lstm_weights() {
+    const int NG = ng(), NPT = npt(), KB = p.P / 32;
+    const int qd = warp & 3, m = warp >> 2, nq = quarter_warps();
+    const int sw = ((g & 1) && (p.P % 64) == 0) ? 4 : 0;
+    for (int k = m; qd + 4 * k < NG; k += nq) {
+      const int n = qd + 4 * k;
+      const uint8_t *row = reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n) * 8 + g) * p.P);
+      for (int c4 = 0; c4 < KB; c4 += 4) {
+        uint32_t r[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kb = c4 + u;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (kb < KB) v = ldg128_nc(row + (((kb * 4 + q) ^ sw) * 16));
+          r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
+        }
+        if (c4 + 4 <= KB) {
+          tmem_st16(tile_taddr(n) + 4 * c4, r);
+        } else {
+          // partial chunk: store the valid blocks one x4 group at a time
+          for (int u = 0; c4 + u < KB; ++u) {
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(
+                             tile_taddr(n) + 4 * (c4 + u)),
+                         "r"(r[4 * u]), "r"(r[4 * u + 1]), "r"(r[4 * u + 2]), "r"(r[4 * u + 3])
+                         : "memory");
+          }
+        }
       }
-      if (!freed) break;
-      const int nl = (int)(n % NT);
-      // publish which tile the slot's next phase carries: a consumer that wants
-      // tile n waits for the tag first, so an mbarrier parity two phases back
-      // can never be mistaken for tile n (warps take tiles round-robin and may
-      // run more than one ring cycle ahead of the slot).
-      if (lane == 0) {
-        rs.tag[slot] = (unsigned)n;
-        mbar_arrive_expect_tx(bar(BAR_FULL + slot), 8 * rowb);
-        // the packed stream holds this CTA's tiles back to back: one 8*P*2-byte copy
-        const bf16 *src = p.wst + ((size_t)rank * NT + nl) * 8 * p.P;
-        bulk_g2s(ringslot(slot), src, 8 * rowb, bar(BAR_FULL + slot));
+      if (p.P & 31) {
+        const uint2 v = ldg64_nc(row + KB * 64 + q * 8);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(tile_taddr(n) + 4 * KB), "r"(v.x),
+                     "r"(v.y)
+                     : "memory");
       }
-      __syncwarp();
-      ++n;
     }
-    // drain: every issued tile has landed before the CTA may exit
-    const unsigned long long first = n > (unsigned long long)NS ? n - NS : 0;
-    for (unsigned long long k = first; k < n; ++k)
-      if (lane == 0) mbar_wait(bar(BAR_FULL + (int)(k % NS)), (uint32_t)((k / NS) & 1));
-    __syncwarp();
+    tmem_wait_st();
+    if (warp == 0) {
+      const uint32_t bytes = (uint32_t)(NPT * 8 * p.P * 2);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar(BAR_FULL), bytes);
+        bulk_g2s(ringslot(0), p.wst + ((size_t)rank * (NG + NPT) + NG) * 8 * p.P, bytes, bar(BAR_FULL));
+      }
+      mbar_wait(bar(BAR_FULL), 0);
+    }
   }
 
-  // consumer: MMA of ring tile n (global index) against A rows = hs rows of the
-  // predictor list (row pointers per lane), then release the slot.  HI: rows
-  // 8..15 of the m16 tile are used (more than 8 predictor rows); otherwise they
-  // are padding and are fed as zeros without touching shared memory.
+  // gates tile n: acc += A(h rows) . W_hh tile^T, B fragments streamed from TMEM
   template <bool HI>
-  __device__ __forceinline__ void ring_mma_kb(float (&acc)[2][4], const uint8_t *brow, int sw, int kb, int MT,
-                                              const uint8_t *ar0, const uint8_t *ar1, const uint8_t *ar2,
-                                              const uint8_t *ar3) const {
-    const uint4 b = lds128(brow + (((kb * 4 + q) ^ sw) * 16));
-    const uint4 x0 = lds128(ar0 + kb * 64);
-    const uint4 x1 = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
-    mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-    mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
-    if (MT > 1) {
-      const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-      mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
-      mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
+  __device__ __forceinline__ void tmem_mma(float (&acc)[2][4], int n, int MT, const uint8_t *ar0, const uint8_t *ar1,
+                                           const uint8_t *ar2, const uint8_t *ar3) const {
+    const int KB = p.P / 32;
+    const uint32_t ta = tile_taddr(n);
+    for (int c4 = 0; c4 < KB; c4 += 4) {
+      uint32_t r[16];
+      if (c4 + 4 <= KB) {
+        tmem_ld16(ta + 4 * c4, r);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c4 + u < KB) {
+            uint4 v;
+            tmem_ld4(ta + 4 * (c4 + u), v);
+            r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
+          }
+        }
+      }
+      tmem_wait_ld();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kb = c4 + u;
+        if (kb < KB) {
+          const uint4 x0 = lds128(ar0 + kb * 64);
+          const uint4 x1 = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
+          mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, r[4 * u], r[4 * u + 1]);
+          mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, r[4 * u + 2], r[4 * u + 3]);
+          if (MT > 1) {
+            const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
+            mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, r[4 * u], r[4 * u + 1]);
+            mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, r[4 * u + 2], r[4 * u + 3]);
+          }
+        }
+      }
+    }
+    if (p.P & 31) {
+      uint32_t t0, t1;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t0), "=r"(t1) : "r"(ta + 4 * KB));
+      tmem_wait_ld();
+      const int o = KB * 64 - q * 8;
+      const uint2 x0 = lds64(ar0 + o), x1 = lds64(ar1 + o);
+      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, t0, t1);
+      if (MT > 1) {
+        const uint2 x2 = lds64(ar2 + o), x3 = lds64(ar3 + o);
+        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, t0, t1);
+      }
     }
   }
+
+  // W_pred tile j (resident in shared memory, packed + swizzled like the stream)
   template <bool HI>
-  __device__ __forceinline__ void ring_mma(float (&acc)[2][4], unsigned long long n, int MT, const uint8_t *ar0,
-                                           const uint8_t *ar1, const uint8_t *ar2, const uint8_t *ar3,
-                                           unsigned long long *pp = nullptr) {
-    const int NS = L.NS, slot = (int)(n % NS);
-    const long long tw = pp ? clock64() : 0;
-    while (rs.tag[slot] != (unsigned)n) __nanosleep(64);
-    mbar_wait(bar(BAR_FULL + slot), (uint32_t)((n / NS) & 1));
-    if (pp) pp[8] += (unsigned long long)(clock64() - tw);
-    // packed rows are unpadded (P*2 bytes); odd rows store 16-byte chunk c at
-    // c ^ 4 so the two rows of each 8-lane LDS.128 phase hit disjoint banks
-    const uint8_t *brow = ringslot(slot) + (size_t)g * p.P * 2;
+  __device__ __forceinline__ void smem_tile_mma(float (&acc)[2][4], int j, int MT, const uint8_t *ar0,
+                                                const uint8_t *ar1, const uint8_t *ar2, const uint8_t *ar3) const {
+    const uint8_t *brow = ringslot(j) + (size_t)g * p.P * 2;
     const int sw = ((g & 1) && (p.P % 64) == 0) ? 4 : 0;
     const int KB = p.P / 32;
-    if (KB == KREG) {
-#pragma unroll
-      for (int kb = 0; kb < KREG; ++kb) ring_mma_kb<HI>(acc, brow, sw, kb, MT, ar0, ar1, ar2, ar3);
-    } else {
 #pragma unroll 4
-      for (int kb = 0; kb < KB; ++kb) ring_mma_kb<HI>(acc, brow, sw, kb, MT, ar0, ar1, ar2, ar3);
+    for (int kb = 0; kb < KB; ++kb) {
+      const uint4 b = lds128(brow + (((kb * 4 + q) ^ sw) * 16));
+      const uint4 x0 = lds128(ar0 + kb * 64);
+      const uint4 x1 = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
+      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
+      mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
+      if (MT > 1) {
+        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
+        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+        mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
+      }
     }
     if (p.P & 31) {
       const int o = KB * 64 - q * 8;
@@ -738,8 +792,6 @@ struct Ctx {
         mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar(BAR_EMPTY + slot));
   }
 
   // broadcast `nbytes16` 16-byte chunks starting at local smem `src` (same
@@ -771,7 +823,7 @@ struct Ctx {
   }
     const int n = rs.npred, MT = (n + 15) / 16;
     const int P = p.P, H = p.H, NG = ng(), NPT = npt();
-    const unsigned long long base = ntile_c;
+
     // arm the h' / g exchange barriers for this step (tx from the other CTAs)
     if (tid == 0 && C > 1) {
       mbar_arrive_expect_tx(bar(BAR_H), (uint32_t)((C - 1) * n * L.UPC * 2));
@@ -799,15 +851,17 @@ struct Ctx {
     }
     const bool hi = n > 8;
     bool e_ready = false;
-    for (int j = warp; j < NG; j += NW) {
+    const int qd = warp & 3, nq = quarter_warps();
+    for (int k = warp >> 2; qd + 4 * k < NG; k += nq) {
+      const int j = qd + 4 * k;
       const int unit = u0 + 2 * j + (q >> 1);
       const int gate0 = (q & 1) * 2;  // q even: (i, f); q odd: (g, o)
       float acc[2][4];
 #pragma unroll
       for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
       LL_SUB(0);
-      if (hi) ring_mma<true>(acc, base + j, MT, ar0, ar1, ar2, ar3, pp);
-      else ring_mma<false>(acc, base + j, MT, ar0, ar1, ar2, ar3, pp);
+      if (hi) tmem_mma<true>(acc, j, MT, ar0, ar1, ar2, ar3);
+      else tmem_mma<false>(acc, j, MT, ar0, ar1, ar2, ar3);
       LL_SUB(1);
       if (!e_ready) {
         mbar_wait(bar(BAR_E), hph & 1u);
@@ -862,8 +916,8 @@ struct Ctx {
       float acc[2][4];
 #pragma unroll
       for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-      if (hi) ring_mma<true>(acc, base + NG + j, MT, br0, br1, br2, br3, pp);
-      else ring_mma<false>(acc, base + NG + j, MT, br0, br1, br2, br3, pp);
+      if (hi) smem_tile_mma<true>(acc, j, MT, br0, br1, br2, br3);
+      else smem_tile_mma<false>(acc, j, MT, br0, br1, br2, br3);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         if (mt >= MT) break;
@@ -875,7 +929,7 @@ struct Ctx {
         }
       }
     }
-    ntile_c = base + NG + NPT;
+
     LL_SUB(5);
     // (4) exchange the g slices
     sync();
@@ -1087,16 +1141,23 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
                      st_labels = 0, st_groups = 0;
   long long algevals = 0;
 
+  __shared__ uint32_t s_tmem;
   cx.init_barriers();
-  if (tid == 0) rs.done = 0;
-  if (tid < NSMAX) rs.tag[tid] = 0xFFFFFFFFu;
-  if (warp < cx.NW) cx.load_weight_slice();
+  cx.load_weight_slice();
+  if constexpr (RING) {
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cx.tmem = s_tmem;
+    cx.load_lstm_weights();
+    tc_fence_before();
+  }
   __syncthreads();
   if (C > 1) cluster_sync_all();  // barriers initialised cluster-wide before any st.async
+  if constexpr (RING) tc_fence_after();
 
-  if (RING && warp == cx.NW) {
-    cx.producer_loop();
-  } else {
+  {
     int cur = 0;                  // f buffer of the current round
     // optional phase profile (thread 0 of the first CTA): 0 wait_f, 1 build_z, 2 joint,
     // 3 exchange, 4 decide, 5 predictor, 6 append/outer, 7 total
@@ -1260,7 +1321,6 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
     if ((cx.fpend >> 0) & 1u) cx.wait_f(0);
     if ((cx.fpend >> 1) & 1u) cx.wait_f(1);
     cx.sync();
-    if (tid == 0) rs.done = 1;
     if (prof) {
       LL_PHASE(6);
       pt[7] = (unsigned long long)(clock64() - t_start);
@@ -1284,7 +1344,12 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
       }
     }
   }
+  if constexpr (RING) tc_fence_before();
   __syncthreads();
+  if constexpr (RING) {
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc(cx.tmem, 512);
+  }
   if (C > 1) cluster_sync_all();  // no CTA exits while peers may still st.async into it
 }
 

@@ -111,7 +111,6 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
   const int forceC = env_int("LL_CLUSTER", 0);
   const int forceR = env_int("LL_GROUP_ROWS", 0);
   const int forceW = env_int("LL_WINDOW", 0);
-  const int forceNS = env_int("LL_RING", 0);
   const bool ring = bf && lstm;
   if (bf && H > KREG * 32 + 16) return false;        // joint slice must fit the register tile
   const int ncl = nclusters > 0 ? nclusters : 8;
@@ -125,6 +124,10 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
     if (bf) {
       if (H % (8 * C)) continue;
       if (lstm && P % (8 * C)) continue;             // h' slice: whole 16-byte chunks
+      if (ring) {                                    // W_hh tiles of a CTA must fit TMEM (512 columns)
+        const int NG = P / C / 2, tcols = 4 * (P / 32) + ((P & 31) ? 2 : 0);
+        if ((NG + 3) / 4 * tcols > 512) continue;
+      }
     } else {
       if (H % C) continue;
       if (lstm && P % C) continue;
@@ -137,13 +140,9 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
       if (R * W > MAX_JR) continue;
       for (; W >= 1; W >>= 1) {
         cf.C = C; cf.R = R; cf.W = W; cf.WF = W + (maxd > 1 ? maxd - 1 : 0);
-        // as many ring slots as fit (2..NSMAX)
-        for (int NS = ring ? (forceNS ? forceNS : NSMAX) : 0; NS >= (ring ? 2 : 0); --NS) {
-          cf.NS = NS;
-          cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, NS);
-          if (cf.L.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) return true;
-          if (!ring) break;
-        }
+        cf.NS = 0;
+        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0);
+        if (cf.L.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) return true;
         if (forceW) break;
       }
     }
@@ -163,7 +162,7 @@ int max_clusters(int C, const Layout &L) {
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3((L.NW + L.ring) * 32);
+  cfg.blockDim = dim3(L.NW * 32);
   cfg.dynamicSmemBytes = L.total;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -190,7 +189,7 @@ ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_gro
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3((L.NW + L.ring) * 32);
+  cfg.blockDim = dim3(L.NW * 32);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = st;
   cfg.attrs = attr;

@@ -305,8 +305,64 @@ int main3() {
   return 0;
 }
 
+
+
+// TMEM -> register load bandwidth: every warp reads `cols` columns of its lane quarter
+__global__ void tmem_bw(long long *cyc, float *out, int iters, int cols) {
+  __shared__ uint32_t taddr_s;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc(&taddr_s, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t base = taddr_s + ((uint32_t)(32 * (warp & 3)) << 16);
+  uint32_t r[16];
+  for (int i = 0; i < 16; ++i) r[i] = threadIdx.x * 16 + i;
+  if (warp < 4)
+    for (int c = 0; c < 512; c += 16) tmem_st16(base + c, r);
+  tmem_wait_st();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t acc = 0;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    for (int c = 0; c < cols; c += 16) {
+      tmem_ld16(base + ((c + it * 16) & 511), r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc += r[i];
+    }
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = (float)acc;
+  if ((threadIdx.x & 31) == 0) cyc[warp] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(taddr_s, 512);
+}
+
+int main4() {
+  long long *cyc, h[32];
+  float *out;
+  cudaMalloc(&cyc, 4096);
+  cudaMalloc(&out, 1 << 20);
+  for (int warps : {1, 4, 8, 10}) {
+    tmem_bw<<<1, 32 * warps>>>(cyc, out, 100, 80);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(h, cyc, 8 * warps, cudaMemcpyDeviceToHost);
+    long long mx = 0;
+    for (int w = 0; w < warps; ++w) mx = h[w] > mx ? h[w] : mx;
+    const double bytes = 100.0 * 80 * 32 * 4 * warps;
+    printf("tcgen05.ld 32x32b.x16 (wait each), %2d warps x 80 cols: %.0f cycles/iter, %.0f B/cycle/SM (%s)\n", warps,
+           (double)mx / 100, bytes / mx, cudaGetErrorString(e));
+  }
+  return 0;
+}
+
 int main(int argc, char **argv) {
   if (argc > 1 && argv[1][0] == '3') return main3();
+  if (argc > 1 && argv[1][0] == '4') return main4();
   if (argc > 1) return main2();
   return main1();
 }
