@@ -559,22 +559,34 @@ struct Ctx {
   // k, then lane s walks slot s's window in frame order (Alg. 3 lines 9-11
   // and 15-19 for each frame; TDT: blank advances by max(d, 1)).
   // Also rebuilds the scanning list and checks the speculative window X.
+  __device__ void resolve_rows() {
+    // lane r < C reads CTA r's partial; butterfly max over the lanes
+    const uint64_t *pt = part(par);
+    for (int k = warp; k < rs.nz; k += NW) {
+      const int jr = rs.zdst[k];
+      uint64_t tkey = 0, dkey = 0;
+      if (lane < C) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)lane * L.JR + jr) * 2);
+        tkey = ((uint64_t)v.y << 32) | v.x;
+        dkey = ((uint64_t)v.w << 32) | v.z;
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        if (o < C) {
+          tkey = umax64(tkey, shfl_xor_u64(tkey, o));
+          if (p.nD > 0) dkey = umax64(dkey, shfl_xor_u64(dkey, o));
+        }
+      }
+      if (lane == 0) rs.dec[jr] = key_index(tkey) | ((p.nD > 0 ? key_index(dkey) : 0) << 24);
+    }
+  }
+
   __device__ void decide(long long &algevals, int Xnext) {
     if (warp != 0) return;
     const int W = p.W;
-    int e = 0x7FFFFFFF;
-    int my_jr = -1;
-    if (lane < rs.nz) {
-      int y, di;
-      my_jr = rs.zdst[lane];
-      final_keys(my_jr, y, di);
-      e = y | (di << 24);
-    }
     int used = 0;
     bool sc = false;
-    // publish the decisions by joint row, then walk each slot's window
-    if (lane < rs.nz) rs.dec[my_jr] = e;
-    __syncwarp();
+    // walk each slot's window (decisions resolved by resolve_rows)
     if (lane < p.R && rs.scanning[lane]) {
       const int s = lane;
       const int t0 = rs.t[s], Ls = rs.L[s];
@@ -657,20 +669,22 @@ struct Ctx {
   // holds, for every 32-wide K block kb, the 16-byte B fragment of row g,
   // chunk 4kb + q in columns 4kb..4kb+3 (plus 2 columns for a 16-wide tail).
   __device__ int tcols() const { return 4 * (p.P / 32) + ((p.P & 31) ? 2 : 0); }
+  // gate tile n belongs to warp w = n % NW (its k-th tile, k = n / NW); the
+  // warp can only reach TMEM lane quarter w % 4, so the quarter's columns are
+  // shared by its nq warps: slot k * nq + w / 4.
+  __device__ int quarter_warps(int qd) const { return (NW - qd + 3) / 4; }
   __device__ uint32_t tile_taddr(int n) const {
-    return tmem + ((uint32_t)(32 * (n & 3)) << 16) + (uint32_t)((n >> 2) * tcols());
+    const int w = n % NW, k = n / NW, qd = w & 3;
+    const int slot = k * quarter_warps(qd) + (w >> 2);
+    return tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(slot * tcols());
   }
-  // warps of lane quarter qd = warp & 3 take that quarter's tiles round-robin
-  __device__ int quarter_warps() const { return (NW - (warp & 3) + 3) / 4; }
 
   // Kernel start: W_hh tiles of this CTA from the packed stream into TMEM,
   // W_pred tiles into shared memory (one bulk copy).
   __device__ void load_lstm_weights() {
     const int NG = ng(), NPT = npt(), KB = p.P / 32;
-    const int qd = warp & 3, m = warp >> 2, nq = quarter_warps();
     const int sw = ((g & 1) && (p.P % 64) == 0) ? 4 : 0;
-    for (int k = m; qd + 4 * k < NG; k += nq) {
-      const int n = qd + 4 * k;
+    for (int n = warp; n < NG; n += NW) {
       const uint8_t *row = reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n) * 8 + g) * p.P);
       for (int c4 = 0; c4 < KB; c4 += 4) {
         uint32_t r[16];
@@ -712,11 +726,14 @@ struct Ctx {
   }
 
   // gates tile n: acc += A(h rows) . W_hh tile^T, B fragments streamed from TMEM
+  // (next 16 columns loaded while the current ones are consumed; two
+  // accumulator chains over K, summed in a fixed order).
   template <bool HI>
   __device__ __forceinline__ void tmem_mma(float (&acc)[2][4], int n, int MT, const uint8_t *ar0, const uint8_t *ar1,
                                            const uint8_t *ar2, const uint8_t *ar3) const {
     const int KB = p.P / 32;
     const uint32_t ta = tile_taddr(n);
+    float acc2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     for (int c4 = 0; c4 < KB; c4 += 4) {
       uint32_t r[16];
       if (c4 + 4 <= KB) {
@@ -736,14 +753,15 @@ struct Ctx {
       for (int u = 0; u < 4; ++u) {
         const int kb = c4 + u;
         if (kb < KB) {
-          const uint4 x0 = lds128(ar0 + kb * 64);
-          const uint4 x1 = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
-          mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, r[4 * u], r[4 * u + 1]);
-          mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, r[4 * u + 2], r[4 * u + 3]);
+          float(&A)[2][4] = (u & 1) ? acc2 : acc;
+          const uint4 xa = lds128(ar0 + kb * 64);
+          const uint4 xb = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
+          mma_bf16_16816(A[0], xa.x, xb.x, xa.y, xb.y, r[4 * u], r[4 * u + 1]);
+          mma_bf16_16816(A[0], xa.z, xb.z, xa.w, xb.w, r[4 * u + 2], r[4 * u + 3]);
           if (MT > 1) {
             const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-            mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, r[4 * u], r[4 * u + 1]);
-            mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, r[4 * u + 2], r[4 * u + 3]);
+            mma_bf16_16816(A[1], x2.x, x3.x, x2.y, x3.y, r[4 * u], r[4 * u + 1]);
+            mma_bf16_16816(A[1], x2.z, x3.z, x2.w, x3.w, r[4 * u + 2], r[4 * u + 3]);
           }
         }
       }
@@ -760,6 +778,10 @@ struct Ctx {
         mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, t0, t1);
       }
     }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][e] += acc2[a][e];
   }
 
   // W_pred tile j (resident in shared memory, packed + swizzled like the stream)
@@ -851,9 +873,7 @@ struct Ctx {
     }
     const bool hi = n > 8;
     bool e_ready = false;
-    const int qd = warp & 3, nq = quarter_warps();
-    for (int k = warp >> 2; qd + 4 * k < NG; k += nq) {
-      const int j = qd + 4 * k;
+    for (int j = warp; j < NG; j += NW) {
       const int unit = u0 + 2 * j + (q >> 1);
       const int gate0 = (q & 1) * 2;  // q even: (i, f); q odd: (g, o)
       float acc[2][4];
@@ -1253,6 +1273,8 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
           LL_PHASE(3);
           st_rounds++;
           st_rowevals += rs.nz;
+          cx.resolve_rows();
+          cx.sync();
           cx.decide(algevals, p.spec_prefetch ? (cur ^ 1) : -1);
           cx.par ^= 1;
           cx.sync();
