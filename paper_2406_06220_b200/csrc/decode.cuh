@@ -835,7 +835,7 @@ struct Ctx {
     }
   }
 
-  __device__ void predictor_lstm_ring(unsigned long long *pp = nullptr) {
+  __device__ void predictor_lstm_tmem(unsigned long long *pp = nullptr) {
     long long tm = pp ? clock64() : 0;
 #define LL_SUB(k)                                          \
   if (pp) {                                                \
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
           st_pred++;
           st_predrows += rs.npred;
           if constexpr (PRED == 1) cx.predictor_stateless();
-          else if constexpr (RING) cx.predictor_lstm_ring(prof ? pp : nullptr);
+          else if constexpr (RING) cx.predictor_lstm_tmem(prof ? pp : nullptr);
           else cx.predictor_lstm_f32();
         }
         LL_PHASE(5);
