@@ -87,6 +87,8 @@ struct DecodeParams {
   int *group_counter;
   unsigned long long *stats;     // see ll.h ll_stats
   unsigned long long *prof;      // optional per-phase clock64 totals (LL_PROFILE)
+  int prof_mode;                 // 1: phase profile of the decode
+  volatile unsigned *trace;      // debug: host-mapped progress markers [gridDim.x][8] (LL debug hook)
   // ll_debug_joint mode
   const float *dbg_g;
   float *dbg_logits;
@@ -146,7 +148,7 @@ struct RowState {
   int fy[MAX_R], ft[MAX_R], fd[MAX_R];
   int fbase[2][MAX_R], fcnt[2][MAX_R];   // frames held in fbuf[X] for each slot
   int slist[MAX_R], plist[MAX_R];
-  int zsrc[MAX_JR], zdst[MAX_JR];        // live joint rows: f row offset (elements) / z row
+  int zsrc[MAX_JR], zdst[MAX_JR];        // live joint rows k: f row offset (elements) / logical row s*W+j
   int dec[MAX_JR];                        // per joint row: token | dur_index << 24
   int nscan, npred, nactive, nz, ready;
   int grp[2];                            // group index broadcast (double-buffered)
@@ -174,6 +176,7 @@ struct Ctx {
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
   int u0, d0;                 // LSTM units / W_pred output dims owned
   int par;                    // partial-buffer parity
+  int iw;                     // issuing warp for bulk copies (a warp without a joint tile if any)
   uint32_t fph, fpend, xph;   // phase / pending bits (replicated in every consumer thread)
   uint32_t hph;               // BAR_H / BAR_G / BAR_E phase
   unsigned long long ntile_c; // weight-ring tiles consumed so far (replicated)
@@ -195,6 +198,7 @@ struct Ctx {
     u0 = rank * L.UPC;
     d0 = rank * L.DPC;
     par = 0;
+    iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
   }
   __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
@@ -262,7 +266,7 @@ struct Ctx {
     if ((fpend >> X) & 1u) wait_f(X);  // drain a stale speculative copy first
     const int n = rs.nscan;
     const uint32_t frb = (uint32_t)(p.H * sizeof(T));
-    if (warp == 0) {
+    if (warp == iw) {
       uint32_t bytes = 0;
       int s = 0, base = 0, cnt = 0;
       if (lane < n) {
@@ -319,7 +323,7 @@ struct Ctx {
     const int H = p.H, W = p.W;
     const int nz = rs.nz;
     for (int k = warp; k < nz; k += NW) {
-      const int jr = rs.zdst[k], s = jr / W;
+      const int jr = k, s = rs.zdst[k] / W;     // z row = compact index k
       if constexpr (BF) {
         const uint4 *frp = reinterpret_cast<const uint4 *>(fbuf(X)) + rs.zsrc[k] / 8;
         const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
@@ -518,7 +522,7 @@ struct Ctx {
     const uint64_t *wk = wkey();
     uint64_t *pt = part(par);
     if (tid < nz) {
-      const int jr = rs.zdst[tid];
+      const int jr = tid;                       // compact joint row
       uint64_t tkey = 0, dkey = 0;
 #pragma unroll
       for (int w = 0; w < MAX_NW; ++w) {
@@ -566,7 +570,7 @@ struct Ctx {
       const int jr = rs.zdst[k];
       uint64_t tkey = 0, dkey = 0;
       if (lane < C) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)lane * L.JR + jr) * 2);
+        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)lane * L.JR + k) * 2);
         tkey = ((uint64_t)v.y << 32) | v.x;
         dkey = ((uint64_t)v.w << 32) | v.z;
       }
@@ -632,6 +636,9 @@ struct Ctx {
       rs.ready = all_ok;
     }
     algevals += used;
+    __syncwarp();
+    // the next round's joint-row plan (only valid if the window is ready)
+    if (all_ok && Xnext >= 0) plan_z(Xnext);
   }
 
   // warp 0: rebuild the compacted scanning / predictor lists (ascending slot order)
@@ -1190,10 +1197,20 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
     const long long now = clock64();             \
     pt[k] += (unsigned long long)(now - t_mark); \
     t_mark = now;                                \
+  }                                              \
+  if (p.trace && tid == 0) {                     \
+    p.trace[blockIdx.x * 8 + 0] = (k);           \
+    p.trace[blockIdx.x * 8 + 1] = (unsigned)st_rounds; \
+    p.trace[blockIdx.x * 8 + 2] = (unsigned)st_outer;  \
+    p.trace[blockIdx.x * 8 + 3] = (unsigned)k_grp;     \
+    p.trace[blockIdx.x * 8 + 4] = (unsigned)rs.nz;     \
+    p.trace[blockIdx.x * 8 + 5] = (unsigned)rs.nscan;  \
+    p.trace[blockIdx.x * 8 + 6] = cx.fph | (cx.fpend << 4) | (cx.xph << 8) | (cx.hph << 12) | ((unsigned)cur << 16); \
   }
-    int k = 0;
+    int k = 0, k_grp = 0;
     for (;; ++k) {
       const int grp = cx.next_group(k);
+      k_grp = grp;
       if (grp >= p.n_groups) break;
       st_groups++;
       // ---- group init (warp 0: lane = row slot) -----------------------------
@@ -1245,6 +1262,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
         // first window of every active row, overlapping the predictor phase
         if ((cx.fpend >> cur) & 1u) cur ^= 1;
         cx.issue_f(cur, false);
+        cx.sync();                     // fbase/fcnt (written by the issuing warp) visible to warp 0
         LL_PHASE(6);
         // predictor (Alg. 3 line 6): only rows that found a label and stay active
         if (rs.npred > 0) {
@@ -1256,18 +1274,20 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
         }
         LL_PHASE(5);
         // ---- frame loop: rounds of W-frame windows until no row scans ---------
+        bool planned = false;          // first round: plan after the predictor phase
         while (rs.nscan > 0) {
-          const int MT = (cx.L.JR + 15) / 16;
           cx.wait_f(cur);
-          cx.plan_z(cur);
-          cx.sync();                   // f landed, plan visible, predictor's g written
+          if (!planned) {
+            cx.plan_z(cur);
+            cx.sync();                 // plan visible, predictor's g written
+          }
           LL_PHASE(0);
           cx.build_z(cur);
           cx.sync();
           // speculative: a row whose window is all blank needs the next window
           if (p.spec_prefetch) cx.issue_f(cur ^ 1, true);
           LL_PHASE(1);
-          cx.joint_keys(MT, 0, nullptr, 0);
+          cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
           LL_PHASE(2);
           cx.exchange_keys();
           LL_PHASE(3);
@@ -1278,10 +1298,16 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
           cx.decide(algevals, p.spec_prefetch ? (cur ^ 1) : -1);
           cx.par ^= 1;
           cx.sync();
+          planned = false;
           if (rs.nscan > 0) {
             cur ^= 1;
             // TDT may jump past the prefetched frames (or no speculation): reload
-            if (!rs.ready) cx.issue_f(cur, false);
+            if (!rs.ready) {
+              cx.issue_f(cur, false);
+              cx.sync();                 // fbase/fcnt visible to warp 0's plan_z
+            } else {
+              planned = true;            // decide() planned the next round from fbuf[cur]
+            }
           } else if (p.spec_prefetch) {
             cur ^= 1;                    // the other buffer holds a stale speculative copy
           }
@@ -1410,6 +1436,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) debug_joint_kernel(const
     }
     __syncthreads();
     cx.issue_f(0, false);   // the workspace holds f as [n][1][H] (T_max = 1)
+    __syncthreads();
     cx.wait_f(0);
     cx.plan_z(0);
     __syncthreads();

@@ -52,6 +52,7 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
 }
 
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+void *g_trace = nullptr;  // debug: host-mapped progress markers (env LL_TRACE_PTR)
 
 int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
@@ -353,6 +354,11 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   p.group_counter = (int *)ws + 1;
   p.stats = (unsigned long long *)(ws + 64);
   p.prof = env_int("LL_PROFILE", 0) ? (unsigned long long *)(ws + 256) : nullptr;
+  p.prof_mode = env_int("LL_PROFILE", 0);
+  {
+    const char *tp = getenv("LL_TRACE_PTR");
+    p.trace = (tp && *tp) ? (volatile unsigned *)strtoull(tp, nullptr, 0) : nullptr;
+  }
   int used = 0;
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
   if (bf)
