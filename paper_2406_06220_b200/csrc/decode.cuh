@@ -46,6 +46,7 @@ constexpr int MAX_R = 32;        // rows per group (<= 32: one lane per row)
 constexpr int MAX_JR = 32;       // joint rows per round R*W (<= 32: one lane per joint row)
 constexpr int MAX_DUR = 16;
 constexpr int MAX_CTX = 4;
+enum { SC_OUTER, SC_ROUNDS, SC_ALGEVALS, SC_PRED, SC_PREDROWS, SC_LABELS, SC_GROUPS, SC_ROWEVALS, SC_N };
 constexpr int MAX_NW = 10;       // consumer warps per CTA (+1 producer warp: <= 352 threads, <= 184 regs)
 constexpr int MAX_C = 16;        // cluster size
 constexpr int KREG = 20;         // 32-wide K blocks of the joint weight slice held in registers (H <= 656)
@@ -539,6 +540,8 @@ struct Ctx {
         st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, dkey, mapa_u32(bb, (uint32_t)dst));
       }
     }
+  }
+  __device__ void exchange_wait() {
     mbar_wait(bar(BAR_X + par), (xph >> par) & 1u);
     xph ^= 1u << par;
   }
@@ -585,7 +588,7 @@ struct Ctx {
     }
   }
 
-  __device__ void decide(long long &algevals, int Xnext) {
+  __device__ void decide(unsigned *algevals, int Xnext) {
     if (warp != 0) return;
     const int W = p.W;
     int used = 0;
@@ -635,7 +638,7 @@ struct Ctx {
       rs.nscan = __popc(ms);
       rs.ready = all_ok;
     }
-    algevals += used;
+    if (lane == 0) *algevals += (unsigned)used;
     __syncwarp();
     // the next round's joint-row plan (only valid if the window is ready)
     if (all_ok && Xnext >= 0) plan_z(Xnext);
@@ -1156,7 +1159,7 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // The decode kernel.  PRED: 0 = LSTM, 1 = stateless.
 // ---------------------------------------------------------------------------
 template <typename T, int PRED>
-__global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
@@ -1164,9 +1167,10 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
   constexpr bool RING = sizeof(T) == 2 && PRED == 0;
-  unsigned long long st_outer = 0, st_rounds = 0, st_rowevals = 0, st_pred = 0, st_predrows = 0,
-                     st_labels = 0, st_groups = 0;
-  long long algevals = 0;
+  // statistics: counted by thread 0 only, in shared memory (no registers held)
+  __shared__ unsigned s_cnt[SC_N];
+  if (tid < SC_N) s_cnt[tid] = 0;
+  const bool t0 = tid == 0;
 
   __shared__ uint32_t s_tmem;
   cx.init_barriers();
@@ -1188,9 +1192,12 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
     int cur = 0;                  // f buffer of the current round
     // optional phase profile (thread 0 of the first CTA): 0 wait_f, 1 build_z, 2 joint,
     // 3 exchange, 4 decide, 5 predictor, 6 append/outer, 7 total
-    unsigned long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    unsigned long long pp[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    __shared__ unsigned long long pt[16], pp[9];   // written by thread 0 of the profiled CTA only
     const bool prof = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
+    if (prof) {
+      for (int kk = 0; kk < 16; ++kk) pt[kk] = 0;
+      for (int kk = 0; kk < 9; ++kk) pp[kk] = 0;
+    }
     long long t_mark = clock64(), t_start = t_mark;
 #define LL_PHASE(k)                              \
   if (prof) {                                    \
@@ -1200,8 +1207,8 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
   }                                              \
   if (p.trace && tid == 0) {                     \
     p.trace[blockIdx.x * 8 + 0] = (k);           \
-    p.trace[blockIdx.x * 8 + 1] = (unsigned)st_rounds; \
-    p.trace[blockIdx.x * 8 + 2] = (unsigned)st_outer;  \
+    p.trace[blockIdx.x * 8 + 1] = s_cnt[SC_ROUNDS];    \
+    p.trace[blockIdx.x * 8 + 2] = s_cnt[SC_OUTER];     \
     p.trace[blockIdx.x * 8 + 3] = (unsigned)k_grp;     \
     p.trace[blockIdx.x * 8 + 4] = (unsigned)rs.nz;     \
     p.trace[blockIdx.x * 8 + 5] = (unsigned)rs.nscan;  \
@@ -1212,7 +1219,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
       const int grp = cx.next_group(k);
       k_grp = grp;
       if (grp >= p.n_groups) break;
-      st_groups++;
+      if (t0) s_cnt[SC_GROUPS]++;
       // ---- group init (warp 0: lane = row slot) -----------------------------
       if (warp == 0 && lane < R) {
         const int b = grp * R + lane;
@@ -1251,7 +1258,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
 
       // ---- outer loop over labels (Alg. 3 line 5) -----------------------------
       while (rs.nactive > 0) {
-        st_outer++;
+        if (t0) s_cnt[SC_OUTER]++;
         if (warp == 0 && lane < R) {
           rs.scanning[lane] = rs.active[lane];
           rs.found[lane] = 0;
@@ -1263,16 +1270,18 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
         if ((cx.fpend >> cur) & 1u) cur ^= 1;
         cx.issue_f(cur, false);
         cx.sync();                     // fbase/fcnt (written by the issuing warp) visible to warp 0
-        LL_PHASE(6);
+        LL_PHASE(11);
         // predictor (Alg. 3 line 6): only rows that found a label and stay active
         if (rs.npred > 0) {
-          st_pred++;
-          st_predrows += rs.npred;
+          if (t0) {
+            s_cnt[SC_PRED]++;
+            s_cnt[SC_PREDROWS] += rs.npred;
+          }
           if constexpr (PRED == 1) cx.predictor_stateless();
           else if constexpr (RING) cx.predictor_lstm_tmem(prof ? pp : nullptr);
           else cx.predictor_lstm_f32();
         }
-        LL_PHASE(5);
+        LL_PHASE(10);
         // ---- frame loop: rounds of W-frame windows until no row scans ---------
         bool planned = false;          // first round: plan after the predictor phase
         while (rs.nscan > 0) {
@@ -1283,19 +1292,27 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
           }
           LL_PHASE(0);
           cx.build_z(cur);
+          LL_PHASE(1);
           cx.sync();
           // speculative: a row whose window is all blank needs the next window
           if (p.spec_prefetch) cx.issue_f(cur ^ 1, true);
-          LL_PHASE(1);
-          cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
           LL_PHASE(2);
-          cx.exchange_keys();
+          cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
           LL_PHASE(3);
-          st_rounds++;
-          st_rowevals += rs.nz;
+          cx.exchange_keys();
+          LL_PHASE(4);
+          cx.exchange_wait();
+          LL_PHASE(5);
+          if (t0) {
+            s_cnt[SC_ROUNDS]++;
+            s_cnt[SC_ROWEVALS] += rs.nz;
+          }
           cx.resolve_rows();
+          LL_PHASE(6);
           cx.sync();
-          cx.decide(algevals, p.spec_prefetch ? (cur ^ 1) : -1);
+          LL_PHASE(7);
+          cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
+          LL_PHASE(8);
           cx.par ^= 1;
           cx.sync();
           planned = false;
@@ -1311,7 +1328,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
           } else if (p.spec_prefetch) {
             cur ^= 1;                    // the other buffer holds a stale speculative copy
           }
-          LL_PHASE(4);
+          LL_PHASE(9);
         }
         // ---- append + time rules + guard (BatchedHyps.add_results, :196-199) --
         if (warp == 0 && lane < R) {
@@ -1361,7 +1378,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
           tot = rs.len[lane];
         }
         for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        st_labels += tot;
+        if (t0) s_cnt[SC_LABELS] += tot;
       }
     }
     cx.final_acks(k);
@@ -1370,21 +1387,21 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
     if ((cx.fpend >> 1) & 1u) cx.wait_f(1);
     cx.sync();
     if (prof) {
-      LL_PHASE(6);
-      pt[7] = (unsigned long long)(clock64() - t_start);
-      for (int kk = 0; kk < 8; ++kk) p.prof[kk] = pt[kk];
-      for (int kk = 0; kk < 9; ++kk) p.prof[8 + kk] = pp[kk];
+      LL_PHASE(11);
+      pt[15] = (unsigned long long)(clock64() - t_start);
+      for (int kk = 0; kk < 16; ++kk) p.prof[kk] = pt[kk];
+      for (int kk = 0; kk < 9; ++kk) p.prof[16 + kk] = pp[kk];
     }
 #undef LL_PHASE
     if (rank == 0 && tid == 0 && p.stats) {
-      atomicAdd(p.stats + 0, st_outer);
-      atomicAdd(p.stats + 1, st_rounds);
-      atomicAdd(p.stats + 2, (unsigned long long)algevals);
-      atomicAdd(p.stats + 3, st_pred);
-      atomicAdd(p.stats + 4, st_predrows);
-      atomicAdd(p.stats + 5, st_labels);
-      atomicAdd(p.stats + 6, st_groups);
-      atomicAdd(p.stats + 8, st_rowevals);
+      atomicAdd(p.stats + 0, (unsigned long long)s_cnt[SC_OUTER]);
+      atomicAdd(p.stats + 1, (unsigned long long)s_cnt[SC_ROUNDS]);
+      atomicAdd(p.stats + 2, (unsigned long long)s_cnt[SC_ALGEVALS]);
+      atomicAdd(p.stats + 3, (unsigned long long)s_cnt[SC_PRED]);
+      atomicAdd(p.stats + 4, (unsigned long long)s_cnt[SC_PREDROWS]);
+      atomicAdd(p.stats + 5, (unsigned long long)s_cnt[SC_LABELS]);
+      atomicAdd(p.stats + 6, (unsigned long long)s_cnt[SC_GROUPS]);
+      atomicAdd(p.stats + 8, (unsigned long long)s_cnt[SC_ROWEVALS]);
       if (blockIdx.x == 0) {
         p.stats[7] = (unsigned long long)C;
         p.stats[9] = (unsigned long long)p.W;
@@ -1407,7 +1424,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) decode_kernel(const __gr
 // Runs with W = 1: every row is one slot with one frame.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) debug_joint_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
@@ -1444,6 +1461,7 @@ __global__ void __launch_bounds__((MAX_NW + 1) * 32, 1) debug_joint_kernel(const
     __syncthreads();
     cx.joint_keys(MT, M, p.dbg_logits, base);
     cx.exchange_keys();
+    cx.exchange_wait();
     if (cx.rank == 0 && warp == 0 && lane < M) {
       int y, di;
       cx.final_keys(lane, y, di);

@@ -15,16 +15,21 @@ for _ in range(3):
     dec.decode(e, l)
 st = dec.stats()
 off = dec.ws_ptr - dec.workspace.data_ptr()
-ws = dec.workspace[off + 256: off + 256 + 17 * 8].cpu().numpy().view(np.uint64)
-names = ["wait_f", "build_z", "joint", "exchange", "decide", "predictor", "outer/append", "TOTAL"]
-tot = float(ws[7])
+ws = dec.workspace[off + 256: off + 256 + 25 * 8].cpu().numpy().view(np.uint64)
+names = ["wait_f+plan", "build_z", "sync+spec issue", "joint", "exchange send", "exchange wait",
+         "resolve", "sync", "decide", "sync+reload", "predictor", "outer/append", "", "", "", "TOTAL"]
+tot = float(ws[15])
 print(cfg, st)
 rounds = st['joint_rounds'] / st['groups']
-for n, v in zip(names, ws[:8]):
-    print(f"{n:14s} {int(v):>12d} cycles  {100*v/tot:5.1f}%  per-round {v/max(1, rounds):8.0f}")
-print("per predictor step:", ws[5] / max(1, st['predictor_steps'] / st['groups']))
+outer = st['outer_steps'] / st['groups']
+print(f"per group: rounds {rounds:.1f}  outer steps {outer:.1f}  total cycles {int(tot)}")
+for i, n in enumerate(names):
+    if not n:
+        continue
+    v = ws[i]
+    per = outer if i in (10, 11) else rounds
+    print(f"{n:16s} {int(v):>10d} cycles  {100*v/tot:5.1f}%  per-{'step ' if i in (10, 11) else 'round'} {v/max(1, per):8.0f}")
 sub = ["E'/setup", "gate MMA+wait", "gate epilogue", "sync", "h' exchange", "pred tiles", "sync2", "g exchange"]
 npred = max(1, st['predictor_steps'] / st['groups'])
 for i, nm in enumerate(sub):
-    print(f"  pred.{nm:16s} {ws[8+i]/npred:9.0f} cycles/step")
-print(f"  pred.tile-wait     {ws[16]/npred:9.0f} cycles/step (inside MMA)")
+    print(f"  pred.{nm:16s} {ws[16+i]/npred:9.0f} cycles/step")
