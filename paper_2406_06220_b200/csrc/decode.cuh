@@ -50,7 +50,10 @@ enum { SC_OUTER, SC_ROUNDS, SC_ALGEVALS, SC_PRED, SC_PREDROWS, SC_LABELS, SC_GRO
 constexpr int MAX_NW = 10;       // consumer warps per CTA (+1 producer warp: <= 352 threads, <= 184 regs)
 constexpr int MAX_C = 16;        // cluster size
 constexpr int KREG = 20;         // 32-wide K blocks of the joint weight slice held in registers (H <= 656)
+constexpr int KREG_SMALL = 4;    // small-H instantiation (H <= 144): no register budget lost to padding
 constexpr int NSMAX = 8;         // weight-ring slots
+constexpr int TL_N = 128;        // timeline: rounds / predictor steps recorded
+constexpr int TL_PH = 16;        // timeline: phase slots per event
 
 // mbarrier indices
 enum {
@@ -87,8 +90,7 @@ struct DecodeParams {
   int *status;                   // bit0 bad length, bit1 capacity
   int *group_counter;
   unsigned long long *stats;     // see ll.h ll_stats
-  unsigned long long *prof;      // optional per-phase clock64 totals (LL_PROFILE)
-  int prof_mode;                 // 1: phase profile of the decode
+  unsigned long long *prof;      // optional per-warp timeline of block 0 (LL_TIMELINE_PTR)
   volatile unsigned *trace;      // debug: host-mapped progress markers [gridDim.x][8] (LL debug hook)
   // ll_debug_joint mode
   const float *dbg_g;
@@ -113,14 +115,10 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.tiles_max = (NT + C - 1) / C;
   L.UPC = lstm ? P / C : 0;
   L.DPC = H / C;
-  int nw = bf ? L.tiles_max : 8;
-  if (nw < 8) nw = 8;
-  if (nw > MAX_NW) nw = MAX_NW;
-  L.NW = nw;
+  L.NW = bf ? MAX_NW : 8;          // bf16: one vocab tile per warp (<= MAX_NW tiles per CTA)
   L.ring = (bf && lstm) ? 1 : 0;   // bf16 LSTM: W_hh in TMEM, W_pred tiles resident in smem
   L.NS = L.ring ? L.DPC / 8 : 0;   // W_pred tiles of this CTA
   (void)NS;
-  if (L.ring) L.NW = MAX_NW;       // one extra warp for the predictor phases
   L.JR = R * W;
   L.JRp = (L.JR + 15) / 16 * 16;
   if (L.JRp < R) L.JRp = (R + 15) / 16 * 16;
@@ -164,11 +162,14 @@ __device__ __forceinline__ void csync(int nthreads) {
 }
 
 // Per-CTA context of the cluster kernel.
-template <typename T>
+// HC / PC / CC: compile-time joint dim H, predictor dim P and cluster size
+// (0 = runtime).  The production shape (H = P = 640, 16-CTA clusters) is
+// instantiated with all three fixed so that loops unroll and addressing folds.
+template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0>
 struct Ctx {
   static constexpr bool BF = sizeof(T) == 2;
   const DecodeParams &p;
-  Layout L;
+  const Layout &L;            // in shared memory (uniform; keeps it out of registers)
   uint8_t *sm;
   RowState &rs;
   uint64_t *bars;
@@ -181,15 +182,37 @@ struct Ctx {
   uint32_t fph, fpend, xph;   // phase / pending bits (replicated in every consumer thread)
   uint32_t hph;               // BAR_H / BAR_G / BAR_E phase
   unsigned long long ntile_c; // weight-ring tiles consumed so far (replicated)
-  uint4 wreg[KREG];           // this warp's joint weight tile (bf16), K-permuted fragments
+  // optional timeline (LL_TIMELINE_PTR): clock64 of every warp at phase
+  // boundaries of the first TL_N rounds / predictor steps of block 0
+  unsigned long long *tl;
+  int tl_round, tl_step;
+  __device__ void tl_stamp(int area, int idx, int ph) const {
+    if (tl != nullptr && idx < TL_N && lane == 0) tl[(((size_t)area * TL_N + idx) * TL_PH + ph) * MAX_NW + warp] = clock64();
+  }
+  // after a (deferred-blocking) bar.sync: a dependent shared load first, so the
+  // stamp is taken after the barrier has released this warp
+  __device__ void tl_stamp_bar(int area, int idx, int ph) const {
+    if (tl != nullptr) {
+      const int v = *(volatile int *)&rs.nz;
+      if (v >= -1) tl_stamp(area, idx, ph);
+    }
+  }
+  __device__ void tl_round_(int ph) const { tl_stamp(0, tl_round, ph); }
+  __device__ void tl_round_bar(int ph) const { tl_stamp_bar(0, tl_round, ph); }
+  __device__ void tl_pred(int ph) const { tl_stamp(1, tl_step, ph); }
+  __device__ void tl_pred_bar(int ph) const { tl_stamp_bar(1, tl_step, ph); }
+  uint4 wreg[KR];             // this warp's joint weight tile (bf16), K-permuted fragments
   uint2 wtail;
-  __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm, uint64_t *bars_)
-      : p(p_), sm(sm_), rs(rs_), bars(bars_), fph(0), fpend(0), xph(0), hph(0), ntile_c(0) {
-    C = (int)cluster_size();
+  __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm, uint64_t *bars_, Layout &sL)
+      : p(p_), L(sL), sm(sm_), rs(rs_), bars(bars_), fph(0), fpend(0), xph(0), hph(0), ntile_c(0) {
+    tl = (p.prof != nullptr && blockIdx.x == 0) ? p.prof : nullptr;
+    tl_round = tl_step = 0;
+    C = CC ? CC : (int)cluster_size();
     rank = (int)cluster_rank();
-    L = make_layout(BF, lstm, p.H, p.P, p.V1, p.nD, p.R, p.W, p.WF, C, p.NS);
+    if (threadIdx.x == 0) sL = make_layout(BF, lstm, Hd(), Pd(), p.V1, p.nD, p.R, p.W, p.WF, C, p.NS);
+    __syncthreads();
     tid = threadIdx.x; warp = tid >> 5; lane = tid & 31;
-    NW = L.NW;               // consumer warps
+    NW = BF ? MAX_NW : L.NW;  // consumer warps
     NCT = NW * 32;           // consumer threads
     g = lane >> 2; q = lane & 3;
     const int NT = (p.V1 + p.nD + 7) / 8;
@@ -201,17 +224,19 @@ struct Ctx {
     par = 0;
     iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
   }
+  __device__ __forceinline__ int Hd() const { return HC ? HC : p.H; }
+  __device__ __forceinline__ int Pd() const { return PC ? PC : p.P; }
   __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
   __device__ uint8_t *zs() const { return sm + L.off_z; }
-  __device__ uint8_t *fbuf(int X) const { return sm + L.off_f + (size_t)X * p.R * p.WF * p.H * sizeof(T); }
+  __device__ uint8_t *fbuf(int X) const { return sm + L.off_f + (size_t)X * p.R * p.WF * Hd() * sizeof(T); }
   __device__ float *gs() const { return (float *)(sm + L.off_g); }
   __device__ float *cs() const { return (float *)(sm + L.off_c); }
   __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
   __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * L.hstride; }
   __device__ float *es() const { return (float *)(sm + L.off_es); }
-  __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * p.P * 2; }
+  __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * Pd() * 2; }
   __device__ void sync() const { csync(NCT); }
 
   __device__ void init_barriers() {
@@ -227,7 +252,7 @@ struct Ctx {
   // -------------------------------------------------------------------------
   __device__ void load_weight_slice() {
     const int nrows = L.tiles_max * 8;
-    const int V1 = p.V1, NV = p.V1 + p.nD, H = p.H;
+    const int V1 = p.V1, NV = p.V1 + p.nD, H = Hd();
     float *bs = bsl();
     for (int r = tid; r < nrows; r += NCT) {
       const int v = tile0 * 8 + r;
@@ -244,7 +269,7 @@ struct Ctx {
                                      : (const bf16 *)p.w_dur + (size_t)(v - V1) * H)
                            : nullptr;
 #pragma unroll
-      for (int kb = 0; kb < KREG; ++kb)
+      for (int kb = 0; kb < KR; ++kb)
         wreg[kb] = (ok && kb < KB) ? ldg128_nc(src + kb * 32 + q * 8) : make_uint4(0, 0, 0, 0);
       wtail = (ok && (H & 31)) ? ldg64_nc(src + KB * 32 + q * 4) : make_uint2(0, 0);
     }
@@ -266,7 +291,7 @@ struct Ctx {
   __device__ void issue_f(int X, bool spec) {
     if ((fpend >> X) & 1u) wait_f(X);  // drain a stale speculative copy first
     const int n = rs.nscan;
-    const uint32_t frb = (uint32_t)(p.H * sizeof(T));
+    const uint32_t frb = (uint32_t)(Hd() * sizeof(T));
     if (warp == iw) {
       uint32_t bytes = 0;
       int s = 0, base = 0, cnt = 0;
@@ -305,7 +330,7 @@ struct Ctx {
       const int s = rs.slist[lane / W], j = lane % W;
       const int fr = rs.t[s] + j - rs.fbase[X][s];
       live = rs.t[s] + j < rs.L[s] && fr >= 0 && fr < rs.fcnt[X][s];
-      src = (s * p.WF + fr) * p.H;
+      src = (s * p.WF + fr) * Hd();
       dst = s * W + j;
     }
     const unsigned m = __ballot_sync(0xffffffffu, live);
@@ -321,29 +346,50 @@ struct Ctx {
   // rows keep stale values: an MMA output row depends only on its own A row
   // and those rows are never read.  Warp per joint row, 8 columns per lane.
   __device__ void build_z(int X) {
-    const int H = p.H, W = p.W;
+    const int H = Hd(), W = p.W;
     const int nz = rs.nz;
-    for (int k = warp; k < nz; k += NW) {
-      const int jr = k, s = rs.zdst[k] / W;     // z row = compact index k
-      if constexpr (BF) {
+    if constexpr (BF) {
+      // one joint row per warp pass, up to 3 16-byte chunks per lane (H <= 768):
+      // all shared loads of the row are issued before any store (the compiler
+      // cannot prove that z does not alias f / g)
+      const int HC = H / 8;
+      for (int k = warp; k < nz; k += NW) {
+        const int s = rs.zdst[k] / W;
         const uint4 *frp = reinterpret_cast<const uint4 *>(fbuf(X)) + rs.zsrc[k] / 8;
         const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
-        uint4 *zr = reinterpret_cast<uint4 *>(zs() + (size_t)jr * L.zstride);
-#pragma unroll 3
-        for (int c = lane; c < H / 8; c += 32) {
-          const uint4 fv = frp[c];
-          const float4 g0 = gr[2 * c], g1 = gr[2 * c + 1];
-          uint4 o;
-          o.x = pack_bf16x2(fmaxf(bf16_lo(fv.x) + g0.x, 0.f), fmaxf(bf16_hi(fv.x) + g0.y, 0.f));
-          o.y = pack_bf16x2(fmaxf(bf16_lo(fv.y) + g0.z, 0.f), fmaxf(bf16_hi(fv.y) + g0.w, 0.f));
-          o.z = pack_bf16x2(fmaxf(bf16_lo(fv.z) + g1.x, 0.f), fmaxf(bf16_hi(fv.z) + g1.y, 0.f));
-          o.w = pack_bf16x2(fmaxf(bf16_lo(fv.w) + g1.z, 0.f), fmaxf(bf16_hi(fv.w) + g1.w, 0.f));
-          zr[c] = o;
+        uint4 *zr = reinterpret_cast<uint4 *>(zs() + (size_t)k * L.zstride);
+        uint4 fv[3];
+        float4 ga[3], gb[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int c = lane + 32 * u;
+          if (c < HC) {
+            fv[u] = frp[c];
+            ga[u] = gr[2 * c];
+            gb[u] = gr[2 * c + 1];
+          }
         }
-      } else {
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int c = lane + 32 * u;
+          if (c < HC) {
+            const uint4 f = fv[u];
+            const float4 g0 = ga[u], g1 = gb[u];
+            uint4 o;
+            o.x = pack_bf16x2(fmaxf(bf16_lo(f.x) + g0.x, 0.f), fmaxf(bf16_hi(f.x) + g0.y, 0.f));
+            o.y = pack_bf16x2(fmaxf(bf16_lo(f.y) + g0.z, 0.f), fmaxf(bf16_hi(f.y) + g0.w, 0.f));
+            o.z = pack_bf16x2(fmaxf(bf16_lo(f.z) + g1.x, 0.f), fmaxf(bf16_hi(f.z) + g1.y, 0.f));
+            o.w = pack_bf16x2(fmaxf(bf16_lo(f.w) + g1.z, 0.f), fmaxf(bf16_hi(f.w) + g1.w, 0.f));
+            zr[c] = o;
+          }
+        }
+      }
+    } else {
+      for (int k = warp; k < nz; k += NW) {
+        const int s = rs.zdst[k] / W;
         const float4 *frp = reinterpret_cast<const float4 *>(fbuf(X)) + rs.zsrc[k] / 4;
         const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
-        float4 *zr = reinterpret_cast<float4 *>(zs() + (size_t)jr * L.zstride);
+        float4 *zr = reinterpret_cast<float4 *>(zs() + (size_t)k * L.zstride);
         for (int c = lane; c < H / 4; c += 32) {
           const float4 fv = frp[c], gv = gr[c];
           zr[c] = make_float4(fmaxf(fv.x + gv.x, 0.f), fmaxf(fv.y + gv.y, 0.f), fmaxf(fv.z + gv.z, 0.f),
@@ -360,15 +406,15 @@ struct Ctx {
   // -------------------------------------------------------------------------
   template <int MT>
   __device__ __forceinline__ void joint_mma(float (&acc)[2][2][4]) const {
-    const int KB = p.H / 32;
+    const int KB = Hd() / 32;
     const uint8_t *a0 = zs() + (size_t)g * L.zstride + q * 16;
     const uint8_t *a1 = a0 + (size_t)8 * L.zstride;
     const uint8_t *a2 = a0 + (size_t)16 * L.zstride;
     const uint8_t *a3 = a0 + (size_t)24 * L.zstride;
-    if (KB == KREG) {
+    if (KB == KR) {
       // hot path (H = 640): fully unrolled, no guards, loads can be hoisted
 #pragma unroll
-      for (int kb = 0; kb < KREG; ++kb) {
+      for (int kb = 0; kb < KR; ++kb) {
         const uint4 b = wreg[kb];
         const uint4 x0 = lds128(a0 + kb * 64), x1 = lds128(a1 + kb * 64);
         mma_bf16_16816(acc[0][kb & 1], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
@@ -381,7 +427,7 @@ struct Ctx {
       }
     } else {
 #pragma unroll
-      for (int kb = 0; kb < KREG; ++kb) {
+      for (int kb = 0; kb < KR; ++kb) {
         if (kb < KB) {
           const uint4 b = wreg[kb];
           const uint4 x0 = lds128(a0 + kb * 64), x1 = lds128(a1 + kb * 64);
@@ -394,7 +440,7 @@ struct Ctx {
           }
         }
       }
-      if (p.H & 31) {
+      if (Hd() & 31) {
         const int o = KB * 64 - q * 8;
         const uint2 x0 = lds64(a0 + o), x1 = lds64(a1 + o);
         mma_bf16_16816(acc[0][0], x0.x, x1.x, x0.y, x1.y, wtail.x, wtail.y);
@@ -407,7 +453,7 @@ struct Ctx {
   }
 
   __device__ void joint_keys(int MT, int nrows_valid, float *logits, int row_base) {
-    const int V1 = p.V1, NV = p.V1 + p.nD, H = p.H;
+    const int V1 = p.V1, NV = p.V1 + p.nD, H = Hd();
     uint64_t *wk = wkey();
     if constexpr (BF) {
       float acc[2][2][4];  // [m-tile][K chain][frag]
@@ -563,29 +609,25 @@ struct Ctx {
   }
 
   // Apply the decisions of one round (warp 0): lane k resolves live joint row
-  // k, then lane s walks slot s's window in frame order (Alg. 3 lines 9-11
-  // and 15-19 for each frame; TDT: blank advances by max(d, 1)).
-  // Also rebuilds the scanning list and checks the speculative window X.
-  __device__ void resolve_rows() {
-    // lane r < C reads CTA r's partial; butterfly max over the lanes
+  // k from the C partial keys (a fixed-order max, so the result is independent
+  // of arrival order), then lane s walks slot s's window in frame order (Alg. 3
+  // lines 9-11 and 15-19 for each frame; TDT: blank advances by max(d, 1),
+  // PAPER.md:213).  decide() also rebuilds the scanning list and checks the
+  // speculative window.
+  __device__ void resolve_rows_w0() {
     const uint64_t *pt = part(par);
-    for (int k = warp; k < rs.nz; k += NW) {
-      const int jr = rs.zdst[k];
+    const int nz = rs.nz;
+    if (lane < nz) {
       uint64_t tkey = 0, dkey = 0;
-      if (lane < C) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)lane * L.JR + k) * 2);
-        tkey = ((uint64_t)v.y << 32) | v.x;
-        dkey = ((uint64_t)v.w << 32) | v.z;
+#pragma unroll 4
+      for (int r = 0; r < C; ++r) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + lane) * 2);
+        tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
+        dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
       }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        if (o < C) {
-          tkey = umax64(tkey, shfl_xor_u64(tkey, o));
-          if (p.nD > 0) dkey = umax64(dkey, shfl_xor_u64(dkey, o));
-        }
-      }
-      if (lane == 0) rs.dec[jr] = key_index(tkey) | ((p.nD > 0 ? key_index(dkey) : 0) << 24);
+      rs.dec[rs.zdst[lane]] = key_index(tkey) | ((p.nD > 0 ? key_index(dkey) : 0) << 24);
     }
+    __syncwarp();
   }
 
   __device__ void decide(unsigned *algevals, int Xnext) {
@@ -614,8 +656,9 @@ struct Ctx {
         pos += p.tdt ? (d > 1 ? d : 1) : 1;
       }
       rs.t[s] = t0 + pos;
+      // the per-frame label counter restarts whenever t advanced (reading A6/A14)
+      if (pos > 0 || !found) rs.k[s] = 0;
       if (!found) {
-        rs.k[s] = 0;
         if (rs.t[s] >= Ls) rs.active[s] = 0;
         else sc = true;
       }
@@ -678,7 +721,7 @@ struct Ctx {
   // columns [tcol(n), tcol(n) + tcols): thread (g, q) of a warp in that quarter
   // holds, for every 32-wide K block kb, the 16-byte B fragment of row g,
   // chunk 4kb + q in columns 4kb..4kb+3 (plus 2 columns for a 16-wide tail).
-  __device__ int tcols() const { return 4 * (p.P / 32) + ((p.P & 31) ? 2 : 0); }
+  __device__ int tcols() const { return 4 * (Pd() / 32) + ((Pd() & 31) ? 2 : 0); }
   // gate tile n belongs to warp w = n % NW (its k-th tile, k = n / NW); the
   // warp can only reach TMEM lane quarter w % 4, so the quarter's columns are
   // shared by its nq warps: slot k * nq + w / 4.
@@ -692,10 +735,10 @@ struct Ctx {
   // Kernel start: W_hh tiles of this CTA from the packed stream into TMEM,
   // W_pred tiles into shared memory (one bulk copy).
   __device__ void load_lstm_weights() {
-    const int NG = ng(), NPT = npt(), KB = p.P / 32;
-    const int sw = ((g & 1) && (p.P % 64) == 0) ? 4 : 0;
+    const int NG = ng(), NPT = npt(), KB = Pd() / 32;
+    const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
     for (int n = warp; n < NG; n += NW) {
-      const uint8_t *row = reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n) * 8 + g) * p.P);
+      const uint8_t *row = reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n) * 8 + g) * Pd());
       for (int c4 = 0; c4 < KB; c4 += 4) {
         uint32_t r[16];
 #pragma unroll
@@ -717,7 +760,7 @@ struct Ctx {
           }
         }
       }
-      if (p.P & 31) {
+      if (Pd() & 31) {
         const uint2 v = ldg64_nc(row + KB * 64 + q * 8);
         asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(tile_taddr(n) + 4 * KB), "r"(v.x),
                      "r"(v.y)
@@ -726,57 +769,76 @@ struct Ctx {
     }
     tmem_wait_st();
     if (warp == 0) {
-      const uint32_t bytes = (uint32_t)(NPT * 8 * p.P * 2);
+      const uint32_t bytes = (uint32_t)(NPT * 8 * Pd() * 2);
       if (lane == 0) {
         mbar_arrive_expect_tx(bar(BAR_FULL), bytes);
-        bulk_g2s(ringslot(0), p.wst + ((size_t)rank * (NG + NPT) + NG) * 8 * p.P, bytes, bar(BAR_FULL));
+        bulk_g2s(ringslot(0), p.wst + ((size_t)rank * (NG + NPT) + NG) * 8 * Pd(), bytes, bar(BAR_FULL));
       }
       mbar_wait(bar(BAR_FULL), 0);
     }
   }
 
-  // gates tile n: acc += A(h rows) . W_hh tile^T, B fragments streamed from TMEM
-  // (next 16 columns loaded while the current ones are consumed; two
-  // accumulator chains over K, summed in a fixed order).
+  // gates tile n: acc += A(h rows) . W_hh tile^T, B fragments streamed from TMEM.
+  // Software-pipelined: the 8 columns (2 K blocks) of chunk c+1 are loaded
+  // while chunk c is consumed (tcgen05.wait::ld waits for all outstanding
+  // loads, so it is issued once per chunk, before the next load); two
+  // accumulator chains over K (one per K block of a chunk), summed in a fixed
+  // order.
+  template <bool HI>
+  __device__ __forceinline__ void chunk_mma(float (&acc)[2][4], float (&acc2)[2][4], const uint32_t (&r)[8], int kb0,
+                                            int MT, const uint8_t *ar0, const uint8_t *ar1, const uint8_t *ar2,
+                                            const uint8_t *ar3) const {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int kb = kb0 + u;
+      float(&A)[2][4] = u ? acc2 : acc;
+      const uint4 xa = lds128(ar0 + kb * 64);
+      const uint4 xb = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
+      mma_bf16_16816(A[0], xa.x, xb.x, xa.y, xb.y, r[4 * u], r[4 * u + 1]);
+      mma_bf16_16816(A[0], xa.z, xb.z, xa.w, xb.w, r[4 * u + 2], r[4 * u + 3]);
+      if (MT > 1) {
+        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
+        mma_bf16_16816(A[1], x2.x, x3.x, x2.y, x3.y, r[4 * u], r[4 * u + 1]);
+        mma_bf16_16816(A[1], x2.z, x3.z, x2.w, x3.w, r[4 * u + 2], r[4 * u + 3]);
+      }
+    }
+  }
+
   template <bool HI>
   __device__ __forceinline__ void tmem_mma(float (&acc)[2][4], int n, int MT, const uint8_t *ar0, const uint8_t *ar1,
                                            const uint8_t *ar2, const uint8_t *ar3) const {
-    const int KB = p.P / 32;
+    const int KB = Pd() / 32, NCH = KB / 2;
     const uint32_t ta = tile_taddr(n);
     float acc2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    for (int c4 = 0; c4 < KB; c4 += 4) {
-      uint32_t r[16];
-      if (c4 + 4 <= KB) {
-        tmem_ld16(ta + 4 * c4, r);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (c4 + u < KB) {
-            uint4 v;
-            tmem_ld4(ta + 4 * (c4 + u), v);
-            r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
-          }
-        }
-      }
-      tmem_wait_ld();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int kb = c4 + u;
-        if (kb < KB) {
-          float(&A)[2][4] = (u & 1) ? acc2 : acc;
-          const uint4 xa = lds128(ar0 + kb * 64);
-          const uint4 xb = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
-          mma_bf16_16816(A[0], xa.x, xb.x, xa.y, xb.y, r[4 * u], r[4 * u + 1]);
-          mma_bf16_16816(A[0], xa.z, xb.z, xa.w, xb.w, r[4 * u + 2], r[4 * u + 3]);
-          if (MT > 1) {
-            const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-            mma_bf16_16816(A[1], x2.x, x3.x, x2.y, x3.y, r[4 * u], r[4 * u + 1]);
-            mma_bf16_16816(A[1], x2.z, x3.z, x2.w, x3.w, r[4 * u + 2], r[4 * u + 3]);
-          }
-        }
+    uint32_t ra[8], rb[8];
+    if (NCH > 0) tmem_ld8(ta, ra);
+    for (int c = 0; c < NCH; c += 2) {
+      tmem_wait_ld();                                   // chunk c (ra) landed
+      if (c + 1 < NCH) tmem_ld8(ta + 8 * (c + 1), rb);
+      chunk_mma<HI>(acc, acc2, ra, 2 * c, MT, ar0, ar1, ar2, ar3);
+      if (c + 1 < NCH) {
+        tmem_wait_ld();                                 // chunk c+1 (rb) landed
+        if (c + 2 < NCH) tmem_ld8(ta + 8 * (c + 2), ra);
+        chunk_mma<HI>(acc, acc2, rb, 2 * (c + 1), MT, ar0, ar1, ar2, ar3);
       }
     }
-    if (p.P & 31) {
+    // odd last K block (P % 64), one x4 load
+    for (int kb = 2 * NCH; kb < KB; ++kb) {
+      uint4 v;
+      tmem_ld4(ta + 4 * kb, v);
+      tmem_wait_ld();
+      float(&A)[2][4] = (kb & 1) ? acc2 : acc;
+      const uint4 xa = lds128(ar0 + kb * 64);
+      const uint4 xb = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
+      mma_bf16_16816(A[0], xa.x, xb.x, xa.y, xb.y, v.x, v.y);
+      mma_bf16_16816(A[0], xa.z, xb.z, xa.w, xb.w, v.z, v.w);
+      if (MT > 1) {
+        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
+        mma_bf16_16816(A[1], x2.x, x3.x, x2.y, x3.y, v.x, v.y);
+        mma_bf16_16816(A[1], x2.z, x3.z, x2.w, x3.w, v.z, v.w);
+      }
+    }
+    if (Pd() & 31) {
       uint32_t t0, t1;
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t0), "=r"(t1) : "r"(ta + 4 * KB));
       tmem_wait_ld();
@@ -798,9 +860,9 @@ struct Ctx {
   template <bool HI>
   __device__ __forceinline__ void smem_tile_mma(float (&acc)[2][4], int j, int MT, const uint8_t *ar0,
                                                 const uint8_t *ar1, const uint8_t *ar2, const uint8_t *ar3) const {
-    const uint8_t *brow = ringslot(j) + (size_t)g * p.P * 2;
-    const int sw = ((g & 1) && (p.P % 64) == 0) ? 4 : 0;
-    const int KB = p.P / 32;
+    const uint8_t *brow = ringslot(j) + (size_t)g * Pd() * 2;
+    const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
+    const int KB = Pd() / 32;
 #pragma unroll 4
     for (int kb = 0; kb < KB; ++kb) {
       const uint4 b = lds128(brow + (((kb * 4 + q) ^ sw) * 16));
@@ -814,7 +876,7 @@ struct Ctx {
         mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
       }
     }
-    if (p.P & 31) {
+    if (Pd() & 31) {
       const int o = KB * 64 - q * 8;
       const uint2 b = lds64(brow + KB * 64 + q * 8);
       const uint2 x0 = lds64(ar0 + o), x1 = lds64(ar1 + o);
@@ -845,16 +907,10 @@ struct Ctx {
     }
   }
 
-  __device__ void predictor_lstm_tmem(unsigned long long *pp = nullptr) {
-    long long tm = pp ? clock64() : 0;
-#define LL_SUB(k)                                          \
-  if (pp) {                                                \
-    const long long nw = clock64();                        \
-    pp[k] += (unsigned long long)(nw - tm);                \
-    tm = nw;                                               \
-  }
+  __device__ void predictor_lstm_tmem() {
+    tl_pred(0);
     const int n = rs.npred, MT = (n + 15) / 16;
-    const int P = p.P, H = p.H, NG = ng(), NPT = npt();
+    const int P = Pd(), H = Hd(), NG = ng(), NPT = npt();
 
     // arm the h' / g exchange barriers for this step (tx from the other CTAs)
     if (tid == 0 && C > 1) {
@@ -889,10 +945,9 @@ struct Ctx {
       float acc[2][4];
 #pragma unroll
       for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-      LL_SUB(0);
       if (hi) tmem_mma<true>(acc, j, MT, ar0, ar1, ar2, ar3);
       else tmem_mma<false>(acc, j, MT, ar0, ar1, ar2, ar3);
-      LL_SUB(1);
+      if (j == warp) tl_pred(1);
       if (!e_ready) {
         mbar_wait(bar(BAR_E), hph & 1u);
         e_ready = true;
@@ -925,10 +980,10 @@ struct Ctx {
       }
     }
     if (!e_ready) mbar_wait(bar(BAR_E), hph & 1u);  // keep every thread's view of the phase in step
-    LL_SUB(2);
+    tl_pred(2);
     // (2) exchange the h' slices (this CTA's units) with every CTA
     sync();
-    LL_SUB(3);
+    tl_pred_bar(3);
     if (C > 1) {
       // rows: slot ids; the destination row is the slot's NEXT parity
       if (tid < n) {
@@ -939,7 +994,7 @@ struct Ctx {
       bcast_rows(sm + L.off_hs, L.hstride, u0 * 2, L.UPC * 2, n, rs.zsrc, BAR_H);
       mbar_wait(bar(BAR_H), hph & 1u);
     }
-    LL_SUB(4);
+    tl_pred(4);
     const uint8_t *br0 = arow(g, 1), *br1 = arow(g + 8, 1), *br2 = arow(g + 16, 1), *br3 = arow(g + 24, 1);
     // (3) g = W_pred h' + b_pred for this CTA's output dims
     for (int j = warp; j < NPT; j += NW) {
@@ -960,10 +1015,10 @@ struct Ctx {
       }
     }
 
-    LL_SUB(5);
+    tl_pred(5);
     // (4) exchange the g slices
     sync();
-    LL_SUB(6);
+    tl_pred_bar(6);
     if (C > 1) {
       bcast_rows((const uint8_t *)gs(), H * 4, d0 * 4, L.DPC * 4, n, rs.plist, BAR_G);
       mbar_wait(bar(BAR_G), hph & 1u);
@@ -974,8 +1029,8 @@ struct Ctx {
       rs.hpar[s] ^= 1;
     }
     sync();
-    LL_SUB(7);
-#undef LL_SUB
+    tl_pred_bar(7);
+    ++tl_step;
   }
 
   // -------------------------------------------------------------------------
@@ -1007,7 +1062,7 @@ struct Ctx {
   }
 
   __device__ void load_h_rows_f32(int n, int which /*0: current hpar, 1: next*/) {
-    const int P = p.P;
+    const int P = Pd();
     float *z = (float *)zs();
     const int zst = L.zstride / 4;
     for (int idx = tid; idx < n * P; idx += NCT) {
@@ -1024,7 +1079,7 @@ struct Ctx {
   }
 
   __device__ void predictor_lstm_f32() {
-    const int n = rs.npred, P = p.P, H = p.H;
+    const int n = rs.npred, P = Pd(), H = Hd();
     const float *tab = p.tab;
     load_h_rows_f32(n, 0);
     for (int uu = warp; uu < L.UPC; uu += NW) {
@@ -1079,7 +1134,7 @@ struct Ctx {
   }
 
   __device__ void predictor_stateless() {
-    const int n = rs.npred, H = p.H, V1 = p.V1;
+    const int n = rs.npred, H = Hd(), V1 = p.V1;
     const int c4 = H / 4;
     for (int idx = tid; idx < n * c4; idx += NCT) {
       const int i = idx / c4, c = idx % c4;
@@ -1158,12 +1213,13 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // ---------------------------------------------------------------------------
 // The decode kernel.  PRED: 0 = LSTM, 1 = stateless.
 // ---------------------------------------------------------------------------
-template <typename T, int PRED>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  Ctx<T> cx(p, smem, rs, PRED == 0, s_bars);
+  __shared__ Layout s_layout;
+  Ctx<T, KR, HC, PC, CC> cx(p, smem, rs, PRED == 0, s_bars, s_layout);
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
   constexpr bool RING = sizeof(T) == 2 && PRED == 0;
@@ -1190,21 +1246,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
 
   {
     int cur = 0;                  // f buffer of the current round
-    // optional phase profile (thread 0 of the first CTA): 0 wait_f, 1 build_z, 2 joint,
-    // 3 exchange, 4 decide, 5 predictor, 6 append/outer, 7 total
-    __shared__ unsigned long long pt[16], pp[9];   // written by thread 0 of the profiled CTA only
-    const bool prof = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
-    if (prof) {
-      for (int kk = 0; kk < 16; ++kk) pt[kk] = 0;
-      for (int kk = 0; kk < 9; ++kk) pp[kk] = 0;
-    }
-    long long t_mark = clock64(), t_start = t_mark;
 #define LL_PHASE(k)                              \
-  if (prof) {                                    \
-    const long long now = clock64();             \
-    pt[k] += (unsigned long long)(now - t_mark); \
-    t_mark = now;                                \
-  }                                              \
   if (p.trace && tid == 0) {                     \
     p.trace[blockIdx.x * 8 + 0] = (k);           \
     p.trace[blockIdx.x * 8 + 1] = s_cnt[SC_ROUNDS];    \
@@ -1246,8 +1288,8 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         // LSTM initial state h = c = 0 (reading A8)
         for (int i = tid; i < R * cx.L.UPC; i += cx.NCT) cx.cs()[i] = 0.f;
         if constexpr (RING) {
-          for (int i = tid; i < R * p.P / 8; i += cx.NCT) {
-            const int s = i / (p.P / 8), c = i % (p.P / 8);
+          for (int i = tid; i < R * cx.Pd() / 8; i += cx.NCT) {
+            const int s = i / (cx.Pd() / 8), c = i % (cx.Pd() / 8);
             *reinterpret_cast<uint4 *>(cx.hsrow(0, s) + c * 16) = make_uint4(0, 0, 0, 0);
           }
         }
@@ -1271,6 +1313,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         cx.issue_f(cur, false);
         cx.sync();                     // fbase/fcnt (written by the issuing warp) visible to warp 0
         LL_PHASE(11);
+        cx.tl_pred_bar(8);
         // predictor (Alg. 3 line 6): only rows that found a label and stay active
         if (rs.npred > 0) {
           if (t0) {
@@ -1278,41 +1321,51 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             s_cnt[SC_PREDROWS] += rs.npred;
           }
           if constexpr (PRED == 1) cx.predictor_stateless();
-          else if constexpr (RING) cx.predictor_lstm_tmem(prof ? pp : nullptr);
+          else if constexpr (RING) cx.predictor_lstm_tmem();
           else cx.predictor_lstm_f32();
         }
         LL_PHASE(10);
         // ---- frame loop: rounds of W-frame windows until no row scans ---------
         bool planned = false;          // first round: plan after the predictor phase
         while (rs.nscan > 0) {
+          cx.tl_round_(0);
           cx.wait_f(cur);
           if (!planned) {
             cx.plan_z(cur);
             cx.sync();                 // plan visible, predictor's g written
           }
           LL_PHASE(0);
+          cx.tl_round_bar(1);
           cx.build_z(cur);
           LL_PHASE(1);
+          cx.tl_round_(2);
           cx.sync();
           // speculative: a row whose window is all blank needs the next window
           if (p.spec_prefetch) cx.issue_f(cur ^ 1, true);
           LL_PHASE(2);
+          cx.tl_round_bar(3);
           cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
           LL_PHASE(3);
+          cx.tl_round_(4);
           cx.exchange_keys();
           LL_PHASE(4);
-          cx.exchange_wait();
-          LL_PHASE(5);
-          if (t0) {
-            s_cnt[SC_ROUNDS]++;
-            s_cnt[SC_ROWEVALS] += rs.nz;
+          cx.tl_round_(5);
+          if (warp == 0) {
+            // warp 0 alone: cross-CTA argmax, decisions, next round's plan
+            cx.exchange_wait();
+            LL_PHASE(5);
+            cx.tl_round_(6);
+            if (t0) {
+              s_cnt[SC_ROUNDS]++;
+              s_cnt[SC_ROWEVALS] += rs.nz;
+            }
+            cx.resolve_rows_w0();
+            cx.tl_round_(7);
+            cx.tl_round_(8);
+            cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
+            LL_PHASE(8);
+            cx.tl_round_(9);
           }
-          cx.resolve_rows();
-          LL_PHASE(6);
-          cx.sync();
-          LL_PHASE(7);
-          cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
-          LL_PHASE(8);
           cx.par ^= 1;
           cx.sync();
           planned = false;
@@ -1329,6 +1382,8 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             cur ^= 1;                    // the other buffer holds a stale speculative copy
           }
           LL_PHASE(9);
+          cx.tl_round_bar(10);
+          ++cx.tl_round;
         }
         // ---- append + time rules + guard (BatchedHyps.add_results, :196-199) --
         if (warp == 0 && lane < R) {
@@ -1386,12 +1441,6 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
     if ((cx.fpend >> 0) & 1u) cx.wait_f(0);
     if ((cx.fpend >> 1) & 1u) cx.wait_f(1);
     cx.sync();
-    if (prof) {
-      LL_PHASE(11);
-      pt[15] = (unsigned long long)(clock64() - t_start);
-      for (int kk = 0; kk < 16; ++kk) p.prof[kk] = pt[kk];
-      for (int kk = 0; kk < 9; ++kk) p.prof[16 + kk] = pp[kk];
-    }
 #undef LL_PHASE
     if (rank == 0 && tid == 0 && p.stats) {
       atomicAdd(p.stats + 0, (unsigned long long)s_cnt[SC_OUTER]);
@@ -1423,12 +1472,13 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
 // f rows [n][H] (workspace, produced by the encoder projection) + g [n][H].
 // Runs with W = 1: every row is one slot with one frame.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int KR>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  Ctx<T> cx(p, smem, rs, false, s_bars);
+  __shared__ Layout s_layout;
+  Ctx<T, KR> cx(p, smem, rs, false, s_bars, s_layout);
   const int C = cx.C, tid = cx.tid, warp = cx.warp, lane = cx.lane, R = p.R;
   cx.init_barriers();
   cx.load_weight_slice();

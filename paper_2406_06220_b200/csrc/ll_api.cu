@@ -152,9 +152,17 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
 }
 
 // Resident clusters of size C for the decode kernel (1 CTA per SM).
-template <typename T, int PRED>
+// Register-tile width of the joint weight slice: KREG_SMALL K blocks for small
+// joints, KREG (H <= 656) otherwise; fp32 keeps no weights in registers.
+inline int kreg_for(bool bf, int H) { return !bf ? 1 : (H <= KREG_SMALL * 32 + 16 ? KREG_SMALL : KREG); }
+// Production shape (FastConformer joint, BASELINE configs 2-5): H = P = 640 in
+// 16-CTA clusters, compiled with those dims fixed.
+constexpr int FC_H = 640, FC_P = 640, FC_C = 16;
+inline bool is_fc(bool bf, int H, int P, int C) { return bf && H == FC_H && P == FC_P && C == FC_C; }
+
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0>
 int max_clusters(int C, const Layout &L) {
-  auto kern = decode_kernel<T, PRED>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -176,10 +184,10 @@ int max_clusters(int C, const Layout &L) {
   return n;
 }
 
-template <typename T, int PRED>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0>
 ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
                         int &used_clusters) {
-  auto kern = decode_kernel<T, PRED>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -209,9 +217,9 @@ ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_gro
   return LL_OK;
 }
 
-template <typename T>
+template <typename T, int KR>
 ll_status launch_debug(const DecodeParams &p, int C, const Layout &L, int n_chunks, cudaStream_t st) {
-  auto kern = debug_joint_kernel<T>;
+  auto kern = debug_joint_kernel<T, KR>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -288,8 +296,15 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   {
     // re-choose R / W with the number of clusters that can actually be resident
     int ncl = 0;
-    if (bf) ncl = lstm ? max_clusters<bf16, 0>(cf.C, cf.L) : max_clusters<bf16, 1>(cf.C, cf.L);
-    else ncl = lstm ? max_clusters<float, 0>(cf.C, cf.L) : max_clusters<float, 1>(cf.C, cf.L);
+    if (is_fc(bf, H, P, cf.C))
+      ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L)
+                 : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L);
+    else if (bf && kreg_for(bf, H) == KREG)
+      ncl = lstm ? max_clusters<bf16, 0, KREG>(cf.C, cf.L) : max_clusters<bf16, 1, KREG>(cf.C, cf.L);
+    else if (bf)
+      ncl = lstm ? max_clusters<bf16, 0, KREG_SMALL>(cf.C, cf.L) : max_clusters<bf16, 1, KREG_SMALL>(cf.C, cf.L);
+    else
+      ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
     if (ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl)) return LL_ERR_UNSUPPORTED;
   }
   const int C = cf.C, R = cf.R;
@@ -353,20 +368,30 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   p.status = (int *)ws;
   p.group_counter = (int *)ws + 1;
   p.stats = (unsigned long long *)(ws + 64);
-  p.prof = env_int("LL_PROFILE", 0) ? (unsigned long long *)(ws + 256) : nullptr;
-  p.prof_mode = env_int("LL_PROFILE", 0);
+  {
+    // debug: per-warp clock64 timeline of block 0 into a caller-provided device
+    // buffer of [2][TL_N][TL_PH][MAX_NW] u64 (tools/timeline.py)
+    const char *tp = getenv("LL_TIMELINE_PTR");
+    p.prof = (tp && *tp) ? (unsigned long long *)strtoull(tp, nullptr, 0) : nullptr;
+  }
   {
     const char *tp = getenv("LL_TRACE_PTR");
     p.trace = (tp && *tp) ? (volatile unsigned *)strtoull(tp, nullptr, 0) : nullptr;
   }
   int used = 0;
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
-  if (bf)
-    s = lstm ? launch_decode<bf16, 0>(p, C, L, p.n_groups, st, used)
-             : launch_decode<bf16, 1>(p, C, L, p.n_groups, st, used);
+  if (is_fc(bf, H, P, C))
+    s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C>(p, C, L, p.n_groups, st, used)
+             : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C>(p, C, L, p.n_groups, st, used);
+  else if (bf && kreg_for(bf, H) == KREG)
+    s = lstm ? launch_decode<bf16, 0, KREG>(p, C, L, p.n_groups, st, used)
+             : launch_decode<bf16, 1, KREG>(p, C, L, p.n_groups, st, used);
+  else if (bf)
+    s = lstm ? launch_decode<bf16, 0, KREG_SMALL>(p, C, L, p.n_groups, st, used)
+             : launch_decode<bf16, 1, KREG_SMALL>(p, C, L, p.n_groups, st, used);
   else
-    s = lstm ? launch_decode<float, 0>(p, C, L, p.n_groups, st, used)
-             : launch_decode<float, 1>(p, C, L, p.n_groups, st, used);
+    s = lstm ? launch_decode<float, 0, 1>(p, C, L, p.n_groups, st, used)
+             : launch_decode<float, 1, 1>(p, C, L, p.n_groups, st, used);
   if (s == LL_OK && g_ev_after && cudaEventRecord(g_ev_after, st) != cudaSuccess) return LL_ERR_CUDA;
   return s;
 }
@@ -486,7 +511,9 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   p.dbg_g = g_rows; p.dbg_logits = out_logits; p.dbg_argmax = out_argmax; p.dbg_dargmax = out_dur_argmax;
   p.dbg_n = n;
   const int chunks = (n + R - 1) / R;
-  return bf ? launch_debug<bf16>(p, C, L, chunks, st) : launch_debug<float>(p, C, L, chunks, st);
+  if (bf && kreg_for(bf, H) == KREG) return launch_debug<bf16, KREG>(p, C, L, chunks, st);
+  if (bf) return launch_debug<bf16, KREG_SMALL>(p, C, L, chunks, st);
+  return launch_debug<float, 1>(p, C, L, chunks, st);
 }
 
 }  // extern "C"

@@ -13,7 +13,7 @@ import os
 from ctypes import POINTER, c_char_p, c_int32, c_size_t, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libll.so")
+LIB_PATH = os.environ.get("LL_LIB_PATH") or os.path.join(HERE, "libll.so")  # override: experiments only
 
 LL_OK, LL_ERR_INVALID_ARGUMENT, LL_ERR_UNSUPPORTED, LL_ERR_WORKSPACE, LL_ERR_CUDA, LL_ERR_CAPACITY = range(6)
 LL_BF16, LL_F32 = 0, 1

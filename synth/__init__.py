@@ -25,7 +25,8 @@ import numpy as np
 
 __all__ = [
     "ModelSpec", "bf16_round", "make_weights", "make_inputs", "make_planted_rnnt",
-    "make_planted_tdt", "cat_dog_fixture", "tdt_forced_fixture", "CONFIGS",
+    "make_planted_tdt", "cat_dog_fixture", "tdt_forced_fixture", "guard_after_blank_fixture",
+    "guard_after_blank_tdt_fixture", "CONFIGS",
     "sweep_lengths", "frame_seconds",
 ]
 
@@ -347,6 +348,38 @@ def cat_dog_fixture():
     dog = [(0, b, b), (1, b, D), (1, D, b), (2, D, b), (3, D, O), (3, O, G), (3, G, b)]
     spec, w, enc, lengths = _table_fixture([cat, dog], 4, 7)
     return spec, w, enc, lengths, CAT_DOG_VOCAB
+
+
+GUARD_VOCAB = ["<b>", "A", "B", "C", "D", "E", "F"]
+
+
+def guard_after_blank_fixture():
+    """Max-symbols guard (reading A6) after a frame advance, m = 3, one RNN-T
+    utterance and one TDT utterance-equivalent, as table weights.
+
+    RNN-T alignment over T=4: frame 0 emits A then blank; frame 1 emits B, C,
+    D (the guard fires after the 3rd label at frame 1, no blank evaluation);
+    frames 2, 3 blank.  The label counter must restart at the frame advance
+    (the blank at frame 0), so all three labels at frame 1 are emitted:
+    A,B,C,D @ [0,1,1,1].  Returns (spec, weights, enc, lengths, vocab)."""
+    A, B_, C, D, b = 1, 2, 3, 4, 0
+    steps = [(0, b, A), (0, A, b), (1, A, B_), (1, B_, C), (1, C, D), (2, D, b), (3, D, b)]
+    spec, w, enc, lengths = _table_fixture([steps], 4, 7)
+    spec = dataclasses.replace(spec, max_symbols=3)
+    return spec, w, enc, lengths, GUARD_VOCAB
+
+
+def guard_after_blank_tdt_fixture():
+    """TDT form of guard_after_blank_fixture (durations {0,1,2}, m = 3): frame 0
+    emits (A,0) then (blank,1); frame 1 emits (B,0), (C,0), (D,0) -- the guard
+    fires after the third zero-duration label at frame 1 -- then (blank,1) at
+    frames 2 and 3.  Expected A,B,C,D @ [0,1,1,1], durations [0,0,0,0]."""
+    A, B_, C, D, b = 1, 2, 3, 4, 0
+    steps = [(0, b, A, 0), (0, A, b, 1), (1, A, B_, 0), (1, B_, C, 0), (1, C, D, 0), (2, D, b, 1),
+             (3, D, b, 1)]
+    spec, w, enc, lengths = _table_fixture([steps], 4, 7, durations=[0, 1, 2])
+    spec = dataclasses.replace(spec, max_symbols=3)
+    return spec, w, enc, lengths, GUARD_VOCAB
 
 
 def tdt_forced_fixture():

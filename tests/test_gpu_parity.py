@@ -92,6 +92,42 @@ def test_tdt_forced_through_abi():
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("tdt", [False, True])
+@pytest.mark.parametrize("window", [1, 0])
+def test_guard_counter_restarts_after_blank(dtype, tdt, window, monkeypatch):
+    """Reading A6/A14: after a frame advance inside a multi-frame window the
+    label counter restarts, so frame 1 emits m = 3 labels (A,B,C,D @ [0,1,1,1],
+    hand-derived; pinned on the oracle in test_oracle.py)."""
+    if window:
+        monkeypatch.setenv("LL_WINDOW", str(window))
+    fx = synth.guard_after_blank_tdt_fixture() if tdt else synth.guard_after_blank_fixture()
+    spec, w, enc, lengths, vocab = fx
+    hyps, _ = gpu_decode(spec, w, enc, lengths, dtype)
+    assert [vocab[y] for y in hyps[0][0]] == list("ABCD")
+    assert hyps[0][1] == [0, 1, 1, 1]
+    if tdt:
+        assert hyps[0][2] == [0, 0, 0, 0]
+
+
+@pytest.mark.parametrize("kind", ["stateless", "lstm"])
+def test_tiny_low_blank_bias_sweep(kind):
+    """Random tiny models with blank biases in [-0.5, 2] (many labels per frame,
+    blanks between them: the guard after a frame advance is exercised), 60
+    seeds x 2 rows, windows of 8 frames; every row teacher-forced in float64."""
+    base = synth.CONFIGS["tiny"]["spec"]
+    sp = synth.ModelSpec(base.num_tokens, base.enc_dim, base.pred_dim, base.joint_dim, kind, 1, None,
+                         base.blank_id, base.max_symbols)
+    decs = 0
+    for seed in range(60):
+        bb = float(np.random.default_rng(seed).uniform(-0.5, 2.0))
+        w = synth.make_weights(sp, 5000 + seed, blank_bias=bb)
+        enc, lengths = synth.make_inputs(7000 + seed, 2, 30, sp.enc_dim, 5, 30)
+        hyps, _ = gpu_decode(sp, w, enc, lengths, "f32")
+        decs += verify_all(sp, w, enc, lengths, hyps)[1]
+    assert decs > 1000
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("cfg", ["tiny", "tiny-tdt"])
 def test_tiny_random_family(dtype, cfg):
     """BASELINE configs (1) and (3)-tiny on many seeds (random family, guard and

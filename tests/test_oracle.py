@@ -60,6 +60,25 @@ def test_tdt_forced_alignment():
 
 
 # ---------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("tdt", [False, True])
+def test_guard_counter_restarts_after_blank(tdt):
+    """Reading A6 / A14: the per-frame label counter k restarts whenever t
+    advances (here: a blank at frame 0), so frame 1 emits m = 3 labels before
+    the guard moves on.  Hand-derived from the rules of PAPER.md:53-54 (t moves
+    only on blank) plus the guard: A,B,C,D @ [0,1,1,1].  Label-looping (Alg. 3)
+    must agree."""
+    fx = synth.guard_after_blank_tdt_fixture() if tdt else synth.guard_after_blank_fixture()
+    spec, w, enc, lengths, vocab = fx
+    model = Transducer.from_spec(spec, w)
+    r = decode_sequential(model, enc[0], int(lengths[0]), spec.max_symbols)
+    assert [vocab[y] for y in r.tokens] == list("ABCD")
+    assert r.timestamps == [0, 1, 1, 1]
+    if tdt:
+        assert r.durations == [0, 0, 0, 0]
+    lab, _ = decode_label_looping(model, enc, lengths, spec.max_symbols)
+    assert (lab[0].tokens, lab[0].timestamps) == (r.tokens, r.timestamps)
+
+
 @pytest.mark.parametrize("kind", ["lstm", "stateless"])
 def test_always_blank(kind):
     """always-blank -> empty output, L joint evals, 1 predictor call."""

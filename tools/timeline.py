@@ -1,0 +1,59 @@
+"""Per-warp clock64 timeline of block 0 (cluster 0, rank 0) of the decode
+kernel: every warp stamps phase boundaries of the first TL_N joint rounds and
+predictor steps (decode.cuh tl_* hooks, enabled by LL_TIMELINE_PTR).
+
+    python tools/timeline.py [config]          (GPU box)
+
+Prints, per phase, the critical-path increment (latest warp at this boundary
+minus latest warp at the previous one) and the warp skew at the boundary,
+averaged over the recorded events."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+TL_N, TL_PH, NW = 128, 16, 10
+buf = torch.zeros(2 * TL_N * TL_PH * NW, dtype=torch.int64, device="cuda")
+os.environ["LL_TIMELINE_PTR"] = str(buf.data_ptr())
+import bench
+from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "fc-rnnt"
+spec, w, enc, lengths = bench.workload(cfg, 1000)
+model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16")
+dec = LabelLoopingDecoder(model, spec.max_symbols, enc.shape[0], enc.shape[1])
+e = torch.from_numpy(enc).to("cuda", torch.bfloat16); l = torch.from_numpy(lengths).cuda()
+for _ in range(3):
+    buf.zero_()
+    dec.decode(e, l)
+torch.cuda.synchronize()
+print(cfg, dec.stats())
+tl = buf.cpu().numpy().reshape(2, TL_N, TL_PH, NW).astype(np.float64)
+
+def report(area, name, order, labels):
+    x = tl[area]
+    ev = [i for i in range(TL_N) if (x[i, order[0]] > 0).any() and (x[i, order[-1]] > 0).any()]
+    print(f"\n{name}: {len(ev)} events recorded")
+    tot = np.zeros(len(order))
+    skew = np.zeros(len(order))
+    for i in ev:
+        mx = [x[i, ph][x[i, ph] > 0].max() if (x[i, ph] > 0).any() else np.nan for ph in order]
+        mn = [x[i, ph][x[i, ph] > 0].min() if (x[i, ph] > 0).any() else np.nan for ph in order]
+        for k in range(1, len(order)):
+            tot[k] += mx[k] - mx[k - 1]
+            skew[k] += mx[k] - mn[k]
+    n = max(1, len(ev))
+    for k in range(1, len(order)):
+        print(f"  {labels[k]:28s} {tot[k]/n:8.0f} cyc   (warp skew at end {skew[k]/n:6.0f})")
+    print(f"  {'TOTAL':28s} {tot.sum()/n:8.0f} cyc")
+    # next-event gap: from the last stamp of event i to the first of event i+1
+    gaps = [x[ev[j + 1], order[0]][x[ev[j + 1], order[0]] > 0].max() - x[ev[j], order[-1]].max()
+            for j in range(len(ev) - 1) if ev[j + 1] == ev[j] + 1]
+    if gaps:
+        print(f"  {'(gap to next event)':28s} {np.median(gaps):8.0f} cyc median")
+    return ev
+
+report(0, "joint rounds", list(range(11)),
+       ["", "wait_f/plan (+sync)", "build_z", "sync (bar)", "spec issue + joint", "exchange send",
+        "exchange wait", "resolve", "sync (bar)", "decide", "sync+reload (bar)"])
+report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 5, 6, 7],
+       ["", "outer-step entry", "first gate tile", "rest tiles + E' wait", "sync (bar)", "h' exchange",
+        "W_pred tiles", "sync (bar)", "g exchange + sync"])
