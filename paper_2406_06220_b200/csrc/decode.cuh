@@ -127,7 +127,13 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.hstride = (int)(align_up((size_t)P * 2, 128) + 64);
   size_t o = 0;
   L.off_b = o;    o = align_up(o + (size_t)L.tiles_max * 8 * 4, 128);
-  L.off_z = o;    o = align_up(o + (size_t)L.JRp * L.zstride, 128);
+  L.off_z = o;    // joint operand rows; in the bf16 LSTM predictor: W_pred partials [NW][3][2][32] float4
+  {
+    size_t zb = (size_t)L.JRp * L.zstride;
+    const size_t wp = (size_t)L.NW * 3 * 2 * 32 * 16;
+    if (L.ring && zb < wp) zb = wp;
+    o = align_up(o + zb, 128);
+  }
   L.off_f = o;    o = align_up(o + (size_t)2 * R * WF * H * (bf ? 2 : 4), 128);
   L.off_g = o;    o = align_up(o + (size_t)R * H * 4, 128);
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * 4, 128);
@@ -149,6 +155,7 @@ struct RowState {
   int slist[MAX_R], plist[MAX_R];
   int zsrc[MAX_JR], zdst[MAX_JR];        // live joint rows k: f row offset (elements) / logical row s*W+j
   int dec[MAX_JR];                        // per joint row: token | dur_index << 24
+  int zbeg[MAX_R], zcnt[MAX_R];          // per slot: first compact joint row of its window, live rows
   int nscan, npred, nactive, nz, ready;
   int grp[2];                            // group index broadcast (double-buffered)
   int ack[2];
@@ -338,6 +345,14 @@ struct Ctx {
       const int k = __popc(m & ((1u << lane) - 1u));
       rs.zsrc[k] = src;
       rs.zdst[k] = dst;
+    }
+    // per slot: its live rows are frames j = 0 .. zcnt-1 at compact rows zbeg + j
+    if (lane < p.R) rs.zcnt[lane] = 0;
+    __syncwarp();
+    if (lane < rs.nscan) {
+      const int s = rs.slist[lane], b0 = lane * W;
+      rs.zbeg[s] = __popc(m & ((1u << b0) - 1u));
+      rs.zcnt[s] = __popc((m >> b0) & ((1u << W) - 1u));
     }
     if (lane == 0) rs.nz = __popc(m);
   }
@@ -717,17 +732,19 @@ struct Ctx {
   __device__ int ng() const { return L.UPC / 2; }
   __device__ int npt() const { return L.DPC / 8; }
 
-  // TMEM geometry of the W_hh tiles: gate tile n lives in lane quarter n % 4,
-  // columns [tcol(n), tcol(n) + tcols): thread (g, q) of a warp in that quarter
-  // holds, for every 32-wide K block kb, the 16-byte B fragment of row g,
-  // chunk 4kb + q in columns 4kb..4kb+3 (plus 2 columns for a 16-wide tail).
+  // W_hh tile PAIRS: pair pp (units u0 + 4pp .. u0 + 4pp + 3) is two 8-row
+  // tiles, half 0 = gates (i, f) and half 1 = gates (g, o), row c of a half =
+  // unit 4pp + c/2, gate 2*half + (c & 1) (packed by pack_lstm_stream).
+  // Pair pp belongs to warp pp % NW; a warp can only reach TMEM lane quarter
+  // warp % 4, so the quarter's columns are shared by its warps: the warp's k-th
+  // tile (k = 2 * (pp / NW) + half) sits in column slot k * nq + warp / 4.
+  // Thread (g, q) of the warp holds, for every 32-wide K block kb, the 16-byte
+  // fragment (row g, chunk 4kb + q) in columns 4kb..4kb+3 (+2 for a 16-wide tail).
   __device__ int tcols() const { return 4 * (Pd() / 32) + ((Pd() & 31) ? 2 : 0); }
-  // gate tile n belongs to warp w = n % NW (its k-th tile, k = n / NW); the
-  // warp can only reach TMEM lane quarter w % 4, so the quarter's columns are
-  // shared by its nq warps: slot k * nq + w / 4.
+  __device__ int npairs() const { return L.UPC / 4; }
   __device__ int quarter_warps(int qd) const { return (NW - qd + 3) / 4; }
-  __device__ uint32_t tile_taddr(int n) const {
-    const int w = n % NW, k = n / NW, qd = w & 3;
+  __device__ uint32_t pair_taddr(int pp, int half) const {
+    const int w = pp % NW, k = 2 * (pp / NW) + half, qd = w & 3;
     const int slot = k * quarter_warps(qd) + (w >> 2);
     return tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(slot * tcols());
   }
@@ -737,8 +754,11 @@ struct Ctx {
   __device__ void load_lstm_weights() {
     const int NG = ng(), NPT = npt(), KB = Pd() / 32;
     const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
-    for (int n = warp; n < NG; n += NW) {
-      const uint8_t *row = reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n) * 8 + g) * Pd());
+    for (int n = 2 * warp; n < NG; n += 2 * NW) {   // stream tile n = 2 * pair + half
+     for (int half = 0; half < 2; ++half) {
+      const uint32_t ta = pair_taddr(n / 2, half);
+      const uint8_t *row =
+          reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n + half) * 8 + g) * Pd());
       for (int c4 = 0; c4 < KB; c4 += 4) {
         uint32_t r[16];
 #pragma unroll
@@ -749,12 +769,12 @@ struct Ctx {
           r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
         }
         if (c4 + 4 <= KB) {
-          tmem_st16(tile_taddr(n) + 4 * c4, r);
+          tmem_st16(ta + 4 * c4, r);
         } else {
           // partial chunk: store the valid blocks one x4 group at a time
           for (int u = 0; c4 + u < KB; ++u) {
             asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(
-                             tile_taddr(n) + 4 * (c4 + u)),
+                             ta + 4 * (c4 + u)),
                          "r"(r[4 * u]), "r"(r[4 * u + 1]), "r"(r[4 * u + 2]), "r"(r[4 * u + 3])
                          : "memory");
           }
@@ -762,10 +782,11 @@ struct Ctx {
       }
       if (Pd() & 31) {
         const uint2 v = ldg64_nc(row + KB * 64 + q * 8);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(tile_taddr(n) + 4 * KB), "r"(v.x),
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(ta + 4 * KB), "r"(v.x),
                      "r"(v.y)
                      : "memory");
       }
+     }
     }
     tmem_wait_st();
     if (warp == 0) {
@@ -778,112 +799,108 @@ struct Ctx {
     }
   }
 
-  // gates tile n: acc += A(h rows) . W_hh tile^T, B fragments streamed from TMEM.
-  // Software-pipelined: the 8 columns (2 K blocks) of chunk c+1 are loaded
-  // while chunk c is consumed (tcgen05.wait::ld waits for all outstanding
-  // loads, so it is issued once per chunk, before the next load); two
-  // accumulator chains over K (one per K block of a chunk), summed in a fixed
-  // order.
-  template <bool HI>
-  __device__ __forceinline__ void chunk_mma(float (&acc)[2][4], float (&acc2)[2][4], const uint32_t (&r)[8], int kb0,
-                                            int MT, const uint8_t *ar0, const uint8_t *ar1, const uint8_t *ar2,
-                                            const uint8_t *ar3) const {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int kb = kb0 + u;
-      float(&A)[2][4] = u ? acc2 : acc;
-      const uint4 xa = lds128(ar0 + kb * 64);
-      const uint4 xb = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
-      mma_bf16_16816(A[0], xa.x, xb.x, xa.y, xb.y, r[4 * u], r[4 * u + 1]);
-      mma_bf16_16816(A[0], xa.z, xb.z, xa.w, xb.w, r[4 * u + 2], r[4 * u + 3]);
-      if (MT > 1) {
-        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-        mma_bf16_16816(A[1], x2.x, x3.x, x2.y, x3.y, r[4 * u], r[4 * u + 1]);
-        mma_bf16_16816(A[1], x2.z, x3.z, x2.w, x3.w, r[4 * u + 2], r[4 * u + 3]);
-      }
-    }
-  }
-
-  template <bool HI>
-  __device__ __forceinline__ void tmem_mma(float (&acc)[2][4], int n, int MT, const uint8_t *ar0, const uint8_t *ar1,
-                                           const uint8_t *ar2, const uint8_t *ar3) const {
-    const int KB = Pd() / 32, NCH = KB / 2;
-    const uint32_t ta = tile_taddr(n);
-    float acc2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    uint32_t ra[8], rb[8];
-    if (NCH > 0) tmem_ld8(ta, ra);
-    for (int c = 0; c < NCH; c += 2) {
-      tmem_wait_ld();                                   // chunk c (ra) landed
-      if (c + 1 < NCH) tmem_ld8(ta + 8 * (c + 1), rb);
-      chunk_mma<HI>(acc, acc2, ra, 2 * c, MT, ar0, ar1, ar2, ar3);
-      if (c + 1 < NCH) {
-        tmem_wait_ld();                                 // chunk c+1 (rb) landed
-        if (c + 2 < NCH) tmem_ld8(ta + 8 * (c + 2), ra);
-        chunk_mma<HI>(acc, acc2, rb, 2 * (c + 1), MT, ar0, ar1, ar2, ar3);
-      }
-    }
-    // odd last K block (P % 64), one x4 load
-    for (int kb = 2 * NCH; kb < KB; ++kb) {
-      uint4 v;
-      tmem_ld4(ta + 4 * kb, v);
-      tmem_wait_ld();
-      float(&A)[2][4] = (kb & 1) ? acc2 : acc;
-      const uint4 xa = lds128(ar0 + kb * 64);
-      const uint4 xb = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
-      mma_bf16_16816(A[0], xa.x, xb.x, xa.y, xb.y, v.x, v.y);
-      mma_bf16_16816(A[0], xa.z, xb.z, xa.w, xb.w, v.z, v.w);
-      if (MT > 1) {
-        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-        mma_bf16_16816(A[1], x2.x, x3.x, x2.y, x3.y, v.x, v.y);
-        mma_bf16_16816(A[1], x2.z, x3.z, x2.w, x3.w, v.z, v.w);
-      }
-    }
-    if (Pd() & 31) {
-      uint32_t t0, t1;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t0), "=r"(t1) : "r"(ta + 4 * KB));
-      tmem_wait_ld();
-      const int o = KB * 64 - q * 8;
-      const uint2 x0 = lds64(ar0 + o), x1 = lds64(ar1 + o);
-      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, t0, t1);
-      if (MT > 1) {
-        const uint2 x2 = lds64(ar2 + o), x3 = lds64(ar3 + o);
-        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, t0, t1);
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[a][e] += acc2[a][e];
-  }
-
-  // W_pred tile j (resident in shared memory, packed + swizzled like the stream)
-  template <bool HI>
-  __device__ __forceinline__ void smem_tile_mma(float (&acc)[2][4], int j, int MT, const uint8_t *ar0,
-                                                const uint8_t *ar1, const uint8_t *ar2, const uint8_t *ar3) const {
-    const uint8_t *brow = ringslot(j) + (size_t)g * Pd() * 2;
-    const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
+  // Gate GEMM of W_hh tile pair pp against NB groups of 8 predictor rows, as
+  // m16n8k16 MMAs with the WEIGHTS as the A operand (16 gate rows: half 0 ->
+  // rows 0-7, half 1 -> rows 8-15) and h as the B operand (8 rows per group),
+  // so one MMA covers 16 gate rows of <= 8 predictor rows.  A fragments come
+  // from TMEM (tcgen05.ld, both halves of a 4-block chunk, one wait), B
+  // fragments from shared memory (one 16-byte load per row and K block, the K
+  // permutation of common.cuh).  Two accumulator chains over K, summed by the
+  // caller in a fixed order.
+  template <int NB>
+  __device__ __forceinline__ void gates_pair(float (&acc)[NB][2][4], int pp, const uint8_t *const *hrow) const {
     const int KB = Pd() / 32;
-#pragma unroll 4
-    for (int kb = 0; kb < KB; ++kb) {
-      const uint4 b = lds128(brow + (((kb * 4 + q) ^ sw) * 16));
-      const uint4 x0 = lds128(ar0 + kb * 64);
-      const uint4 x1 = HI ? lds128(ar1 + kb * 64) : make_uint4(0, 0, 0, 0);
-      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-      mma_bf16_16816(acc[0], x0.z, x1.z, x0.w, x1.w, b.z, b.w);
-      if (MT > 1) {
-        const uint4 x2 = lds128(ar2 + kb * 64), x3 = lds128(ar3 + kb * 64);
-        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
-        mma_bf16_16816(acc[1], x2.z, x3.z, x2.w, x3.w, b.z, b.w);
+    const uint32_t ta0 = pair_taddr(pp, 0), ta1 = pair_taddr(pp, 1);
+#pragma unroll 1
+    for (int c4 = 0; c4 < KB; c4 += 4) {
+      uint32_t r0[16], r1[16];
+      if (c4 + 4 <= KB) {
+        tmem_ld16(ta0 + 4 * c4, r0);
+        tmem_ld16(ta1 + 4 * c4, r1);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (c4 + u < KB) {
+            uint4 v0, v1;
+            tmem_ld4(ta0 + 4 * (c4 + u), v0);
+            tmem_ld4(ta1 + 4 * (c4 + u), v1);
+            r0[4 * u] = v0.x; r0[4 * u + 1] = v0.y; r0[4 * u + 2] = v0.z; r0[4 * u + 3] = v0.w;
+            r1[4 * u] = v1.x; r1[4 * u + 1] = v1.y; r1[4 * u + 2] = v1.z; r1[4 * u + 3] = v1.w;
+          }
+        }
+      }
+      tmem_wait_ld();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kb = c4 + u;
+        if (kb < KB) {
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const uint4 x = lds128(hrow[nb] + kb * 64);
+            mma_bf16_16816(acc[nb][u & 1], r0[4 * u], r1[4 * u], r0[4 * u + 1], r1[4 * u + 1], x.x, x.y);
+            mma_bf16_16816(acc[nb][u & 1], r0[4 * u + 2], r1[4 * u + 2], r0[4 * u + 3], r1[4 * u + 3], x.z, x.w);
+          }
+        }
       }
     }
-    if (Pd() & 31) {
-      const int o = KB * 64 - q * 8;
-      const uint2 b = lds64(brow + KB * 64 + q * 8);
-      const uint2 x0 = lds64(ar0 + o), x1 = lds64(ar1 + o);
-      mma_bf16_16816(acc[0], x0.x, x1.x, x0.y, x1.y, b.x, b.y);
-      if (MT > 1) {
-        const uint2 x2 = lds64(ar2 + o), x3 = lds64(ar3 + o);
-        mma_bf16_16816(acc[1], x2.x, x3.x, x2.y, x3.y, b.x, b.y);
+    if (Pd() & 31) {   // 16-wide K tail: lane q owns columns [4q, 4q + 4) of the block
+      uint32_t t0, t1, t2, t3;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t0), "=r"(t1) : "r"(ta0 + 4 * KB));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t2), "=r"(t3) : "r"(ta1 + 4 * KB));
+      tmem_wait_ld();
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const uint2 x = lds64(hrow[nb] + KB * 64 - q * 8);
+        mma_bf16_16816(acc[nb][0], t0, t2, t1, t3, x.x, x.y);
+      }
+    }
+  }
+
+  // W_pred part of the predictor: partial g = W_pred[this CTA's rows, K blocks
+  // of this warp] h' for NB groups of 8 rows.  A = W_pred m-tiles (tiles 2t,
+  // 2t+1 of the resident smem copy, rows >= DPC read as zero), B = h' rows.
+  // K blocks are split over the warps: warp w takes kb = w, w + NW, ... (and
+  // warp 0 the 16-wide tail).
+  template <int NB>
+  __device__ __forceinline__ void wpred_partial(float (&acc)[3][NB][4], const uint8_t *const *hrow) const {
+    const int KB = Pd() / 32, NPT = npt();
+    const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) acc[t][nb][0] = acc[t][nb][1] = acc[t][nb][2] = acc[t][nb][3] = 0.f;
+    for (int kb = warp; kb < KB; kb += NW) {
+      uint4 x[NB];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) x[nb] = lds128(hrow[nb] + kb * 64);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        if (2 * t < NPT) {
+          const uint32_t co = (uint32_t)(((kb * 4 + q) ^ sw) * 16);
+          const uint4 wa = lds128(ringslot(2 * t) + (size_t)g * Pd() * 2 + co);
+          const uint4 wb = 2 * t + 1 < NPT ? lds128(ringslot(2 * t + 1) + (size_t)g * Pd() * 2 + co)
+                                           : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            mma_bf16_16816(acc[t][nb], wa.x, wb.x, wa.y, wb.y, x[nb].x, x[nb].y);
+            mma_bf16_16816(acc[t][nb], wa.z, wb.z, wa.w, wb.w, x[nb].z, x[nb].w);
+          }
+        }
+      }
+    }
+    if ((Pd() & 31) && warp == 0) {
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        if (2 * t < NPT) {
+          const uint2 wa = lds64(ringslot(2 * t) + (size_t)g * Pd() * 2 + KB * 64 + q * 8);
+          const uint2 wb = 2 * t + 1 < NPT ? lds64(ringslot(2 * t + 1) + (size_t)g * Pd() * 2 + KB * 64 + q * 8)
+                                           : make_uint2(0, 0);
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const uint2 x = lds64(hrow[nb] + KB * 64 - q * 8);
+            mma_bf16_16816(acc[t][nb], wa.x, wb.x, wa.y, wb.y, x.x, x.y);
+          }
+        }
       }
     }
   }
@@ -907,25 +924,97 @@ struct Ctx {
     }
   }
 
+  // Gate epilogue for n8 row group nb of pair pp: the two chains summed, gates
+  // of a unit paired across lanes g and g ^ 1 (one shuffle each way), the cell
+  // update (PyTorch LSTM, reading A9) for predictor row 8nb + 2q (even g) or
+  // 8nb + 2q + 1 (odd g): c' = s(f) c + s(i) tanh(g), h' = s(o) tanh(c').
+  __device__ __forceinline__ void gate_epilogue(const float (&a)[2][4], int pp, int nb, int n) const {
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = a[0][e] + a[1][e];
+    const bool ev = (g & 1) == 0;
+    // even g holds (i, g) of rows 2q, 2q+1; odd g holds (f, o)
+    const float r0 = __shfl_xor_sync(0xffffffffu, ev ? v[1] : v[0], 4);
+    const float r1 = __shfl_xor_sync(0xffffffffu, ev ? v[3] : v[2], 4);
+    const int i = 8 * nb + 2 * q + (ev ? 0 : 1);
+    if (i < n) {
+      const int ul = 4 * pp + (g >> 1);                 // unit within this CTA's slice
+      const float *ep = es() + (size_t)i * 4 * L.UPC + ul;
+      const float gi = (ev ? v[0] : r0) + ep[0];
+      const float gf = (ev ? r0 : v[1]) + ep[L.UPC];
+      const float gg = (ev ? v[2] : r1) + ep[2 * L.UPC];
+      const float go = (ev ? r1 : v[3]) + ep[3 * L.UPC];
+      const int s = rs.plist[i];
+      float *cp = cs() + (size_t)s * L.UPC + ul;
+      const float cn = sigmoidf_(gf) * *cp + sigmoidf_(gi) * tanhf(gg);
+      *cp = cn;
+      reinterpret_cast<bf16 *>(hsrow(rs.hpar[s] ^ 1, s))[u0 + ul] = __float2bfloat16_rn(sigmoidf_(go) * tanhf(cn));
+    }
+  }
+
+  // Gate GEMM + epilogue for row groups nb0 .. nb0 + NB - 1 (NB <= 2 per pass
+  // keeps the accumulators and both TMEM fragments in registers).
+  template <int NB>
+  __device__ __forceinline__ void gates_all(int n, int nb0, bool &e_ready) {
+    const uint8_t *hrow[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int i = 8 * (nb0 + nb) + g;
+      const int s = rs.plist[i < n ? i : 0];
+      hrow[nb] = hsrow(rs.hpar[s], s) + q * 16;
+    }
+    for (int pp = warp; pp < npairs(); pp += NW) {
+      float acc[NB][2][4];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) acc[nb][c][0] = acc[nb][c][1] = acc[nb][c][2] = acc[nb][c][3] = 0.f;
+      gates_pair<NB>(acc, pp, hrow);
+      if (pp == warp && nb0 == 0) tl_pred(1);
+      if (!e_ready) {
+        mbar_wait(bar(BAR_E), hph & 1u);
+        e_ready = true;
+      }
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) gate_epilogue(acc[nb], pp, nb0 + nb, n);
+    }
+  }
+
+  // Partial W_pred products of NB row groups (rows 8*nb0 ...) -> shared memory
+  // (the z region, idle during the predictor): wpart[warp][t][nb][lane][4].
+  template <int NB>
+  __device__ __forceinline__ void wpred_store(int nb0, int n) {
+    const uint8_t *hrow[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int i = 8 * (nb0 + nb) + g;
+      const int s = rs.plist[i < n ? i : 0];
+      hrow[nb] = hsrow(rs.hpar[s] ^ 1, s) + q * 16;
+    }
+    float acc[3][NB][4];
+    wpred_partial<NB>(acc, hrow);
+    float4 *wp = reinterpret_cast<float4 *>(zs());
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+        wp[((warp * 3 + t) * 2 + nb) * 32 + lane] = make_float4(acc[t][nb][0], acc[t][nb][1], acc[t][nb][2],
+                                                                acc[t][nb][3]);
+  }
+
   __device__ void predictor_lstm_tmem() {
     tl_pred(0);
-    const int n = rs.npred, MT = (n + 15) / 16;
-    const int P = Pd(), H = Hd(), NG = ng(), NPT = npt();
+    const int n = rs.npred;
+    const int P = Pd(), H = Hd();
 
     // arm the h' / g exchange barriers for this step (tx from the other CTAs)
     if (tid == 0 && C > 1) {
       mbar_arrive_expect_tx(bar(BAR_H), (uint32_t)((C - 1) * n * L.UPC * 2));
       mbar_arrive_expect_tx(bar(BAR_G), (uint32_t)((C - 1) * n * L.DPC * 4));
     }
-    // A rows: h of the predictor rows (row i -> slot plist[i]); pad rows reuse row 0
-    auto arow = [&](int i, int hpx) -> const uint8_t * {
-      const int s = rs.plist[i < n ? i : 0];
-      return hsrow(hpx ? (rs.hpar[s] ^ 1) : rs.hpar[s], s) + q * 16;
-    };
-    const uint8_t *ar0 = arow(g, 0), *ar1 = arow(g + 8, 0), *ar2 = arow(g + 16, 0), *ar3 = arow(g + 24, 0);
     // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units.
     // E'[y_i] slices of this CTA's units (4 gates x UPC floats per row) are
-    // staged into shared memory by bulk copies that overlap the first tiles.
+    // staged into shared memory by bulk copies that overlap the gate GEMM.
     if (warp == 0) {
       const uint32_t segb = (uint32_t)(L.UPC * 4);
       if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)(4 * n) * segb);
@@ -937,49 +1026,14 @@ struct Ctx {
                  segb, bar(BAR_E));
       }
     }
-    const bool hi = n > 8;
-    bool e_ready = false;
-    for (int j = warp; j < NG; j += NW) {
-      const int unit = u0 + 2 * j + (q >> 1);
-      const int gate0 = (q & 1) * 2;  // q even: (i, f); q odd: (g, o)
-      float acc[2][4];
-#pragma unroll
-      for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-      if (hi) tmem_mma<true>(acc, j, MT, ar0, ar1, ar2, ar3);
-      else tmem_mma<false>(acc, j, MT, ar0, ar1, ar2, ar3);
-      if (j == warp) tl_pred(1);
-      if (!e_ready) {
-        mbar_wait(bar(BAR_E), hph & 1u);
-        e_ready = true;
+    {
+      bool e_ready = false;
+      for (int nb0 = 0; nb0 * 8 < n; nb0 += 2) {
+        if (n - nb0 * 8 > 8) gates_all<2>(n, nb0, e_ready);
+        else gates_all<1>(n, nb0, e_ready);
       }
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        if (mt >= MT) break;
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const int i = mt * 16 + g + rr * 8;
-          const bool valid = i < n;
-          float e0 = 0.f, e1 = 0.f;
-          if (valid) {
-            const float *ep = es() + (size_t)i * 4 * L.UPC + (unit - u0);
-            e0 = ep[(size_t)gate0 * L.UPC];
-            e1 = ep[(size_t)(gate0 + 1) * L.UPC];
-          }
-          const float v0 = acc[mt][rr * 2 + 0] + e0, v1 = acc[mt][rr * 2 + 1] + e1;
-          const float o0 = __shfl_xor_sync(0xffffffffu, v0, 1);
-          const float o1 = __shfl_xor_sync(0xffffffffu, v1, 1);
-          if (valid && (q & 1) == 0) {
-            const int s = rs.plist[i];
-            const float ig = sigmoidf_(v0), fg = sigmoidf_(v1), gg = tanhf(o0), og = sigmoidf_(o1);
-            float *cp = cs() + (size_t)s * L.UPC + (unit - u0);
-            const float cn = fg * *cp + ig * gg;
-            *cp = cn;
-            reinterpret_cast<bf16 *>(hsrow(rs.hpar[s] ^ 1, s))[unit] = __float2bfloat16_rn(og * tanhf(cn));
-          }
-        }
-      }
+      if (!e_ready) mbar_wait(bar(BAR_E), hph & 1u);  // keep every thread's view of the phase in step
     }
-    if (!e_ready) mbar_wait(bar(BAR_E), hph & 1u);  // keep every thread's view of the phase in step
     tl_pred(2);
     // (2) exchange the h' slices (this CTA's units) with every CTA
     sync();
@@ -995,34 +1049,50 @@ struct Ctx {
       mbar_wait(bar(BAR_H), hph & 1u);
     }
     tl_pred(4);
-    const uint8_t *br0 = arow(g, 1), *br1 = arow(g + 8, 1), *br2 = arow(g + 16, 1), *br3 = arow(g + 24, 1);
-    // (3) g = W_pred h' + b_pred for this CTA's output dims
-    for (int j = warp; j < NPT; j += NW) {
-      float acc[2][4];
+    // (3) g = W_pred h' + b_pred for this CTA's output dims: K split over the
+    // warps (partials in shared memory), then one thread per (row, 4 dims)
+    // sums the partials in a fixed warp order, adds the bias, stores g locally
+    // and st.async's it to every other CTA (completing tx on their BAR_G).
+    const uint32_t bg = smem_u32(bar(BAR_G));
+    for (int nb0 = 0; nb0 * 8 < n; nb0 += 2) {
+      if (n - nb0 * 8 > 8) wpred_store<2>(nb0, n);
+      else wpred_store<1>(nb0, n);
+      sync();
+      const int nrows = min(16, n - nb0 * 8);
+      const int D4 = L.DPC / 4;
+      const float4 *wp = reinterpret_cast<const float4 *>(zs());
+      for (int idx = tid; idx < nrows * D4; idx += NCT) {
+        const int ii = idx / D4, d = (idx % D4) * 4;    // row within the pass, first of 4 dims
+        const int i = nb0 * 8 + ii, nb = ii >> 3, il = ii & 7;
+        const int t = d >> 4, hi = (d >> 3) & 1, gq = d & 7, qq = il >> 1, e = hi * 2 + (il & 1);
+        float out[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) acc[a][0] = acc[a][1] = acc[a][2] = acc[a][3] = 0.f;
-      if (hi) smem_tile_mma<true>(acc, j, MT, br0, br1, br2, br3);
-      else smem_tile_mma<false>(acc, j, MT, br0, br1, br2, br3);
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        if (mt >= MT) break;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int i = mt * 16 + g + (e >> 1) * 8;
-          const int d = d0 + j * 8 + 2 * q + (e & 1);
-          if (i < n) gs()[(size_t)rs.plist[i] * H + d] = acc[mt][e] + __bfloat162float(((const bf16 *)p.b_pred)[d]);
+        for (int j = 0; j < 4; ++j) {
+          const int ln = (gq + j) * 4 + qq;
+          float acc = 0.f;
+          for (int w = 0; w < NW; ++w) {
+            const float *f4 = reinterpret_cast<const float *>(wp + ((w * 3 + t) * 2 + nb) * 32 + ln);
+            acc += f4[e];
+          }
+          out[j] = acc + __bfloat162float(((const bf16 *)p.b_pred)[d0 + d + j]);
+        }
+        const int s = rs.plist[i];
+        float *dst = gs() + (size_t)s * H + d0 + d;
+        *reinterpret_cast<float4 *>(dst) = make_float4(out[0], out[1], out[2], out[3]);
+        const uint64_t lo = ((uint64_t)__float_as_uint(out[1]) << 32) | __float_as_uint(out[0]);
+        const uint64_t hi2 = ((uint64_t)__float_as_uint(out[3]) << 32) | __float_as_uint(out[2]);
+        const uint32_t la = smem_u32(dst);
+        for (int c = 1; c < C; ++c) {
+          const uint32_t dr = (uint32_t)((rank + c) % C);
+          st_async_u64x2(mapa_u32(la, dr), lo, hi2, mapa_u32(bg, dr));
         }
       }
+      sync();   // partial buffer reused by the next pass
     }
-
-    tl_pred(5);
-    // (4) exchange the g slices
-    sync();
+    tl_pred_bar(5);
     tl_pred_bar(6);
-    if (C > 1) {
-      bcast_rows((const uint8_t *)gs(), H * 4, d0 * 4, L.DPC * 4, n, rs.plist, BAR_G);
-      mbar_wait(bar(BAR_G), hph & 1u);
-    }
+    // (4) the other CTAs' g slices
+    if (C > 1) mbar_wait(bar(BAR_G), hph & 1u);
     hph ^= 1u;
     if (warp == 0 && lane < n) {
       const int s = rs.plist[lane];
@@ -1186,11 +1256,12 @@ struct Ctx {
 };
 
 // ---------------------------------------------------------------------------
-// Pack the bf16 LSTM weights into the per-CTA tile stream read by the producer
-// warp: for cluster rank r, tiles n < NG are W_hh rows {gate*P + r*UPC + 2n + c/4 :
-// gate = c%4} (c < 8), tiles NG + k are W_pred rows r*DPC + 8k + c.  Rows are
-// stored unpadded; in odd rows the 16-byte chunk j is stored at j ^ 4 (the
-// bank swizzle undone by ring_mma).  One thread per 16-byte chunk.
+// Pack the bf16 LSTM weights into the per-CTA tile stream: for cluster rank r,
+// tiles n < NG are W_hh tile pairs (n = 2 * pair + half): row c is unit
+// r*UPC + 4*pair + c/2, gate 2*half + (c & 1) (gate order i, f, g, o); tiles
+// NG + k are W_pred rows r*DPC + 8k + c.  Rows are stored unpadded; in odd rows
+// the 16-byte chunk j is stored at j ^ 4 (bank swizzle).  One thread per
+// 16-byte chunk.
 // ---------------------------------------------------------------------------
 __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst, int P, int C, int UPC, int DPC) {
   const int NG = UPC / 2, NPT = DPC / 8, NT = NG + NPT;
@@ -1203,7 +1274,7 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
     const int n = (int)((rowid / 8) % NT);
     const int r = (int)(rowid / (8 * NT));
     const bf16 *src;
-    if (n < NG) src = w_hh + ((size_t)(c & 3) * P + r * UPC + 2 * n + (c >> 2)) * P;
+    if (n < NG) src = w_hh + ((size_t)(2 * (n & 1) + (c & 1)) * P + r * UPC + 4 * (n >> 1) + (c >> 1)) * P;
     else src = w_pred + (size_t)(r * DPC + 8 * (n - NG) + c) * P;
     const int jd = (c & 1) && (P % 64) == 0 ? (j ^ 4) : j;
     reinterpret_cast<uint4 *>(wst + (size_t)rowid * P)[jd] = reinterpret_cast<const uint4 *>(src)[j];

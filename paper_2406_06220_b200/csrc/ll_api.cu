@@ -125,9 +125,12 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
     if (bf) {
       if (H % (8 * C)) continue;
       if (lstm && P % (8 * C)) continue;             // h' slice: whole 16-byte chunks
-      if (ring) {                                    // W_hh tiles of a CTA must fit TMEM (512 columns)
-        const int NG = P / C / 2, tcols = 4 * (P / 32) + ((P & 31) ? 2 : 0);
-        if ((NG + 3) / 4 * tcols > 512) continue;
+      if (ring) {
+        // W_hh tile pairs of a CTA must fit TMEM (512 columns): warp w holds
+        // 2 * ceil(pairs / NW) tiles in lane quarter w % 4, shared by <= 3 warps
+        const int pairs = P / C / 4, tcols = 4 * (P / 32) + ((P & 31) ? 2 : 0);
+        if (2 * ((pairs + MAX_NW - 1) / MAX_NW) * 3 * tcols > 512) continue;
+        if (H / C > 48) continue;                    // W_pred: <= 3 m16 tiles per CTA
       }
     } else {
       if (H % C) continue;
