@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="fc-rnnt", choices=list(synth.CONFIGS))
+    ap.add_argument("--config", default="fc-rnnt", choices=list(synth.CONFIGS) + list(synth.SWEEPS))
+    ap.add_argument("--chunk", type=int, default=1024, help="sweep: utterances per decode launch")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--family", default="planted", choices=["planted", "random"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -172,10 +173,26 @@ def _limit_threads():
         pass
 
 
+def sweep_sample(cfg_name, n):
+    """The first n utterances (by id) of a sweep workload: (spec, w, enc, lengths)."""
+    c = synth.SWEEPS[cfg_name]
+    spec = c["spec"]
+    w, codes = synth.planted_weights(spec, 1000)
+    L = synth.sweep_lengths(c["length_seed"], c["n_utt"])[:n]
+    T = int(L.max())
+    enc = np.zeros((n, T, spec.enc_dim), dtype=np.float32)
+    for u in range(n):
+        enc[u, :L[u]] = synth.planted_utterance(spec, codes, c["length_seed"], u, int(L[u]))[0]
+    return spec, w, enc, L.astype(np.int32)
+
+
 def run_reference(a, rank, world):
     if rank != 0:
         return
-    spec, w, enc, lengths = workload(a.config, 1000, a.family)
+    if a.config in synth.SWEEPS:
+        spec, w, enc, lengths = sweep_sample(a.config, a.cpu_sample or 64)
+    else:
+        spec, w, enc, lengths = workload(a.config, 1000, a.family)
     n = a.cpu_sample or enc.shape[0]
     times = []
     for i in range(a.warmup + a.steps):
@@ -214,6 +231,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    if a.config in synth.SWEEPS:
+        return run_sweep(a, rank, world, local, dev)
 
     spec, w, enc_np, len_np = workload(a.config, 1000 + rank, a.family)
     B, T = enc_np.shape[0], enc_np.shape[1]
@@ -349,6 +368,138 @@ def main():
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
                                 "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch, "
                                           f"{dt:.1f} s wall"}
+    clocks = clk.summary()
+    if clocks:
+        line["clocks"] = clocks
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_sweep(a, rank, world, local, dev):
+    """BASELINE config (5): 8192 utterances with LibriSpeech-like lengths,
+    length-bucketed into batches of 32 and assigned to ranks by LPT
+    (paper_2406_06220_b200.shard); each rank decodes its shard longest-first in
+    launches of `--chunk` utterances (one stream, no host sync between them),
+    packs its ragged hypotheses on the device, and the hypotheses are gathered
+    over NCCL (the only collective).  A step = the whole sweep, gather included."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_06220_b200 import ll, shard
+    from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
+
+    c = synth.SWEEPS[a.config]
+    spec = c["spec"]
+    tdt = spec.is_tdt
+    w, codes = synth.planted_weights(spec, 1000)
+    L_all = synth.sweep_lengths(c["length_seed"], c["n_utt"])
+    ids = shard.rank_shard(L_all, world, rank, c["batch"])
+    model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16", device=f"cuda:{local}")
+    # inputs: planted utterances (each from its own seeded stream), laid out per
+    # chunk as [B_c, T_c, D_e] bf16 on the device; the ragged frames are also
+    # kept in pinned host memory for the end-to-end leg
+    chunks, planted = [], {}
+    for c0 in range(0, len(ids), a.chunk):
+        cid = ids[c0:c0 + a.chunk]
+        Lc = L_all[cid]
+        T = int(Lc.max())
+        enc = torch.zeros(len(cid), T, spec.enc_dim, dtype=torch.bfloat16, device=dev)
+        host = []
+        for i, u in enumerate(cid):
+            e, pl = synth.planted_utterance(spec, codes, c["length_seed"], int(u), int(L_all[u]))
+            planted[int(u)] = pl
+            eh = torch.from_numpy(e).to(torch.bfloat16)
+            host.append(eh)
+            enc[i, :e.shape[0]] = eh.to(dev)
+        frames = torch.cat(host).pin_memory()
+        rows = torch.cat([torch.arange(int(l), device=dev) + i * T for i, l in enumerate(Lc)])
+        chunks.append(dict(ids=torch.from_numpy(cid).to(dev), enc=enc, lengths=torch.from_numpy(Lc.astype(np.int32)).to(dev),
+                           dec=LabelLoopingDecoder(model, spec.max_symbols, len(cid), T), frames=frames, rows=rows))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step(e2e=False):
+        for ch in chunks:
+            if e2e:   # H2D of the chunk's ragged frames, scattered into the padded layout
+                dst = ch["enc"].view(-1, spec.enc_dim)
+                dst.index_copy_(0, ch["rows"], ch["frames"].to(dev, non_blocking=True))
+            s = ch["dec"].launch(ch["enc"], ch["lengths"])
+            if s != ll.LL_OK:
+                raise ll.LLError(s, "decode")
+        packed = shard.pack_hypotheses([ch["ids"] for ch in chunks], [ch["dec"].lengths_out for ch in chunks],
+                                       [ch["dec"].tokens for ch in chunks], [ch["dec"].timestamps for ch in chunks],
+                                       [ch["dec"].durs for ch in chunks] if tdt else None)
+        bufs = shard.gather_ragged(packed, tdt, unpack=False) if world > 1 else [packed]
+        if e2e and bufs is not None:   # D2H of the gathered hypotheses
+            return [b.cpu() for b in bufs]
+        return bufs
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    for ch in chunks:
+        if ch["dec"].sync() != ll.LL_OK:
+            raise RuntimeError("sweep decode failed")
+    # correctness of the sweep: every utterance of this shard equals its planted alignment
+    bad = 0
+    for ch in chunks:
+        hy = ch["dec"]
+        n = ch["ids"].numel()
+        tok, ts, ln = hy.tokens[:n].cpu(), hy.timestamps[:n].cpu(), hy.lengths_out[:n].cpu()
+        du = hy.durs[:n].cpu() if tdt else None
+        for i, u in enumerate(ch["ids"].cpu().tolist()):
+            k = int(ln[i])
+            got = (tok[i, :k].tolist(), ts[i, :k].tolist()) + ((du[i, :k].tolist(),) if tdt else ())
+            bad += got != tuple(planted[u])
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            ev0[i].record(stream)
+            step()
+            ev1[i].record(stream)
+        torch.cuda.synchronize()
+    ms = [ev0[i].elapsed_time(ev1[i]) for i in range(a.steps)]
+    e2e_ms, d2h = [], 0
+    for i in range(a.steps):
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        got = step(e2e=True)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        d2h = sum(b.numel() * 4 for b in got) if got is not None else 0
+    t_all = torch.tensor([sum(ms), sum(e2e_ms), float(bad)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+    tot_ms, e2e_tot, bad_max = float(t_all[0]), float(t_all[1]), int(t_all[2])
+    audio_s = float(L_all.sum()) * synth.frame_seconds
+    n_utt = int(c["n_utt"])
+    value = a.steps * audio_s / (tot_ms / 1e3)
+    h2d = sum(ch["frames"].numel() * 2 + ch["lengths"].numel() * 4 for ch in chunks)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": a.config, "family": "planted", "utterances": n_utt, "batch": c["batch"],
+                   "chunk": a.chunk, "frames": int(L_all.sum()), "audio_s_per_step": audio_s,
+                   "l2": "flushed (512 MiB) between steps", "parallelism": f"LPT length-bucketed x{world}, NCCL gather"},
+        "utterances_per_s": a.steps * n_utt / (tot_ms / 1e3),
+        "e2e": {"value": a.steps * audio_s / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_tot / a.steps},
+        "gpu_launches": a.steps * len(chunks) * (3 if spec.pred_kind == "lstm" else 2 + spec.context),
+        "hypotheses_equal_planted": bad_max == 0,
+    }
     clocks = clk.summary()
     if clocks:
         line["clocks"] = clocks

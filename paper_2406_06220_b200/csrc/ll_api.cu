@@ -21,7 +21,8 @@ using namespace ll;
 
 namespace {
 
-constexpr size_t HDR_BYTES = 4096;  // [0] status, [1] group counter, [16..] stats (u64 x 8 at byte 64)
+constexpr size_t HDR_BYTES = 4096;
+constexpr int RPREF_MANY = 7;       // rows per group when the batch spans many waves (measured)  // [0] status, [1] group counter, [16..] stats (u64 x 8 at byte 64)
 constexpr size_t SMEM_LIMIT = 232448;
 
 struct Ws {
@@ -116,6 +117,10 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
   if (bf && H > KREG * 32 + 16) return false;        // joint slice must fit the register tile
   const int ncl = nclusters > 0 ? nclusters : 8;
   int Rpref = forceR ? forceR : (B + ncl - 1) / ncl;
+  // throughput mode: when one wave would need more than 8 rows per group, run
+  // many waves of small groups instead (groups are taken from a work counter,
+  // so the clusters stay busy; small groups keep the multi-frame window wide)
+  if (!forceR && Rpref > 8) Rpref = RPREF_MANY;
   if (Rpref < 1) Rpref = 1;
   if (Rpref > MAX_R) Rpref = MAX_R;
   for (int C = 1; C <= MAX_C; C *= 2) {

@@ -27,7 +27,7 @@ __all__ = [
     "ModelSpec", "bf16_round", "make_weights", "make_inputs", "make_planted_rnnt",
     "make_planted_tdt", "cat_dog_fixture", "tdt_forced_fixture", "guard_after_blank_fixture",
     "guard_after_blank_tdt_fixture", "CONFIGS",
-    "sweep_lengths", "frame_seconds",
+    "sweep_lengths", "frame_seconds", "planted_weights", "planted_utterance", "SWEEPS",
 ]
 
 frame_seconds = 0.08  # 8x subsampling of 10 ms frames
@@ -285,6 +285,62 @@ def make_planted_tdt(spec: ModelSpec, seed: int, B: int, T_max: int, len_lo: int
     return ({k: bf16_round(v) for k, v in w.items()}, bf16_round(enc), lengths, planted)
 
 
+def planted_weights(spec: ModelSpec, seed: int):
+    """The planted-family weights alone (RNN-T or TDT), identical to the ones
+    make_planted_rnnt / make_planted_tdt return for the same seed."""
+    nD = len(spec.durations) if spec.is_tdt else 0
+    rng, w, codes, nd = _planted_base(spec, seed, nD)
+    if spec.is_tdt:
+        dur0 = 1 + _CODE_DIMS
+        w["w_dur"][:, :nd] = 0.0
+        w["b_dur"][:] = 0.0
+        for i in range(nD):
+            w["w_dur"][i, dur0 + i] = 4.0
+        w["w_out"][:, dur0:dur0 + nD] = 0.0
+    return {k: bf16_round(v) for k, v in w.items()}, codes
+
+
+def planted_utterance(spec: ModelSpec, codes, seed: int, uid: int, L: int, rho: float = 0.28,
+                      p_token: float = 0.55, token_dur_p=(0.45, 0.30, 0.15, 0.10),
+                      blank_dur_p=(0.2, 0.3, 0.3, 0.2)):
+    """One planted utterance of the sweep workload (BASELINE config 5), drawn
+    from its own seeded stream (seed, uid) so that any subset of a large sweep
+    can be regenerated independently.  Same planted recipe as
+    make_planted_rnnt / make_planted_tdt.  Returns (enc [L, D_e] bf16-rounded
+    float32, planted alignment)."""
+    rng = np.random.Generator(np.random.PCG64([seed, uid]))
+    nD = len(spec.durations) if spec.is_tdt else 0
+    nd = 1 + _CODE_DIMS + nD
+    enc = rng.normal(0.0, 1.0, size=(L, spec.enc_dim)).astype(np.float32)
+    enc[:, :nd] = 0.0
+    if not spec.is_tdt:
+        enc[:, 0] = 1.0
+        frames = [t for t in range(L) if rng.random() < rho]
+        toks = _planted_tokens(rng, len(frames), spec.num_tokens, spec.blank_id, codes)
+        for t, y in zip(frames, toks):
+            enc[t, 0] = -1.0
+            enc[t, 1:1 + _CODE_DIMS] = codes[y]
+        return bf16_round(enc), (toks, frames)
+    D = list(spec.durations)
+    dur0 = 1 + _CODE_DIMS
+    t, prev = 0, None
+    toks, stamps, durs = [], [], []
+    while t < L:
+        is_tok = rng.random() < p_token
+        d = int(rng.choice([1, 2, 3, 4], p=token_dur_p if is_tok else blank_dur_p))
+        enc[t, dur0 + D.index(d)] = 1.0
+        if is_tok:
+            y = _planted_tokens(rng, 1, spec.num_tokens, spec.blank_id, codes, prev)[0]
+            prev = y
+            enc[t, 0] = -1.0
+            enc[t, 1:1 + _CODE_DIMS] = codes[y]
+            toks.append(y); stamps.append(t); durs.append(d)
+        else:
+            enc[t, 0] = 1.0
+        t += d
+    return bf16_round(enc), (toks, stamps, durs)
+
+
 # ---------------------------------------------------------------------------
 # Paper worked example, Fig. 2 (PAPER.md:161-173): B=2, T=4, transcripts
 # "CAT" / "DOG", alignments  C b b A T b b  /  b D b b O G b.
@@ -410,4 +466,11 @@ CONFIGS = {
     # (4) large-batch stateless (context 2): B=512, lengths 50..1500, enc 1024
     "stateless-b512": dict(spec=ModelSpec(1025, 1024, 640, 640, "stateless", 2, None, 0, 10), B=512,
                            T_max=1500, len_lo=50, len_hi=1500),
+}
+
+# (5) batch-sharded sweep: 8192 utterances with LibriSpeech-like lengths (seed
+# 2024), FastConformer shapes, RNN-T and TDT; batches of 32.
+SWEEPS = {
+    "sweep-rnnt": dict(spec=CONFIGS["fc-rnnt"]["spec"], n_utt=8192, batch=32, length_seed=2024),
+    "sweep-tdt": dict(spec=CONFIGS["fc-tdt"]["spec"], n_utt=8192, batch=32, length_seed=2024),
 }
