@@ -29,20 +29,25 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + SOURCES
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """Build libll.so; variant="timeline" builds libll_timeline.so with the
+    per-warp clock64 timeline hooks compiled in (tools/timeline.py)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libll_{variant}.so")
+    if not force and os.path.exists(lib) and not any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS):
+        return lib
+    defs = {"": [], "timeline": ["-DLL_TIMELINE"], "trace": ["-DLL_DEBUG_TRACE"]}[variant]
+    cmd = [NVCC] + FLAGS + defs + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp"] + SOURCES
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libll.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    if not variant:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+            fh.write(r.stderr)
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

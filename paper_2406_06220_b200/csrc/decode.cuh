@@ -184,13 +184,23 @@ struct Ctx {
   int C, rank, tid, warp, lane, NW, NCT, g, q;
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
   int u0, d0;                 // LSTM units / W_pred output dims owned
-  int par;                    // partial-buffer parity
   int iw;                     // issuing warp for bulk copies (a warp without a joint tile if any)
-  uint32_t fph, fpend, xph;   // phase / pending bits (replicated in every consumer thread)
-  uint32_t hph;               // BAR_H / BAR_G / BAR_E phase
+  // Barrier phase bookkeeping, replicated in every consumer thread and packed
+  // into one register: bits 0-1 fph (BAR_F+X phase), 2-3 fpend (bulk copy into
+  // fbuf[X] outstanding), 4-5 xph (BAR_X+par phase), 6 hph (BAR_H/G/E phase),
+  // 7 par (partial-key buffer parity).
+  uint32_t phs;
+  __device__ __forceinline__ uint32_t fph(int X) const { return (phs >> X) & 1u; }
+  __device__ __forceinline__ uint32_t fpend(int X) const { return (phs >> (2 + X)) & 1u; }
+  __device__ __forceinline__ uint32_t xph(int X) const { return (phs >> (4 + X)) & 1u; }
+  __device__ __forceinline__ uint32_t hph() const { return (phs >> 6) & 1u; }
+  __device__ __forceinline__ int par() const { return (int)((phs >> 7) & 1u); }
+  __device__ __forceinline__ void flip_par() { phs ^= 1u << 7; }
   unsigned long long ntile_c; // weight-ring tiles consumed so far (replicated)
-  // optional timeline (LL_TIMELINE_PTR): clock64 of every warp at phase
-  // boundaries of the first TL_N rounds / predictor steps of block 0
+  // optional timeline (debug builds with -DLL_TIMELINE, buffer from
+  // LL_TIMELINE_PTR): clock64 of every warp at phase boundaries of the first
+  // TL_N rounds / predictor steps of block 0.  Compiled out of libll.so.
+#ifdef LL_TIMELINE
   unsigned long long *tl;
   int tl_round, tl_step;
   __device__ void tl_stamp(int area, int idx, int ph) const {
@@ -204,6 +214,19 @@ struct Ctx {
       if (v >= -1) tl_stamp(area, idx, ph);
     }
   }
+  __device__ void tl_init() {
+    tl_init();
+  }
+  __device__ void tl_next_round() { ++tl_round; }
+  __device__ void tl_next_step() { ++tl_step; }
+#else
+  __device__ __forceinline__ void tl_stamp(int, int, int) const {}
+  __device__ __forceinline__ void tl_stamp_bar(int, int, int) const {}
+  __device__ __forceinline__ void tl_init() {}
+  __device__ __forceinline__ void tl_next_round() {}
+  __device__ __forceinline__ void tl_next_step() {}
+  static constexpr int tl_round = 0, tl_step = 0;
+#endif
   __device__ void tl_round_(int ph) const { tl_stamp(0, tl_round, ph); }
   __device__ void tl_round_bar(int ph) const { tl_stamp_bar(0, tl_round, ph); }
   __device__ void tl_pred(int ph) const { tl_stamp(1, tl_step, ph); }
@@ -211,9 +234,8 @@ struct Ctx {
   uint4 wreg[KR];             // this warp's joint weight tile (bf16), K-permuted fragments
   uint2 wtail;
   __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm, uint64_t *bars_, Layout &sL)
-      : p(p_), L(sL), sm(sm_), rs(rs_), bars(bars_), fph(0), fpend(0), xph(0), hph(0), ntile_c(0) {
-    tl = (p.prof != nullptr && blockIdx.x == 0) ? p.prof : nullptr;
-    tl_round = tl_step = 0;
+      : p(p_), L(sL), sm(sm_), rs(rs_), bars(bars_), phs(0), ntile_c(0) {
+    tl_init();
     C = CC ? CC : (int)cluster_size();
     rank = (int)cluster_rank();
     if (threadIdx.x == 0) sL = make_layout(BF, lstm, Hd(), Pd(), p.V1, p.nD, p.R, p.W, p.WF, C, p.NS);
@@ -228,7 +250,6 @@ struct Ctx {
     tile0 = rank * base + (rank < rem ? rank : rem);
     u0 = rank * L.UPC;
     d0 = rank * L.DPC;
-    par = 0;
     iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
   }
   __device__ __forceinline__ int Hd() const { return HC ? HC : p.H; }
@@ -291,12 +312,12 @@ struct Ctx {
   // only warp 0 issues.  Caller guarantees nobody reads fbuf[X] meanwhile.
   // -------------------------------------------------------------------------
   __device__ void wait_f(int X) {
-    mbar_wait(bar(BAR_F + X), (fph >> X) & 1u);
-    fph ^= 1u << X;
-    fpend &= ~(1u << X);
+    mbar_wait(bar(BAR_F + X), fph(X));
+    phs ^= 1u << X;
+    phs &= ~(1u << (2 + X));
   }
   __device__ void issue_f(int X, bool spec) {
-    if ((fpend >> X) & 1u) wait_f(X);  // drain a stale speculative copy first
+    if (fpend(X)) wait_f(X);  // drain a stale speculative copy first
     const int n = rs.nscan;
     const uint32_t frb = (uint32_t)(Hd() * sizeof(T));
     if (warp == iw) {
@@ -323,7 +344,7 @@ struct Ctx {
         }
       }
     }
-    fpend |= 1u << X;
+    phs |= 1u << (2 + X);
   }
 
   // warp 0: the live joint rows of the round (window frames of scanning slots
@@ -579,10 +600,10 @@ struct Ctx {
   // of any other (it needs everyone's partials to leave a round).
   __device__ void exchange_keys() {
     const int nz = rs.nz;
-    if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par), (uint32_t)(C * nz * 16));
+    if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par()), (uint32_t)(C * nz * 16));
     sync();
     const uint64_t *wk = wkey();
-    uint64_t *pt = part(par);
+    uint64_t *pt = part(par());
     if (tid < nz) {
       const int jr = tid;                       // compact joint row
       uint64_t tkey = 0, dkey = 0;
@@ -595,7 +616,7 @@ struct Ctx {
         }
       }
       const uint32_t slot = smem_u32(pt + ((size_t)rank * L.JR + jr) * 2);
-      const uint32_t bb = smem_u32(bar(BAR_X + par));
+      const uint32_t bb = smem_u32(bar(BAR_X + par()));
       for (int d = 0; d < C; ++d) {
         const int dst = (rank + d) % C;
         st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, dkey, mapa_u32(bb, (uint32_t)dst));
@@ -603,13 +624,13 @@ struct Ctx {
     }
   }
   __device__ void exchange_wait() {
-    mbar_wait(bar(BAR_X + par), (xph >> par) & 1u);
-    xph ^= 1u << par;
+    mbar_wait(bar(BAR_X + par()), xph(par()));
+    phs ^= 1u << (4 + par());
   }
 
   // Final argmax of joint row jr from the C partials (after exchange_keys).
   __device__ void final_keys(int jr, int &y, int &di) const {
-    const uint64_t *pt = part(par);
+    const uint64_t *pt = part(par());
     uint64_t tkey = 0, dkey = 0;
 #pragma unroll
     for (int r = 0; r < MAX_C; ++r) {
@@ -630,7 +651,7 @@ struct Ctx {
   // PAPER.md:213).  decide() also rebuilds the scanning list and checks the
   // speculative window.
   __device__ void resolve_rows_w0() {
-    const uint64_t *pt = part(par);
+    const uint64_t *pt = part(par());
     const int nz = rs.nz;
     if (lane < nz) {
       uint64_t tkey = 0, dkey = 0;
@@ -972,7 +993,7 @@ struct Ctx {
       gates_pair<NB>(acc, pp, hrow);
       if (pp == warp && nb0 == 0) tl_pred(1);
       if (!e_ready) {
-        mbar_wait(bar(BAR_E), hph & 1u);
+        mbar_wait(bar(BAR_E), hph());
         e_ready = true;
       }
 #pragma unroll
@@ -1032,7 +1053,7 @@ struct Ctx {
         if (n - nb0 * 8 > 8) gates_all<2>(n, nb0, e_ready);
         else gates_all<1>(n, nb0, e_ready);
       }
-      if (!e_ready) mbar_wait(bar(BAR_E), hph & 1u);  // keep every thread's view of the phase in step
+      if (!e_ready) mbar_wait(bar(BAR_E), hph());  // keep every thread's view of the phase in step
     }
     tl_pred(2);
     // (2) exchange the h' slices (this CTA's units) with every CTA
@@ -1046,7 +1067,7 @@ struct Ctx {
       }
       sync();
       bcast_rows(sm + L.off_hs, L.hstride, u0 * 2, L.UPC * 2, n, rs.zsrc, BAR_H);
-      mbar_wait(bar(BAR_H), hph & 1u);
+      mbar_wait(bar(BAR_H), hph());
     }
     tl_pred(4);
     // (3) g = W_pred h' + b_pred for this CTA's output dims: K split over the
@@ -1092,15 +1113,15 @@ struct Ctx {
     tl_pred_bar(5);
     tl_pred_bar(6);
     // (4) the other CTAs' g slices
-    if (C > 1) mbar_wait(bar(BAR_G), hph & 1u);
-    hph ^= 1u;
+    if (C > 1) mbar_wait(bar(BAR_G), hph());
+    phs ^= 1u << 6;
     if (warp == 0 && lane < n) {
       const int s = rs.plist[lane];
       rs.hpar[s] ^= 1;
     }
     sync();
     tl_pred_bar(7);
-    ++tl_step;
+    tl_next_step();
   }
 
   // -------------------------------------------------------------------------
@@ -1317,6 +1338,9 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
 
   {
     int cur = 0;                  // f buffer of the current round
+#ifndef LL_DEBUG_TRACE
+#define LL_PHASE(k)
+#else
 #define LL_PHASE(k)                              \
   if (p.trace && tid == 0) {                     \
     p.trace[blockIdx.x * 8 + 0] = (k);           \
@@ -1325,8 +1349,10 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
     p.trace[blockIdx.x * 8 + 3] = (unsigned)k_grp;     \
     p.trace[blockIdx.x * 8 + 4] = (unsigned)rs.nz;     \
     p.trace[blockIdx.x * 8 + 5] = (unsigned)rs.nscan;  \
-    p.trace[blockIdx.x * 8 + 6] = cx.fph | (cx.fpend << 4) | (cx.xph << 8) | (cx.hph << 12) | ((unsigned)cur << 16); \
+    p.trace[blockIdx.x * 8 + 6] = cx.phs | ((unsigned)cur << 16); \
   }
+#endif
+
     int k = 0, k_grp = 0;
     for (;; ++k) {
       const int grp = cx.next_group(k);
@@ -1380,7 +1406,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         cx.rebuild_lists();
         cx.sync();
         // first window of every active row, overlapping the predictor phase
-        if ((cx.fpend >> cur) & 1u) cur ^= 1;
+        if (cx.fpend(cur)) cur ^= 1;
         cx.issue_f(cur, false);
         cx.sync();                     // fbase/fcnt (written by the issuing warp) visible to warp 0
         LL_PHASE(11);
@@ -1437,7 +1463,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             LL_PHASE(8);
             cx.tl_round_(9);
           }
-          cx.par ^= 1;
+          cx.flip_par();
           cx.sync();
           planned = false;
           if (rs.nscan > 0) {
@@ -1454,7 +1480,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
           }
           LL_PHASE(9);
           cx.tl_round_bar(10);
-          ++cx.tl_round;
+          cx.tl_next_round();
         }
         // ---- append + time rules + guard (BatchedHyps.add_results, :196-199) --
         if (warp == 0 && lane < R) {
@@ -1509,8 +1535,8 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
     }
     cx.final_acks(k);
     // drain outstanding f bulk copies before the CTA exits
-    if ((cx.fpend >> 0) & 1u) cx.wait_f(0);
-    if ((cx.fpend >> 1) & 1u) cx.wait_f(1);
+    if (cx.fpend(0)) cx.wait_f(0);
+    if (cx.fpend(1)) cx.wait_f(1);
     cx.sync();
 #undef LL_PHASE
     if (rank == 0 && tid == 0 && p.stats) {
@@ -1589,7 +1615,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __gri
       p.dbg_argmax[base + lane] = y;
       if (p.dbg_dargmax) p.dbg_dargmax[base + lane] = di;
     }
-    cx.par ^= 1;
+    cx.flip_par();
     __syncthreads();
   }
   if (C > 1) cluster_sync_all();  // no CTA exits while peers may still st.async into it

@@ -21,8 +21,8 @@ using namespace ll;
 
 namespace {
 
-constexpr size_t HDR_BYTES = 4096;
-constexpr int RPREF_MANY = 7;       // rows per group when the batch spans many waves (measured)  // [0] status, [1] group counter, [16..] stats (u64 x 8 at byte 64)
+constexpr size_t HDR_BYTES = 4096;  // [0] status, [1] group counter, [16..] stats (u64 x 8 at byte 64)
+constexpr int RPREF_MANY = 7;       // rows per group when the batch spans many waves (measured)
 constexpr size_t SMEM_LIMIT = 232448;
 
 struct Ws {

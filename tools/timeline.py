@@ -10,6 +10,9 @@ averaged over the recorded events."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+from paper_2406_06220_b200 import build as llbuild
+from paper_2406_06220_b200 import ll
+ll.LIB_PATH = llbuild.build(variant="timeline")   # timeline hooks compiled in
 TL_N, TL_PH, NW = 128, 16, 10
 buf = torch.zeros(2 * TL_N * TL_PH * NW, dtype=torch.int64, device="cuda")
 os.environ["LL_TIMELINE_PTR"] = str(buf.data_ptr())
