@@ -201,8 +201,8 @@ struct Ctx {
   // LL_TIMELINE_PTR): clock64 of every warp at phase boundaries of the first
   // TL_N rounds / predictor steps of block 0.  Compiled out of libll.so.
 #ifdef LL_TIMELINE
-  unsigned long long *tl;
-  int tl_round, tl_step;
+  unsigned long long *tl = nullptr;
+  int tl_round = 0, tl_step = 0;
   __device__ void tl_stamp(int area, int idx, int ph) const {
     if (tl != nullptr && idx < TL_N && lane == 0) tl[(((size_t)area * TL_N + idx) * TL_PH + ph) * MAX_NW + warp] = clock64();
   }
@@ -214,9 +214,7 @@ struct Ctx {
       if (v >= -1) tl_stamp(area, idx, ph);
     }
   }
-  __device__ void tl_init() {
-    tl_init();
-  }
+  __device__ void tl_init() { tl = (p.prof != nullptr && blockIdx.x == 0) ? p.prof : nullptr; }
   __device__ void tl_next_round() { ++tl_round; }
   __device__ void tl_next_step() { ++tl_step; }
 #else
@@ -388,7 +386,7 @@ struct Ctx {
       // one joint row per warp pass, up to 3 16-byte chunks per lane (H <= 768):
       // all shared loads of the row are issued before any store (the compiler
       // cannot prove that z does not alias f / g)
-      const int HC = H / 8;
+      const int NCH = H / 8;
       for (int k = warp; k < nz; k += NW) {
         const int s = rs.zdst[k] / W;
         const uint4 *frp = reinterpret_cast<const uint4 *>(fbuf(X)) + rs.zsrc[k] / 8;
@@ -399,7 +397,7 @@ struct Ctx {
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           const int c = lane + 32 * u;
-          if (c < HC) {
+          if (c < NCH) {
             fv[u] = frp[c];
             ga[u] = gr[2 * c];
             gb[u] = gr[2 * c + 1];
@@ -408,7 +406,7 @@ struct Ctx {
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           const int c = lane + 32 * u;
-          if (c < HC) {
+          if (c < NCH) {
             const uint4 f = fv[u];
             const float4 g0 = ga[u], g1 = gb[u];
             uint4 o;
@@ -1090,11 +1088,13 @@ struct Ctx {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int ln = (gq + j) * 4 + qq;
+          float part[MAX_NW];
+#pragma unroll
+          for (int w = 0; w < MAX_NW; ++w)   // all loads first, then a fixed-order sum
+            part[w] = w < NW ? reinterpret_cast<const float *>(wp + ((w * 3 + t) * 2 + nb) * 32 + ln)[e] : 0.f;
           float acc = 0.f;
-          for (int w = 0; w < NW; ++w) {
-            const float *f4 = reinterpret_cast<const float *>(wp + ((w * 3 + t) * 2 + nb) * 32 + ln);
-            acc += f4[e];
-          }
+#pragma unroll
+          for (int w = 0; w < MAX_NW; ++w) acc += part[w];
           out[j] = acc + __bfloat162float(((const bf16 *)p.b_pred)[d0 + d + j]);
         }
         const int s = rs.plist[i];
