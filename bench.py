@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=1024, help="sweep: utterances per decode launch")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--family", default="planted", choices=["planted", "random"])
+    ap.add_argument("--frame-looping", action="store_true",
+                    help="time the Alg. 2 frame-looping baseline (ll_decode_rnnt_frame_looping) instead")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0: auto)")
     return ap.parse_args()
@@ -237,7 +239,7 @@ def main():
     spec, w, enc_np, len_np = workload(a.config, 1000 + rank, a.family)
     B, T = enc_np.shape[0], enc_np.shape[1]
     model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16", device=f"cuda:{local}")
-    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, frame_looping=a.frame_looping)
     enc = torch.from_numpy(enc_np).to(dev, torch.bfloat16)
     lengths = torch.from_numpy(len_np).to(dev)
     stream = torch.cuda.current_stream()
@@ -344,6 +346,7 @@ def main():
         "warmup": a.warmup, "ms_per_step": tot_ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": a.config, "family": a.family, "B": B, "T_max": T,
+                   "algorithm": "frame-looping (Alg. 2 baseline)" if a.frame_looping else "label-looping (Alg. 3)",
                    "frames": int(len_np.sum()), "audio_s_per_step": audio_s, "l2": "flushed (512 MiB) between steps",
                    "parallelism": f"utterance-sharded x{world}"},
         "utterances_per_s": utt_s,

@@ -141,6 +141,25 @@ ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B
                         int32_t *out_lengths, int32_t out_capacity,
                         void *workspace, size_t workspace_bytes, ll_stream stream);
 
+/*
+ * Frame-looping BASELINE (Alg. 2, "Batched Inference of Transducer",
+ * PAPER.md:84-115) on the same kernels, for the paper's label- vs frame-looping
+ * comparison.  Same arguments, ownership, errors and
+ * results as ll_decode_rnnt (the hypotheses are identical: both reach the
+ * greedy result of Alg. 1).  Control flow: all rows advance through frames in
+ * lockstep (line 22); at frame t the joint is evaluated for the rows not yet
+ * done with t, rows that emit a label get a predictor update and are evaluated
+ * again at t (lines 11-20) until they emit a blank or hit max_symbols.  Unlike
+ * the paper's listing, the predictor output of rows whose state did not change is
+ * reused, not recomputed (a stronger baseline).  RNN-T only.
+ */
+ll_status ll_decode_rnnt_frame_looping(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                                       const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                                       int32_t blank_id, int32_t max_symbols,
+                                       int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_lengths,
+                                       int32_t out_capacity, void *workspace, size_t workspace_bytes,
+                                       ll_stream stream);
+
 /* Waits for the work enqueued on `stream` and returns the device-side status of
  * the last decode that used `workspace`: LL_OK, LL_ERR_INVALID_ARGUMENT (some
  * lengths[b] > T_max; that row decodes as empty), LL_ERR_CAPACITY, or

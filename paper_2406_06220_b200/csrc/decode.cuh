@@ -78,6 +78,7 @@ struct DecodeParams {
   int NS;                        // weight-ring slots (bf16 LSTM), 0 otherwise
   int n_groups, cap;
   int spec_prefetch;             // speculative next-window prefetch
+  int frame_looping;             // 1: Alg. 2 baseline control flow (RNN-T, W = 1)
   const int *lengths;
   const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
   const void *w_out, *b_out, *w_dur, *b_dur;
@@ -721,6 +722,44 @@ struct Ctx {
     if (all_ok && Xnext >= 0) plan_z(Xnext);
   }
 
+  // Frame-looping baseline (Alg. 2), warp 0: the one-frame
+  // decisions of a round at the common frame t.  Blank -> the row is done with
+  // this frame; label -> append (t), predictor update before the row's next
+  // evaluation, k += 1, and after the m-th label the row is done with this frame
+  // without a blank evaluation (guard, reading A6).
+  __device__ void decide_fl(unsigned *algevals) {
+    if (warp != 0) return;
+    int used = 0;
+    if (lane < p.R && rs.scanning[lane]) {
+      const int s = lane;
+      const int y = rs.dec[s * p.W] & 0xFFFFFF;
+      used = 1;
+      if (y == p.blank) {
+        rs.scanning[s] = 0;
+      } else {
+        const int pos = rs.len[s];
+        if (rank == 0) {
+          if (pos < p.cap) {
+            p.out_tokens[(size_t)rs.b[s] * p.cap + pos] = y;
+            p.out_timestamps[(size_t)rs.b[s] * p.cap + pos] = rs.t[s];
+          } else {
+            atomicOr(p.status, 2);
+          }
+        }
+        rs.len[s] = pos + 1;
+        rs.last[s] = y;
+        for (int c = MAX_CTX - 1; c > 0; --c) rs.ctx[c][s] = rs.ctx[c - 1][s];
+        rs.ctx[0][s] = y;
+        rs.needp[s] = 1;
+        rs.k[s] += 1;
+        if (rs.k[s] == p.max_sym) rs.scanning[s] = 0;
+      }
+    }
+    used = __reduce_add_sync(0xffffffffu, used);
+    if (lane == 0) *algevals += (unsigned)used;
+    __syncwarp();
+  }
+
   // warp 0: rebuild the compacted scanning / predictor lists (ascending slot order)
   __device__ void rebuild_lists() {
     if (warp == 0) {
@@ -1305,7 +1344,9 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // ---------------------------------------------------------------------------
 // The decode kernel.  PRED: 0 = LSTM, 1 = stateless.
 // ---------------------------------------------------------------------------
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0>
+// FL: frame-looping baseline (Alg. 2) instead of label-looping (separate
+// instantiations, so the label-looping kernels carry none of its code).
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
@@ -1395,6 +1436,63 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
       cx.rebuild_lists();
       cx.sync();
 
+      // ---- frame-looping baseline (Alg. 2): frames in lockstep ----------------
+      if constexpr (FL) {
+        if (warp == 0 && lane < R) rs.scanning[lane] = rs.active[lane];
+        __syncwarp();
+        cx.rebuild_lists();
+        cx.sync();
+        while (rs.nactive > 0) {
+          if (t0) s_cnt[SC_OUTER]++;
+          if (rs.npred > 0) {          // rows that emitted a label: predictor update
+            if (t0) {
+              s_cnt[SC_PRED]++;
+              s_cnt[SC_PREDROWS] += rs.npred;
+            }
+            if constexpr (PRED == 1) cx.predictor_stateless();
+            else if constexpr (RING) cx.predictor_lstm_tmem();
+            else cx.predictor_lstm_f32();
+            if (warp == 0 && lane < R) rs.needp[lane] = 0;
+            __syncwarp();
+          }
+          if (rs.nscan == 0) {         // every row is done with frame t: t += 1 for all (line 22)
+            if (warp == 0 && lane < R && rs.active[lane]) {
+              rs.t[lane] += 1;
+              rs.k[lane] = 0;
+              rs.active[lane] = rs.t[lane] < rs.L[lane];
+              rs.scanning[lane] = rs.active[lane];
+            }
+            __syncwarp();
+            cx.rebuild_lists();
+            cx.sync();
+            continue;
+          }
+          // one joint round at frame t for the rows still scanning it (lines 7-8 / 18-19)
+          if (cx.fpend(cur)) cur ^= 1;
+          cx.issue_f(cur, false);
+          cx.sync();
+          cx.wait_f(cur);
+          cx.plan_z(cur);
+          cx.sync();
+          cx.build_z(cur);
+          cx.sync();
+          cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
+          cx.exchange_keys();
+          if (warp == 0) {
+            cx.exchange_wait();
+            if (t0) {
+              s_cnt[SC_ROUNDS]++;
+              s_cnt[SC_ROWEVALS] += rs.nz;
+            }
+            cx.resolve_rows_w0();
+            cx.decide_fl(s_cnt + SC_ALGEVALS);
+          }
+          cx.flip_par();
+          cx.sync();
+          cx.rebuild_lists();
+          cx.sync();
+        }
+      } else
       // ---- outer loop over labels (Alg. 3 line 5) -----------------------------
       while (rs.nactive > 0) {
         if (t0) s_cnt[SC_OUTER]++;

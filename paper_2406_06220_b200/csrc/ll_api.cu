@@ -168,9 +168,9 @@ inline int kreg_for(bool bf, int H) { return !bf ? 1 : (H <= KREG_SMALL * 32 + 1
 constexpr int FC_H = 640, FC_P = 640, FC_C = 16;
 inline bool is_fc(bool bf, int H, int P, int C) { return bf && H == FC_H && P == FC_P && C == FC_C; }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false>
 int max_clusters(int C, const Layout &L) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -192,10 +192,10 @@ int max_clusters(int C, const Layout &L) {
   return n;
 }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false>
 ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
                         int &used_clusters) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -272,7 +272,7 @@ ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw
   return cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
 }
 
-ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int32_t B, int32_t T_max,
+ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt, ll_prec prec, int32_t B, int32_t T_max,
                       const int32_t *lengths, const ll_predictor *pr, const ll_joint *jn,
                       int32_t blank_id, int32_t max_symbols, const int32_t *durations, int32_t nD,
                       int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_durations,
@@ -314,6 +314,11 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
     else
       ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
     if (ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl)) return LL_ERR_UNSUPPORTED;
+  }
+  if (frame_looping) {   // Alg. 2 evaluates one frame per joint call
+    cf.W = 1;
+    cf.WF = 1;
+    cf.L = make_layout(bf, lstm, H, P, V1, nD, cf.R, 1, 1, cf.C, 0);
   }
   const int C = cf.C, R = cf.R;
   const Layout &L = cf.L;
@@ -361,7 +366,8 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   p.NS = cf.NS;
   p.n_groups = (B + R - 1) / R;
   p.cap = cap;
-  p.spec_prefetch = env_int("LL_SPEC_PREFETCH", 1);
+  p.spec_prefetch = frame_looping ? 0 : env_int("LL_SPEC_PREFETCH", 1);
+  p.frame_looping = frame_looping ? 1 : 0;
   p.lengths = lengths;
   p.f = ws + w.f;
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
@@ -388,7 +394,20 @@ ll_status decode_impl(bool tdt, const void *enc, ll_dtype dt, ll_prec prec, int3
   }
   int used = 0;
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
-  if (is_fc(bf, H, P, C))
+  if (frame_looping) {   // Alg. 2 baseline instantiations
+    if (is_fc(bf, H, P, C))
+      s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, true>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, true>(p, C, L, p.n_groups, st, used);
+    else if (bf && kreg_for(bf, H) == KREG)
+      s = lstm ? launch_decode<bf16, 0, KREG, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
+    else if (bf)
+      s = lstm ? launch_decode<bf16, 0, KREG_SMALL, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG_SMALL, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
+    else
+      s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
+               : launch_decode<float, 1, 1, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
+  } else if (is_fc(bf, H, P, C))
     s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C>(p, C, L, p.n_groups, st, used)
              : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C>(p, C, L, p.n_groups, st, used);
   else if (bf && kreg_for(bf, H) == KREG)
@@ -443,7 +462,17 @@ ll_status ll_decode_rnnt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t 
                          int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
                          int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
                          void *workspace, size_t workspace_bytes, ll_stream stream) {
-  return decode_impl(false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+  return decode_impl(false, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+                     nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
+                     workspace_bytes, stream);
+}
+
+ll_status ll_decode_rnnt_frame_looping(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                                       const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                                       int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
+                                       int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
+                                       void *workspace, size_t workspace_bytes, ll_stream stream) {
+  return decode_impl(false, true, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
                      workspace_bytes, stream);
 }
@@ -454,7 +483,7 @@ ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B
                         int32_t num_durations, int32_t *out_tokens, int32_t *out_timestamps,
                         int32_t *out_durations, int32_t *out_lengths, int32_t out_capacity,
                         void *workspace, size_t workspace_bytes, ll_stream stream) {
-  return decode_impl(true, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+  return decode_impl(true, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      durations, num_durations, out_tokens, out_timestamps, out_durations, out_lengths,
                      out_capacity, workspace, workspace_bytes, stream);
 }

@@ -84,7 +84,12 @@ class LabelLoopingDecoder:
     """Owns the workspace and output buffers for batches up to (B_max, T_max)."""
 
     def __init__(self, model: Model, max_symbols: int, B_max: int, T_max: int, cap: Optional[int] = None,
-                 prec: int = ll.LL_PREC_FAST):
+                 prec: int = ll.LL_PREC_FAST, frame_looping: bool = False):
+        """frame_looping=True runs the Alg. 2 baseline (ll_decode_rnnt_frame_looping,
+        RNN-T only) instead of label-looping."""
+        if frame_looping and model.durations is not None:
+            raise ValueError("frame-looping baseline: RNN-T only")
+        self.frame_looping = bool(frame_looping)
         self.model = model
         self.max_symbols = int(max_symbols)
         self.B_max, self.T_max = int(B_max), int(T_max)
@@ -111,7 +116,8 @@ class LabelLoopingDecoder:
         assert B <= self.B_max and T <= self.T_max and enc.is_contiguous() and lengths.dtype == torch.int32
         st = (stream or torch.cuda.current_stream()).cuda_stream
         if m.durations is None:
-            return ll.ll_decode_rnnt(enc.data_ptr(), m.dtype_code, self.prec, B, T, lengths.data_ptr(),
+            fn = ll.ll_decode_rnnt_frame_looping if self.frame_looping else ll.ll_decode_rnnt
+            return fn(enc.data_ptr(), m.dtype_code, self.prec, B, T, lengths.data_ptr(),
                                      m.pred, m.joint, m.blank_id, self.max_symbols, self.tokens.data_ptr(),
                                      self.timestamps.data_ptr(), self.lengths_out.data_ptr(), self.cap,
                                      self.ws_ptr, self.ws_bytes, st)

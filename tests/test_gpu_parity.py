@@ -260,3 +260,57 @@ def test_determinism_and_batch_composition():
     for b in [0, 5, 19]:
         ha, _ = gpu_decode(spec, w, enc[b:b + 1], lengths[b:b + 1], model=model)
         assert ha[0] == h1[b]
+
+
+# ------------------------------------------------------------------ frame-looping
+# The Alg. 2 baseline (ll_decode_rnnt_frame_looping) on the same kernels: the
+# hypotheses must equal label-looping's (both reach Alg. 1's greedy result) and
+# the batched joint-call count must equal the oracle's Alg. 2 count.
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_frame_looping_cat_dog(dtype, monkeypatch):
+    monkeypatch.setenv("LL_GROUP_ROWS", "2")          # both utterances in one batch
+    spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
+    model = gpu_model(spec, w, dtype)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, 2, enc.shape[1], frame_looping=True)
+    out = dec.decode(torch.from_numpy(enc).to("cuda", model.tdtype), torch.from_numpy(lengths).cuda())
+    hyps = out.hypotheses()
+    assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
+    assert [h[1] for h in hyps] == [[0, 2, 2], [1, 3, 3]]
+    from oracle import decode_frame_looping
+    _, cnt = decode_frame_looping(Transducer.from_spec(spec, w), enc, lengths, spec.max_symbols)
+    st = dec.stats()
+    assert st["joint_rounds"] == cnt["joint_calls"]
+    assert st["joint_evals"] == 14
+
+
+@pytest.mark.parametrize("kind", ["stateless", "lstm"])
+def test_frame_looping_equals_label_looping_tiny(kind):
+    """Random tiny models (guard exercised): frame-looping == label-looping on
+    the GPU, and every row passes the float64 verifier."""
+    base = synth.CONFIGS["tiny"]["spec"]
+    sp = synth.ModelSpec(base.num_tokens, base.enc_dim, base.pred_dim, base.joint_dim, kind, 1, None,
+                         base.blank_id, base.max_symbols)
+    for seed in range(20):
+        bb = float(np.random.default_rng(seed).uniform(-0.5, 2.0))
+        w = synth.make_weights(sp, 5000 + seed, blank_bias=bb)
+        enc, lengths = synth.make_inputs(7000 + seed, 4, 30, sp.enc_dim, 0, 30)
+        model = gpu_model(sp, w, "f32")
+        ref, _ = gpu_decode(sp, w, enc, lengths, "f32", model=model)
+        dec = LabelLoopingDecoder(model, sp.max_symbols, 4, 30, frame_looping=True)
+        hyps = dec.decode(torch.from_numpy(enc).to("cuda", model.tdtype), torch.from_numpy(lengths).cuda()).hypotheses()
+        assert hyps == ref, seed
+        verify_all(sp, w, enc, lengths, hyps)
+
+
+def test_frame_looping_fc_planted():
+    """Config (2) at full size through the frame-looping baseline: equal to the
+    planted alignment (the same closed form label-looping meets)."""
+    c = synth.CONFIGS["fc-rnnt"]
+    spec = c["spec"]
+    w, enc, lengths, planted = synth.make_planted_rnnt(spec, 5, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+    model = gpu_model(spec, w)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, c["B"], c["T_max"], frame_looping=True)
+    hyps = dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), torch.from_numpy(lengths).cuda()).hypotheses()
+    for b in range(c["B"]):
+        assert (hyps[b][0], hyps[b][1]) == (planted[b][0], planted[b][1]), b
