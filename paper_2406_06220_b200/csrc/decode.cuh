@@ -1073,14 +1073,14 @@ struct Ctx {
     // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units.
     // E'[y_i] slices of this CTA's units (4 gates x UPC floats per row) are
     // staged into shared memory by bulk copies that overlap the gate GEMM.
-    if (warp == 0) {
-      const uint32_t segb = (uint32_t)(L.UPC * 4);
-      if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)(4 * n) * segb);
+    // (the table's columns are CTA-major: one bulk copy per predictor row)
+    if (warp == NW - 1) {
+      const uint32_t segb = (uint32_t)(4 * L.UPC * 4);
+      if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)n * segb);
       __syncwarp();
-      for (int x = lane; x < 4 * n; x += 32) {
-        const int i = x >> 2, gate = x & 3;
-        const int s = rs.plist[i];
-        bulk_g2s(es() + ((size_t)i * 4 + gate) * L.UPC, p.tab + (size_t)rs.last[s] * 4 * P + (size_t)gate * P + u0,
+      if (lane < n) {
+        const int s = rs.plist[lane];
+        bulk_g2s(es() + (size_t)lane * 4 * L.UPC, p.tab + (size_t)rs.last[s] * 4 * P + (size_t)rank * 4 * L.UPC,
                  segb, bar(BAR_E));
       }
     }
@@ -1314,6 +1314,28 @@ struct Ctx {
     }
   }
 };
+
+// ---------------------------------------------------------------------------
+// W_ih / b_ih / b_hh with the 4P gate rows in CTA-major order: row
+// r*4*UPC + gate*UPC + ul  <-  gate*P + r*UPC + ul (the E' table GEMM then
+// produces, per vocabulary row, one contiguous 4*UPC-float slice per CTA).
+// ---------------------------------------------------------------------------
+__global__ void permute_gate_rows(const bf16 *w_ih, const bf16 *b_ih, const bf16 *b_hh, bf16 *w_out, bf16 *bi_out,
+                                  bf16 *bh_out, int P, int C, int UPC) {
+  const int chunks = P / 8;
+  const long long total = (long long)4 * P * chunks;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i % chunks);
+    const int dst = (int)(i / chunks);
+    const int r = dst / (4 * UPC), gate = (dst / UPC) % 4, ul = dst % UPC;
+    const int src = gate * P + r * UPC + ul;
+    reinterpret_cast<uint4 *>(w_out + (size_t)dst * P)[j] = reinterpret_cast<const uint4 *>(w_ih + (size_t)src * P)[j];
+    if (j == 0) {
+      bi_out[dst] = b_ih[src];
+      bh_out[dst] = b_hh[src];
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Pack the bf16 LSTM weights into the per-CTA tile stream: for cluster rank r,

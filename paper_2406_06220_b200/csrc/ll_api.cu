@@ -26,7 +26,7 @@ constexpr int RPREF_MANY = 7;       // rows per group when the batch spans many 
 constexpr size_t SMEM_LIMIT = 232448;
 
 struct Ws {
-  size_t f, tab, h, g, wst, total;
+  size_t f, tab, h, g, wst, wih, total;
 };
 
 size_t esize(ll_dtype d) { return d == LL_BF16 ? 2 : 4; }
@@ -48,6 +48,8 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
   w.wst = o;  // packed LSTM weight stream (bf16): (4P + H) rows of P
   if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + (4 * P + H) * P * 2, 256);
+  w.wih = o;  // bf16 LSTM: W_ih and b_ih, b_hh with gate rows permuted CTA-major (E' table columns)
+  if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + 4 * P * P * 2 + 2 * 4 * P * 2, 256);
   w.total = o;
   return w;
 }
@@ -335,7 +337,17 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   if (s != LL_OK) return s;
   // (2) model tables
   float *tab = (float *)(ws + w.tab);
-  if (lstm) {
+  if (lstm && ring) {
+    // E' = Emb W_ih^T + b_ih + b_hh with its 4P columns ordered CTA-major (rank r:
+    // gates i,f,g,o of units r*UPC ...), so the decode kernel fetches a predictor
+    // row's slice with ONE bulk copy of 4*UPC floats
+    bf16 *wih = (bf16 *)(ws + w.wih);
+    bf16 *bih = wih + (size_t)4 * P * P, *bhh = bih + 4 * P;
+    permute_gate_rows<<<296, 256, 0, st>>>((const bf16 *)pr->w_ih, (const bf16 *)pr->b_ih, (const bf16 *)pr->b_hh,
+                                           wih, bih, bhh, P, C, L.UPC);
+    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
+    s = linear(bf, pr->embedding, P, wih, P, bih, bhh, tab, 4 * P, V1, 4 * P, P, false, st);
+  } else if (lstm) {
     s = linear(bf, pr->embedding, P, pr->w_ih, P, pr->b_ih, pr->b_hh, tab, 4 * P, V1, 4 * P, P, false, st);
   } else {
     const int c = pr->context, Pc = P / c;
