@@ -1115,7 +1115,9 @@ struct Ctx {
     for (int nb0 = 0; nb0 * 8 < n; nb0 += 2) {
       if (n - nb0 * 8 > 8) wpred_store<2>(nb0, n);
       else wpred_store<1>(nb0, n);
+      if (nb0 == 0) tl_pred(9);
       sync();
+      if (nb0 == 0) tl_pred_bar(10);
       const int nrows = min(16, n - nb0 * 8);
       const int D4 = L.DPC / 4;
       const float4 *wp = reinterpret_cast<const float4 *>(zs());

@@ -57,6 +57,6 @@ def report(area, name, order, labels):
 report(0, "joint rounds", list(range(11)),
        ["", "wait_f/plan (+sync)", "build_z", "sync (bar)", "spec issue + joint", "exchange send",
         "exchange wait", "resolve", "sync (bar)", "decide", "sync+reload (bar)"])
-report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 5, 6, 7],
+report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 9, 10, 5, 6, 7],
        ["", "outer-step entry", "first gate tile", "rest tiles + E' wait", "sync (bar)", "h' exchange",
-        "W_pred tiles", "sync (bar)", "g exchange + sync"])
+        "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)", "g exchange + sync"])
