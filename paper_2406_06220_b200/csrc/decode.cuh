@@ -794,17 +794,20 @@ struct Ctx {
   // tiles, half 0 = gates (i, f) and half 1 = gates (g, o), row c of a half =
   // unit 4pp + c/2, gate 2*half + (c & 1) (packed by pack_lstm_stream).
   // Pair pp belongs to warp pp % NW; a warp can only reach TMEM lane quarter
-  // warp % 4, so the quarter's columns are shared by its warps: the warp's k-th
-  // tile (k = 2 * (pp / NW) + half) sits in column slot k * nq + warp / 4.
-  // Thread (g, q) of the warp holds, for every 32-wide K block kb, the 16-byte
-  // fragment (row g, chunk 4kb + q) in columns 4kb..4kb+3 (+2 for a 16-wide tail).
+  // warp % 4, so the quarter's columns are shared by its warps: the warp's m-th
+  // pair (m = pp / NW) sits in pair slot m * nq + warp / 4 (2 * tcols columns).
+  // Thread (g, q) holds, for every 32-wide K block kb, the m16 A fragments of
+  // the pair interleaved in columns 8kb..8kb+7: (h0.x, h1.x, h0.y, h1.y, h0.z,
+  // h1.z, h0.w, h1.w), h0/h1 = the 16-byte chunk 4kb + q of row g of half 0/1,
+  // so each fragment is 4 consecutive registers of one tcgen05.ld (+4 columns
+  // for a 16-wide tail).
   __device__ int tcols() const { return 4 * (Pd() / 32) + ((Pd() & 31) ? 2 : 0); }
   __device__ int npairs() const { return L.UPC / 4; }
   __device__ int quarter_warps(int qd) const { return (NW - qd + 3) / 4; }
-  __device__ uint32_t pair_taddr(int pp, int half) const {
-    const int w = pp % NW, k = 2 * (pp / NW) + half, qd = w & 3;
-    const int slot = k * quarter_warps(qd) + (w >> 2);
-    return tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(slot * tcols());
+  __device__ uint32_t pair_taddr(int pp) const {
+    const int w = pp % NW, qd = w & 3;
+    const int slot = (pp / NW) * quarter_warps(qd) + (w >> 2);
+    return tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)(slot * 2 * tcols());
   }
 
   // Kernel start: W_hh tiles of this CTA from the packed stream into TMEM,
@@ -812,39 +815,38 @@ struct Ctx {
   __device__ void load_lstm_weights() {
     const int NG = ng(), NPT = npt(), KB = Pd() / 32;
     const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
-    for (int n = 2 * warp; n < NG; n += 2 * NW) {   // stream tile n = 2 * pair + half
-     for (int half = 0; half < 2; ++half) {
-      const uint32_t ta = pair_taddr(n / 2, half);
-      const uint8_t *row =
-          reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n + half) * 8 + g) * Pd());
-      for (int c4 = 0; c4 < KB; c4 += 4) {
+    for (int n = 2 * warp; n < NG; n += 2 * NW) {   // stream tiles n (half 0), n + 1 (half 1) = pair n / 2
+      const uint32_t ta = pair_taddr(n / 2);
+      const uint8_t *row0 =
+          reinterpret_cast<const uint8_t *>(p.wst + (((size_t)rank * (NG + NPT) + n) * 8 + g) * Pd());
+      const uint8_t *row1 = row0 + (size_t)8 * Pd() * 2;
+      for (int c2 = 0; c2 < KB; c2 += 2) {
         uint32_t r[16];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int kb = c4 + u;
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (kb < KB) v = ldg128_nc(row + (((kb * 4 + q) ^ sw) * 16));
-          r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
-        }
-        if (c4 + 4 <= KB) {
-          tmem_st16(ta + 4 * c4, r);
-        } else {
-          // partial chunk: store the valid blocks one x4 group at a time
-          for (int u = 0; c4 + u < KB; ++u) {
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(
-                             ta + 4 * (c4 + u)),
-                         "r"(r[4 * u]), "r"(r[4 * u + 1]), "r"(r[4 * u + 2]), "r"(r[4 * u + 3])
-                         : "memory");
+        for (int u = 0; u < 2; ++u) {
+          const int kb = c2 + u;
+          uint4 v0 = make_uint4(0, 0, 0, 0), v1 = make_uint4(0, 0, 0, 0);
+          if (kb < KB) {
+            v0 = ldg128_nc(row0 + (((kb * 4 + q) ^ sw) * 16));
+            v1 = ldg128_nc(row1 + (((kb * 4 + q) ^ sw) * 16));
           }
+          r[8 * u + 0] = v0.x; r[8 * u + 1] = v1.x; r[8 * u + 2] = v0.y; r[8 * u + 3] = v1.y;
+          r[8 * u + 4] = v0.z; r[8 * u + 5] = v1.z; r[8 * u + 6] = v0.w; r[8 * u + 7] = v1.w;
+        }
+        if (c2 + 2 <= KB) {
+          tmem_st16(ta + 8 * c2, r);
+        } else {   // odd last block: 8 columns
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + 8 * c2),
+                       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                       : "memory");
         }
       }
       if (Pd() & 31) {
-        const uint2 v = ldg64_nc(row + KB * 64 + q * 8);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(ta + 4 * KB), "r"(v.x),
-                     "r"(v.y)
+        const uint2 v0 = ldg64_nc(row0 + KB * 64 + q * 8), v1 = ldg64_nc(row1 + KB * 64 + q * 8);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta + 8 * KB), "r"(v0.x),
+                     "r"(v1.x), "r"(v0.y), "r"(v1.y)
                      : "memory");
       }
-     }
     }
     tmem_wait_st();
     if (warp == 0) {
@@ -868,22 +870,20 @@ struct Ctx {
   template <int NB>
   __device__ __forceinline__ void gates_pair(float (&acc)[NB][2][4], int pp, const uint8_t *const *hrow) const {
     const int KB = Pd() / 32;
-    const uint32_t ta0 = pair_taddr(pp, 0), ta1 = pair_taddr(pp, 1);
+    const uint32_t ta = pair_taddr(pp);
 #pragma unroll 1
     for (int c4 = 0; c4 < KB; c4 += 4) {
-      uint32_t r0[16], r1[16];
+      uint32_t r[32];
       if (c4 + 4 <= KB) {
-        tmem_ld16(ta0 + 4 * c4, r0);
-        tmem_ld16(ta1 + 4 * c4, r1);
+        tmem_ld32(ta + 8 * c4, r);
       } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (c4 + u < KB) {
-            uint4 v0, v1;
-            tmem_ld4(ta0 + 4 * (c4 + u), v0);
-            tmem_ld4(ta1 + 4 * (c4 + u), v1);
-            r0[4 * u] = v0.x; r0[4 * u + 1] = v0.y; r0[4 * u + 2] = v0.z; r0[4 * u + 3] = v0.w;
-            r1[4 * u] = v1.x; r1[4 * u + 1] = v1.y; r1[4 * u + 2] = v1.z; r1[4 * u + 3] = v1.w;
+            uint32_t t[8];
+            tmem_ld8(ta + 8 * (c4 + u), t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) r[8 * u + e] = t[e];
           }
         }
       }
@@ -895,21 +895,20 @@ struct Ctx {
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
             const uint4 x = lds128(hrow[nb] + kb * 64);
-            mma_bf16_16816(acc[nb][u & 1], r0[4 * u], r1[4 * u], r0[4 * u + 1], r1[4 * u + 1], x.x, x.y);
-            mma_bf16_16816(acc[nb][u & 1], r0[4 * u + 2], r1[4 * u + 2], r0[4 * u + 3], r1[4 * u + 3], x.z, x.w);
+            mma_bf16_16816(acc[nb][u & 1], r[8 * u], r[8 * u + 1], r[8 * u + 2], r[8 * u + 3], x.x, x.y);
+            mma_bf16_16816(acc[nb][u & 1], r[8 * u + 4], r[8 * u + 5], r[8 * u + 6], r[8 * u + 7], x.z, x.w);
           }
         }
       }
     }
     if (Pd() & 31) {   // 16-wide K tail: lane q owns columns [4q, 4q + 4) of the block
-      uint32_t t0, t1, t2, t3;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t0), "=r"(t1) : "r"(ta0 + 4 * KB));
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(t2), "=r"(t3) : "r"(ta1 + 4 * KB));
+      uint4 t;
+      tmem_ld4(ta + 8 * KB, t);
       tmem_wait_ld();
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         const uint2 x = lds64(hrow[nb] + KB * 64 - q * 8);
-        mma_bf16_16816(acc[nb][0], t0, t2, t1, t3, x.x, x.y);
+        mma_bf16_16816(acc[nb][0], t.x, t.y, t.z, t.w, x.x, x.y);
       }
     }
   }
