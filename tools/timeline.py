@@ -37,9 +37,10 @@ def report(area, name, order, labels):
     print(f"\n{name}: {len(ev)} events recorded")
     tot = np.zeros(len(order))
     skew = np.zeros(len(order))
+    ev = [i for i in ev if all((x[i, ph] > 0).any() for ph in order)]   # events with every stamp
     for i in ev:
-        mx = [x[i, ph][x[i, ph] > 0].max() if (x[i, ph] > 0).any() else np.nan for ph in order]
-        mn = [x[i, ph][x[i, ph] > 0].min() if (x[i, ph] > 0).any() else np.nan for ph in order]
+        mx = [x[i, ph][x[i, ph] > 0].max() for ph in order]
+        mn = [x[i, ph][x[i, ph] > 0].min() for ph in order]
         for k in range(1, len(order)):
             tot[k] += mx[k] - mx[k - 1]
             skew[k] += mx[k] - mn[k]
