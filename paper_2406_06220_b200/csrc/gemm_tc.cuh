@@ -1,0 +1,163 @@
+// gemm_tc.cuh -- Y[M,N] = X[M,K] . W[N,K]^T + bias[N] (+ bias2[N]) on the
+// 5th-generation tensor cores (sm_100a): TMA (cp.async.bulk.tensor, 128-byte
+// swizzle) stages 128x64 tiles of X and W through a 4-stage shared-memory ring,
+// ONE thread issues tcgen05.mma (kind::f16, M=128, N=128, K=16, fp32
+// accumulator in TMEM) and tcgen05.commit releases each stage; four warps read
+// the accumulator back with tcgen05.ld (lane = output row) for the epilogue
+// (bias, conversion, store).
+//
+// Used for the throughput-bound projections of PAPER.md §3.4 (:216-222): the
+// encoder projection f = W_enc enc + b_enc over all B*T_max frames (Alg. 3
+// line 2) and the model tables (E' = Emb W_ih^T + b_ih + b_hh, G_k).  Shapes
+// it does not cover (K % 64, N % 128, misaligned rows) fall back to the
+// mma.sync kernel of linear.cuh.
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+
+namespace ll {
+
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 64, TC_STAGES = 4;
+constexpr int TC_TILE_A = TC_BM * TC_BK * 2;   // 16 KB
+constexpr int TC_TILE_B = TC_BN * TC_BK * 2;   // 16 KB
+constexpr int TC_SMEM = TC_STAGES * (TC_TILE_A + TC_TILE_B) + 1024;   // + alignment slack
+
+struct TcGemmArgs {
+  const void *bias, *bias2;   // bf16 [N] or nullptr
+  void *Y;
+  int64_t ldy;
+  int M, N, K;
+};
+
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row
+// core groups 1024 bytes apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)(1) << 16;                         // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;      // stride byte offset
+  d |= (uint64_t)1 << 46;                           // version
+  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D fp32, A/B bf16, both K-major, N = 128, M = 128.
+constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
+                              ((uint32_t)(TC_BM >> 4) << 24);
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                                                         const __grid_constant__ CUtensorMap map_w,
+                                                         const __grid_constant__ TcGemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // SW128 atoms: 1024-B aligned
+  __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], done;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
+  const int nk = a.K / TC_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&s_tmem, TC_BN);   // 128 fp32 columns: the 128x128 accumulator
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (threadIdx.x == 0) {
+    // producer (TMA) and MMA issuer in one thread: stage kb is loaded
+    // TC_STAGES - 1 steps ahead of the MMAs that consume it
+    for (int it = 0; it < nk + TC_STAGES - 1; ++it) {
+      if (it < nk) {
+        const int s = it % TC_STAGES;
+        if (it >= TC_STAGES) mbar_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
+        uint8_t *sa = smem + s * (TC_TILE_A + TC_TILE_B), *sb = sa + TC_TILE_A;
+        mbar_arrive_expect_tx(&full[s], TC_TILE_A + TC_TILE_B);
+        tma_load_2d(sa, &map_x, it * TC_BK, m0, &full[s]);
+        tma_load_2d(sb, &map_w, it * TC_BK, n0, &full[s]);
+      }
+      const int kc = it - (TC_STAGES - 1);
+      if (kc >= 0) {
+        const int s = kc % TC_STAGES;
+        mbar_wait(&full[s], (kc / TC_STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * (TC_TILE_A + TC_TILE_B)), sb = sa + TC_TILE_A;
+#pragma unroll
+        for (int k = 0; k < TC_BK / 16; ++k) {   // K = 16 per MMA: +32 bytes inside the swizzle atom
+          const uint64_t da = umma_desc_sw128(sa + k * 32), db = umma_desc_sw128(sb + k * 32);
+          const uint32_t acc = (kc > 0 || k > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+              " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(TC_IDESC), "r"(acc)
+              : "memory");
+        }
+        // the stage is free once these MMAs have read it
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty[s]))
+                     : "memory");
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(&done))
+                 : "memory");
+  }
+  __syncwarp();
+  // epilogue: warp w owns accumulator rows 32w..32w+31 (TMEM lane = row)
+  mbar_wait(&done, 0);
+  tc_fence_after();
+  const int row = m0 + warp * 32 + lane;
+  const bf16 *bias = (const bf16 *)a.bias, *bias2 = (const bf16 *)a.bias2;
+#pragma unroll 1
+  for (int c0 = 0; c0 < TC_BN; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
+    tmem_wait_ld();
+    if (row < a.M) {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = n0 + c0 + j;
+        float x = __uint_as_float(r[j]);
+        if (bias) x += __bfloat162float(bias[n]);
+        if (bias2) x += __bfloat162float(bias2[n]);
+        v[j] = x;
+      }
+      OutT *y = (OutT *)a.Y + (int64_t)row * a.ldy + n0 + c0;
+      if constexpr (sizeof(OutT) == 2) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 o;
+          o.x = pack_bf16x2(v[j], v[j + 1]);
+          o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+          o.z = pack_bf16x2(v[j + 4], v[j + 5]);
+          o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+          *reinterpret_cast<uint4 *>(y + j) = o;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4 *>(y + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, TC_BN);
+}
+
+}  // namespace ll

@@ -13,8 +13,11 @@
 
 #include <algorithm>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/ll.h"
 #include "decode.cuh"
+#include "gemm_tc.cuh"
 #include "linear.cuh"
 
 using namespace ll;
@@ -256,10 +259,66 @@ ll_status launch_debug(const DecodeParams &p, int C, const Layout &L, int n_chun
   return LL_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, cols] matrix with leading
+// dimension ld (elements): 64-column x box_rows boxes, 128-byte swizzle.
+bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {TC_BK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// tcgen05 GEMM (gemm_tc.cuh) when the shape fits its tiles; false = not taken.
+bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const void *bias, const void *bias2, void *Y,
+               int64_t ldy, int M, int N, int K, bool out_bf16, cudaStream_t st, ll_status &s) {
+  if (env_int("LL_GEMM_MMA_SYNC", 0)) return false;
+  if (K % TC_BK || N % TC_BN || (ldx * 2) % 16 || (ldw * 2) % 16 || ((uintptr_t)X & 15) || ((uintptr_t)W & 15))
+    return false;
+  if ((out_bf16 && (ldy * 2) % 16) || (!out_bf16 && (ldy * 4) % 16) || ((uintptr_t)Y & 15)) return false;
+  CUtensorMap mx, mw;
+  if (!make_map_bf16(&mx, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, TC_BM) ||
+      !make_map_bf16(&mw, W, (uint64_t)N, (uint64_t)K, (uint64_t)ldw, TC_BN))
+    return false;
+  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K};
+  dim3 grid(N / TC_BN, (M + TC_BM - 1) / TC_BM);
+  if (out_bf16) {
+    cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    gemm_tc_kernel<bf16><<<grid, 128, TC_SMEM, st>>>(mx, mw, a);
+  } else {
+    cudaFuncSetAttribute(gemm_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    gemm_tc_kernel<float><<<grid, 128, TC_SMEM, st>>>(mx, mw, a);
+  }
+  s = cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
+  return true;
+}
+
 ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw, const void *bias,
                  const void *bias2, void *Y, int64_t ldy, int M, int N, int K, bool out_bf16,
                  cudaStream_t st) {
   if (M <= 0 || N <= 0) return LL_OK;
+  if (bf) {
+    ll_status s;
+    if (linear_tc(X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K, out_bf16, st, s)) return s;
+  }
   LinearArgs a{X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K};
   if (bf) {
     dim3 grid((N + LB_N - 1) / LB_N, (M + LB_M - 1) / LB_M);
