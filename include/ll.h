@@ -160,6 +160,24 @@ ll_status ll_decode_rnnt_frame_looping(const void *enc, ll_dtype dtype, ll_prec 
                                        int32_t out_capacity, void *workspace, size_t workspace_bytes,
                                        ll_stream stream);
 
+/*
+ * Weight-only preprocessing, once per model and workspace: builds the model
+ * tables of a decode call (LSTM: E' = Emb W_ih^T + b_ih + b_hh and the packed
+ * W_hh / W_pred tile stream; stateless: G_k = W_pred[:, k] Emb_k) into
+ * `workspace` and records their fingerprint (weight pointers, shapes, dtype,
+ * cluster layout) for that workspace (the tables sit at batch-independent
+ * offsets, so decodes of any B <= the workspace's B reuse them).  A later ll_decode_* on the
+ * same workspace whose fingerprint matches skips rebuilding them; any other
+ * decode on the workspace rebuilds them and drops the record.  Call it again
+ * after modifying weights IN PLACE (the fingerprint holds pointers, not
+ * contents).  Arguments as ll_decode_*: durations is HOST [num_durations] for
+ * TDT, NULL for RNN-T; B / T_max are the batch shape the workspace was sized
+ * for.  Stream-ordered; host validation errors return synchronously.
+ */
+ll_status ll_prepare(const ll_predictor *pred, const ll_joint *joint, ll_dtype dtype, ll_prec prec,
+                     int32_t B, int32_t T_max, const int32_t *durations, int32_t num_durations,
+                     void *workspace, size_t workspace_bytes, ll_stream stream);
+
 /* Waits for the work enqueued on `stream` and returns the device-side status of
  * the last decode that used `workspace`: LL_OK, LL_ERR_INVALID_ARGUMENT (some
  * lengths[b] > T_max; that row decodes as empty), LL_ERR_CAPACITY, or

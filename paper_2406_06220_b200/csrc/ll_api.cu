@@ -12,6 +12,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include <cudaTypedefs.h>
 
@@ -34,25 +36,27 @@ struct Ws {
 
 size_t esize(ll_dtype d) { return d == LL_BF16 ? 2 : 4; }
 
+// Workspace regions (256-B aligned).  The weight-only tables come first so
+// that their offsets do not depend on the batch shape (ll_prepare).
 Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype dt) {
   Ws w;
   const size_t H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs;
   size_t o = HDR_BYTES;
-  w.f = o;
-  o = align_up(o + (size_t)B * T * H * esize(dt), 256);
   w.tab = o;
   if (pr->kind == LL_PRED_LSTM)
     o = align_up(o + V1 * 4 * P * 4, 256);
   else
     o = align_up(o + (size_t)pr->context * V1 * H * 4, 256);
-  w.h = o;
-  if (pr->kind == LL_PRED_LSTM) o = align_up(o + 2 * (size_t)B * P * esize(dt), 256);
-  w.g = o;
-  if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
   w.wst = o;  // packed LSTM weight stream (bf16): (4P + H) rows of P
   if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + (4 * P + H) * P * 2, 256);
   w.wih = o;  // bf16 LSTM: W_ih and b_ih, b_hh with gate rows permuted CTA-major (E' table columns)
   if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + 4 * P * P * 2 + 2 * 4 * P * 2, 256);
+  w.f = o;
+  o = align_up(o + (size_t)B * T * H * esize(dt), 256);
+  w.h = o;
+  if (pr->kind == LL_PRED_LSTM) o = align_up(o + 2 * (size_t)B * P * esize(dt), 256);
+  w.g = o;
+  if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
   w.total = o;
   return w;
 }
@@ -333,6 +337,86 @@ ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw
   return cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
 }
 
+// Cluster size / group rows / window for a call: choose_config, then again
+// with the number of clusters that can actually be resident.
+bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf) {
+  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return false;
+  int ncl = 0;
+  if (is_fc(bf, H, P, cf.C))
+    ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L)
+               : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L);
+  else if (bf && kreg_for(bf, H) == KREG)
+    ncl = lstm ? max_clusters<bf16, 0, KREG>(cf.C, cf.L) : max_clusters<bf16, 1, KREG>(cf.C, cf.L);
+  else if (bf)
+    ncl = lstm ? max_clusters<bf16, 0, KREG_SMALL>(cf.C, cf.L) : max_clusters<bf16, 1, KREG_SMALL>(cf.C, cf.L);
+  else
+    ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
+  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl));
+}
+
+// ---------------------------------------------------------------------------
+// Weight-only model tables of a call (E' or G_k, the packed W_hh / W_pred
+// stream) and the registry that lets ll_prepare build them once per
+// workspace: a decode whose weights / shapes / cluster config match the
+// fingerprint ll_prepare recorded for its workspace skips rebuilding them.
+// ---------------------------------------------------------------------------
+struct TableKey {
+  const void *ptr[8];
+  int dims[10];
+  bool operator==(const TableKey &o) const { return memcmp(this, &o, sizeof(TableKey)) == 0; }
+};
+
+TableKey table_key(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, int C, const Layout &L) {
+  TableKey k;
+  memset(&k, 0, sizeof(k));
+  k.ptr[0] = pr->embedding; k.ptr[1] = pr->w_ih; k.ptr[2] = pr->w_hh; k.ptr[3] = pr->b_ih;
+  k.ptr[4] = pr->b_hh; k.ptr[5] = jn->w_pred; k.ptr[6] = jn->b_pred;
+  k.dims[0] = pr->kind; k.dims[1] = pr->num_tokens; k.dims[2] = pr->hidden; k.dims[3] = pr->context;
+  k.dims[4] = jn->joint_dim; k.dims[5] = (int)dt; k.dims[6] = jn->num_outputs; k.dims[8] = C;
+  k.dims[9] = L.UPC * 1000 + L.DPC;
+  return k;
+}
+
+std::mutex g_prep_mu;
+std::unordered_map<const void *, TableKey> g_prepared;   // workspace -> tables it holds
+
+ll_status build_tables(bool bf, const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, const Ws &w, uint8_t *ws,
+                       int C, const Layout &L, cudaStream_t st) {
+  const bool lstm = pr->kind == LL_PRED_LSTM, ring = bf && lstm;
+  const int H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs;
+  ll_status s = LL_OK;
+  float *tab = (float *)(ws + w.tab);
+  if (lstm && ring) {
+    // E' = Emb W_ih^T + b_ih + b_hh with its 4P columns ordered CTA-major (rank r:
+    // gates i,f,g,o of units r*UPC ...), so the decode kernel fetches a predictor
+    // row's slice with ONE bulk copy of 4*UPC floats
+    bf16 *wih = (bf16 *)(ws + w.wih);
+    bf16 *bih = wih + (size_t)4 * P * P, *bhh = bih + 4 * P;
+    permute_gate_rows<<<296, 256, 0, st>>>((const bf16 *)pr->w_ih, (const bf16 *)pr->b_ih, (const bf16 *)pr->b_hh,
+                                           wih, bih, bhh, P, C, L.UPC);
+    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
+    s = linear(bf, pr->embedding, P, wih, P, bih, bhh, tab, 4 * P, V1, 4 * P, P, false, st);
+  } else if (lstm) {
+    s = linear(bf, pr->embedding, P, pr->w_ih, P, pr->b_ih, pr->b_hh, tab, 4 * P, V1, 4 * P, P, false, st);
+  } else {
+    const int c = pr->context, Pc = P / c;
+    for (int k = 0; k < c && s == LL_OK; ++k) {
+      const uint8_t *emb = (const uint8_t *)pr->embedding + (size_t)k * V1 * Pc * esize(dt);
+      const uint8_t *wp = (const uint8_t *)jn->w_pred + (size_t)k * Pc * esize(dt);
+      s = linear(bf, emb, Pc, wp, P, k == 0 ? jn->b_pred : nullptr, nullptr, tab + (size_t)k * V1 * H, H,
+                 V1, H, Pc, false, st);
+    }
+  }
+  if (s != LL_OK) return s;
+  if (ring) {
+    // contiguous per-CTA tile stream of W_hh / W_pred
+    pack_lstm_stream<<<296, 256, 0, st>>>((const bf16 *)pr->w_hh, (const bf16 *)jn->w_pred,
+                                          (bf16 *)(ws + w.wst), P, C, L.UPC, L.DPC);
+    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
+  }
+  return LL_OK;
+}
+
 ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt, ll_prec prec, int32_t B, int32_t T_max,
                       const int32_t *lengths, const ll_predictor *pr, const ll_joint *jn,
                       int32_t blank_id, int32_t max_symbols, const int32_t *durations, int32_t nD,
@@ -361,21 +445,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   int maxd = 1;
   for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
   Config cf;
-  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return LL_ERR_UNSUPPORTED;
-  {
-    // re-choose R / W with the number of clusters that can actually be resident
-    int ncl = 0;
-    if (is_fc(bf, H, P, cf.C))
-      ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L)
-                 : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L);
-    else if (bf && kreg_for(bf, H) == KREG)
-      ncl = lstm ? max_clusters<bf16, 0, KREG>(cf.C, cf.L) : max_clusters<bf16, 1, KREG>(cf.C, cf.L);
-    else if (bf)
-      ncl = lstm ? max_clusters<bf16, 0, KREG_SMALL>(cf.C, cf.L) : max_clusters<bf16, 1, KREG_SMALL>(cf.C, cf.L);
-    else
-      ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
-    if (ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl)) return LL_ERR_UNSUPPORTED;
-  }
+  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return LL_ERR_UNSUPPORTED;
   if (frame_looping) {   // Alg. 2 evaluates one frame per joint call
     cf.W = 1;
     cf.WF = 1;
@@ -394,35 +464,24 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   // (1) encoder projection for all frames: f [B*T_max, H]
   s = linear(bf, enc, De, jn->w_enc, De, jn->b_enc, nullptr, ws + w.f, H, B * T_max, H, De, bf, st);
   if (s != LL_OK) return s;
-  // (2) model tables
+  // (2) model tables (weight-only; skipped if ll_prepare built exactly these
+  // into this workspace)
   float *tab = (float *)(ws + w.tab);
-  if (lstm && ring) {
-    // E' = Emb W_ih^T + b_ih + b_hh with its 4P columns ordered CTA-major (rank r:
-    // gates i,f,g,o of units r*UPC ...), so the decode kernel fetches a predictor
-    // row's slice with ONE bulk copy of 4*UPC floats
-    bf16 *wih = (bf16 *)(ws + w.wih);
-    bf16 *bih = wih + (size_t)4 * P * P, *bhh = bih + 4 * P;
-    permute_gate_rows<<<296, 256, 0, st>>>((const bf16 *)pr->w_ih, (const bf16 *)pr->b_ih, (const bf16 *)pr->b_hh,
-                                           wih, bih, bhh, P, C, L.UPC);
-    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
-    s = linear(bf, pr->embedding, P, wih, P, bih, bhh, tab, 4 * P, V1, 4 * P, P, false, st);
-  } else if (lstm) {
-    s = linear(bf, pr->embedding, P, pr->w_ih, P, pr->b_ih, pr->b_hh, tab, 4 * P, V1, 4 * P, P, false, st);
-  } else {
-    const int c = pr->context, Pc = P / c;
-    for (int k = 0; k < c && s == LL_OK; ++k) {
-      const uint8_t *emb = (const uint8_t *)pr->embedding + (size_t)k * V1 * Pc * esize(dt);
-      const uint8_t *wp = (const uint8_t *)jn->w_pred + (size_t)k * Pc * esize(dt);
-      s = linear(bf, emb, Pc, wp, P, k == 0 ? jn->b_pred : nullptr, nullptr, tab + (size_t)k * V1 * H, H,
-                 V1, H, Pc, false, st);
+  {
+    const TableKey key = table_key(pr, jn, dt, C, L);
+    bool cached = false;
+    {
+      std::lock_guard<std::mutex> lk(g_prep_mu);
+      auto it = g_prepared.find(workspace);
+      if (it != g_prepared.end()) {
+        cached = it->second == key;
+        if (!cached) g_prepared.erase(it);   // about to be overwritten with other tables
+      }
     }
-  }
-  if (s != LL_OK) return s;
-  if (ring) {
-    // (2b) contiguous per-CTA tile stream of W_hh / W_pred for the producer warp
-    pack_lstm_stream<<<296, 256, 0, st>>>((const bf16 *)pr->w_hh, (const bf16 *)jn->w_pred,
-                                          (bf16 *)(ws + w.wst), P, C, L.UPC, L.DPC);
-    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
+    if (!cached) {
+      s = build_tables(bf, pr, jn, dt, w, ws, C, L, st);
+      if (s != LL_OK) return s;
+    }
   }
   // (3) decode
   DecodeParams p;
@@ -557,6 +616,34 @@ ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B
   return decode_impl(true, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      durations, num_durations, out_tokens, out_timestamps, out_durations, out_lengths,
                      out_capacity, workspace, workspace_bytes, stream);
+}
+
+ll_status ll_prepare(const ll_predictor *pred, const ll_joint *joint, ll_dtype dtype, ll_prec prec, int32_t B,
+                     int32_t T_max, const int32_t *durations, int32_t num_durations, void *workspace,
+                     size_t workspace_bytes, ll_stream stream) {
+  if (B < 0 || T_max < 0) return LL_ERR_INVALID_ARGUMENT;
+  if (!workspace || ((uintptr_t)workspace & 255)) return LL_ERR_INVALID_ARGUMENT;
+  const int nD = durations ? num_durations : 0;
+  if (durations) {
+    if (nD < 1) return LL_ERR_INVALID_ARGUMENT;
+    for (int i = 0; i < nD; ++i)
+      if (durations[i] < 0) return LL_ERR_INVALID_ARGUMENT;
+  }
+  ll_status s = check_model(pred, joint, dtype, prec, nD, true);
+  if (s != LL_OK) return s;
+  if (workspace_bytes < ll_workspace_size(B, T_max, pred, joint, dtype, prec, nD)) return LL_ERR_WORKSPACE;
+  const bool bf = dtype == LL_BF16, lstm = pred->kind == LL_PRED_LSTM;
+  int maxd = 1;
+  for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
+  Config cf;
+  if (!decode_config(bf, lstm, joint->joint_dim, joint->pred_dim, joint->num_outputs, nD, maxd, B, cf))
+    return LL_ERR_UNSUPPORTED;
+  const Ws w = ws_layout(B, T_max, pred, joint, dtype);
+  s = build_tables(bf, pred, joint, dtype, w, (uint8_t *)workspace, cf.C, cf.L, (cudaStream_t)stream);
+  if (s != LL_OK) return s;
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  g_prepared[workspace] = table_key(pred, joint, dtype, cf.C, cf.L);
+  return LL_OK;
 }
 
 ll_status ll_sync(void *workspace, ll_stream stream) {

@@ -109,6 +109,17 @@ class LabelLoopingDecoder:
         self.durs = torch.zeros_like(self.tokens) if nD else None
         self.lengths_out = torch.zeros(self.B_max, dtype=torch.int32, device=dev)
 
+    def prepare(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """ll_prepare: build the weight-only model tables into this decoder's
+        workspace once; later decodes skip them while the weights (pointers)
+        and shapes stay the same."""
+        m = self.model
+        st = (stream or torch.cuda.current_stream()).cuda_stream
+        s = ll.ll_prepare(m.pred, m.joint, m.dtype_code, self.prec, self.B_max, self.T_max, m.durations,
+                          m.num_durations, self.ws_ptr, self.ws_bytes, st)
+        if s != ll.LL_OK:
+            raise ll.LLError(s, "ll_prepare")
+
     def launch(self, enc: torch.Tensor, lengths: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int:
         """Enqueue a decode of enc [B, T, D_e] (device, model dtype) with lengths [B] int32 (device)."""
         m = self.model

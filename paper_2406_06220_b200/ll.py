@@ -21,7 +21,8 @@ LL_PREC_FAST, LL_PREC_EXACT = 0, 1
 LL_PRED_LSTM, LL_PRED_STATELESS = 0, 1
 
 # Every symbol include/ll.h declares (checked by tests/test_abi.py).
-EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_rnnt_frame_looping", "ll_decode_tdt", "ll_sync",
+EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_rnnt_frame_looping", "ll_decode_tdt", "ll_prepare",
+            "ll_sync",
             "ll_status_string",
             "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version"]
 
@@ -69,6 +70,9 @@ def load_library() -> ctypes.CDLL:
                                   c_int32, POINTER(c_int32), c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_int32, c_void_p, c_size_t, c_void_p]
     lib.ll_decode_tdt.restype = c_int32
+    lib.ll_prepare.argtypes = [P, J, c_int32, c_int32, c_int32, c_int32, POINTER(c_int32), c_int32, c_void_p,
+                               c_size_t, c_void_p]
+    lib.ll_prepare.restype = c_int32
     lib.ll_sync.argtypes = [c_void_p, c_void_p]
     lib.ll_sync.restype = c_int32
     lib.ll_status_string.argtypes = [c_int32]
@@ -105,6 +109,15 @@ def ll_decode_rnnt(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, m
                                              ctypes.byref(joint), blank_id, max_symbols, out_tokens,
                                              out_timestamps, out_lengths, out_capacity, workspace,
                                              workspace_bytes, stream))
+
+
+def ll_prepare(pred, joint, dtype, prec, B, T_max, durations, num_durations, workspace, workspace_bytes,
+               stream) -> int:
+    dur = None
+    if durations is not None:
+        dur = (c_int32 * len(durations))(*durations)
+    return int(load_library().ll_prepare(ctypes.byref(pred), ctypes.byref(joint), dtype, prec, B, T_max, dur,
+                                         num_durations, workspace, workspace_bytes, stream))
 
 
 def ll_decode_rnnt_frame_looping(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,

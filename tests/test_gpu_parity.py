@@ -314,3 +314,31 @@ def test_frame_looping_fc_planted():
     hyps = dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), torch.from_numpy(lengths).cuda()).hypotheses()
     for b in range(c["B"]):
         assert (hyps[b][0], hyps[b][1]) == (planted[b][0], planted[b][1]), b
+
+
+# ------------------------------------------------------------------ ll_prepare
+def test_prepare_tables_reuse_and_invalidate():
+    """ll_prepare builds the weight-only tables once: decodes after it equal
+    decodes without it (also for a smaller batch on the same workspace), and a
+    decode with OTHER weights on the prepared workspace rebuilds its tables."""
+    c = synth.CONFIGS["fc-rnnt"]
+    spec = c["spec"]
+    wa, enc, lengths, planted = synth.make_planted_rnnt(spec, 5, 12, 120, 60, 120)
+    wb = synth.make_weights(spec, 77, blank_bias=3.0)
+    ma, mb = gpu_model(spec, wa), gpu_model(spec, wb)
+    ref_b, _ = gpu_decode(spec, wb, enc, lengths, model=mb)
+    dec = LabelLoopingDecoder(ma, spec.max_symbols, 12, 120)
+    dec.prepare()
+    e = torch.from_numpy(enc).to("cuda", torch.bfloat16)
+    l = torch.from_numpy(lengths).cuda()
+    for _ in range(2):
+        h = dec.decode(e, l).hypotheses()
+        assert [(x[0], x[1]) for x in h] == [(p[0], p[1]) for p in planted]
+    h5 = dec.decode(e[:5], l[:5]).hypotheses()           # smaller batch, same prepared tables
+    assert [(x[0], x[1]) for x in h5] == [(p[0], p[1]) for p in planted[:5]]
+    dec.model = mb                                          # other weights, same workspace
+    hb = dec.decode(e, l).hypotheses()
+    assert hb == ref_b
+    dec.model = ma                                          # back: tables were rebuilt for mb
+    h = dec.decode(e, l).hypotheses()
+    assert [(x[0], x[1]) for x in h] == [(p[0], p[1]) for p in planted]
