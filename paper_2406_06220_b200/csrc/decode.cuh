@@ -649,9 +649,10 @@ struct Ctx {
   // lines 9-11 and 15-19 for each frame; TDT: blank advances by max(d, 1),
   // PAPER.md:213).  decide() also rebuilds the scanning list and checks the
   // speculative window.
-  __device__ void resolve_rows_w0() {
+  __device__ int resolve_rows_w0() {
     const uint64_t *pt = part(par());
     const int nz = rs.nz;
+    int dec = 0;
     if (lane < nz) {
       uint64_t tkey = 0, dkey = 0;
 #pragma unroll 4
@@ -660,9 +661,70 @@ struct Ctx {
         tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
         dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
       }
-      rs.dec[rs.zdst[lane]] = key_index(tkey) | ((p.nD > 0 ? key_index(dkey) : 0) << 24);
+      dec = key_index(tkey) | ((p.nD > 0 ? key_index(dkey) : 0) << 24);
+      rs.dec[rs.zdst[lane]] = dec;
     }
     __syncwarp();
+    return dec;   // lane k: decision of compact joint row k
+  }
+
+  // RNN-T decisions of a round without a per-slot loop: a ballot marks the
+  // non-blank joint rows; slot s's window occupies compact rows zbeg[s] ..
+  // zbeg[s] + zcnt[s] - 1 in frame order (plan_z), so its first non-blank frame
+  // is the lowest set bit of that range (Alg. 3 lines 9-11 / 15-19 for every
+  // frame of the window at once); `dec` is lane k's decision (resolve_rows_w0).
+  __device__ void decide_rnnt(int dec, unsigned *algevals, int Xnext) {
+    if (warp != 0) return;
+    const int W = p.W;
+    const unsigned nb = __ballot_sync(0xffffffffu, lane < rs.nz && (dec & 0xFFFFFF) != p.blank);
+    const bool scan = lane < p.R && rs.scanning[lane];
+    int b0 = 0, c = 0;
+    unsigned m = 0;
+    if (scan) {
+      b0 = rs.zbeg[lane];
+      c = rs.zcnt[lane];
+      m = (nb >> b0) & ((1u << c) - 1u);   // c <= W <= 8
+    }
+    const bool found = m != 0u;
+    const int pos = found ? __ffs(m) - 1 : c;
+    const int y = __shfl_sync(0xffffffffu, dec, found ? b0 + pos : 0) & 0xFFFFFF;
+    int used = scan ? (found ? pos + 1 : c) : 0;
+    bool sc = false;
+    if (scan) {
+      const int s = lane, t0 = rs.t[s];
+      if (found) {
+        rs.found[s] = 1;
+        rs.fy[s] = y;
+        rs.ft[s] = t0 + pos;
+        rs.fd[s] = 0;
+      }
+      rs.t[s] = t0 + pos;
+      // the per-frame label counter restarts whenever t advanced (reading A6/A14)
+      if (pos > 0 || !found) rs.k[s] = 0;
+      if (!found) {
+        if (t0 + pos >= rs.L[s]) rs.active[s] = 0;
+        else sc = true;
+      }
+      rs.scanning[s] = sc;
+    }
+    const unsigned ms = __ballot_sync(0xffffffffu, sc);
+    if (sc) rs.slist[__popc(ms & ((1u << lane) - 1u))] = lane;
+    bool ok = true;
+    if (sc) {
+      const int s = lane;
+      int need = rs.L[s] - rs.t[s];
+      if (need > W) need = W;
+      ok = Xnext >= 0 && rs.t[s] >= rs.fbase[Xnext][s] && rs.t[s] + need <= rs.fbase[Xnext][s] + rs.fcnt[Xnext][s];
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+    used = __reduce_add_sync(0xffffffffu, used);
+    if (lane == 0) {
+      rs.nscan = __popc(ms);
+      rs.ready = all_ok;
+      *algevals += (unsigned)used;
+    }
+    __syncwarp();
+    if (all_ok && Xnext >= 0) plan_z(Xnext);
   }
 
   __device__ void decide(unsigned *algevals, int Xnext) {
@@ -1577,10 +1639,11 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               s_cnt[SC_ROUNDS]++;
               s_cnt[SC_ROWEVALS] += rs.nz;
             }
-            cx.resolve_rows_w0();
+            const int dec = cx.resolve_rows_w0();
             cx.tl_round_(7);
             cx.tl_round_(8);
-            cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
+            if (p.tdt) cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
+            else cx.decide_rnnt(dec, s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
             LL_PHASE(8);
             cx.tl_round_(9);
           }
