@@ -173,7 +173,7 @@ __device__ __forceinline__ void csync(int nthreads) {
 // HC / PC / CC: compile-time joint dim H, predictor dim P and cluster size
 // (0 = runtime).  The production shape (H = P = 640, 16-CTA clusters) is
 // instantiated with all three fixed so that loops unroll and addressing folds.
-template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0>
+template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0>
 struct Ctx {
   static constexpr bool BF = sizeof(T) == 2;
   const DecodeParams &p;
@@ -252,12 +252,20 @@ struct Ctx {
     iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
   }
   __device__ __forceinline__ int Hd() const { return HC ? HC : p.H; }
+  __device__ __forceinline__ bool is_tdt() const { return TM == 0 ? p.tdt != 0 : TM == 2; }
   __device__ __forceinline__ int Pd() const { return PC ? PC : p.P; }
   __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
   __device__ uint8_t *zs() const { return sm + L.off_z; }
   __device__ uint8_t *fbuf(int X) const { return sm + L.off_f + (size_t)X * p.R * p.WF * Hd() * sizeof(T); }
   __device__ float *gs() const { return (float *)(sm + L.off_g); }
+  // bf16 path: g rows are stored as two planes, so that build_z's per-lane
+  // 8-dim chunk c is two CONSECUTIVE float4s across lanes (conflict-free):
+  // dims 8c..8c+3 at float 4c, dims 8c+4..8c+7 at float H/2 + 4c.  f32 path: plain.
+  __device__ __forceinline__ int goff(int d) const {   // d % 4 == 0: float offset of the float4 at dim d
+    if constexpr (BF) return ((d >> 2) & 1) * (Hd() / 2) + (d >> 3) * 4;
+    else return d;
+  }
   __device__ float *cs() const { return (float *)(sm + L.off_c); }
   __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
@@ -391,7 +399,8 @@ struct Ctx {
       for (int k = warp; k < nz; k += NW) {
         const int s = rs.zdst[k] / W;
         const uint4 *frp = reinterpret_cast<const uint4 *>(fbuf(X)) + rs.zsrc[k] / 8;
-        const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
+        const float4 *gr0 = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);   // plane 0
+        const float4 *gr1 = gr0 + H / 8;                                               // plane 1
         uint4 *zr = reinterpret_cast<uint4 *>(zs() + (size_t)k * L.zstride);
         uint4 fv[3];
         float4 ga[3], gb[3];
@@ -400,8 +409,8 @@ struct Ctx {
           const int c = lane + 32 * u;
           if (c < NCH) {
             fv[u] = frp[c];
-            ga[u] = gr[2 * c];
-            gb[u] = gr[2 * c + 1];
+            ga[u] = gr0[c];
+            gb[u] = gr1[c];
           }
         }
 #pragma unroll
@@ -740,7 +749,7 @@ struct Ctx {
       bool found = false;
       while (pos < W && t0 + pos < Ls) {
         const int ee = rs.dec[s * W + pos];
-        const int y = ee & 0xFFFFFF, d = p.tdt ? p.durations[ee >> 24] : 0;
+        const int y = ee & 0xFFFFFF, d = is_tdt() ? p.durations[ee >> 24] : 0;
         ++used;
         if (y != p.blank) {
           rs.found[s] = 1;
@@ -750,7 +759,7 @@ struct Ctx {
           found = true;
           break;
         }
-        pos += p.tdt ? (d > 1 ? d : 1) : 1;
+        pos += is_tdt() ? (d > 1 ? d : 1) : 1;
       }
       rs.t[s] = t0 + pos;
       // the per-frame label counter restarts whenever t advanced (reading A6/A14)
@@ -1200,7 +1209,7 @@ struct Ctx {
           out[j] = acc + __bfloat162float(((const bf16 *)p.b_pred)[d0 + d + j]);
         }
         const int s = rs.plist[i];
-        float *dst = gs() + (size_t)s * H + d0 + d;
+        float *dst = gs() + (size_t)s * H + goff(d0 + d);
         *reinterpret_cast<float4 *>(dst) = make_float4(out[0], out[1], out[2], out[3]);
         const uint64_t lo = ((uint64_t)__float_as_uint(out[1]) << 32) | __float_as_uint(out[0]);
         const uint64_t hi2 = ((uint64_t)__float_as_uint(out[3]) << 32) | __float_as_uint(out[2]);
@@ -1337,7 +1346,7 @@ struct Ctx {
         const float4 v = *reinterpret_cast<const float4 *>(p.tab + ((size_t)kk * V1 + rs.ctx[kk][s]) * H + c * 4);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
-      *reinterpret_cast<float4 *>(gs() + (size_t)s * H + c * 4) = acc;
+      *reinterpret_cast<float4 *>(gs() + (size_t)s * H + goff(c * 4)) = acc;
     }
   }
 
@@ -1431,13 +1440,16 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // ---------------------------------------------------------------------------
 // FL: frame-looping baseline (Alg. 2) instead of label-looping (separate
 // instantiations, so the label-looping kernels carry none of its code).
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false>
+// TM: 0 = RNN-T / TDT chosen at run time (p.tdt), 1 = RNN-T only, 2 = TDT only
+// (the FC instantiations carry only the code of their model family).
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false, int TM = 0>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
   __shared__ Layout s_layout;
-  Ctx<T, KR, HC, PC, CC> cx(p, smem, rs, PRED == 0, s_bars, s_layout);
+  Ctx<T, KR, HC, PC, CC, TM> cx(p, smem, rs, PRED == 0, s_bars, s_layout);
+  const bool tdt = TM == 0 ? p.tdt != 0 : TM == 2;
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
   constexpr bool RING = sizeof(T) == 2 && PRED == 0;
@@ -1642,7 +1654,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             const int dec = cx.resolve_rows_w0();
             cx.tl_round_(7);
             cx.tl_round_(8);
-            if (p.tdt) cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
+            if (tdt) cx.decide(s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
             else cx.decide_rnnt(dec, s_cnt + SC_ALGEVALS, p.spec_prefetch ? (cur ^ 1) : -1);
             LL_PHASE(8);
             cx.tl_round_(9);
@@ -1683,7 +1695,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               }
             }
             rs.len[s] = pos + 1;
-            if (p.tdt && rs.fd[s] > 0) {
+            if (tdt && rs.fd[s] > 0) {
               rs.t[s] += rs.fd[s];
               rs.k[s] = 0;
             } else {
@@ -1780,7 +1792,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __gri
     cx.rebuild_lists();
     for (int idx = tid; idx < M * p.H; idx += blockDim.x) {
       const int i = idx / p.H, c = idx % p.H;
-      cx.gs()[(size_t)i * p.H + c] = p.dbg_g[(size_t)(base + i) * p.H + c];
+      cx.gs()[(size_t)i * p.H + cx.goff(c & ~3) + (c & 3)] = p.dbg_g[(size_t)(base + i) * p.H + c];
     }
     __syncthreads();
     cx.issue_f(0, false);   // the workspace holds f as [n][1][H] (T_max = 1)

@@ -177,9 +177,9 @@ inline int kreg_for(bool bf, int H) { return !bf ? 1 : (H <= KREG_SMALL * 32 + 1
 constexpr int FC_H = 640, FC_P = 640, FC_C = 16;
 inline bool is_fc(bool bf, int H, int P, int C) { return bf && H == FC_H && P == FC_P && C == FC_C; }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false, int TM = 0>
 int max_clusters(int C, const Layout &L) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL, TM>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -201,10 +201,10 @@ int max_clusters(int C, const Layout &L) {
   return n;
 }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false, int TM = 0>
 ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
                         int &used_clusters) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL, TM>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -343,8 +343,8 @@ bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
   if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return false;
   int ncl = 0;
   if (is_fc(bf, H, P, cf.C))
-    ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L)
-               : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C>(cf.C, cf.L);
+    ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, false, 1>(cf.C, cf.L)
+               : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C, false, 1>(cf.C, cf.L);
   else if (bf && kreg_for(bf, H) == KREG)
     ncl = lstm ? max_clusters<bf16, 0, KREG>(cf.C, cf.L) : max_clusters<bf16, 1, KREG>(cf.C, cf.L);
   else if (bf)
@@ -526,8 +526,8 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
   if (frame_looping) {   // Alg. 2 baseline instantiations
     if (is_fc(bf, H, P, C))
-      s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, true>(p, C, L, p.n_groups, st, used)
-               : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, true>(p, C, L, p.n_groups, st, used);
+      s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, true, 1>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, true, 1>(p, C, L, p.n_groups, st, used);
     else if (bf && kreg_for(bf, H) == KREG)
       s = lstm ? launch_decode<bf16, 0, KREG, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
                : launch_decode<bf16, 1, KREG, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
@@ -537,9 +537,12 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     else
       s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
                : launch_decode<float, 1, 1, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
-  } else if (is_fc(bf, H, P, C))
-    s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C>(p, C, L, p.n_groups, st, used)
-             : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C>(p, C, L, p.n_groups, st, used);
+  } else if (is_fc(bf, H, P, C) && tdt)
+    s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, false, 2>(p, C, L, p.n_groups, st, used)
+             : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, false, 2>(p, C, L, p.n_groups, st, used);
+  else if (is_fc(bf, H, P, C))
+    s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, false, 1>(p, C, L, p.n_groups, st, used)
+             : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, false, 1>(p, C, L, p.n_groups, st, used);
   else if (bf && kreg_for(bf, H) == KREG)
     s = lstm ? launch_decode<bf16, 0, KREG>(p, C, L, p.n_groups, st, used)
              : launch_decode<bf16, 1, KREG>(p, C, L, p.n_groups, st, used);
