@@ -247,11 +247,14 @@ struct Ctx {
     const int base = NT / C, rem = NT % C;
     ntiles = base + (rank < rem ? 1 : 0);
     tile0 = rank * base + (rank < rem ? rank : rem);
-    u0 = rank * L.UPC;
-    d0 = rank * L.DPC;
+    u0 = rank * upc();
+    d0 = rank * dpc();
     iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
   }
   __device__ __forceinline__ int Hd() const { return HC ? HC : p.H; }
+  // units / output dims per CTA (compile-time in the FC instantiation)
+  __device__ __forceinline__ int upc() const { return (PC && CC) ? PC / CC : L.UPC; }
+  __device__ __forceinline__ int dpc() const { return (HC && CC) ? HC / CC : L.DPC; }
   __device__ __forceinline__ bool is_tdt() const { return TM == 0 ? p.tdt != 0 : TM == 2; }
   __device__ __forceinline__ int Pd() const { return PC ? PC : p.P; }
   __device__ uint64_t *bar(int i) const { return bars + i; }
@@ -858,8 +861,8 @@ struct Ctx {
   // A producer warp streams the tiles through the NS-slot ring (bulk copies);
   // consumer warp w takes tiles w, w + NW, ... of each phase.
   // -------------------------------------------------------------------------
-  __device__ int ng() const { return L.UPC / 2; }
-  __device__ int npt() const { return L.DPC / 8; }
+  __device__ int ng() const { return upc() / 2; }
+  __device__ int npt() const { return dpc() / 8; }
 
   // W_hh tile PAIRS: pair pp (units u0 + 4pp .. u0 + 4pp + 3) is two 8-row
   // tiles, half 0 = gates (i, f) and half 1 = gates (g, o), row c of a half =
@@ -873,7 +876,7 @@ struct Ctx {
   // so each fragment is 4 consecutive registers of one tcgen05.ld (+4 columns
   // for a 16-wide tail).
   __device__ int tcols() const { return 4 * (Pd() / 32) + ((Pd() & 31) ? 2 : 0); }
-  __device__ int npairs() const { return L.UPC / 4; }
+  __device__ int npairs() const { return upc() / 4; }
   __device__ int quarter_warps(int qd) const { return (NW - qd + 3) / 4; }
   __device__ uint32_t pair_taddr(int pp) const {
     const int w = pp % NW, qd = w & 3;
@@ -997,7 +1000,10 @@ struct Ctx {
     for (int t = 0; t < 3; ++t)
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) acc[t][nb][0] = acc[t][nb][1] = acc[t][nb][2] = acc[t][nb][3] = 0.f;
-    for (int kb = warp; kb < KB; kb += NW) {
+#pragma unroll
+    for (int i = 0; i < (KB + MAX_NW - 1) / MAX_NW; ++i) {   // K blocks warp, warp + NW, ...
+      const int kb = warp + i * NW;
+      if (kb >= KB) break;
       uint4 x[NB];
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) x[nb] = lds128(hrow[nb] + kb * 64);
@@ -1067,13 +1073,13 @@ struct Ctx {
     const int i = 8 * nb + 2 * q + (ev ? 0 : 1);
     if (i < n) {
       const int ul = 4 * pp + (g >> 1);                 // unit within this CTA's slice
-      const float *ep = es() + (size_t)i * 4 * L.UPC + ul;
+      const float *ep = es() + (size_t)i * 4 * upc() + ul;
       const float gi = (ev ? v[0] : r0) + ep[0];
-      const float gf = (ev ? r0 : v[1]) + ep[L.UPC];
-      const float gg = (ev ? v[2] : r1) + ep[2 * L.UPC];
-      const float go = (ev ? r1 : v[3]) + ep[3 * L.UPC];
+      const float gf = (ev ? r0 : v[1]) + ep[upc()];
+      const float gg = (ev ? v[2] : r1) + ep[2 * upc()];
+      const float go = (ev ? r1 : v[3]) + ep[3 * upc()];
       const int s = rs.plist[i];
-      float *cp = cs() + (size_t)s * L.UPC + ul;
+      float *cp = cs() + (size_t)s * upc() + ul;
       const float cn = sigmoidf_(gf) * *cp + sigmoidf_(gi) * tanhf(gg);
       *cp = cn;
       reinterpret_cast<bf16 *>(hsrow(rs.hpar[s] ^ 1, s))[u0 + ul] = __float2bfloat16_rn(sigmoidf_(go) * tanhf(cn));
@@ -1137,20 +1143,20 @@ struct Ctx {
 
     // arm the h' / g exchange barriers for this step (tx from the other CTAs)
     if (tid == 0 && C > 1) {
-      mbar_arrive_expect_tx(bar(BAR_H), (uint32_t)((C - 1) * n * L.UPC * 2));
-      mbar_arrive_expect_tx(bar(BAR_G), (uint32_t)((C - 1) * n * L.DPC * 4));
+      mbar_arrive_expect_tx(bar(BAR_H), (uint32_t)((C - 1) * n * upc() * 2));
+      mbar_arrive_expect_tx(bar(BAR_G), (uint32_t)((C - 1) * n * dpc() * 4));
     }
     // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units.
     // E'[y_i] slices of this CTA's units (4 gates x UPC floats per row) are
     // staged into shared memory by bulk copies that overlap the gate GEMM.
     // (the table's columns are CTA-major: one bulk copy per predictor row)
     if (warp == NW - 1) {
-      const uint32_t segb = (uint32_t)(4 * L.UPC * 4);
+      const uint32_t segb = (uint32_t)(4 * upc() * 4);
       if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)n * segb);
       __syncwarp();
       if (lane < n) {
         const int s = rs.plist[lane];
-        bulk_g2s(es() + (size_t)lane * 4 * L.UPC, p.tab + (size_t)rs.last[s] * 4 * P + (size_t)rank * 4 * L.UPC,
+        bulk_g2s(es() + (size_t)lane * 4 * upc(), p.tab + (size_t)rs.last[s] * 4 * P + (size_t)rank * 4 * upc(),
                  segb, bar(BAR_E));
       }
     }
@@ -1173,7 +1179,7 @@ struct Ctx {
         rs.zsrc[tid] = (rs.hpar[s] ^ 1) * p.R + s;  // row index into hs
       }
       sync();
-      bcast_rows(sm + L.off_hs, L.hstride, u0 * 2, L.UPC * 2, n, rs.zsrc, BAR_H);
+      bcast_rows(sm + L.off_hs, L.hstride, u0 * 2, upc() * 2, n, rs.zsrc, BAR_H);
       mbar_wait(bar(BAR_H), hph());
     }
     tl_pred(4);
@@ -1189,7 +1195,7 @@ struct Ctx {
       sync();
       if (nb0 == 0) tl_pred_bar(10);
       const int nrows = min(16, n - nb0 * 8);
-      const int D4 = L.DPC / 4;
+      const int D4 = dpc() / 4;
       const float4 *wp = reinterpret_cast<const float4 *>(zs());
       for (int idx = tid; idx < nrows * D4; idx += NCT) {
         const int ii = idx / D4, d = (idx % D4) * 4;    // row within the pass, first of 4 dims
@@ -1284,7 +1290,7 @@ struct Ctx {
     const int n = rs.npred, P = Pd(), H = Hd();
     const float *tab = p.tab;
     load_h_rows_f32(n, 0);
-    for (int uu = warp; uu < L.UPC; uu += NW) {
+    for (int uu = warp; uu < upc(); uu += NW) {
       const int unit = u0 + uu;
       float mine[4] = {0.f, 0.f, 0.f, 0.f};
       float acc[MAX_R];
@@ -1301,7 +1307,7 @@ struct Ctx {
         float gate[4];
 #pragma unroll
         for (int gi = 0; gi < 4; ++gi) gate[gi] = mine[gi] + tab[(size_t)y * 4 * P + (size_t)gi * P + unit];
-        float *cp = cs() + (size_t)s * L.UPC + uu;
+        float *cp = cs() + (size_t)s * upc() + uu;
         const float cn = sigmoidf_(gate[1]) * *cp + sigmoidf_(gate[0]) * tanhf(gate[2]);
         *cp = cn;
         ((float *)p.h)[((size_t)(rs.hpar[s] ^ 1) * p.B + rs.b[s]) * P + unit] = sigmoidf_(gate[3]) * tanhf(cn);
@@ -1310,7 +1316,7 @@ struct Ctx {
     __threadfence();
     if (C > 1) cluster_sync_all(); else sync();
     load_h_rows_f32(n, 1);
-    for (int dd = warp; dd < L.DPC; dd += NW) {
+    for (int dd = warp; dd < dpc(); dd += NW) {
       const int d = d0 + dd;
       float acc[MAX_R];
       warp_dot_f32(acc, (const float *)p.w_pred + (size_t)d * P, P, n);
