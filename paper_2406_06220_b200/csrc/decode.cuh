@@ -252,6 +252,16 @@ struct Ctx {
     iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
   }
   __device__ __forceinline__ int Hd() const { return HC ? HC : p.H; }
+  // shared-memory row strides (compile-time in the FC instantiation; must
+  // match make_layout): bf16 z rows / h rows padded by 64 B against bank conflicts
+  __device__ __forceinline__ int zstride() const {
+    if constexpr (BF && HC && PC) return (int)align_up((size_t)(HC > PC ? HC : PC) * 2, 128) + 64;
+    else return L.zstride;
+  }
+  __device__ __forceinline__ int hstride() const {
+    if constexpr (PC != 0) return (int)align_up((size_t)PC * 2, 128) + 64;
+    else return L.hstride;
+  }
   // units / output dims per CTA (compile-time in the FC instantiation)
   __device__ __forceinline__ int upc() const { return (PC && CC) ? PC / CC : L.UPC; }
   __device__ __forceinline__ int dpc() const { return (HC && CC) ? HC / CC : L.DPC; }
@@ -272,7 +282,7 @@ struct Ctx {
   __device__ float *cs() const { return (float *)(sm + L.off_c); }
   __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
-  __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * L.hstride; }
+  __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * hstride(); }
   __device__ float *es() const { return (float *)(sm + L.off_es); }
   __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * Pd() * 2; }
   __device__ void sync() const { csync(NCT); }
@@ -404,7 +414,7 @@ struct Ctx {
         const uint4 *frp = reinterpret_cast<const uint4 *>(fbuf(X)) + rs.zsrc[k] / 8;
         const float4 *gr0 = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);   // plane 0
         const float4 *gr1 = gr0 + H / 8;                                               // plane 1
-        uint4 *zr = reinterpret_cast<uint4 *>(zs() + (size_t)k * L.zstride);
+        uint4 *zr = reinterpret_cast<uint4 *>(zs() + (size_t)k * zstride());
         uint4 fv[3];
         float4 ga[3], gb[3];
 #pragma unroll
@@ -436,7 +446,7 @@ struct Ctx {
         const int s = rs.zdst[k] / W;
         const float4 *frp = reinterpret_cast<const float4 *>(fbuf(X)) + rs.zsrc[k] / 4;
         const float4 *gr = reinterpret_cast<const float4 *>(gs() + (size_t)s * H);
-        float4 *zr = reinterpret_cast<float4 *>(zs() + (size_t)k * L.zstride);
+        float4 *zr = reinterpret_cast<float4 *>(zs() + (size_t)k * zstride());
         for (int c = lane; c < H / 4; c += 32) {
           const float4 fv = frp[c], gv = gr[c];
           zr[c] = make_float4(fmaxf(fv.x + gv.x, 0.f), fmaxf(fv.y + gv.y, 0.f), fmaxf(fv.z + gv.z, 0.f),
@@ -454,10 +464,10 @@ struct Ctx {
   template <int MT>
   __device__ __forceinline__ void joint_mma(float (&acc)[2][2][4]) const {
     const int KB = Hd() / 32;
-    const uint8_t *a0 = zs() + (size_t)g * L.zstride + q * 16;
-    const uint8_t *a1 = a0 + (size_t)8 * L.zstride;
-    const uint8_t *a2 = a0 + (size_t)16 * L.zstride;
-    const uint8_t *a3 = a0 + (size_t)24 * L.zstride;
+    const uint8_t *a0 = zs() + (size_t)g * zstride() + q * 16;
+    const uint8_t *a1 = a0 + (size_t)8 * zstride();
+    const uint8_t *a2 = a0 + (size_t)16 * zstride();
+    const uint8_t *a3 = a0 + (size_t)24 * zstride();
     if (KB == KR) {
       // hot path (H = 640): fully unrolled, no guards, loads can be hoisted
 #pragma unroll
@@ -560,7 +570,7 @@ struct Ctx {
       // butterfly reduction; lane jr keeps the best key of joint row jr.
       uint64_t tkey = 0, dkey = 0;
       const int nrows = ntiles * 8;
-      const int zst = L.zstride / 4;
+      const int zst = zstride() / 4;
       const float *z = (const float *)zs();
       const int M = L.JR;
       for (int lr = warp; lr < nrows; lr += NW) {
@@ -1179,7 +1189,7 @@ struct Ctx {
         rs.zsrc[tid] = (rs.hpar[s] ^ 1) * p.R + s;  // row index into hs
       }
       sync();
-      bcast_rows(sm + L.off_hs, L.hstride, u0 * 2, upc() * 2, n, rs.zsrc, BAR_H);
+      bcast_rows(sm + L.off_hs, hstride(), u0 * 2, upc() * 2, n, rs.zsrc, BAR_H);
       mbar_wait(bar(BAR_H), hph());
     }
     tl_pred(4);
@@ -1246,7 +1256,7 @@ struct Ctx {
   // -------------------------------------------------------------------------
   __device__ __forceinline__ void warp_dot_f32(float (&acc)[MAX_R], const float *wr, int K, int M) const {
     const float *z = (const float *)zs();
-    const int zst = L.zstride / 4;
+    const int zst = zstride() / 4;
 #pragma unroll
     for (int i = 0; i < MAX_R; ++i) acc[i] = 0.f;
     for (int k = lane; k < K; k += 32) {
@@ -1272,7 +1282,7 @@ struct Ctx {
   __device__ void load_h_rows_f32(int n, int which /*0: current hpar, 1: next*/) {
     const int P = Pd();
     float *z = (float *)zs();
-    const int zst = L.zstride / 4;
+    const int zst = zstride() / 4;
     for (int idx = tid; idx < n * P; idx += NCT) {
       const int i = idx / P, c = idx % P;
       const int s = rs.plist[i];
