@@ -69,37 +69,6 @@ enum {
   NBARS = 11 + 2 * NSMAX
 };
 
-struct DecodeParams {
-  int B, T_max, H, P, V1, nD;
-  int blank, max_sym, tdt;
-  int durations[MAX_DUR];
-  int context;
-  int R, W, WF;                  // rows per group, window frames, buffered frames per row
-  int NS;                        // weight-ring slots (bf16 LSTM), 0 otherwise
-  int n_groups, cap;
-  int spec_prefetch;             // speculative next-window prefetch
-  int frame_looping;             // 1: Alg. 2 baseline control flow (RNN-T, W = 1)
-  const int *lengths;
-  const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
-  const void *w_out, *b_out, *w_dur, *b_dur;
-  const void *w_pred, *b_pred, *w_hh;
-  const float *tab;              // LSTM: E' [V1][4P]; stateless: G [ctx][V1][H] (b_pred in G_0)
-  const bf16 *wst;               // bf16 LSTM: per-CTA tile stream [C][NG+NPT][8][P] (packed, swizzled)
-  void *h;                       // f32 LSTM: [2][B][P]
-  float *gglob;                  // f32 LSTM: [B][H]
-  int *out_tokens, *out_timestamps, *out_durations, *out_lengths;
-  int *status;                   // bit0 bad length, bit1 capacity
-  int *group_counter;
-  unsigned long long *stats;     // see ll.h ll_stats
-  unsigned long long *prof;      // optional per-warp timeline of block 0 (LL_TIMELINE_PTR)
-  volatile unsigned *trace;      // debug: host-mapped progress markers [gridDim.x][8] (LL debug hook)
-  // ll_debug_joint mode
-  const float *dbg_g;
-  float *dbg_logits;
-  int *dbg_argmax, *dbg_dargmax;
-  int dbg_n;
-};
-
 // Shared-memory layout (identical on host and device).
 struct Layout {
   int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
@@ -147,6 +116,38 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   return L;
 }
 
+struct DecodeParams {
+  Layout L;                      // shared-memory layout of the launch (read from the constant bank)
+  int B, T_max, H, P, V1, nD;
+  int blank, max_sym, tdt;
+  int durations[MAX_DUR];
+  int context;
+  int R, W, WF;                  // rows per group, window frames, buffered frames per row
+  int NS;                        // weight-ring slots (bf16 LSTM), 0 otherwise
+  int n_groups, cap;
+  int spec_prefetch;             // speculative next-window prefetch
+  int frame_looping;             // 1: Alg. 2 baseline control flow (RNN-T, W = 1)
+  const int *lengths;
+  const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
+  const void *w_out, *b_out, *w_dur, *b_dur;
+  const void *w_pred, *b_pred, *w_hh;
+  const float *tab;              // LSTM: E' [V1][4P]; stateless: G [ctx][V1][H] (b_pred in G_0)
+  const bf16 *wst;               // bf16 LSTM: per-CTA tile stream [C][NG+NPT][8][P] (packed, swizzled)
+  void *h;                       // f32 LSTM: [2][B][P]
+  float *gglob;                  // f32 LSTM: [B][H]
+  int *out_tokens, *out_timestamps, *out_durations, *out_lengths;
+  int *status;                   // bit0 bad length, bit1 capacity
+  int *group_counter;
+  unsigned long long *stats;     // see ll.h ll_stats
+  unsigned long long *prof;      // optional per-warp timeline of block 0 (LL_TIMELINE_PTR)
+  volatile unsigned *trace;      // debug: host-mapped progress markers [gridDim.x][8] (LL debug hook)
+  // ll_debug_joint mode
+  const float *dbg_g;
+  float *dbg_logits;
+  int *dbg_argmax, *dbg_dargmax;
+  int dbg_n;
+};
+
 struct RowState {
   int b[MAX_R], L[MAX_R], t[MAX_R], k[MAX_R], len[MAX_R], last[MAX_R], hpar[MAX_R], hzero[MAX_R];
   int ctx[MAX_CTX][MAX_R];
@@ -177,7 +178,7 @@ template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0>
 struct Ctx {
   static constexpr bool BF = sizeof(T) == 2;
   const DecodeParams &p;
-  const Layout &L;            // in shared memory (uniform; keeps it out of registers)
+  const Layout &L;            // in the kernel parameters (constant bank; uniform, no registers)
   uint8_t *sm;
   RowState &rs;
   uint64_t *bars;
@@ -232,13 +233,12 @@ struct Ctx {
   __device__ void tl_pred_bar(int ph) const { tl_stamp_bar(1, tl_step, ph); }
   uint4 wreg[KR];             // this warp's joint weight tile (bf16), K-permuted fragments
   uint2 wtail;
-  __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm, uint64_t *bars_, Layout &sL)
-      : p(p_), L(sL), sm(sm_), rs(rs_), bars(bars_), phs(0), ntile_c(0) {
+  __device__ Ctx(const DecodeParams &p_, uint8_t *sm_, RowState &rs_, bool lstm, uint64_t *bars_)
+      : p(p_), L(p_.L), sm(sm_), rs(rs_), bars(bars_), phs(0), ntile_c(0) {
+    (void)lstm;
     tl_init();
     C = CC ? CC : (int)cluster_size();
     rank = (int)cluster_rank();
-    if (threadIdx.x == 0) sL = make_layout(BF, lstm, Hd(), Pd(), p.V1, p.nD, p.R, p.W, p.WF, C, p.NS);
-    __syncthreads();
     tid = threadIdx.x; warp = tid >> 5; lane = tid & 31;
     NW = BF ? MAX_NW : L.NW;  // consumer warps
     NCT = NW * 32;           // consumer threads
@@ -1463,8 +1463,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  __shared__ Layout s_layout;
-  Ctx<T, KR, HC, PC, CC, TM> cx(p, smem, rs, PRED == 0, s_bars, s_layout);
+  Ctx<T, KR, HC, PC, CC, TM> cx(p, smem, rs, PRED == 0, s_bars);
   const bool tdt = TM == 0 ? p.tdt != 0 : TM == 2;
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
@@ -1786,8 +1785,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) debug_joint_kernel(const __gri
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  __shared__ Layout s_layout;
-  Ctx<T, KR> cx(p, smem, rs, false, s_bars, s_layout);
+  Ctx<T, KR> cx(p, smem, rs, false, s_bars);
   const int C = cx.C, tid = cx.tid, warp = cx.warp, lane = cx.lane, R = p.R;
   cx.init_barriers();
   cx.load_weight_slice();

@@ -496,6 +496,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.NS = cf.NS;
   p.n_groups = (B + R - 1) / R;
   p.cap = cap;
+  p.L = L;
   p.spec_prefetch = frame_looping ? 0 : env_int("LL_SPEC_PREFETCH", 1);
   p.frame_looping = frame_looping ? 1 : 0;
   p.lengths = lengths;
@@ -707,6 +708,7 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   p.f = ws + w.f;
   p.w_out = joint->w_out; p.b_out = joint->b_out; p.w_dur = joint->w_dur; p.b_dur = joint->b_dur;
   p.dbg_g = g_rows; p.dbg_logits = out_logits; p.dbg_argmax = out_argmax; p.dbg_dargmax = out_dur_argmax;
+  p.L = L;
   p.dbg_n = n;
   const int chunks = (n + R - 1) / R;
   if (bf && kreg_for(bf, H) == KREG) return launch_debug<bf16, KREG>(p, C, L, chunks, st);
