@@ -127,6 +127,7 @@ struct DecodeParams {
   int n_groups, cap;
   int spec_prefetch;             // speculative next-window prefetch
   int frame_looping;             // 1: Alg. 2 baseline control flow (RNN-T, W = 1)
+  int sched;                     // label-looping schedule: 0 = Alg. 3 batched outer loop, 1 = per-row ticks
   const int *lengths;
   const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
   const void *w_out, *b_out, *w_dur, *b_dur;
@@ -155,6 +156,7 @@ struct RowState {
   int fy[MAX_R], ft[MAX_R], fd[MAX_R];
   int fbase[2][MAX_R], fcnt[2][MAX_R];   // frames held in fbuf[X] for each slot
   int slist[MAX_R], plist[MAX_R];
+  int llist[MAX_R], nload;               // per-row schedule: slots whose window must be (re)loaded
   int zsrc[MAX_JR], zdst[MAX_JR];        // live joint rows k: f row offset (elements) / logical row s*W+j
   int dec[MAX_JR];                        // per joint row: token | dur_index << 24
   int zbeg[MAX_R], zcnt[MAX_R];          // per slot: first compact joint row of its window, live rows
@@ -336,15 +338,15 @@ struct Ctx {
     phs ^= 1u << X;
     phs &= ~(1u << (2 + X));
   }
-  __device__ void issue_f(int X, bool spec) {
+  __device__ void issue_f(int X, bool spec, const int *list = nullptr, int nlist = 0) {
     if (fpend(X)) wait_f(X);  // drain a stale speculative copy first
-    const int n = rs.nscan;
+    const int n = list ? nlist : rs.nscan;
     const uint32_t frb = (uint32_t)(Hd() * sizeof(T));
     if (warp == iw) {
       uint32_t bytes = 0;
       int s = 0, base = 0, cnt = 0;
       if (lane < n) {
-        s = rs.slist[lane];
+        s = list ? list[lane] : rs.slist[lane];
         base = rs.t[s] + (spec ? p.W : 0);
         cnt = rs.L[s] - base;
         if (cnt > p.WF) cnt = p.WF;
@@ -842,6 +844,43 @@ struct Ctx {
     used = __reduce_add_sync(0xffffffffu, used);
     if (lane == 0) *algevals += (unsigned)used;
     __syncwarp();
+  }
+
+  // Append + time rules + guard for the slots that found a label this round
+  // (BatchedHyps.add_results; readings A6, A13, A14): warp 0,
+  // lane = slot.  The slot then needs a predictor update before it scans again.
+  __device__ void append_found(bool tdt) {
+    if (warp != 0 || lane >= p.R) return;
+    const int s = lane;
+    if (!rs.found[s]) return;
+    const int b = rs.b[s];
+    const int pos = rs.len[s];
+    if (rank == 0) {
+      if (pos < p.cap) {
+        p.out_tokens[(size_t)b * p.cap + pos] = rs.fy[s];
+        p.out_timestamps[(size_t)b * p.cap + pos] = rs.ft[s];
+        if (p.out_durations) p.out_durations[(size_t)b * p.cap + pos] = rs.fd[s];
+      } else {
+        atomicOr(p.status, 2);
+      }
+    }
+    rs.len[s] = pos + 1;
+    if (tdt && rs.fd[s] > 0) {
+      rs.t[s] += rs.fd[s];
+      rs.k[s] = 0;
+    } else {
+      rs.k[s] += 1;
+      if (rs.k[s] == p.max_sym) {
+        rs.t[s] += 1;
+        rs.k[s] = 0;
+      }
+    }
+    rs.active[s] = rs.t[s] < rs.L[s];
+    rs.needp[s] = rs.active[s];
+    rs.last[s] = rs.fy[s];
+    for (int c = MAX_CTX - 1; c > 0; --c) rs.ctx[c][s] = rs.ctx[c - 1][s];
+    rs.ctx[0][s] = rs.fy[s];
+    rs.found[s] = 0;
   }
 
   // warp 0: rebuild the compacted scanning / predictor lists (ascending slot order)
@@ -1603,6 +1642,104 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
           cx.sync();
           cx.rebuild_lists();
           cx.sync();
+        }
+      } else
+      // ---- per-row schedule (exact reordering of Alg. 3, utterances being
+      // independent): a TICK runs the predictor for the rows that found a label
+      // in the previous tick, then one joint round for every row that scans
+      // (continuing rows and the rows just updated).  A row never waits for the
+      // other rows of its group to find their labels.
+      if (p.sched == 1) {
+        if (warp == 0 && lane < R) {
+          rs.scanning[lane] = 0;
+          rs.found[lane] = 0;
+        }
+        __syncwarp();
+        cx.rebuild_lists();
+        cx.sync();
+        bool have_spec = false;        // fbuf[cur ^ 1] holds the previous tick's speculative windows
+        while (rs.nactive > 0) {
+          if (t0) s_cnt[SC_OUTER]++;
+          if (have_spec) {
+            cx.wait_f(cur ^ 1);
+            cur ^= 1;
+          }
+          // (1) windows: a continuing row whose speculative window starts at its t
+          // reuses it; every other row about to scan gets a fresh window
+          if (warp == 0) {
+            bool ld = false;
+            if (lane < R) {
+              const int s = lane;
+              const bool cont = rs.scanning[s], np = rs.needp[s];
+              const bool reuse = have_spec && cont && rs.fbase[cur][s] == rs.t[s];
+              ld = (cont || np) && !reuse;
+            }
+            const unsigned ml = __ballot_sync(0xffffffffu, ld);
+            if (ld) rs.llist[__popc(ml & ((1u << lane) - 1u))] = lane;
+            if (lane == 0) rs.nload = __popc(ml);
+          }
+          cx.sync();
+          if (rs.nload > 0) cx.issue_f(cur, false, rs.llist, rs.nload);
+          cx.tl_pred_bar(8);
+          // (2) predictor (Alg. 3 line 6) for the rows that found a label
+          if (rs.npred > 0) {
+            if (t0) {
+              s_cnt[SC_PRED]++;
+              s_cnt[SC_PREDROWS] += rs.npred;
+            }
+            if constexpr (PRED == 1) cx.predictor_stateless();
+            else if constexpr (RING) cx.predictor_lstm_tmem();
+            else cx.predictor_lstm_f32();
+          }
+          if (cx.fpend(cur)) cx.wait_f(cur);
+          if (warp == 0 && lane < R) {
+            rs.scanning[lane] = rs.scanning[lane] || rs.needp[lane];
+            rs.needp[lane] = 0;
+          }
+          __syncwarp();
+          cx.rebuild_lists();
+          cx.sync();
+          have_spec = false;
+          if (rs.nscan > 0) {
+            // (3) one joint round (Alg. 3 lines 7-19 over a W-frame window)
+            cx.tl_round_(0);
+            cx.plan_z(cur);
+            cx.sync();
+            cx.tl_round_bar(1);
+            cx.build_z(cur);
+            cx.tl_round_(2);
+            cx.sync();
+            if (p.spec_prefetch) {
+              cx.issue_f(cur ^ 1, true);
+              have_spec = true;
+            }
+            cx.tl_round_bar(3);
+            cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
+            cx.tl_round_(4);
+            cx.exchange_keys();
+            cx.tl_round_(5);
+            if (warp == 0) {
+              cx.exchange_wait();
+              cx.tl_round_(6);
+              if (t0) {
+                s_cnt[SC_ROUNDS]++;
+                s_cnt[SC_ROWEVALS] += rs.nz;
+              }
+              const int dec = cx.resolve_rows_w0();
+              cx.tl_round_(7);
+              cx.tl_round_(8);
+              if (tdt) cx.decide(s_cnt + SC_ALGEVALS, -1);
+              else cx.decide_rnnt(dec, s_cnt + SC_ALGEVALS, -1);
+              cx.append_found(tdt);
+              __syncwarp();
+              cx.rebuild_lists();
+              cx.tl_round_(9);
+            }
+            cx.flip_par();
+            cx.sync();
+            cx.tl_round_bar(10);
+            cx.tl_next_round();
+          }
         }
       } else
       // ---- outer loop over labels (Alg. 3 line 5) -----------------------------

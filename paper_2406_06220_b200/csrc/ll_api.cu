@@ -499,6 +499,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.L = L;
   p.spec_prefetch = frame_looping ? 0 : env_int("LL_SPEC_PREFETCH", 1);
   p.frame_looping = frame_looping ? 1 : 0;
+  p.sched = env_int("LL_SCHEDULE", 1);
   p.lengths = lengths;
   p.f = ws + w.f;
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;

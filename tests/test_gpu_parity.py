@@ -72,6 +72,7 @@ def test_cat_dog_through_abi(dtype, window, monkeypatch):
     if window:
         monkeypatch.setenv("LL_WINDOW", str(window))
         monkeypatch.setenv("LL_GROUP_ROWS", "4")
+        monkeypatch.setenv("LL_SCHEDULE", "0")   # the paper's batched outer loop (Alg. 3 as listed)
     spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
     hyps, dec = gpu_decode(spec, w, enc, lengths, dtype)
     assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
@@ -342,3 +343,24 @@ def test_prepare_tables_reuse_and_invalidate():
     dec.model = ma                                          # back: tables were rebuilt for mb
     h = dec.decode(e, l).hypotheses()
     assert [(x[0], x[1]) for x in h] == [(p[0], p[1]) for p in planted]
+
+
+@pytest.mark.parametrize("cfg", ["fc-rnnt", "fc-tdt"])
+def test_schedules_identical(cfg, monkeypatch):
+    """The per-row tick schedule (default) and the paper's batched outer loop
+    (LL_SCHEDULE=0) are exact reorderings of Alg. 3: identical hypotheses on a
+    random-family FC batch (near-ties included), and identical joint-evaluation
+    counts (the algorithmic decisions)."""
+    c = synth.CONFIGS[cfg]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 41, blank_bias=3.0 if not spec.is_tdt else 1.0)
+    enc, lengths = synth.make_inputs(42, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
+    model = gpu_model(spec, w)
+    out = {}
+    for sched in ("0", "1"):
+        monkeypatch.setenv("LL_SCHEDULE", sched)
+        hyps, dec = gpu_decode(spec, w, enc, lengths, model=model)
+        out[sched] = (hyps, dec.stats())
+    assert out["0"][0] == out["1"][0]
+    assert out["0"][1]["joint_evals"] == out["1"][1]["joint_evals"]
+    assert out["0"][1]["labels"] == out["1"][1]["labels"]
