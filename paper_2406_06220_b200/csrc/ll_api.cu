@@ -27,7 +27,9 @@ using namespace ll;
 namespace {
 
 constexpr size_t HDR_BYTES = 4096;  // [0] status, [1] group counter, [16..] stats (u64 x 8 at byte 64)
-constexpr int RPREF_MANY = 7;       // rows per group when the batch spans many waves (measured)
+// rows per group when the batch spans many waves (measured under the per-row
+// tick schedule: LSTM sweep best at 8, stateless config 4 at 16)
+constexpr int RPREF_MANY_LSTM = 8, RPREF_MANY_STATELESS = 16;
 constexpr size_t SMEM_LIMIT = 232448;
 
 struct Ws {
@@ -129,7 +131,7 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
   // throughput mode: when one wave would need more than 8 rows per group, run
   // many waves of small groups instead (groups are taken from a work counter,
   // so the clusters stay busy; small groups keep the multi-frame window wide)
-  if (!forceR && Rpref > 8) Rpref = RPREF_MANY;
+  if (!forceR && Rpref > 8) Rpref = lstm ? RPREF_MANY_LSTM : RPREF_MANY_STATELESS;
   if (Rpref < 1) Rpref = 1;
   if (Rpref > MAX_R) Rpref = MAX_R;
   for (int C = 1; C <= MAX_C; C *= 2) {
