@@ -1493,11 +1493,13 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // ---------------------------------------------------------------------------
 // The decode kernel.  PRED: 0 = LSTM, 1 = stateless.
 // ---------------------------------------------------------------------------
-// FL: frame-looping baseline (Alg. 2) instead of label-looping (separate
-// instantiations, so the label-looping kernels carry none of its code).
+// LM (loop mode): 0 = label-looping, schedule chosen at run time (p.sched);
+// 1 = label-looping, per-row ticks only; 2 = label-looping, the batched outer
+// loop of Alg. 3 only; 3 = the frame-looping baseline (Alg. 2).  Separate
+// instantiations, so a kernel carries only the control code it runs.
 // TM: 0 = RNN-T / TDT chosen at run time (p.tdt), 1 = RNN-T only, 2 = TDT only
 // (the FC instantiations carry only the code of their model family).
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false, int TM = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
@@ -1588,7 +1590,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
       cx.sync();
 
       // ---- frame-looping baseline (Alg. 2): frames in lockstep ----------------
-      if constexpr (FL) {
+      if constexpr (LM == 3) {
         if (warp == 0 && lane < R) rs.scanning[lane] = rs.active[lane];
         __syncwarp();
         cx.rebuild_lists();
@@ -1649,7 +1651,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
       // in the previous tick, then one joint round for every row that scans
       // (continuing rows and the rows just updated).  A row never waits for the
       // other rows of its group to find their labels.
-      if (p.sched == 1) {
+      if (LM == 1 || (LM == 0 && p.sched == 1)) {
         if (warp == 0 && lane < R) {
           rs.scanning[lane] = 0;
           rs.found[lane] = 0;

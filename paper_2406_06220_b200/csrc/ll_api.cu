@@ -179,9 +179,9 @@ inline int kreg_for(bool bf, int H) { return !bf ? 1 : (H <= KREG_SMALL * 32 + 1
 constexpr int FC_H = 640, FC_P = 640, FC_C = 16;
 inline bool is_fc(bool bf, int H, int P, int C) { return bf && H == FC_H && P == FC_P && C == FC_C; }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false, int TM = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0>
 int max_clusters(int C, const Layout &L) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL, TM>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, LM, TM>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
   if (C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -203,10 +203,10 @@ int max_clusters(int C, const Layout &L) {
   return n;
 }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, bool FL = false, int TM = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0>
 ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
                         int &used_clusters) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, FL, TM>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, LM, TM>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -345,8 +345,8 @@ bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
   if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return false;
   int ncl = 0;
   if (is_fc(bf, H, P, cf.C))
-    ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, false, 1>(cf.C, cf.L)
-               : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C, false, 1>(cf.C, cf.L);
+    ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1>(cf.C, cf.L)
+               : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 1>(cf.C, cf.L);
   else if (bf && kreg_for(bf, H) == KREG)
     ncl = lstm ? max_clusters<bf16, 0, KREG>(cf.C, cf.L) : max_clusters<bf16, 1, KREG>(cf.C, cf.L);
   else if (bf)
@@ -530,23 +530,31 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
   if (frame_looping) {   // Alg. 2 baseline instantiations
     if (is_fc(bf, H, P, C))
-      s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, true, 1>(p, C, L, p.n_groups, st, used)
-               : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, true, 1>(p, C, L, p.n_groups, st, used);
+      s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 3, 1>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 3, 1>(p, C, L, p.n_groups, st, used);
     else if (bf && kreg_for(bf, H) == KREG)
-      s = lstm ? launch_decode<bf16, 0, KREG, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
-               : launch_decode<bf16, 1, KREG, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
+      s = lstm ? launch_decode<bf16, 0, KREG, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used);
     else if (bf)
-      s = lstm ? launch_decode<bf16, 0, KREG_SMALL, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
-               : launch_decode<bf16, 1, KREG_SMALL, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
+      s = lstm ? launch_decode<bf16, 0, KREG_SMALL, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG_SMALL, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used);
     else
-      s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, true>(p, C, L, p.n_groups, st, used)
-               : launch_decode<float, 1, 1, 0, 0, 0, true>(p, C, L, p.n_groups, st, used);
-  } else if (is_fc(bf, H, P, C) && tdt)
-    s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, false, 2>(p, C, L, p.n_groups, st, used)
-             : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, false, 2>(p, C, L, p.n_groups, st, used);
-  else if (is_fc(bf, H, P, C))
-    s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, false, 1>(p, C, L, p.n_groups, st, used)
-             : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, false, 1>(p, C, L, p.n_groups, st, used);
+      s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used)
+               : launch_decode<float, 1, 1, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used);
+  } else if (is_fc(bf, H, P, C)) {   // one instantiation per (predictor, family, schedule)
+    const int k = (tdt ? 2 : 0) + (p.sched == 1 ? 0 : 1);
+    if (lstm) {
+      if (k == 0) s = launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1>(p, C, L, p.n_groups, st, used);
+      else if (k == 1) s = launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 2, 1>(p, C, L, p.n_groups, st, used);
+      else if (k == 2) s = launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 2>(p, C, L, p.n_groups, st, used);
+      else s = launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 2, 2>(p, C, L, p.n_groups, st, used);
+    } else {
+      if (k == 0) s = launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 1>(p, C, L, p.n_groups, st, used);
+      else if (k == 1) s = launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 2, 1>(p, C, L, p.n_groups, st, used);
+      else if (k == 2) s = launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 2>(p, C, L, p.n_groups, st, used);
+      else s = launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 2, 2>(p, C, L, p.n_groups, st, used);
+    }
+  }
   else if (bf && kreg_for(bf, H) == KREG)
     s = lstm ? launch_decode<bf16, 0, KREG>(p, C, L, p.n_groups, st, used)
              : launch_decode<bf16, 1, KREG>(p, C, L, p.n_groups, st, used);
