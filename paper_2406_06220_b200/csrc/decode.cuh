@@ -1122,12 +1122,12 @@ struct Ctx {
     const int i = 8 * nb + 2 * q + (ev ? 0 : 1);
     if (i < n) {
       const int ul = 4 * pp + (g >> 1);                 // unit within this CTA's slice
-      const float *ep = es() + (size_t)i * 4 * upc() + ul;
+      const int s = rs.plist[i];
+      const float *ep = es() + (size_t)s * 4 * upc() + ul;
       const float gi = (ev ? v[0] : r0) + ep[0];
       const float gf = (ev ? r0 : v[1]) + ep[upc()];
       const float gg = (ev ? v[2] : r1) + ep[2 * upc()];
       const float go = (ev ? r1 : v[3]) + ep[3 * upc()];
-      const int s = rs.plist[i];
       float *cp = cs() + (size_t)s * upc() + ul;
       const float cn = sigmoidf_(gf) * *cp + sigmoidf_(gi) * tanhf(gg);
       *cp = cn;
@@ -1185,7 +1185,23 @@ struct Ctx {
                                                                 acc[t][nb][3]);
   }
 
-  __device__ void predictor_lstm_tmem() {
+  // E'[y] slices (this CTA's 4 x UPC gate inputs) of `n` slots into es[slot]
+  // by one bulk copy each, completing on BAR_E (one warp; lane 0 arms it).
+  // The E' table's columns are CTA-major, so each slice is contiguous.
+  __device__ void issue_eprime(const int *slots, int n) {
+    const uint32_t segb = (uint32_t)(4 * upc() * 4);
+    if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)n * segb);
+    __syncwarp();
+    if (lane < n) {
+      const int s = slots[lane];
+      bulk_g2s(es() + (size_t)s * 4 * upc(), p.tab + (size_t)rs.last[s] * 4 * Pd() + (size_t)rank * 4 * upc(), segb,
+               bar(BAR_E));
+    }
+  }
+
+  // eprefetched: the E' slices of this step were issued when the labels were
+  // decided (tick schedule); otherwise they are fetched here.
+  __device__ void predictor_lstm_tmem(bool eprefetched = false) {
     tl_pred(0);
     const int n = rs.npred;
     const int P = Pd(), H = Hd();
@@ -1199,16 +1215,7 @@ struct Ctx {
     // E'[y_i] slices of this CTA's units (4 gates x UPC floats per row) are
     // staged into shared memory by bulk copies that overlap the gate GEMM.
     // (the table's columns are CTA-major: one bulk copy per predictor row)
-    if (warp == NW - 1) {
-      const uint32_t segb = (uint32_t)(4 * upc() * 4);
-      if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)n * segb);
-      __syncwarp();
-      if (lane < n) {
-        const int s = rs.plist[lane];
-        bulk_g2s(es() + (size_t)lane * 4 * upc(), p.tab + (size_t)rs.last[s] * 4 * P + (size_t)rank * 4 * upc(),
-                 segb, bar(BAR_E));
-      }
-    }
+    if (!eprefetched && warp == NW - 1) issue_eprime(rs.plist, n);
     {
       bool e_ready = false;
       for (int nb0 = 0; nb0 * 8 < n; nb0 += 2) {
@@ -1658,6 +1665,10 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         }
         __syncwarp();
         cx.rebuild_lists();
+        __syncwarp();
+        if constexpr (RING) {          // SOS inputs of the first predictor step
+          if (warp == 0 && rs.npred > 0) cx.issue_eprime(rs.plist, rs.npred);
+        }
         cx.sync();
         bool have_spec = false;        // fbuf[cur ^ 1] holds the previous tick's speculative windows
         while (rs.nactive > 0) {
@@ -1690,7 +1701,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               s_cnt[SC_PREDROWS] += rs.npred;
             }
             if constexpr (PRED == 1) cx.predictor_stateless();
-            else if constexpr (RING) cx.predictor_lstm_tmem();
+            else if constexpr (RING) cx.predictor_lstm_tmem(true);
             else cx.predictor_lstm_f32();
           }
           if (cx.fpend(cur)) cx.wait_f(cur);
@@ -1735,6 +1746,10 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               cx.append_found(tdt);
               __syncwarp();
               cx.rebuild_lists();
+              __syncwarp();
+              if constexpr (RING) {    // next tick's predictor inputs, fetched now
+                if (rs.npred > 0) cx.issue_eprime(rs.plist, rs.npred);
+              }
               cx.tl_round_(9);
             }
             cx.flip_par();
