@@ -67,11 +67,21 @@ def workload(cfg_name, seed, family="planted"):
         if spec.is_tdt:
             w, enc, lengths, _ = synth.make_planted_tdt(spec, seed, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
         else:
-            w, enc, lengths, _ = synth.make_planted_rnnt(spec, seed, c["B"], c["T_max"], c["len_lo"], c["len_hi"])
+            w, enc, lengths, _ = synth.make_planted_rnnt(spec, seed, c["B"], c["T_max"], c["len_lo"], c["len_hi"],
+                                                         rho=c.get("rho", 0.28))
     else:
         w = synth.make_weights(spec, seed, blank_bias=3.0 if spec.joint_dim > 64 else 0.5)
         enc, lengths = synth.make_inputs(seed + 1, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     return spec, w, enc, lengths
+
+
+def frame_s_of(cfg_name):
+    """Seconds of audio per encoder frame (8x subsampling: 80 ms, PAPER.md:233;
+    the 4x-subsampling variant: 40 ms)."""
+    return synth.CONFIGS.get(cfg_name, {}).get("frame_s", synth.frame_seconds)
+
+
+spec_name_hint = ["fc-rnnt"]
 
 
 def algorithmic_flops(spec, stats, total_frames):
@@ -149,8 +159,9 @@ def oracle_worker(args):
     return len(r.tokens)
 
 
-def cpu_oracle_time(spec, w, enc, lengths, n_utt):
+def cpu_oracle_time(spec, w, enc, lengths, n_utt, cfg_name="fc-rnnt"):
     """Time the float64 oracle (as it stands) on the host cores: one utterance per task."""
+    spec_name_hint[0] = cfg_name
     import multiprocessing as mp
     cores = os.cpu_count() or 1
     idx = list(range(min(n_utt, enc.shape[0])))
@@ -162,7 +173,7 @@ def cpu_oracle_time(spec, w, enc, lengths, n_utt):
         t0 = time.perf_counter()
         pool.map(oracle_worker, tasks, chunksize=1)
         dt = time.perf_counter() - t0
-    audio = float(sum(int(lengths[b]) for b in idx)) * synth.frame_seconds
+    audio = float(sum(int(lengths[b]) for b in idx)) * frame_s_of(spec_name_hint[0])
     return audio / dt, dt, procs, len(idx), audio
 
 
@@ -198,7 +209,7 @@ def run_reference(a, rank, world):
     n = a.cpu_sample or enc.shape[0]
     times = []
     for i in range(a.warmup + a.steps):
-        v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc, lengths, n)
+        v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc, lengths, n, a.config)
         if i >= a.warmup:
             times.append((v, dt))
     value = statistics.mean(v for v, _ in times)
@@ -317,7 +328,7 @@ def main():
     h2d = enc_h.numel() * enc_h.element_size() + len_h.numel() * 4
     d2h = (out_tok.numel() + out_ts.numel() + out_len.numel()) * 4
 
-    audio_s = float(len_np.sum()) * synth.frame_seconds
+    audio_s = float(len_np.sum()) * frame_s_of(a.config)
     t_all = torch.tensor([tot_ms, sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
@@ -369,7 +380,7 @@ def main():
     }
     if rank == 0 and not a.no_cpu_baseline:
         n = a.cpu_sample or B
-        v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc_np, len_np, n)
+        v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc_np, len_np, n, a.config)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
                                 "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch, "
                                           f"{dt:.1f} s wall"}

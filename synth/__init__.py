@@ -463,6 +463,11 @@ CONFIGS = {
     # (3) TDT at FastConformer shapes, durations {0..4}
     "fc-tdt": dict(spec=ModelSpec(1025, 512, 640, 640, "lstm", 1, (0, 1, 2, 3, 4), 0, 10), B=32,
                    T_max=275, len_lo=225, len_hi=275),
+    # (2') 4x subsampling variant of config 2 (40 ms frames, Table 4
+    # :322-339): the same ~20 s utterances are twice as many frames; planted
+    # token rate halved per frame (same tokens per second)
+    "fc-rnnt-4x": dict(spec=ModelSpec(1025, 512, 640, 640, "lstm", 1, None, 0, 10), B=32, T_max=550,
+                       len_lo=450, len_hi=550, frame_s=0.04, rho=0.14),
     # (4) large-batch stateless (context 2): B=512, lengths 50..1500, enc 1024
     "stateless-b512": dict(spec=ModelSpec(1025, 1024, 640, 640, "stateless", 2, None, 0, 10), B=512,
                            T_max=1500, len_lo=50, len_hi=1500),

@@ -364,3 +364,16 @@ def test_schedules_identical(cfg, monkeypatch):
     assert out["0"][0] == out["1"][0]
     assert out["0"][1]["joint_evals"] == out["1"][1]["joint_evals"]
     assert out["0"][1]["labels"] == out["1"][1]["labels"]
+
+
+def test_fc_rnnt_4x_subsampling_planted():
+    """4x-subsampling variant of config 2 (40 ms frames, T ~ 500; PAPER.md
+    Table 4): decode == planted alignment at full size, sampled rows verified."""
+    c = synth.CONFIGS["fc-rnnt-4x"]
+    spec = c["spec"]
+    w, enc, lengths, planted = synth.make_planted_rnnt(spec, 8, c["B"], c["T_max"], c["len_lo"], c["len_hi"],
+                                                       rho=c["rho"])
+    hyps, _ = gpu_decode(spec, w, enc, lengths, "bf16")
+    for b in range(c["B"]):
+        assert (hyps[b][0], hyps[b][1]) == (planted[b][0], planted[b][1]), b
+    verify_all(spec, w, enc, lengths, hyps, rows=[0, 31])
