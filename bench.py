@@ -216,7 +216,8 @@ def run_reference(a, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(d for _, d in times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if a.config in synth.SWEEPS else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": a.config, "family": a.family, "sample_utts": nutt},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle",
                          "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch per step"},

@@ -377,3 +377,35 @@ def test_fc_rnnt_4x_subsampling_planted():
     for b in range(c["B"]):
         assert (hyps[b][0], hyps[b][1]) == (planted[b][0], planted[b][1]), b
     verify_all(spec, w, enc, lengths, hyps, rows=[0, 31])
+
+
+def test_sweep_chunks_pack_unpack():
+    """Config-5 plumbing on one GPU: utterances of a LibriSpeech-like sweep,
+    LPT-sharded and decoded longest-first in two launches; the device-packed
+    ragged buffer unpacks to exactly the per-utterance planted alignments."""
+    from paper_2406_06220_b200 import shard
+    c = synth.SWEEPS["sweep-tdt"]
+    spec = c["spec"]
+    w, codes = synth.planted_weights(spec, 1000)
+    L_all = synth.sweep_lengths(c["length_seed"], 96)
+    ids = shard.rank_shard(L_all, 2, 1, 16)           # rank 1 of 2
+    model = gpu_model(spec, w)
+    outs, planted = [], {}
+    for c0 in range(0, len(ids), 24):
+        cid = ids[c0:c0 + 24]
+        T = int(L_all[cid].max())
+        enc = np.zeros((len(cid), T, spec.enc_dim), dtype=np.float32)
+        for i, u in enumerate(cid):
+            e, pl = synth.planted_utterance(spec, codes, c["length_seed"], int(u), int(L_all[u]))
+            enc[i, :e.shape[0]] = e
+            planted[int(u)] = pl
+        dec = LabelLoopingDecoder(model, spec.max_symbols, len(cid), T)
+        out = dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16),
+                         torch.from_numpy(L_all[cid].astype(np.int32)).cuda())
+        outs.append((torch.from_numpy(cid).cuda(), out))
+    buf = shard.pack_hypotheses([i for i, _ in outs], [o.lengths for _, o in outs], [o.tokens for _, o in outs],
+                                [o.timestamps for _, o in outs], [o.durations for _, o in outs])
+    got = shard.unpack_hypotheses(buf.cpu().numpy(), True)
+    assert sorted(got) == sorted(int(u) for u in ids)
+    for u in ids:
+        assert got[int(u)] == tuple(planted[int(u)]), int(u)
