@@ -548,7 +548,7 @@ struct Ctx {
           }
           tk[mt][rr] = umax64(tk[mt][rr], shfl_xor_u64(tk[mt][rr], 1));
           tk[mt][rr] = umax64(tk[mt][rr], shfl_xor_u64(tk[mt][rr], 2));
-          if (p.nD > 0) {
+          if (is_tdt()) {
             dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 1));
             dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 2));
           }
@@ -633,9 +633,13 @@ struct Ctx {
 #pragma unroll
       for (int w = 0; w < MAX_NW; ++w) {
         if (w < NW) {
-          const uint4 v = *reinterpret_cast<const uint4 *>(wk + ((size_t)w * L.JR + jr) * 2);
-          tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
-          dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
+          if (is_tdt()) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(wk + ((size_t)w * L.JR + jr) * 2);
+            tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
+            dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
+          } else {   // RNN-T: the token key only
+            tkey = umax64(tkey, wk[((size_t)w * L.JR + jr) * 2]);
+          }
         }
       }
       const uint32_t slot = smem_u32(pt + ((size_t)rank * L.JR + jr) * 2);
@@ -664,7 +668,7 @@ struct Ctx {
       }
     }
     y = key_index(tkey);
-    di = p.nD > 0 ? key_index(dkey) : 0;
+    di = is_tdt() ? key_index(dkey) : 0;
   }
 
   // Apply the decisions of one round (warp 0): lane k resolves live joint row
@@ -681,11 +685,15 @@ struct Ctx {
       uint64_t tkey = 0, dkey = 0;
 #pragma unroll 4
       for (int r = 0; r < C; ++r) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + lane) * 2);
-        tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
-        dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
+        if (is_tdt()) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + lane) * 2);
+          tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
+          dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
+        } else {     // RNN-T: the token key only
+          tkey = umax64(tkey, pt[((size_t)r * L.JR + lane) * 2]);
+        }
       }
-      dec = key_index(tkey) | ((p.nD > 0 ? key_index(dkey) : 0) << 24);
+      dec = key_index(tkey) | ((is_tdt() ? key_index(dkey) : 0) << 24);
       rs.dec[rs.zdst[lane]] = dec;
     }
     __syncwarp();

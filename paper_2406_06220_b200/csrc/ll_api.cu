@@ -713,6 +713,7 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   DecodeParams p;
   memset(&p, 0, sizeof(p));
   p.B = n; p.T_max = 1; p.H = H; p.P = joint->pred_dim; p.V1 = V1; p.nD = num_durations;
+  p.tdt = num_durations > 0 ? 1 : 0;   // the joint's duration head
   p.R = R;
   p.W = 1;
   p.WF = 1;
