@@ -36,7 +36,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     if not force and os.path.exists(lib) and not any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS):
         return lib
     defs = {"": [], "timeline": ["-DLL_TIMELINE"], "trace": ["-DLL_DEBUG_TRACE"]}[variant]
-    cmd = [NVCC] + FLAGS + defs + ["-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp"] + SOURCES
+    tmp = f"{lib}.tmp{os.getpid()}"   # per process: concurrent ranks may build at once; os.replace is atomic
+    cmd = [NVCC] + FLAGS + defs + ["-I", os.path.join(ROOT, "include"), "-o", tmp] + SOURCES
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
@@ -46,7 +47,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     if not variant:
         with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
             fh.write(r.stderr)
-    os.replace(lib + ".tmp", lib)
+    os.replace(tmp, lib)
     return lib
 
 
