@@ -436,6 +436,9 @@ def run_sweep(a, rank, world, local, dev):
         chunks[-1]["dec"].prepare()
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    gather = shard.NcclGather(device=dev)   # ll_gather_ragged on a libll NCCL communicator (world 1 too)
+    for ch in chunks:
+        ch["ids32"] = ch["ids"].to(torch.int32)
 
     def step(e2e=False):
         for ch in chunks:
@@ -445,17 +448,21 @@ def run_sweep(a, rank, world, local, dev):
             s = ch["dec"].launch(ch["enc"], ch["lengths"])
             if s != ll.LL_OK:
                 raise ll.LLError(s, "decode")
-        packed = shard.pack_hypotheses([ch["ids"] for ch in chunks], [ch["dec"].lengths_out for ch in chunks],
-                                       [ch["dec"].tokens for ch in chunks], [ch["dec"].timestamps for ch in chunks],
-                                       [ch["dec"].durs for ch in chunks] if tdt else None)
-        bufs = shard.gather_ragged(packed, tdt, unpack=False) if world > 1 else [packed]
-        if e2e and bufs is not None:   # D2H of the gathered hypotheses
+        bufs = [gather.gather(ch["ids32"], ch["dec"].lengths_out, ch["dec"].tokens, ch["dec"].timestamps,
+                              ch["dec"].durs if tdt else None) for ch in chunks]
+        if rank != 0:
+            return None
+        if e2e:   # D2H of the gathered hypotheses
             return [b.cpu() for b in bufs]
         return bufs
 
     for _ in range(a.warmup):
-        step()
+        gathered = step()
     torch.cuda.synchronize()
+    gathered_ok = True
+    if rank == 0:   # the gathered records hold every utterance once; this rank's equal their planted alignments
+        merged = shard.unpack_records(torch.cat(gathered).cpu().numpy(), tdt)
+        gathered_ok = len(merged) == int(c["n_utt"]) and all(merged[u] == tuple(planted[u]) for u in planted)
     for ch in chunks:
         if ch["dec"].sync() != ll.LL_OK:
             raise RuntimeError("sweep decode failed")
@@ -515,14 +522,18 @@ def run_sweep(a, rank, world, local, dev):
         "utterances_per_s": a.steps * n_utt / (tot_ms / 1e3),
         "e2e": {"value": a.steps * audio_s / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_tot / a.steps},
-        "gpu_launches": a.steps * len(chunks) * 2,   # projection GEMM + decode per chunk (tables prepared)
+        # per chunk: projection GEMM + decode + the two packing kernels of ll_gather_ragged (NCCL's own
+        # all-gather / send-recv kernels not counted); model tables prepared once before timing
+        "gpu_launches": a.steps * len(chunks) * 4,
         "hypotheses_equal_planted": bad_max == 0,
+        "gathered_hypotheses_ok": gathered_ok,
     }
     clocks = clk.summary()
     if clocks:
         line["clocks"] = clocks
     if rank == 0:
         print(json.dumps(line), flush=True)
+    gather.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -222,6 +222,57 @@ ll_status ll_set_timing_events(void *ev_before_decode, void *ev_after_decode);
 /* Library version string. */
 const char *ll_version(void);
 
+/*
+ * Multi-GPU: gathering the ragged hypotheses (SURVEY.md §8(b) ll_gather_ragged;
+ * north_star "NCCL is used only to gather the ragged results").  Utterances are
+ * independent (Alg. 1 decodes each on its own), so ranks decode
+ * disjoint shards with no data-path collective; this is the one exchange.
+ *
+ * NCCL is resolved at run time (dlopen of libnccl.so.2, preferring the copy the
+ * process already loaded, e.g. PyTorch's); without it these calls return
+ * LL_ERR_UNSUPPORTED.  A communicator is an opaque handle (ncclComm_t).
+ *
+ * ll_nccl_unique_id: writes the 128-byte NCCL unique id to HOST `id_out`; call
+ *   on one rank and share the bytes with all ranks (e.g. torch.distributed).
+ * ll_nccl_comm_init: collective over `nranks` processes, one GPU each (the
+ *   current CUDA device); *comm_out receives the handle.
+ * ll_nccl_comm_destroy: frees a handle (NULL is a no-op).
+ */
+ll_status ll_nccl_unique_id(void *id_out);
+ll_status ll_nccl_comm_init(void **comm_out, int32_t nranks, const void *id, int32_t rank);
+ll_status ll_nccl_comm_destroy(void *comm);
+
+/* Device workspace (bytes) ll_gather_ragged needs for B rows of out_capacity. */
+size_t ll_gather_workspace_size(int32_t B, int32_t out_capacity, int32_t with_durations);
+
+/*
+ * ll_gather_ragged: collective over the communicator.  Each rank packs its B
+ * decoded rows (the outputs of one or more ll_decode_* calls, concatenated by
+ * the caller) into one int32 record on the device
+ *     [n, ids[n], lens[n], tokens(ragged), timestamps(ragged)(, durations(ragged))]
+ * with lens[i] = min(lengths[i], out_capacity) and the ragged fields the first
+ * lens[i] entries of each row, in row order; the records of all ranks are then
+ * concatenated in rank order into `root_buf` on rank `root` (ncclAllGather of
+ * the record sizes, then ncclSend / ncclRecv of the records).
+ *   utt_ids      DEVICE int32 [B]: global utterance id of each row
+ *   lengths      DEVICE int32 [B]: the decoders' out_lengths
+ *   tokens, timestamps  DEVICE int32 [B, out_capacity];  durations likewise or NULL
+ *   root_buf     DEVICE int32 [root_capacity] on root (ignored elsewhere)
+ *   root_capacity  elements of root_buf; every rank passes the same value
+ *   root_used    HOST int64 out (every rank): elements written on root
+ *   workspace    DEVICE, >= ll_gather_workspace_size(B, out_capacity, durations != NULL)
+ * Synchronises `stream` once (the record sizes are needed on the host to post
+ * the receives).  Returns LL_ERR_CAPACITY on every rank, with nothing
+ * written and *root_used = the elements needed, when the records do not fit
+ * root_capacity (so every rank can retry with a larger root buffer); LL_ERR_INVALID_ARGUMENT
+ * for NULL pointers or B < 0; LL_ERR_CUDA for CUDA or NCCL failures.  B = 0
+ * contributes the record [0].
+ */
+ll_status ll_gather_ragged(void *comm, int32_t root, int32_t B, const int32_t *utt_ids, const int32_t *lengths,
+                           const int32_t *tokens, const int32_t *timestamps, const int32_t *durations,
+                           int32_t out_capacity, int32_t *root_buf, int64_t root_capacity, int64_t *root_used,
+                           void *workspace, size_t workspace_bytes, ll_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

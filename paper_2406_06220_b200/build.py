@@ -14,12 +14,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libll.so")
-SOURCES = [os.path.join(HERE, "csrc", "ll_api.cu")]
+SOURCES = [os.path.join(HERE, "csrc", "ll_api.cu"), os.path.join(HERE, "csrc", "ll_gather.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "linear.cuh", "decode.cuh", "gemm_tc.cuh")] + \
     [os.path.join(ROOT, "include", "ll.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-ldl"]
 
 
 def needs_build() -> bool:

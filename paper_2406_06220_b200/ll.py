@@ -24,7 +24,9 @@ LL_PRED_LSTM, LL_PRED_STATELESS = 0, 1
 EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_rnnt_frame_looping", "ll_decode_tdt", "ll_prepare",
             "ll_sync",
             "ll_status_string",
-            "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version"]
+            "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version",
+            "ll_nccl_unique_id", "ll_nccl_comm_init", "ll_nccl_comm_destroy", "ll_gather_workspace_size",
+            "ll_gather_ragged"]
 
 
 class ll_predictor(ctypes.Structure):
@@ -86,6 +88,18 @@ def load_library() -> ctypes.CDLL:
     lib.ll_set_timing_events.restype = c_int32
     lib.ll_version.argtypes = []
     lib.ll_version.restype = c_char_p
+    lib.ll_nccl_unique_id.argtypes = [c_void_p]
+    lib.ll_nccl_unique_id.restype = c_int32
+    lib.ll_nccl_comm_init.argtypes = [POINTER(c_void_p), c_int32, c_void_p, c_int32]
+    lib.ll_nccl_comm_init.restype = c_int32
+    lib.ll_nccl_comm_destroy.argtypes = [c_void_p]
+    lib.ll_nccl_comm_destroy.restype = c_int32
+    lib.ll_gather_workspace_size.argtypes = [c_int32, c_int32, c_int32]
+    lib.ll_gather_workspace_size.restype = c_size_t
+    lib.ll_gather_ragged.argtypes = [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_int32, c_void_p, ctypes.c_int64, POINTER(ctypes.c_int64), c_void_p, c_size_t,
+                                     c_void_p]
+    lib.ll_gather_ragged.restype = c_int32
     _lib = lib
     return lib
 
@@ -159,3 +173,36 @@ def ll_debug_joint(enc_rows, g_rows, n, joint, dtype, prec, num_durations, out_l
 
 def ll_set_timing_events(ev_before_decode, ev_after_decode) -> int:
     return int(load_library().ll_set_timing_events(ev_before_decode, ev_after_decode))
+
+
+def ll_nccl_unique_id():
+    """(status, 128-byte NCCL unique id)."""
+    buf = ctypes.create_string_buffer(128)
+    st = int(load_library().ll_nccl_unique_id(buf))
+    return st, buf.raw
+
+
+def ll_nccl_comm_init(nranks: int, uid: bytes, rank: int):
+    """(status, opaque communicator handle)."""
+    comm = c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    st = int(load_library().ll_nccl_comm_init(ctypes.byref(comm), nranks, buf, rank))
+    return st, comm.value
+
+
+def ll_nccl_comm_destroy(comm) -> int:
+    return int(load_library().ll_nccl_comm_destroy(comm))
+
+
+def ll_gather_workspace_size(B: int, out_capacity: int, with_durations: bool) -> int:
+    return int(load_library().ll_gather_workspace_size(B, out_capacity, int(bool(with_durations))))
+
+
+def ll_gather_ragged(comm, root, B, utt_ids, lengths, tokens, timestamps, durations, out_capacity, root_buf,
+                     root_capacity, workspace, workspace_bytes, stream):
+    """(status, elements written on root / needed on LL_ERR_CAPACITY)."""
+    used = ctypes.c_int64(0)
+    st = int(load_library().ll_gather_ragged(comm, root, B, utt_ids, lengths, tokens, timestamps, durations,
+                                             out_capacity, root_buf, root_capacity, ctypes.byref(used),
+                                             workspace, workspace_bytes, stream))
+    return st, int(used.value)

@@ -10,9 +10,14 @@ the end (north_star: "NCCL is used only to gather the ragged results").
   ends with its longest row, so length-sorted batches waste the fewest
   frames); batches go to ranks by LPT greedy (longest processing time first,
   to the least-loaded rank) on the cost max_len(batch).
-* ``pack_hypotheses`` / ``gather_ragged``: device-side packing of one rank's
-  results into a flat int32 buffer and an all-gather of the ragged buffers over
-  ``torch.distributed`` (NCCL on GPUs, gloo in the CPU tests).
+* ``NcclGather``: the native exchange -- ``ll_gather_ragged`` of the C ABI
+  (packing kernels + ncclAllGather of the record sizes + ncclSend/ncclRecv of
+  the records to the root) on a libll NCCL communicator whose unique id is
+  broadcast over ``torch.distributed``.  ``unpack_records`` parses the root
+  buffer.  This is what bench.py's sweep uses on GPUs.
+* ``pack_hypotheses`` / ``gather_ragged``: the same record format built with
+  torch ops and all-gathered over ``torch.distributed`` -- the host-side model
+  of the exchange, exercised with gloo (world size 2) in the CPU tests.
 
 Everything here is plumbing: no step of the decoding method runs in this file.
 """
@@ -101,6 +106,78 @@ def unpack_hypotheses(buf: np.ndarray, with_durations: bool) -> Dict[int, Tuple[
         a, b = starts[i], starts[i + 1]
         out[int(ids[i])] = tuple(f[a:b].tolist() for f in fields)
     return out
+
+
+def unpack_records(buf: np.ndarray, with_durations: bool) -> Dict[int, Tuple[list, ...]]:
+    """Parse a concatenation of records (the root buffer of ll_gather_ragged:
+    one record per rank per call) into {utterance id: hypothesis}."""
+    nf = 3 if with_durations else 2
+    out: Dict[int, Tuple[list, ...]] = {}
+    off = 0
+    while off < len(buf):
+        n = int(buf[off])
+        tot = int(buf[off + 1 + n:off + 1 + 2 * n].astype(np.int64).sum())
+        size = 1 + 2 * n + nf * tot
+        out.update(unpack_hypotheses(buf[off:off + size], with_durations))
+        off += size
+    return out
+
+
+class NcclGather:
+    """The C-ABI gather (ll_gather_ragged) on one libll NCCL communicator per
+    process group.  Collective: construct and call on every rank."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        from . import ll
+        self.ll = ll
+        init = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if init else 0
+        self.world = dist.get_world_size(group) if init else 1
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        uid = b"\0" * 128
+        if self.rank == 0:
+            st, uid = ll.ll_nccl_unique_id()
+            if st != ll.LL_OK:
+                raise ll.LLError(st, "ll_nccl_unique_id")
+        if self.world > 1:   # share the id (the process group's own backend carries it)
+            t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).clone()
+            if dist.get_backend(group) == "nccl":
+                t = t.to(self.device)
+            dist.broadcast(t, 0, group=group)
+            uid = bytes(t.cpu().numpy().tobytes())
+        st, self.comm = ll.ll_nccl_comm_init(self.world, uid, self.rank)
+        if st != ll.LL_OK:
+            raise ll.LLError(st, "ll_nccl_comm_init")
+        self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._root = torch.empty(1 << 16, dtype=torch.int32, device=self.device)
+
+    def gather(self, ids, lengths, tokens, timestamps, durations=None, root: int = 0, stream=None):
+        """Gather one set of decoded rows (ids/lengths [B], tokens... [B, cap] int32
+        device tensors) on `root`.  Returns the root's int32 device buffer
+        (records of all ranks in rank order) on root, None elsewhere."""
+        ll = self.ll
+        B, cap = int(ids.numel()), int(tokens.shape[1])
+        need = ll.ll_gather_workspace_size(B, cap, durations is not None)
+        if self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        ptr = lambda t: None if t is None else t.data_ptr()
+        for _ in range(2):   # at most one retry: LL_ERR_CAPACITY reports the size needed on every rank
+            st, used = ll.ll_gather_ragged(self.comm, root, B, ptr(ids), ptr(lengths), ptr(tokens), ptr(timestamps),
+                                           ptr(durations), cap, ptr(self._root), self._root.numel(),
+                                           ptr(self._ws), self._ws.numel(), s)
+            if st != ll.LL_ERR_CAPACITY:
+                break
+            self._root = torch.empty(max(used, 2 * self._root.numel()), dtype=torch.int32, device=self.device)
+        if st != ll.LL_OK:
+            raise ll.LLError(st, "ll_gather_ragged")
+        return self._root[:used].clone() if self.rank == root else None
+
+    def close(self):
+        if self.comm:
+            self.ll.ll_nccl_comm_destroy(self.comm)
+            self.comm = None
 
 
 def gather_ragged(packed: torch.Tensor, with_durations: bool, group=None, unpack: bool = True):

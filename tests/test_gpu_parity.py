@@ -409,3 +409,40 @@ def test_sweep_chunks_pack_unpack():
     assert sorted(got) == sorted(int(u) for u in ids)
     for u in ids:
         assert got[int(u)] == tuple(planted[int(u)]), int(u)
+    # the native exchange (ll_gather_ragged, world size 1): one record per
+    # launch, byte-identical to the torch-built record, parsing to the same map
+    g = shard.NcclGather()
+    try:
+        recs = [g.gather(i.to(torch.int32), o.lengths, o.tokens, o.timestamps, o.durations) for i, o in outs]
+    finally:
+        g.close()
+    for (i, o), r in zip(outs, recs):
+        assert torch.equal(r, shard.pack_hypotheses(i, o.lengths, o.tokens, o.timestamps, o.durations))
+    assert shard.unpack_records(torch.cat(recs).cpu().numpy(), True) == got
+
+
+@pytest.mark.parametrize("B,cap,tdt", [(0, 5, False), (1, 1, True), (37, 7, False), (1500, 9, True), (2100, 3, False)])
+def test_native_gather_records(B, cap, tdt):
+    """ll_gather_ragged's packing kernels on ragged rows: lengths beyond the
+    capacity are clamped, empty rows and B = 0 give well-formed records, more
+    than 1024 rows exercise the multi-pass scan; the result equals the
+    torch-built record element by element.  A root buffer that is too small is
+    reported (LL_ERR_CAPACITY with the size needed) and the retry succeeds."""
+    from paper_2406_06220_b200 import shard
+    gen = torch.Generator().manual_seed(B * 31 + cap)
+    ids = torch.randperm(max(B, 1) * 3, generator=gen)[:B].to(torch.int32).cuda()
+    lens = torch.randint(0, cap + 4, (B,), generator=gen, dtype=torch.int32).cuda()
+    tok = torch.randint(0, 1 << 20, (B, cap), generator=gen, dtype=torch.int32).cuda()
+    ts = torch.randint(0, 1 << 20, (B, cap), generator=gen, dtype=torch.int32).cuda()
+    du = torch.randint(0, 5, (B, cap), generator=gen, dtype=torch.int32).cuda() if tdt else None
+    g = shard.NcclGather()
+    try:
+        g._root = torch.empty(1, dtype=torch.int32, device="cuda")   # force the capacity path
+        got = g.gather(ids, lens, tok, ts, du)
+        again = g.gather(ids, lens, tok, ts, du)
+    finally:
+        g.close()
+    ref = shard.pack_hypotheses(ids, lens, tok, ts, du)
+    assert torch.equal(got, ref) and torch.equal(again, ref)
+    if B == 0:
+        assert got.tolist() == [0]

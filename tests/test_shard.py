@@ -60,6 +60,23 @@ def _fake_results(ids, cap, tdt, seed):
 
 
 @pytest.mark.parametrize("tdt", [False, True])
+def test_unpack_records_concatenation(tdt):
+    """The root buffer of ll_gather_ragged is a concatenation of records (one
+    per rank per call, an empty record being [0]); unpack_records parses it to
+    the union of the records' hypotheses."""
+    parts, want = [], {}
+    for k, ids in enumerate([np.array([5, 2]), np.array([], dtype=np.int64), np.array([9, 1, 4])]):
+        lens, tok, ts, du = _fake_results(ids, 6, tdt, 10 + k)
+        buf = shard.pack_hypotheses(torch.from_numpy(ids), torch.from_numpy(lens), torch.from_numpy(tok),
+                                    torch.from_numpy(ts), None if du is None else torch.from_numpy(du))
+        parts.append(buf)
+        want.update(shard.unpack_hypotheses(buf.numpy(), tdt))
+    assert parts[1].tolist() == [0]
+    got = shard.unpack_records(torch.cat(parts).numpy(), tdt)
+    assert got == want and sorted(got) == [1, 2, 4, 5, 9]
+
+
+@pytest.mark.parametrize("tdt", [False, True])
 def test_pack_unpack_roundtrip(tdt):
     ids = np.array([7, 3, 11, 0])
     lens, tok, ts, du = _fake_results(ids, 9, tdt, 1)
