@@ -365,6 +365,7 @@ struct Ctx {
           bulk_g2s(fbuf(X) + (size_t)s * p.WF * frb, src, bytes, bar(BAR_F + X));
         }
       }
+      __syncwarp();   // reconverge before the caller's (aligned) CTA barrier
     }
     phs |= 1u << (2 + X);
   }
@@ -903,10 +904,11 @@ struct Ctx {
       const unsigned below = (1u << lane) - 1u;
       if (sc) rs.slist[__popc(ms & below)] = lane;
       if (pr) rs.plist[__popc(mp & below)] = lane;
-      if (lane == 0) {
-        rs.nscan = __popc(ms);
-        rs.npred = __popc(mp);
-        rs.nactive = __popc(ma);
+      if (lane == 0) {   // written only when they change: the other warps may be reading them
+        const int ns = __popc(ms), np = __popc(mp), na = __popc(ma);
+        if (rs.nscan != ns) rs.nscan = ns;
+        if (rs.npred != np) rs.npred = np;
+        if (rs.nactive != na) rs.nactive = na;
       }
     }
   }
@@ -1418,6 +1420,7 @@ struct Ctx {
       }
       *reinterpret_cast<float4 *>(gs() + (size_t)s * H + goff(c * 4)) = acc;
     }
+    sync();   // every warp is done with plist / npred before warp 0 rebuilds the lists
   }
 
   // -------------------------------------------------------------------------
@@ -1624,6 +1627,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             __syncwarp();
           }
           if (rs.nscan == 0) {         // every row is done with frame t: t += 1 for all (line 22)
+            cx.sync();                 // every warp has read the counters rebuilt below
             if (warp == 0 && lane < R && rs.active[lane]) {
               rs.t[lane] += 1;
               rs.k[lane] = 0;
@@ -1711,14 +1715,17 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             if constexpr (PRED == 1) cx.predictor_stateless();
             else if constexpr (RING) cx.predictor_lstm_tmem(true);
             else cx.predictor_lstm_f32();
+            // the predicted rows scan from now on (with no predictor rows the
+            // lists are unchanged, and rewriting the counters here would race
+            // with the other warps' read of npred above: no barrier separates them)
+            if (warp == 0 && lane < R) {
+              rs.scanning[lane] = rs.scanning[lane] || rs.needp[lane];
+              rs.needp[lane] = 0;
+            }
+            __syncwarp();
+            cx.rebuild_lists();
           }
           if (cx.fpend(cur)) cx.wait_f(cur);
-          if (warp == 0 && lane < R) {
-            rs.scanning[lane] = rs.scanning[lane] || rs.needp[lane];
-            rs.needp[lane] = 0;
-          }
-          __syncwarp();
-          cx.rebuild_lists();
           cx.sync();
           have_spec = false;
           if (rs.nscan > 0) {

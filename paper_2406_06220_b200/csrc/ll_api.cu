@@ -134,7 +134,10 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
   if (!forceR && Rpref > 8) Rpref = lstm ? RPREF_MANY_LSTM : RPREF_MANY_STATELESS;
   if (Rpref < 1) Rpref = 1;
   if (Rpref > MAX_R) Rpref = MAX_R;
-  for (int C = 1; C <= MAX_C; C *= 2) {
+  // clusters of >= 2 CTAs: the kernels' DSMEM traffic (st.async to mapa'd
+  // addresses) is defined for real clusters (compute-sanitizer rejects a
+  // 1-CTA cluster)
+  for (int C = 2; C <= MAX_C; C *= 2) {
     if (forceC && C != forceC) continue;
     const int NT = (V1 + nD + 7) / 8;
     if (bf && (NT + C - 1) / C > MAX_NW) continue;   // one vocab tile per warp
