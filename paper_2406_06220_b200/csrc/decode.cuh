@@ -893,6 +893,10 @@ struct Ctx {
   }
 
   // warp 0: rebuild the compacted scanning / predictor lists (ascending slot order)
+  // GUARDED: the counters are written only when they change, for call sites
+  // where other warps may still be reading them (no barrier since their last
+  // read); the hot per-tick sites follow a CTA barrier and write unguarded.
+  template <bool GUARDED = true>
   __device__ void rebuild_lists() {
     if (warp == 0) {
       const bool sc = lane < p.R && rs.scanning[lane];
@@ -904,11 +908,16 @@ struct Ctx {
       const unsigned below = (1u << lane) - 1u;
       if (sc) rs.slist[__popc(ms & below)] = lane;
       if (pr) rs.plist[__popc(mp & below)] = lane;
-      if (lane == 0) {   // written only when they change: the other warps may be reading them
-        const int ns = __popc(ms), np = __popc(mp), na = __popc(ma);
-        if (rs.nscan != ns) rs.nscan = ns;
-        if (rs.npred != np) rs.npred = np;
-        if (rs.nactive != na) rs.nactive = na;
+      if constexpr (GUARDED) {   // one lane per counter: the three compares are one load
+        if (lane < 3) {
+          int *cnt = lane == 0 ? &rs.nscan : lane == 1 ? &rs.npred : &rs.nactive;
+          const int v = __popc(lane == 0 ? ms : lane == 1 ? mp : ma);
+          if (*cnt != v) *cnt = v;
+        }
+      } else if (lane == 0) {
+        rs.nscan = __popc(ms);
+        rs.npred = __popc(mp);
+        rs.nactive = __popc(ma);
       }
     }
   }
@@ -1723,7 +1732,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               rs.needp[lane] = 0;
             }
             __syncwarp();
-            cx.rebuild_lists();
+            cx.template rebuild_lists<false>();   // after the predictor's / round's barriers
           }
           if (cx.fpend(cur)) cx.wait_f(cur);
           cx.sync();
@@ -1760,7 +1769,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               else cx.decide_rnnt(dec, s_cnt + SC_ALGEVALS, -1);
               cx.append_found(tdt);
               __syncwarp();
-              cx.rebuild_lists();
+              cx.template rebuild_lists<false>();   // after the predictor's / round's barriers
               __syncwarp();
               if constexpr (RING) {    // next tick's predictor inputs, fetched now
                 if (rs.npred > 0) cx.issue_eprime(rs.plist, rs.npred);
