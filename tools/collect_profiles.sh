@@ -7,6 +7,15 @@ o=gpurun_out
 for c in fc-rnnt fc-tdt stateless-b512; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $o/${t}_bench_$c.json 2> $o/${t}_bench_$c.err
 done
+timeout 600 python bench.py --config fc-rnnt-4x --steps 10 --warmup 3 > $o/${t}_bench_fc-rnnt-4x.json 2> $o/${t}_bench_fc-rnnt-4x.err
+for c in fc-rnnt stateless-b512 fc-rnnt-4x; do
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --frame-looping --no-cpu-baseline \
+    > $o/${t}_bench_${c}_frame-looping.json 2> $o/${t}_bench_${c}_frame-looping.err
+done
+for c in fc-rnnt fc-tdt; do
+  LL_SCHEDULE=0 timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline \
+    > $o/${t}_bench_${c}_alg3-batched.json 2> $o/${t}_bench_${c}_alg3-batched.err
+done
 for c in sweep-rnnt sweep-tdt; do
   timeout 900 python bench.py --config $c --steps 3 --warmup 1 --no-cpu-baseline > $o/${t}_bench_$c.json 2> $o/${t}_bench_$c.err
 done
