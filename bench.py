@@ -466,12 +466,26 @@ def run_sweep(a, rank, world, local, dev):
     for ch in chunks:
         ch["ids32"] = ch["ids"].to(torch.int32)
 
+    h2d_s = torch.cuda.Stream(device=dev)
+    ev_in = [torch.cuda.Event() for _ in chunks]
+    ev_dec = [torch.cuda.Event() for _ in chunks]
+    for e in ev_dec:
+        e.record(stream)
+
     def step(e2e=False):
-        for ch in chunks:
-            if e2e:   # H2D of the chunk's ragged frames, scattered into the padded layout
-                dst = ch["enc"].view(-1, spec.enc_dim)
-                dst.index_copy_(0, ch["rows"], ch["frames"].to(dev, non_blocking=True))
-            s = ch["dec"].launch(ch["enc"], ch["lengths"])
+        if e2e:   # H2D of every chunk's ragged frames (scattered into the padded layout) on a copy
+            # stream, so chunk k+1's copy overlaps chunk k's decode
+            with torch.cuda.stream(h2d_s):
+                for k, ch in enumerate(chunks):
+                    h2d_s.wait_event(ev_dec[k])     # the chunk's previous decode has read its inputs
+                    dst = ch["enc"].view(-1, spec.enc_dim)
+                    dst.index_copy_(0, ch["rows"], ch["frames"].to(dev, non_blocking=True))
+                    ev_in[k].record(h2d_s)
+        for k, ch in enumerate(chunks):
+            if e2e:
+                stream.wait_event(ev_in[k])
+            s = ch["dec"].launch(ch["enc"], ch["lengths"], stream)
+            ev_dec[k].record(stream)
             if s != ll.LL_OK:
                 raise ll.LLError(s, "decode")
         bufs = [gather.gather(ch["ids32"], ch["dec"].lengths_out, ch["dec"].tokens, ch["dec"].timestamps,
