@@ -133,3 +133,22 @@ def test_no_oracle_in_product_path():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 assert not pat.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_gather_validation(lib):
+    """ll_gather_ragged / NCCL helpers: host-side argument checks return before
+    any NCCL or CUDA call."""
+    F = FAKE
+    assert ll.ll_gather_workspace_size(-1, 5, False) == 0
+    assert ll.ll_gather_workspace_size(0, 5, False) > 0
+    assert ll.ll_gather_workspace_size(100, 5, True) > ll.ll_gather_workspace_size(100, 5, False)
+    assert lib.ll_nccl_unique_id(None) == ll.LL_ERR_INVALID_ARGUMENT
+    assert ll.ll_nccl_comm_init(0, b"\0" * 128, 0)[0] == ll.LL_ERR_INVALID_ARGUMENT
+    assert ll.ll_nccl_comm_init(2, b"\0" * 128, 2)[0] == ll.LL_ERR_INVALID_ARGUMENT
+    assert ll.ll_nccl_comm_destroy(None) == ll.LL_OK
+    args = dict(comm=F, root=0, B=4, utt_ids=F, lengths=F, tokens=F, timestamps=F, durations=None,
+                out_capacity=8, root_buf=F, root_capacity=1000, workspace=F, workspace_bytes=1 << 30, stream=None)
+    for bad in [dict(comm=None), dict(B=-1), dict(workspace=None), dict(out_capacity=-1), dict(root_capacity=-1),
+                dict(utt_ids=None), dict(lengths=None), dict(tokens=None), dict(timestamps=None)]:
+        kw = {**args, **bad}
+        assert ll.ll_gather_ragged(*kw.values())[0] == ll.LL_ERR_INVALID_ARGUMENT, bad
