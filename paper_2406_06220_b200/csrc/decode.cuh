@@ -684,7 +684,7 @@ struct Ctx {
     int dec = 0;
     if (lane < nz) {
       uint64_t tkey = 0, dkey = 0;
-#pragma unroll 4
+#pragma unroll 16
       for (int r = 0; r < C; ++r) {
         if (is_tdt()) {
           const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + lane) * 2);
