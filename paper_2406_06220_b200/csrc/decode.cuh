@@ -645,6 +645,7 @@ struct Ctx {
       }
       const uint32_t slot = smem_u32(pt + ((size_t)rank * L.JR + jr) * 2);
       const uint32_t bb = smem_u32(bar(BAR_X + par()));
+#pragma unroll 16
       for (int d = 0; d < C; ++d) {
         const int dst = (rank + d) % C;
         st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, dkey, mapa_u32(bb, (uint32_t)dst));
@@ -1295,6 +1296,7 @@ struct Ctx {
         const uint64_t lo = ((uint64_t)__float_as_uint(out[1]) << 32) | __float_as_uint(out[0]);
         const uint64_t hi2 = ((uint64_t)__float_as_uint(out[3]) << 32) | __float_as_uint(out[2]);
         const uint32_t la = smem_u32(dst);
+#pragma unroll 16
         for (int c = 1; c < C; ++c) {
           const uint32_t dr = (uint32_t)((rank + c) % C);
           st_async_u64x2(mapa_u32(la, dr), lo, hi2, mapa_u32(bg, dr));
