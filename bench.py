@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--family", default="planted", choices=["planted", "random"])
     ap.add_argument("--frame-looping", action="store_true",
                     help="time the Alg. 2 frame-looping baseline (ll_decode_rnnt_frame_looping) instead")
+    ap.add_argument("--schedule", default="ticks", choices=["ticks", "batched"],
+                    help="label-looping schedule: per-row ticks (default) or the batched outer loop of Alg. 3 as listed")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0: auto)")
     return ap.parse_args()
@@ -241,6 +243,9 @@ def main():
     from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
     llbuild.build()
+    if a.schedule == "batched":     # the paper's batched outer loop (Alg. 3 as listed), this thread
+        if ll.ll_set_options(ll.options(schedule=0).opts) != ll.LL_OK:
+            raise RuntimeError("ll_set_options")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -165,12 +165,13 @@ ll_status ll_decode_rnnt_frame_looping(const void *enc, ll_dtype dtype, ll_prec 
  * tables of a decode call (LSTM: E' = Emb W_ih^T + b_ih + b_hh and the packed
  * W_hh / W_pred tile stream; stateless: G_k = W_pred[:, k] Emb_k) into
  * `workspace` and records their fingerprint (weight pointers, shapes, dtype,
- * cluster layout) for that workspace (the tables sit at batch-independent
+ * cluster layout, workspace size) for that workspace (the tables sit at batch-independent
  * offsets, so decodes of any B <= the workspace's B reuse them).  A later ll_decode_* on the
  * same workspace whose fingerprint matches skips rebuilding them; any other
  * decode on the workspace rebuilds them and drops the record.  Call it again
  * after modifying weights IN PLACE (the fingerprint holds pointers, not
- * contents).  Arguments as ll_decode_*: durations is HOST [num_durations] for
+ * contents), and ll_release() the workspace before freeing it or the weights.
+ * Arguments as ll_decode_*: durations is HOST [num_durations] for
  * TDT, NULL for RNN-T; B / T_max are the batch shape the workspace was sized
  * for.  Stream-ordered; host validation errors return synchronously.
  */
@@ -221,6 +222,66 @@ ll_status ll_set_timing_events(void *ev_before_decode, void *ev_after_decode);
 
 /* Library version string. */
 const char *ll_version(void);
+
+/*
+ * Drops the record ll_prepare() keeps for `workspace` (its model tables are
+ * rebuilt by the next decode on it).  Call it before freeing or reusing a
+ * workspace's memory: the record is keyed by the workspace address and the
+ * weight pointers, and a caching allocator can hand the same addresses to
+ * other weights.  Unknown or NULL workspaces are a no-op.  Host-only, no
+ * stream work.  (ll_debug_joint drops the record of the workspace it uses.)
+ */
+ll_status ll_release(void *workspace);
+
+/*
+ * Test / debug options of the decode calls made AFTERWARDS FROM THIS HOST
+ * THREAD (thread-local; ll_set_options(NULL) restores the defaults).  The
+ * production path reads no environment variable: every knob that changes the
+ * kernel path is here, explicit.  Zero / -1 fields mean "library default".
+ *
+ *  cluster_size, group_rows, window   force the cluster size C (2..16), rows
+ *                 per group R (1..32) and multi-frame window W (1..8; R*W <= 32)
+ *                 instead of the occupancy-based choice.
+ *  max_clusters   cap on concurrently resident clusters (0: all).
+ *  schedule       -1 default (per-row ticks), 0 the batched outer loop of
+ *                 Alg. 3 as listed, 1 per-row ticks.
+ *  spec_prefetch  -1 default (on), 0 off, 1 on: speculative next-window copies.
+ *  gemm_mma_sync  1: encoder projection on the mma.sync GEMM instead of tcgen05.
+ *  timeline       DEVICE u64 buffer for the per-warp timeline (libll_timeline
+ *                 builds only; ignored by libll.so).
+ *  trace          host-mapped u32 progress markers (libll_trace builds only).
+ *
+ *  Probe (parity tests of the production FastConformer instantiations, H = P
+ *  = 640 in 16-CTA clusters, per-row tick schedule; other shapes return
+ *  LL_ERR_UNSUPPORTED while a probe is set).  The SAME decode kernel code is
+ *  instantiated with a probe hook that also writes, per cluster region
+ *  r < probe_regions (at most probe_regions clusters run):
+ *    probe_logits  DEVICE f32 [probe_regions][probe_rows][V+1+|D|]: the logits
+ *                  (token then duration) of every joint row the kernel evaluated
+ *    probe_lmeta   DEVICE i32 [probe_regions][probe_rows][4]: (utterance b,
+ *                  frame t, labels emitted by b before this evaluation, 0)
+ *    probe_g       DEVICE f32 [probe_regions][probe_rows][H]: the predictor
+ *                  output g = W_pred dec + b_pred after every predictor step
+ *    probe_gmeta   DEVICE i32 [probe_regions][probe_rows][4]: (b, labels the
+ *                  predictor has consumed = hypothesis length, 0, 0)
+ *    probe_counts  DEVICE i32 [probe_regions][2]: logit rows, g rows written
+ *                  (values > probe_rows mean the region was truncated)
+ *  Set probe_logits = NULL to disable the probe.
+ */
+typedef struct {
+  int32_t cluster_size, group_rows, window, max_clusters;
+  int32_t schedule, spec_prefetch, gemm_mma_sync;
+  void *timeline;
+  void *trace;
+  float *probe_logits;
+  int32_t *probe_lmeta;
+  float *probe_g;
+  int32_t *probe_gmeta;
+  int32_t *probe_counts;
+  int32_t probe_rows, probe_regions;
+} ll_options;
+
+ll_status ll_set_options(const ll_options *options);
 
 /*
  * Multi-GPU: gathering the ragged hypotheses (SURVEY.md §8(b) ll_gather_ragged;

@@ -10,10 +10,10 @@
 //
 //   outer step (label loop, Alg. 3 line 5):
 //     predictor phase (Alg. 3 line 6) for rows that found a label and are still
-//       active.  LSTM (bf16): gates = E'[y] + W_hh h on tensor cores; the W_hh /
-//       W_pred tiles of this CTA stream through a shared-memory ring filled by
-//       a dedicated producer warp with bulk (TMA-engine) copies -- it runs ahead
-//       and prefetches the next step's tiles while the scan is running; gate
+//       active.  LSTM (bf16): gates = E'[y] + W_hh h on tensor cores; this CTA's
+//       W_hh slice is resident in TMEM for the whole kernel (loaded once, read
+//       with tcgen05.ld as the m16 A operand of mma.sync) and its W_pred slice
+//       is resident in shared memory; E'[y] slices arrive by bulk copies; gate
 //       nonlinearities + cell update fused in the epilogue (c stays in its
 //       owner CTA); h' and g = W_pred h' + b_pred slices are exchanged between
 //       the CTAs with st.async + mbarriers (no global memory, no cluster
@@ -47,7 +47,7 @@ constexpr int MAX_JR = 32;       // joint rows per round R*W (<= 32: one lane pe
 constexpr int MAX_DUR = 16;
 constexpr int MAX_CTX = 4;
 enum { SC_OUTER, SC_ROUNDS, SC_ALGEVALS, SC_PRED, SC_PREDROWS, SC_LABELS, SC_GROUPS, SC_ROWEVALS, SC_N };
-constexpr int MAX_NW = 10;       // consumer warps per CTA (+1 producer warp: <= 352 threads, <= 184 regs)
+constexpr int MAX_NW = 10;       // warps per CTA (320 threads; 168 registers per thread at most)
 constexpr int MAX_C = 16;        // cluster size
 constexpr int KREG = 20;         // 32-wide K blocks of the joint weight slice held in registers (H <= 656)
 constexpr int KREG_SMALL = 4;    // small-H instantiation (H <= 144): no register budget lost to padding
@@ -142,6 +142,10 @@ struct DecodeParams {
   unsigned long long *stats;     // see ll.h ll_stats
   unsigned long long *prof;      // optional per-warp timeline of block 0 (LL_TIMELINE_PTR)
   volatile unsigned *trace;      // debug: host-mapped progress markers [gridDim.x][8] (LL debug hook)
+  // probe (parity tests, ll.h ll_options): DBG instantiations only
+  float *probe_logits, *probe_g;
+  int *probe_lmeta, *probe_gmeta, *probe_counts;
+  int probe_rows, probe_regions;
   // ll_debug_joint mode
   const float *dbg_g;
   float *dbg_logits;
@@ -1719,7 +1723,9 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // instantiations, so a kernel carries only the control code it runs.
 // TM: 0 = RNN-T / TDT chosen at run time (p.tdt), 1 = RNN-T only, 2 = TDT only
 // (the FC instantiations carry only the code of their model family).
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0>
+// DBG: 1 = the probe hook (ll.h ll_options): the same kernel also writes the
+// logits of every joint row and g after every predictor step (parity tests).
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
@@ -1885,6 +1891,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         }
         cx.sync();
         bool have_spec = false;        // fbuf[cur ^ 1] holds the previous tick's speculative windows
+        [[maybe_unused]] int dbg_l = 0, dbg_gr = 0;   // probe rows written by this cluster
         while (rs.nactive > 0) {
           if (t0) s_cnt[SC_OUTER]++;
           if (have_spec) {
@@ -1917,6 +1924,25 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
             if constexpr (PRED == 1) cx.predictor_stateless();
             else if constexpr (RING) cx.predictor_lstm_tmem(true);
             else cx.predictor_lstm_f32();
+            if constexpr (DBG != 0) {    // probe: g rows of the predicted slots (rank 0 writes)
+              const int n = rs.npred, H = cx.Hd(), region = blockIdx.x / C;
+              if (rank == 0) {
+                for (int idx = tid; idx < n * H; idx += cx.NCT) {
+                  const int i = idx / H, d = idx % H, row = dbg_gr + i;
+                  if (row < p.probe_rows)
+                    p.probe_g[((size_t)region * p.probe_rows + row) * H + d] =
+                        cx.gs()[(size_t)rs.plist[i] * H + cx.goff(d & ~3) + (d & 3)];
+                }
+                if (tid < n && dbg_gr + tid < p.probe_rows) {
+                  const int s = rs.plist[tid];
+                  *reinterpret_cast<int4 *>(p.probe_gmeta + ((size_t)region * p.probe_rows + dbg_gr + tid) * 4) =
+                      make_int4(rs.b[s], rs.len[s], 0, 0);
+                }
+                if (t0) p.probe_counts[2 * region + 1] = dbg_gr + n;
+              }
+              dbg_gr += n;
+              cx.sync();
+            }
             // the predicted rows scan from now on (with no predictor rows the
             // lists are unchanged, and rewriting the counters here would race
             // with the other warps' read of npred above: no barrier separates them)
@@ -1944,7 +1970,20 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
               have_spec = true;
             }
             cx.tl_round_bar(3);
-            cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
+            if constexpr (DBG != 0) {    // probe: logits + (b, t, labels so far) of every joint row
+              const int nz = rs.nz, NV = p.V1 + p.nD, region = blockIdx.x / C;
+              if (rank == 0 && warp == 0 && lane < nz && dbg_l + lane < p.probe_rows) {
+                const int s = rs.zdst[lane] / p.W, j = rs.zdst[lane] % p.W;
+                *reinterpret_cast<int4 *>(p.probe_lmeta + ((size_t)region * p.probe_rows + dbg_l + lane) * 4) =
+                    make_int4(rs.b[s], rs.t[s] + j, rs.len[s], 0);
+              }
+              if (rank == 0 && t0) p.probe_counts[2 * region] = dbg_l + nz;
+              cx.joint_keys((nz + 15) / 16, max(0, min(nz, p.probe_rows - dbg_l)),
+                            p.probe_logits + (size_t)region * p.probe_rows * NV, dbg_l);
+              dbg_l += nz;
+            } else {
+              cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);
+            }
             cx.tl_round_(4);
             cx.exchange_keys();
             cx.tl_round_(5);

@@ -64,12 +64,17 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
 }
 
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
-void *g_trace = nullptr;  // debug: host-mapped progress markers (env LL_TRACE_PTR)
 
-int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
+// Test / debug options of this host thread (ll_set_options; ll.h).  The
+// production path reads no environment variable.
+ll_options default_options() {
+  ll_options o;
+  memset(&o, 0, sizeof(o));
+  o.schedule = -1;
+  o.spec_prefetch = -1;
+  return o;
 }
+thread_local ll_options g_opt = default_options();
 
 ll_status check_model(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, ll_prec prec,
                       int nD, bool need_pred) {
@@ -121,9 +126,9 @@ static int pow2ceil(int x) {
 // assume 8).  R is chosen so that all groups of the batch run in one wave.
 bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf,
                    int nclusters = 0) {
-  const int forceC = env_int("LL_CLUSTER", 0);
-  const int forceR = env_int("LL_GROUP_ROWS", 0);
-  const int forceW = env_int("LL_WINDOW", 0);
+  const int forceC = g_opt.cluster_size;
+  const int forceR = g_opt.group_rows;
+  const int forceW = g_opt.window;
   const bool ring = bf && lstm;
   if (bf && H > KREG * 32 + 16) return false;        // joint slice must fit the register tile
   const int ncl = nclusters > 0 ? nclusters : 8;
@@ -206,10 +211,10 @@ int max_clusters(int C, const Layout &L) {
   return n;
 }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0>
 ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
                         int &used_clusters) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, LM, TM>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, LM, TM, DBG>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -231,8 +236,8 @@ ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_gro
     cudaGetLastError();
     return LL_ERR_UNSUPPORTED;
   }
-  const int cap = env_int("LL_MAX_CLUSTERS", 0);
-  if (cap > 0) max_clusters = std::min(max_clusters, cap);
+  if (g_opt.max_clusters > 0) max_clusters = std::min(max_clusters, g_opt.max_clusters);
+  if (p.probe_logits && p.probe_regions > 0) max_clusters = std::min(max_clusters, p.probe_regions);
   used_clusters = std::min(n_groups, max_clusters);
   cfg.gridDim = dim3(used_clusters * C);
   if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return LL_ERR_CUDA;
@@ -299,7 +304,7 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t rows, uint64_t col
 // tcgen05 GEMM (gemm_tc.cuh) when the shape fits its tiles; false = not taken.
 bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const void *bias, const void *bias2, void *Y,
                int64_t ldy, int M, int N, int K, bool out_bf16, cudaStream_t st, ll_status &s) {
-  if (env_int("LL_GEMM_MMA_SYNC", 0)) return false;
+  if (g_opt.gemm_mma_sync) return false;
   if (K % TC_BK || N % TC_BN || (ldx * 2) % 16 || (ldw * 2) % 16 || ((uintptr_t)X & 15) || ((uintptr_t)W & 15))
     return false;
   if ((out_bf16 && (ldy * 2) % 16) || (!out_bf16 && (ldy * 4) % 16) || ((uintptr_t)Y & 15)) return false;
@@ -368,12 +373,15 @@ bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
 struct TableKey {
   const void *ptr[8];
   int dims[10];
+  size_t ws_bytes;
   bool operator==(const TableKey &o) const { return memcmp(this, &o, sizeof(TableKey)) == 0; }
 };
 
-TableKey table_key(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, int C, const Layout &L) {
+TableKey table_key(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, int C, const Layout &L,
+                   size_t ws_bytes) {
   TableKey k;
   memset(&k, 0, sizeof(k));
+  k.ws_bytes = ws_bytes;
   k.ptr[0] = pr->embedding; k.ptr[1] = pr->w_ih; k.ptr[2] = pr->w_hh; k.ptr[3] = pr->b_ih;
   k.ptr[4] = pr->b_hh; k.ptr[5] = jn->w_pred; k.ptr[6] = jn->b_pred;
   k.dims[0] = pr->kind; k.dims[1] = pr->num_tokens; k.dims[2] = pr->hidden; k.dims[3] = pr->context;
@@ -473,7 +481,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   // into this workspace)
   float *tab = (float *)(ws + w.tab);
   {
-    const TableKey key = table_key(pr, jn, dt, C, L);
+    const TableKey key = table_key(pr, jn, dt, C, L, workspace_bytes);
     bool cached = false;
     {
       std::lock_guard<std::mutex> lk(g_prep_mu);
@@ -502,9 +510,9 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.n_groups = (B + R - 1) / R;
   p.cap = cap;
   p.L = L;
-  p.spec_prefetch = frame_looping ? 0 : env_int("LL_SPEC_PREFETCH", 1);
+  p.spec_prefetch = frame_looping ? 0 : (g_opt.spec_prefetch < 0 ? 1 : g_opt.spec_prefetch);
   p.frame_looping = frame_looping ? 1 : 0;
-  p.sched = env_int("LL_SCHEDULE", 1);
+  p.sched = g_opt.schedule < 0 ? 1 : g_opt.schedule;
   p.lengths = lengths;
   p.f = ws + w.f;
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
@@ -519,15 +527,20 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.status = (int *)ws;
   p.group_counter = (int *)ws + 1;
   p.stats = (unsigned long long *)(ws + 64);
-  {
-    // debug: per-warp clock64 timeline of block 0 into a caller-provided device
-    // buffer of [2][TL_N][TL_PH][MAX_NW] u64 (tools/timeline.py)
-    const char *tp = getenv("LL_TIMELINE_PTR");
-    p.prof = (tp && *tp) ? (unsigned long long *)strtoull(tp, nullptr, 0) : nullptr;
-  }
-  {
-    const char *tp = getenv("LL_TRACE_PTR");
-    p.trace = (tp && *tp) ? (volatile unsigned *)strtoull(tp, nullptr, 0) : nullptr;
+  // debug builds only: per-warp clock64 timeline of block 0 ([2][TL_N][TL_PH][MAX_NW]
+  // u64, tools/timeline.py) and host-mapped progress markers (tools/hang_trace.py)
+  p.prof = (unsigned long long *)g_opt.timeline;
+  p.trace = (volatile unsigned *)g_opt.trace;
+  // probe (parity tests): the FC tick-schedule kernels with the probe hook
+  const bool probe = g_opt.probe_logits != nullptr;
+  if (probe) {
+    if (frame_looping || p.sched != 1 || !is_fc(bf, H, P, C) || !g_opt.probe_lmeta || !g_opt.probe_g ||
+        !g_opt.probe_gmeta || !g_opt.probe_counts || g_opt.probe_rows < 1 || g_opt.probe_regions < 1)
+      return LL_ERR_UNSUPPORTED;
+    p.probe_logits = g_opt.probe_logits; p.probe_lmeta = g_opt.probe_lmeta;
+    p.probe_g = g_opt.probe_g; p.probe_gmeta = g_opt.probe_gmeta; p.probe_counts = g_opt.probe_counts;
+    p.probe_rows = g_opt.probe_rows; p.probe_regions = g_opt.probe_regions;
+    if (cudaMemsetAsync(p.probe_counts, 0, sizeof(int) * 2 * p.probe_regions, st) != cudaSuccess) return LL_ERR_CUDA;
   }
   int used = 0;
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
@@ -544,6 +557,13 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     else
       s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used)
                : launch_decode<float, 1, 1, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used);
+  } else if (probe) {   // the production FC tick kernels + the probe hook (ll.h ll_options)
+    if (lstm)
+      s = tdt ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 2, 1>(p, C, L, p.n_groups, st, used)
+              : launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1, 1>(p, C, L, p.n_groups, st, used);
+    else
+      s = tdt ? launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 2, 1>(p, C, L, p.n_groups, st, used)
+              : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 1, 1>(p, C, L, p.n_groups, st, used);
   } else if (is_fc(bf, H, P, C)) {   // one instantiation per (predictor, family, schedule)
     const int k = (tdt ? 2 : 0) + (p.sched == 1 ? 0 : 1);
     if (lstm) {
@@ -582,7 +602,27 @@ ll_status ll_set_timing_events(void *ev_before_decode, void *ev_after_decode) {
   return LL_OK;
 }
 
-const char *ll_version(void) { return "ll 0.1 (sm_100a, label-looping arXiv 2406.06220)"; }
+const char *ll_version(void) { return "ll 0.2 (sm_100a, label-looping arXiv 2406.06220)"; }
+
+ll_status ll_release(void *workspace) {
+  if (!workspace) return LL_OK;
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  g_prepared.erase(workspace);
+  return LL_OK;
+}
+
+ll_status ll_set_options(const ll_options *o) {
+  if (!o) {
+    g_opt = default_options();
+    return LL_OK;
+  }
+  if (o->cluster_size < 0 || o->cluster_size > MAX_C || o->group_rows < 0 || o->group_rows > MAX_R ||
+      o->window < 0 || o->window > 8 || o->max_clusters < 0 || o->schedule < -1 || o->schedule > 1 ||
+      o->spec_prefetch < -1 || o->spec_prefetch > 1 || o->probe_rows < 0 || o->probe_regions < 0)
+    return LL_ERR_INVALID_ARGUMENT;
+  g_opt = *o;
+  return LL_OK;
+}
 
 const char *ll_status_string(ll_status s) {
   switch (s) {
@@ -660,7 +700,7 @@ ll_status ll_prepare(const ll_predictor *pred, const ll_joint *joint, ll_dtype d
   s = build_tables(bf, pred, joint, dtype, w, (uint8_t *)workspace, cf.C, cf.L, (cudaStream_t)stream);
   if (s != LL_OK) return s;
   std::lock_guard<std::mutex> lk(g_prep_mu);
-  g_prepared[workspace] = table_key(pred, joint, dtype, cf.C, cf.L);
+  g_prepared[workspace] = table_key(pred, joint, dtype, cf.C, cf.L, workspace_bytes);
   return LL_OK;
 }
 
@@ -699,6 +739,7 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   dummy.hidden = joint->pred_dim;
   if (workspace_bytes < ll_workspace_size(n, 1, &dummy, joint, dtype, prec, num_durations))
     return LL_ERR_WORKSPACE;
+  ll_release(workspace);   // its f rows overwrite the region prepared tables would occupy
   const bool bf = dtype == LL_BF16;
   const int H = joint->joint_dim, V1 = joint->num_outputs, De = joint->enc_dim;
   Config cf;

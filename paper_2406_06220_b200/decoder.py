@@ -109,6 +109,18 @@ class LabelLoopingDecoder:
         self.durs = torch.zeros_like(self.tokens) if nD else None
         self.lengths_out = torch.zeros(self.B_max, dtype=torch.int32, device=dev)
 
+    def release(self) -> None:
+        """ll_release: drop the library's ll_prepare record of this workspace
+        (called before the workspace memory goes back to the allocator)."""
+        if getattr(self, "ws_ptr", None):
+            ll.ll_release(self.ws_ptr)
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
     def prepare(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """ll_prepare: build the weight-only model tables into this decoder's
         workspace once; later decodes skip them while the weights (pointers)
@@ -182,3 +194,32 @@ def debug_joint(model: Model, enc_rows: torch.Tensor, g_rows: torch.Tensor, want
         raise ll.LLError(s, "ll_debug_joint")
     torch.cuda.current_stream().synchronize()
     return logits, am, dam
+
+
+def probe_decode(dec: "LabelLoopingDecoder", enc: torch.Tensor, lengths: torch.Tensor, rows: int = 8192,
+                 regions: int = 8):
+    """Decode through the production FastConformer kernel instantiation with its
+    probe hook (ll.h ll_options): returns (DecodeOutput, joint rows, g rows) where
+    joint rows = list of (b, t, n_labels, logits [V+1+|D|]) and g rows = list of
+    (b, n_labels, g [H]) as numpy arrays (parity tests only)."""
+    m = dec.model
+    NV = m.V1 + m.num_durations
+    dev = m.device
+    pl = torch.full((regions, rows, NV), float("nan"), dtype=torch.float32, device=dev)
+    lm = torch.zeros(regions, rows, 4, dtype=torch.int32, device=dev)
+    pg = torch.full((regions, rows, m.H), float("nan"), dtype=torch.float32, device=dev)
+    gm = torch.zeros(regions, rows, 4, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(regions, 2, dtype=torch.int32, device=dev)
+    with ll.options(probe_logits=pl.data_ptr(), probe_lmeta=lm.data_ptr(), probe_g=pg.data_ptr(),
+                    probe_gmeta=gm.data_ptr(), probe_counts=cnt.data_ptr(), probe_rows=rows,
+                    probe_regions=regions):
+        out = dec.decode(enc, lengths)
+    torch.cuda.synchronize()
+    cnt = cnt.cpu().numpy()
+    if (cnt > rows).any():
+        raise RuntimeError(f"probe truncated: {cnt.max()} rows > {rows}")
+    pl, lm, pg, gm = pl.cpu().numpy(), lm.cpu().numpy(), pg.cpu().numpy(), gm.cpu().numpy()
+    joint = [(int(lm[r, i, 0]), int(lm[r, i, 1]), int(lm[r, i, 2]), pl[r, i]) for r in range(regions)
+             for i in range(cnt[r, 0])]
+    gro = [(int(gm[r, i, 0]), int(gm[r, i, 1]), pg[r, i]) for r in range(regions) for i in range(cnt[r, 1])]
+    return out, joint, gro

@@ -24,7 +24,7 @@ LL_PRED_LSTM, LL_PRED_STATELESS = 0, 1
 EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_rnnt_frame_looping", "ll_decode_tdt", "ll_prepare",
             "ll_sync",
             "ll_status_string",
-            "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version",
+            "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version", "ll_release", "ll_set_options",
             "ll_nccl_unique_id", "ll_nccl_comm_init", "ll_nccl_comm_destroy", "ll_gather_workspace_size",
             "ll_gather_ragged"]
 
@@ -40,6 +40,22 @@ class ll_joint(ctypes.Structure):
                 ("num_outputs", c_int32), ("w_enc", c_void_p), ("b_enc", c_void_p), ("w_pred", c_void_p),
                 ("b_pred", c_void_p), ("w_out", c_void_p), ("b_out", c_void_p), ("w_dur", c_void_p),
                 ("b_dur", c_void_p)]
+
+
+class ll_options(ctypes.Structure):
+    _fields_ = [("cluster_size", c_int32), ("group_rows", c_int32), ("window", c_int32),
+                ("max_clusters", c_int32), ("schedule", c_int32), ("spec_prefetch", c_int32),
+                ("gemm_mma_sync", c_int32), ("timeline", c_void_p), ("trace", c_void_p),
+                ("probe_logits", c_void_p), ("probe_lmeta", c_void_p), ("probe_g", c_void_p),
+                ("probe_gmeta", c_void_p), ("probe_counts", c_void_p), ("probe_rows", c_int32),
+                ("probe_regions", c_int32)]
+
+
+def default_options() -> ll_options:
+    o = ll_options()
+    o.schedule = -1
+    o.spec_prefetch = -1
+    return o
 
 
 class LLError(RuntimeError):
@@ -86,6 +102,10 @@ def load_library() -> ctypes.CDLL:
     lib.ll_debug_joint.restype = c_int32
     lib.ll_set_timing_events.argtypes = [c_void_p, c_void_p]
     lib.ll_set_timing_events.restype = c_int32
+    lib.ll_release.argtypes = [c_void_p]
+    lib.ll_release.restype = c_int32
+    lib.ll_set_options.argtypes = [POINTER(ll_options)]
+    lib.ll_set_options.restype = c_int32
     lib.ll_version.argtypes = []
     lib.ll_version.restype = c_char_p
     lib.ll_nccl_unique_id.argtypes = [c_void_p]
@@ -173,6 +193,34 @@ def ll_debug_joint(enc_rows, g_rows, n, joint, dtype, prec, num_durations, out_l
 
 def ll_set_timing_events(ev_before_decode, ev_after_decode) -> int:
     return int(load_library().ll_set_timing_events(ev_before_decode, ev_after_decode))
+
+
+def ll_release(workspace) -> int:
+    return int(load_library().ll_release(workspace))
+
+
+def ll_set_options(opts) -> int:
+    """opts: an ll_options struct, or None for the library defaults."""
+    return int(load_library().ll_set_options(None if opts is None else ctypes.byref(opts)))
+
+
+class options:
+    """Context manager over ll_set_options (test / debug knobs of ll.h, this host
+    thread only): `with ll.options(window=1, schedule=0): ...`."""
+
+    def __init__(self, **kw):
+        self.opts = default_options()
+        for k, v in kw.items():
+            setattr(self.opts, k, v)
+
+    def __enter__(self):
+        s = ll_set_options(self.opts)
+        if s != LL_OK:
+            raise LLError(s, "ll_set_options")
+        return self.opts
+
+    def __exit__(self, *exc):
+        ll_set_options(None)
 
 
 def ll_nccl_unique_id():

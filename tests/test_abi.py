@@ -152,3 +152,29 @@ def test_gather_validation(lib):
                 dict(utt_ids=None), dict(lengths=None), dict(tokens=None), dict(timestamps=None)]:
         kw = {**args, **bad}
         assert ll.ll_gather_ragged(*kw.values())[0] == ll.LL_ERR_INVALID_ARGUMENT, bad
+
+
+def test_options_validation_and_release(lib):
+    """ll_set_options: explicit knobs (no environment variables on the
+    production path), validated on the host; NULL restores the defaults.
+    ll_release of an unknown / NULL workspace is a no-op."""
+    assert ll.ll_set_options(None) == ll.LL_OK
+    for bad in [dict(window=9), dict(group_rows=33), dict(cluster_size=17), dict(schedule=2),
+                dict(spec_prefetch=-2), dict(max_clusters=-1), dict(probe_rows=-1)]:
+        o = ll.default_options()
+        for k, v in bad.items():
+            setattr(o, k, v)
+        assert ll.ll_set_options(o) == ll.LL_ERR_INVALID_ARGUMENT, bad
+    with ll.options(window=2, group_rows=4, schedule=0):
+        pass
+    assert ll.ll_set_options(None) == ll.LL_OK
+    assert ll.ll_release(None) == ll.LL_OK
+    assert ll.ll_release(0x100000) == ll.LL_OK
+
+
+def test_no_environment_knobs_in_library():
+    """The production library reads no environment variable:
+    getenv is not referenced by the C ABI sources."""
+    for f in ("ll_api.cu", "ll_gather.cu", "decode.cuh", "common.cuh", "gemm_tc.cuh", "linear.cuh"):
+        src = open(os.path.join(ROOT, "paper_2406_06220_b200", "csrc", f)).read()
+        assert "getenv" not in src, f

@@ -63,18 +63,18 @@ def test_debug_joint_logits(dtype, tol, shape, tdt):
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("window", [1, 0])
-def test_cat_dog_through_abi(dtype, window, monkeypatch):
+def test_cat_dog_through_abi(dtype, window):
     """Fig. 2 worked example through ll_decode_rnnt.  With a
     one-frame window (W=1, the paper's inner loop) the device runs exactly the
     golden 4 predictor steps and 8 joint rounds of Alg. 3; with the default
     multi-frame window the hypotheses are identical and the decisions used
     equal the frame-by-frame count."""
-    if window:
-        monkeypatch.setenv("LL_WINDOW", str(window))
-        monkeypatch.setenv("LL_GROUP_ROWS", "4")
-        monkeypatch.setenv("LL_SCHEDULE", "0")   # the paper's batched outer loop (Alg. 3 as listed)
+    # window 1: one frame per round, both rows in one group, the paper's batched
+    # outer loop (Alg. 3 as listed)
+    opts = dict(window=1, group_rows=4, schedule=0) if window else {}
     spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
-    hyps, dec = gpu_decode(spec, w, enc, lengths, dtype)
+    with ll.options(**opts):
+        hyps, dec = gpu_decode(spec, w, enc, lengths, dtype)
     assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
     assert [h[1] for h in hyps] == [[0, 2, 2], [1, 3, 3]]
     st = dec.stats()
@@ -95,15 +95,14 @@ def test_tdt_forced_through_abi():
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("tdt", [False, True])
 @pytest.mark.parametrize("window", [1, 0])
-def test_guard_counter_restarts_after_blank(dtype, tdt, window, monkeypatch):
+def test_guard_counter_restarts_after_blank(dtype, tdt, window):
     """Reading A6/A14: after a frame advance inside a multi-frame window the
     label counter restarts, so frame 1 emits m = 3 labels (A,B,C,D @ [0,1,1,1],
     hand-derived; pinned on the oracle in test_oracle.py)."""
-    if window:
-        monkeypatch.setenv("LL_WINDOW", str(window))
     fx = synth.guard_after_blank_tdt_fixture() if tdt else synth.guard_after_blank_fixture()
     spec, w, enc, lengths, vocab = fx
-    hyps, _ = gpu_decode(spec, w, enc, lengths, dtype)
+    with ll.options(window=window):
+        hyps, _ = gpu_decode(spec, w, enc, lengths, dtype)
     assert [vocab[y] for y in hyps[0][0]] == list("ABCD")
     assert hyps[0][1] == [0, 1, 1, 1]
     if tdt:
@@ -269,12 +268,12 @@ def test_determinism_and_batch_composition():
 # the batched joint-call count must equal the oracle's Alg. 2 count.
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-def test_frame_looping_cat_dog(dtype, monkeypatch):
-    monkeypatch.setenv("LL_GROUP_ROWS", "2")          # both utterances in one batch
+def test_frame_looping_cat_dog(dtype):
     spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
     model = gpu_model(spec, w, dtype)
     dec = LabelLoopingDecoder(model, spec.max_symbols, 2, enc.shape[1], frame_looping=True)
-    out = dec.decode(torch.from_numpy(enc).to("cuda", model.tdtype), torch.from_numpy(lengths).cuda())
+    with ll.options(group_rows=2):                      # both utterances in one batch
+        out = dec.decode(torch.from_numpy(enc).to("cuda", model.tdtype), torch.from_numpy(lengths).cuda())
     hyps = out.hypotheses()
     assert [[vocab[y] for y in h[0]] for h in hyps] == [list("CAT"), list("DOG")]
     assert [h[1] for h in hyps] == [[0, 2, 2], [1, 3, 3]]
@@ -346,9 +345,9 @@ def test_prepare_tables_reuse_and_invalidate():
 
 
 @pytest.mark.parametrize("cfg", ["fc-rnnt", "fc-tdt"])
-def test_schedules_identical(cfg, monkeypatch):
+def test_schedules_identical(cfg):
     """The per-row tick schedule (default) and the paper's batched outer loop
-    (LL_SCHEDULE=0) are exact reorderings of Alg. 3: identical hypotheses on a
+    (ll_options.schedule = 0) are exact reorderings of Alg. 3: identical hypotheses on a
     random-family FC batch (near-ties included), and identical joint-evaluation
     counts (the algorithmic decisions)."""
     c = synth.CONFIGS[cfg]
@@ -357,13 +356,13 @@ def test_schedules_identical(cfg, monkeypatch):
     enc, lengths = synth.make_inputs(42, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     model = gpu_model(spec, w)
     out = {}
-    for sched in ("0", "1"):
-        monkeypatch.setenv("LL_SCHEDULE", sched)
-        hyps, dec = gpu_decode(spec, w, enc, lengths, model=model)
-        out[sched] = (hyps, dec.stats())
-    assert out["0"][0] == out["1"][0]
-    assert out["0"][1]["joint_evals"] == out["1"][1]["joint_evals"]
-    assert out["0"][1]["labels"] == out["1"][1]["labels"]
+    for sched in (0, 1):
+        with ll.options(schedule=sched):
+            hyps, dec = gpu_decode(spec, w, enc, lengths, model=model)
+            out[sched] = (hyps, dec.stats())
+    assert out[0][0] == out[1][0]
+    assert out[0][1]["joint_evals"] == out[1][1]["joint_evals"]
+    assert out[0][1]["labels"] == out[1][1]["labels"]
 
 
 def test_fc_rnnt_4x_subsampling_planted():
@@ -446,3 +445,91 @@ def test_native_gather_records(B, cap, tdt):
     assert torch.equal(got, ref) and torch.equal(again, ref)
     if B == 0:
         assert got.tolist() == [0]
+
+
+# ------------------------------------------------------------------ production-instantiation probe
+# The logit tolerance and the predictor output checked on the PRODUCTION
+# FastConformer kernel (decode_kernel<bf16, *, KREG, 640, 640, 16, ticks, family>
+# with its probe hook, ll.h ll_options): every joint row the kernel evaluated
+# (speculative window frames included) and g after every predictor step, against
+# float64 along the kernel's own label history (teacher forcing).
+G_TOL = 2e-3   # bf16 h through the recurrence and W_pred
+
+
+def _oracle_g_sequence(o, tokens):
+    """g after consuming SOS, tokens[0], ..., tokens[n-1], for n = 0..len(tokens)."""
+    st = o.pred_init()
+    dec, st = o.pred_step(st, o.blank)
+    gs = [o.pred_proj(dec)]
+    for y in tokens:
+        dec, st = o.pred_step(st, int(y))
+        gs.append(o.pred_proj(dec))
+    return gs
+
+
+@pytest.mark.parametrize("kind,tdt", [("lstm", False), ("lstm", True), ("stateless", False)])
+def test_production_kernel_logits_and_g(kind, tdt):
+    from paper_2406_06220_b200.decoder import probe_decode
+    durs = (0, 1, 2, 3, 4) if tdt else None
+    De = 1024 if kind == "stateless" else 512
+    spec = synth.ModelSpec(1025, De, 640, 640, kind, 2 if kind == "stateless" else 1, durs, 0, 10)
+    w = synth.make_weights(spec, 61, blank_bias=1.0 if tdt else 3.0)
+    B, T = 16, 80
+    enc, lengths = synth.make_inputs(62, B, T, spec.enc_dim, 40, T)
+    model = gpu_model(spec, w)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T)
+    out, jrows, grows = probe_decode(dec, torch.from_numpy(enc).to("cuda", torch.bfloat16),
+                                     torch.from_numpy(lengths).cuda())
+    hyps = out.hypotheses()
+    verify_all(spec, w, enc, lengths, hyps)
+    o = Transducer.from_spec(spec, w)
+    gseq = {b: _oracle_g_sequence(o, hyps[b][0]) for b in range(B)}
+    fs = {b: o.enc_proj(enc[b][:int(lengths[b])]) for b in range(B)}
+    st = dec.stats()
+    assert len(jrows) == st["joint_rows_computed"] and len(grows) == st["predictor_rows"]
+    lerr = 0.0
+    for b, t, n, lg in jrows:
+        assert 0 <= b < B and 0 <= t < lengths[b] and 0 <= n <= len(hyps[b][0])
+        l, dl = o.joint(fs[b][t], gseq[b][n])
+        ref = np.concatenate([l, dl]) if tdt else l
+        lerr = max(lerr, float(np.abs(lg.astype(np.float64) - ref).max()))
+    gerr = 0.0
+    for b, n, g in grows:
+        gerr = max(gerr, float(np.abs(g.astype(np.float64) - gseq[b][n]).max()))
+    print(f"{kind} tdt={tdt}: {len(jrows)} joint rows max |logit err| {lerr:.3g}; "
+          f"{len(grows)} g rows max |g err| {gerr:.3g}")
+    assert lerr < 2e-3, lerr
+    assert gerr < G_TOL, gerr
+
+
+_CFG4 = {}
+
+
+def _verify_rows(rows):
+    a = _CFG4   # inherited through fork (the encoder outputs are ~3 GB: never pickled)
+    return verify_all(a["spec"], a["w"], a["enc"], a["lengths"], a["hyps"], rows=rows)
+
+
+def test_config4_random_family_full_batch():
+    """Config (4) in the launch configuration bench.py times (B=512, lengths
+    50..1500, D_e=1024, stateless context 2, throughput mode: many waves of small
+    groups) on the RANDOM family (near-ties present): all 512 rows pass the
+    teacher-forced float64 verifier."""
+    import multiprocessing as mp
+    c = synth.CONFIGS["stateless-b512"]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 71, blank_bias=3.0)
+    enc, lengths = synth.make_inputs(72, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
+    hyps, dec = gpu_decode(spec, w, enc, lengths, "bf16")
+    st = dec.stats()
+    # throughput mode: groups of <= 16 rows taken from the work counter in many waves
+    assert st["group_rows"] <= 16 and st["groups"] >= c["B"] // 16
+    chunks = [list(range(i, c["B"], 32)) for i in range(32)]
+    _CFG4.update(spec=spec, w=w, enc=enc, lengths=lengths, hyps=hyps)
+    with mp.get_context("fork").Pool(min(32, mp.cpu_count())) as pool:
+        res = pool.map(_verify_rows, chunks)
+    _CFG4.clear()
+    ties = sum(r[0] for r in res)
+    decs = sum(r[1] for r in res)
+    print(f"config 4 random family: {decs} decisions, {ties} near-ties, {st['labels']} labels")
+    assert decs > c["B"] * 50

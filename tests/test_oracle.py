@@ -440,3 +440,97 @@ def test_enumeration_counts_closed_form():
     assert sum(1 for _ in rnnt_alignments(3, [1, 2], 3)) == 15 ** 3
     # TDT: small case counted by hand: L=1, one token + blank, D={1}: (b,1) or (y,1)
     assert sum(1 for _ in tdt_alignments(1, [0, 1], 0, [1], 1)) == 2
+
+
+# ---------------------------------------------------------------- verifier near-tie branch (tol = 1e-3)
+# The GPU parity tests accept a decision y iff it is the float64 argmax or
+# max(l) - l[y] < 1e-3 (north_star); these pins fix that branch with table
+# models whose logits are set exactly (z is one-hot per (t, last label), so the
+# logits of a state are one column of W_out: synth._table_fixture).
+NEAR = 1e-3
+
+
+def _table(steps, T, V1, durations=None, edits=()):
+    """Table model realising `steps`, then W_out / W_dur entries overwritten:
+    edits = [(head, row, t, last, value)] with head 'out' or 'dur'."""
+    spec, w, enc, lengths = synth._table_fixture([steps], T, V1, durations=durations)
+    w = {k: np.asarray(v, dtype=np.float64) for k, v in w.items()}
+    for head, row, t, last, val in edits:
+        w["w_" + head][row, t * V1 + last] = val
+    return spec, Transducer.from_spec(spec, w), np.asarray(enc, dtype=np.float64), int(lengths[0])
+
+
+def test_verifier_near_tie_label_accepted_within_tol():
+    """A non-argmax label 5e-4 below the max is accepted at tol 1e-3 and counted
+    as a near-tie; the same output is rejected at tol 0."""
+    b, A, B_ = 0, 1, 2
+    spec, model, enc, L = _table([(0, b, A)], 2, 4, edits=[("out", B_, 0, b, 10.0 - 5e-4)])
+    assert decode_sequential(model, enc[0], L, 3).tokens == [A]
+    r = verify_rnnt(model, enc[0], L, 3, [B_], [0], tol=NEAR)
+    assert r.ok and r.near_ties == 1 and r.decisions == 3     # B@0 (tie), blank@0, blank@1
+    assert not verify_rnnt(model, enc[0], L, 3, [B_], [0], tol=0).ok
+    assert verify_rnnt(model, enc[0], L, 3, [A], [0], tol=NEAR).near_ties == 0
+
+
+def test_verifier_label_beyond_tol_rejected():
+    """Gap 2e-3 > 1e-3: the non-argmax label is rejected."""
+    b, A, B_ = 0, 1, 2
+    spec, model, enc, L = _table([(0, b, A)], 2, 4, edits=[("out", B_, 0, b, 10.0 - 2e-3)])
+    r = verify_rnnt(model, enc[0], L, 3, [B_], [0], tol=NEAR)
+    assert not r.ok and "rejected" in r.message
+
+
+def test_verifier_third_best_rejected_despite_small_top2_gap():
+    """The tolerance is measured from the MAXIMUM, not from the runner-up: with
+    a top-2 gap of 5e-4, a third label 1.5e-3 below the max is rejected while
+    the runner-up is accepted."""
+    b, A, B_, C = 0, 1, 2, 3
+    spec, model, enc, L = _table([(0, b, A)], 2, 4,
+                                 edits=[("out", B_, 0, b, 10.0 - 5e-4), ("out", C, 0, b, 10.0 - 1.5e-3)])
+    assert verify_rnnt(model, enc[0], L, 3, [B_], [0], tol=NEAR).ok
+    assert not verify_rnnt(model, enc[0], L, 3, [C], [0], tol=NEAR).ok
+
+
+def test_verifier_near_tie_blank():
+    """A blank decision 5e-4 below a label is accepted (near-tie) at tol 1e-3;
+    at 2e-3 it is rejected."""
+    b, A = 0, 1
+    for gap, ok in [(5e-4, True), (2e-3, False)]:
+        spec, model, enc, L = _table([(0, b, A)], 2, 4, edits=[("out", b, 0, b, 10.0 - gap)])
+        r = verify_rnnt(model, enc[0], L, 3, [], [], tol=NEAR)
+        assert r.ok == ok
+        if ok:
+            assert r.near_ties == 1
+
+
+def test_verifier_tdt_alternative_blank_duration():
+    """TDT: the emitted events are reachable ONLY through the non-argmax blank
+    duration at t = 0 (d = 2, 5e-4 below d = 1): the verifier's search over
+    acceptable blank durations (oracle/verify.py) must find it; at a 2e-3 gap
+    it must not.  The argmax path (blank d=1, then Y@1) is the oracle output."""
+    b, X, Y = 0, 1, 2
+    D = [0, 1, 2]
+    steps = [(0, b, b, 1), (1, b, Y, 1), (2, b, X, 2)]
+    for gap, ok in [(5e-4, True), (2e-3, False)]:
+        spec, model, enc, L = _table(steps, 4, 4, durations=D, edits=[("dur", 2, 0, b, 10.0 - gap)])
+        ref = decode_sequential(model, enc[0], L, 3)
+        assert (ref.tokens, ref.timestamps, ref.durations) == ([Y], [1], [1])
+        assert verify_tdt(model, enc[0], L, 3, ref.tokens, ref.timestamps, ref.durations, tol=0).ok
+        r = verify_tdt(model, enc[0], L, 3, [X], [2], [2], tol=NEAR)
+        assert r.ok == ok, r.message
+        if ok:
+            assert r.near_ties == 1
+        assert not verify_tdt(model, enc[0], L, 3, [X], [2], [2], tol=0).ok
+
+
+def test_verifier_tdt_label_duration_near_tie():
+    """TDT label durations use the same rule: a label's duration 5e-4 below the
+    argmax duration is accepted (near-tie), 2e-3 below is rejected."""
+    b, X = 0, 1
+    D = [0, 1, 2]
+    steps = [(0, b, X, 1), (1, X, b, 1), (2, X, b, 1)]
+    for gap, ok in [(5e-4, True), (2e-3, False)]:
+        spec, model, enc, L = _table(steps, 3, 4, durations=D, edits=[("dur", 2, 0, b, 10.0 - gap)])
+        # X@0 with d = 2 jumps to t = 2 (blank, d=1) -> end
+        r = verify_tdt(model, enc[0], L, 3, [X], [0], [2], tol=NEAR)
+        assert r.ok == ok, r.message

@@ -1,4 +1,4 @@
-"""LSTM ring-path correctness at a given cluster size (env LL_CLUSTER)."""
+"""LSTM ring-path correctness for given dims (cluster size chosen by the library)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))

@@ -13,7 +13,7 @@ for c in fc-rnnt stateless-b512 fc-rnnt-4x; do
     > $o/${t}_bench_${c}_frame-looping.json 2> $o/${t}_bench_${c}_frame-looping.err
 done
 for c in fc-rnnt fc-tdt; do
-  LL_SCHEDULE=0 timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline \
+  timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline --schedule batched \
     > $o/${t}_bench_${c}_alg3-batched.json 2> $o/${t}_bench_${c}_alg3-batched.err
 done
 for c in sweep-rnnt sweep-tdt; do

@@ -7,7 +7,7 @@ Covers: the generic cluster kernel (tiny RNN-T / TDT, stateless), the
 FastConformer-shape kernels (LSTM predictor with W_hh in TMEM, tcgen05 GEMM
 projections, tick schedule; RNN-T and TDT, planted family so every row emits
 labels), the stateless FC-shape kernel, the frame-looping baseline, the
-batched Alg. 3 schedule (LL_SCHEDULE=0) and the native ragged gather (world
+batched Alg. 3 schedule (ll_options.schedule = 0) and the native ragged gather (world
 size 1).  Each decode's hypotheses are compared
 with the planted alignment / checked for well-formedness; the point of the run
 is the sanitizer's report."""
@@ -20,7 +20,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
-from paper_2406_06220_b200 import shard  # noqa: E402
+from paper_2406_06220_b200 import ll, shard  # noqa: E402
 from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model  # noqa: E402
 
 
@@ -67,8 +67,8 @@ if __name__ == "__main__":
     if len(sys.argv) > 1:   # one case: tiny | fc | fc-batched
         {"tiny": lambda: run_tiny("tiny"), "fc": lambda: run_planted("fc-rnnt", 6)}.get(sys.argv[1], lambda: None)()
         if sys.argv[1] == "fc-batched":
-            os.environ["LL_SCHEDULE"] = "0"
-            run_planted("fc-rnnt", 6)
+            with ll.options(schedule=0):
+                run_planted("fc-rnnt", 6)
         torch.cuda.synchronize()
         sys.exit(0)
     run_tiny("tiny")
@@ -77,10 +77,9 @@ if __name__ == "__main__":
     run_planted("fc-tdt", 6, gather=True)
     run_planted("fc-rnnt", 4, frame_looping=True)
     run_planted("stateless-b512", 20)
-    os.environ["LL_SCHEDULE"] = "0"   # the paper's batched outer loop (Alg. 3 as listed)
-    run_tiny("tiny")
-    run_planted("fc-rnnt", 6)
-    run_planted("fc-tdt", 6)
-    del os.environ["LL_SCHEDULE"]
+    with ll.options(schedule=0):   # the paper's batched outer loop (Alg. 3 as listed)
+        run_tiny("tiny")
+        run_planted("fc-rnnt", 6)
+        run_planted("fc-tdt", 6)
     torch.cuda.synchronize()
     print("sanitize_run done", flush=True)

@@ -1,4 +1,4 @@
-"""Time the fc-rnnt / fc-tdt decode under several (R, W, ring) configurations (env overrides)."""
+"""Time the fc-rnnt / fc-tdt decode under several (R, W, ring) configurations (ll_options overrides)."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -10,9 +10,10 @@ model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "b
 dec = LabelLoopingDecoder(model, spec.max_symbols, enc.shape[0], enc.shape[1])
 e = torch.from_numpy(enc).to("cuda", torch.bfloat16); l = torch.from_numpy(lengths).cuda()
 ref = None
-for R, W, NS in [(4, 8, 0), (5, 6, 0), (5, 4, 0), (4, 4, 0), (5, 2, 0), (8, 4, 0), (11, 2, 0), (16, 2, 0), (5, 4, 4), (5, 1, 0)]:
-    os.environ["LL_GROUP_ROWS"] = str(R); os.environ["LL_WINDOW"] = str(W)
-    os.environ["LL_RING"] = str(NS) if NS else ""
+from paper_2406_06220_b200 import ll
+for R, W in [(4, 8), (5, 6), (5, 4), (4, 4), (5, 2), (8, 4), (11, 2), (16, 2), (5, 1)]:
+    NS = 0
+    ll.ll_set_options(ll.options(group_rows=R, window=W).opts)
     try:
         for _ in range(2):
             out = dec.decode(e, l)

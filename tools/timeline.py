@@ -1,6 +1,6 @@
 """Per-warp clock64 timeline of block 0 (cluster 0, rank 0) of the decode
 kernel: every warp stamps phase boundaries of the first TL_N joint rounds and
-predictor steps (decode.cuh tl_* hooks, enabled by LL_TIMELINE_PTR).
+predictor steps (decode.cuh tl_* hooks, buffer passed as ll_options.timeline).
 
     python tools/timeline.py [config]          (GPU box)
 
@@ -15,7 +15,7 @@ from paper_2406_06220_b200 import ll
 ll.LIB_PATH = llbuild.build(variant="timeline")   # timeline hooks compiled in
 TL_N, TL_PH, NW = 128, 16, 10
 buf = torch.zeros(2 * TL_N * TL_PH * NW, dtype=torch.int64, device="cuda")
-os.environ["LL_TIMELINE_PTR"] = str(buf.data_ptr())
+ll.ll_set_options(ll.options(timeline=buf.data_ptr()).opts)   # this thread, for every decode below
 import bench
 from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
