@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="fc-rnnt", choices=list(synth.CONFIGS) + list(synth.SWEEPS))
     ap.add_argument("--chunk", type=int, default=1024, help="sweep: utterances per decode launch")
+    ap.add_argument("--streams", type=int, default=1, help="sweep: concurrent decode streams (one workspace each)")
+    ap.add_argument("--clock-window", type=float, default=1.0,
+                    help="seconds of identical (untimed) steps the clock sampler watches at least")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--family", default="planted", choices=["planted", "random"])
     ap.add_argument("--frame-looping", action="store_true",
@@ -97,6 +100,61 @@ def algorithmic_flops(spec, stats, total_frames):
     return a1, a2, a3
 
 
+# Primitive latencies measured on the B200 itself (tools/microbench.cu,
+# profiles/r01_microbench.txt), in SM cycles.
+LAT_HMMA = 20.8        # dependent mma.sync.m16n8k16 bf16
+LAT_LDS = 28.6         # dependent shared-memory load
+LAT_BAR = 30.7         # CTA barrier (bar.sync)
+LAT_XCTA = 125.7 / 2   # st.async + mbarrier, one way between two CTAs of a 16-CTA cluster
+
+
+def chain_floor_cycles(spec):
+    """Lower bounds (cycles) on one joint round and one predictor step of the
+    decode kernel's dependent chain (DESIGN.md §7 "dependency-chain floor"):
+    only the latencies no implementation of the cluster decomposition can
+    avoid -- the K-chain of the tensor-core contraction (two accumulator chains
+    over K), one shared-memory read, the CTA barriers and the one-way DSMEM
+    exchanges; no bandwidth term, no control code."""
+    H, P = spec.joint_dim, spec.pred_dim
+    joint = LAT_LDS + LAT_BAR + (H // 16) / 2 * LAT_HMMA + LAT_XCTA + LAT_BAR
+    if spec.pred_kind == "lstm":
+        pred = ((P // 16) / 2 * LAT_HMMA + LAT_LDS + LAT_XCTA          # gates + cell, h' exchange
+                + (P // 16) / 10 * LAT_HMMA + LAT_LDS + LAT_BAR        # W_pred, K split over 10 warps
+                + LAT_XCTA + LAT_BAR)                                  # g exchange
+    else:
+        pred = LAT_LDS + LAT_BAR                                       # table lookup
+    return joint, pred
+
+
+def chain_floor_ms(spec, rounds, pred_steps, sm_mhz):
+    j, pr = chain_floor_cycles(spec)
+    return (rounds * j + pred_steps * pr) / (sm_mhz * 1e3)
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def spawn_ranks(a):
+    """`--gpus N` without a torchrun environment: re-launch this command under
+    torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -110,7 +168,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -221,8 +279,11 @@ def run_reference(a, rank, world):
         "higher_is_better": True, "scaling": "strong" if a.config in synth.SWEEPS else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": a.config, "family": a.family, "sample_utts": nutt},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle",
-                         "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch per step"},
+        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": procs, "kind": "oracle",
+                              "impl": "oracle/ Python + numpy float64, sequential greedy (Alg. 1), "
+                                      "one process per utterance",
+                              "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch per step"},
+                             **cpu_info()),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -230,9 +291,13 @@ def run_reference(a, rank, world):
 
 def main():
     a = parse()
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        sys.exit(spawn_ranks(a))   # one process per GPU under torch.distributed.run
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         return run_reference(a, rank, world)
 
@@ -253,6 +318,7 @@ def main():
     if a.config in synth.SWEEPS:
         return run_sweep(a, rank, world, local, dev)
 
+    # weak scaling: every rank decodes its own batch (seed 1000 + rank)
     spec, w, enc_np, len_np = workload(a.config, 1000 + rank, a.family)
     B, T = enc_np.shape[0], enc_np.shape[1]
     model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16", device=f"cuda:{local}")
@@ -292,6 +358,15 @@ def main():
             ll.ll_set_timing_events(None, None)
             ev_s1[i].record(stream)
         torch.cuda.synchronize()
+        # the clock record needs a sustained window: identical untimed steps
+        # until --clock-window seconds have passed (the timed K steps above are
+        # the measurement)
+        t_end = time.perf_counter() + a.clock_window
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                flush.zero_()
+                step()
+            torch.cuda.synchronize()
     if dec.sync() != ll.LL_OK:
         raise RuntimeError("timed decode failed")
     step_ms = [ev_s0[i].elapsed_time(ev_s1[i]) for i in range(a.steps)]
@@ -359,15 +434,19 @@ def main():
     h2d = enc_h.numel() * enc_h.element_size() + len_h.numel() * 4
     d2h = sum(t.numel() * 4 for t in outs[0])
 
+    # whole-job aggregate: the audio / utterances of ALL ranks over the max-over-ranks time
     audio_s = float(len_np.sum()) * frame_s_of(a.config)
     t_all = torch.tensor([tot_ms, sum(e2e_ms)], dtype=torch.float64, device=dev)
+    work = torch.tensor([audio_s, float(B)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM)
         dist.barrier()
     tot_ms_max, e2e_ms_max = float(t_all[0]), float(t_all[1])
-    value = world * a.steps * audio_s / (tot_ms_max / 1e3)
-    utt_s = world * a.steps * B / (tot_ms_max / 1e3)
-    e2e_value = world * a.steps * audio_s / (e2e_ms_max / 1e3)
+    audio_all, utt_all = float(work[0]), float(work[1])
+    value = a.steps * audio_all / (tot_ms_max / 1e3)
+    utt_s = a.steps * utt_all / (tot_ms_max / 1e3)
+    e2e_value = a.steps * audio_all / (e2e_ms_max / 1e3)
 
     # roofline of the dominant kernel (the persistent decode kernel)
     a1, a2, a3 = algorithmic_flops(spec, stats, int(len_np.sum()))
@@ -382,6 +461,10 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         traffic = json.load(open(tr_path)).get(a.config)
+    clocks = clk.summary()
+    sm_mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    floor = chain_floor_ms(spec, stats["chain_rounds"], stats["chain_pred_steps"], sm_mhz)
+    jf, pf = chain_floor_cycles(spec)
 
     rows = stats["joint_evals"]
     line = {
@@ -389,10 +472,12 @@ def main():
         "warmup": a.warmup, "ms_per_step": tot_ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": a.config, "family": a.family, "B": B, "T_max": T,
-                   "algorithm": "frame-looping (Alg. 2 baseline)" if a.frame_looping else "label-looping (Alg. 3)",
+                   "algorithm": "frame-looping (Alg. 2 baseline)" if a.frame_looping else
+                   ("label-looping (Alg. 3), batched outer loop" if a.schedule == "batched"
+                    else "label-looping (Alg. 3), per-row ticks"),
                    "frames": int(len_np.sum()), "audio_s_per_step": audio_s, "l2": "flushed (512 MiB) between steps",
                    "model_tables": "prepared once per model (ll_prepare), outside the step",
-                   "parallelism": f"utterance-sharded x{world}"},
+                   "parallelism": f"utterance-sharded x{world} (each rank its own B={B} batch)"},
         "utterances_per_s": utt_s,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms_max / a.steps,
@@ -403,21 +488,30 @@ def main():
                      "kernel_ms": kern_mean, "kernel_share_of_step": kern_mean / (tot_ms_max / a.steps),
                      "flops_per_launch": a2 + a3,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF"},
+        "chain_floor": {"ms": floor, "frac": floor / kern_mean, "kernel_ms": kern_mean,
+                        "critical_cluster": {"joint_rounds": stats["chain_rounds"],
+                                             "predictor_steps": stats["chain_pred_steps"]},
+                        "cycles_per_round": jf, "cycles_per_predictor_step": pf, "sm_mhz": sm_mhz,
+                        "basis": "dependent-latency lower bound per phase from measured primitive latencies "
+                                 "(profiles/r01_microbench.txt; DESIGN.md §7)"},
         "decode_stats": {"labels": stats["labels"], "tokens_per_frame": stats["labels"] / max(1, int(len_np.sum())),
                          "outer_steps": stats["outer_steps"], "joint_rounds": stats["joint_rounds"],
                          "mean_active_rows": rows / max(1, stats["joint_rounds"]),
                          "predictor_steps": stats["predictor_steps"], "groups": stats["groups"],
-                         "cluster_size": stats["cluster_size"]},
+                         "cluster_size": stats["cluster_size"], "window": stats["window"],
+                         "group_rows": stats["group_rows"]},
         "context": "paper: 5197.2 non-encoder RTFx RNNT-L B=32 with CUDA graphs on one RTX A6000, bf16 (PAPER.md:354)",
     }
     if rank == 0 and not a.no_cpu_baseline:
         n = a.cpu_sample or B
         v, dt, procs, nutt, audio = cpu_oracle_time(spec, w, enc_np, len_np, n, a.config)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
-                                "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch, "
-                                          f"{dt:.1f} s wall"}
-    clocks = clk.summary()
+        line["cpu_baseline"] = dict({"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
+                                     "impl": "oracle/ Python + numpy float64, sequential greedy (Alg. 1), "
+                                             "one process per utterance",
+                                     "sample": f"{nutt} utterances ({audio:.1f} audio-s) of the {a.config} batch, "
+                                               f"{dt:.1f} s wall"}, **cpu_info())
     if clocks:
+        clocks["window"] = f"the {a.steps} timed steps + identical untimed steps to >= {a.clock_window} s"
         line["clocks"] = clocks
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -428,10 +522,13 @@ def main():
 def run_sweep(a, rank, world, local, dev):
     """BASELINE config (5): 8192 utterances with LibriSpeech-like lengths,
     length-bucketed into batches of 32 and assigned to ranks by LPT
-    (paper_2406_06220_b200.shard); each rank decodes its shard longest-first in
-    launches of `--chunk` utterances (one stream, no host sync between them),
-    packs its ragged hypotheses on the device, and the hypotheses are gathered
-    over NCCL (the only collective).  A step = the whole sweep, gather included."""
+    (paper_2406_06220_b200.shard).  Each rank decodes its shard longest-first in
+    launches of `--chunk` utterances spread round-robin over `--streams` CUDA
+    streams (one workspace each; no host sync between launches), every launch
+    writing its rows of the rank's [n, cap] output buffers; then the rank's
+    ragged hypotheses are gathered on rank 0 with ll_gather_ragged (NCCL, the
+    only collective).  A step = the whole sweep, gather included; strong
+    scaling (the total work is fixed)."""
     import torch
     import torch.distributed as dist
     from paper_2406_06220_b200 import ll, shard
@@ -443,12 +540,24 @@ def run_sweep(a, rank, world, local, dev):
     w, codes = synth.planted_weights(spec, 1000)
     L_all = synth.sweep_lengths(c["length_seed"], c["n_utt"])
     ids = shard.rank_shard(L_all, world, rank, c["batch"])
+    n_loc = len(ids)
+    T_glob = int(L_all.max())
     model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16", device=f"cuda:{local}")
+    nstreams = max(1, a.streams)
+    decs = [LabelLoopingDecoder(model, spec.max_symbols, a.chunk, T_glob) for _ in range(nstreams)]
+    for d in decs:
+        d.prepare()
+    cap = decs[0].cap
+    # the rank's output buffers: every launch writes its rows (contiguous row slices)
+    out_tok = torch.zeros(max(n_loc, 1), cap, dtype=torch.int32, device=dev)
+    out_ts = torch.zeros_like(out_tok)
+    out_du = torch.zeros_like(out_tok) if tdt else None
+    out_len = torch.zeros(max(n_loc, 1), dtype=torch.int32, device=dev)
     # inputs: planted utterances (each from its own seeded stream), laid out per
-    # chunk as [B_c, T_c, D_e] bf16 on the device; the ragged frames are also
+    # launch as [B_c, T_c, D_e] bf16 on the device; the ragged frames are also
     # kept in pinned host memory for the end-to-end leg
     chunks, planted = [], {}
-    for c0 in range(0, len(ids), a.chunk):
+    for c0 in range(0, n_loc, a.chunk):
         cid = ids[c0:c0 + a.chunk]
         Lc = L_all[cid]
         T = int(Lc.max())
@@ -462,22 +571,25 @@ def run_sweep(a, rank, world, local, dev):
             enc[i, :e.shape[0]] = eh.to(dev)
         frames = torch.cat(host).pin_memory()
         rows = torch.cat([torch.arange(int(l), device=dev) + i * T for i, l in enumerate(Lc)])
-        chunks.append(dict(ids=torch.from_numpy(cid).to(dev), enc=enc, lengths=torch.from_numpy(Lc.astype(np.int32)).to(dev),
-                           dec=LabelLoopingDecoder(model, spec.max_symbols, len(cid), T), frames=frames, rows=rows))
-        chunks[-1]["dec"].prepare()
+        sl = slice(c0, c0 + len(cid))
+        chunks.append(dict(enc=enc, lengths=torch.from_numpy(Lc.astype(np.int32)).to(dev), frames=frames, rows=rows,
+                           out=(out_tok[sl], out_ts[sl], None if out_du is None else out_du[sl], out_len[sl]),
+                           frames_n=int(Lc.sum())))
+    ids32 = torch.from_numpy(ids.astype(np.int32)).to(dev)
     stream = torch.cuda.current_stream()
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nstreams - 1)]
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     gather = shard.NcclGather(device=dev)   # ll_gather_ragged on a libll NCCL communicator (world 1 too)
-    for ch in chunks:
-        ch["ids32"] = ch["ids"].to(torch.int32)
 
     h2d_s = torch.cuda.Stream(device=dev)
     ev_in = [torch.cuda.Event() for _ in chunks]
     ev_dec = [torch.cuda.Event() for _ in chunks]
-    for e in ev_dec:
+    ev_fork, ev_join = torch.cuda.Event(), [torch.cuda.Event() for _ in streams]
+    ev_k = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in chunks]
+    for e in ev_dec + [x for p in ev_k for x in p]:
         e.record(stream)
 
-    def step(e2e=False):
+    def step(e2e=False, timed=False):
         if e2e:   # H2D of every chunk's ragged frames (scattered into the padded layout) on a copy
             # stream, so chunk k+1's copy overlaps chunk k's decode
             with torch.cuda.stream(h2d_s):
@@ -486,56 +598,80 @@ def run_sweep(a, rank, world, local, dev):
                     dst = ch["enc"].view(-1, spec.enc_dim)
                     dst.index_copy_(0, ch["rows"], ch["frames"].to(dev, non_blocking=True))
                     ev_in[k].record(h2d_s)
+        ev_fork.record(stream)
+        for s_ in streams[1:]:
+            s_.wait_event(ev_fork)
         for k, ch in enumerate(chunks):
+            j = k % nstreams
+            st = streams[j]
             if e2e:
-                stream.wait_event(ev_in[k])
-            s = ch["dec"].launch(ch["enc"], ch["lengths"], stream)
-            ev_dec[k].record(stream)
+                st.wait_event(ev_in[k])
+            if timed:
+                ll.ll_set_timing_events(ev_k[k][0].cuda_event, ev_k[k][1].cuda_event)
+            s = decs[j].launch(ch["enc"], ch["lengths"], st, out=ch["out"])
+            if timed:
+                ll.ll_set_timing_events(None, None)
+            ev_dec[k].record(st)
             if s != ll.LL_OK:
                 raise ll.LLError(s, "decode")
-        bufs = [gather.gather(ch["ids32"], ch["dec"].lengths_out, ch["dec"].tokens, ch["dec"].timestamps,
-                              ch["dec"].durs if tdt else None) for ch in chunks]
+        for j, s_ in enumerate(streams[1:], 1):
+            ev_join[j].record(s_)
+            stream.wait_event(ev_join[j])
+        buf = gather.gather(ids32, out_len[:n_loc], out_tok[:n_loc], out_ts[:n_loc],
+                            out_du[:n_loc] if tdt else None)
         if rank != 0:
             return None
-        if e2e:   # D2H of the gathered hypotheses
-            return [b.cpu() for b in bufs]
-        return bufs
+        return buf.cpu() if e2e else buf   # e2e: D2H of the gathered hypotheses
 
     for _ in range(a.warmup):
         gathered = step()
     torch.cuda.synchronize()
     gathered_ok = True
     if rank == 0:   # the gathered records hold every utterance once; this rank's equal their planted alignments
-        merged = shard.unpack_records(torch.cat(gathered).cpu().numpy(), tdt)
+        merged = shard.unpack_records(gathered.cpu().numpy(), tdt)
         gathered_ok = len(merged) == int(c["n_utt"]) and all(merged[u] == tuple(planted[u]) for u in planted)
-    for ch in chunks:
-        if ch["dec"].sync() != ll.LL_OK:
+    for d in decs:
+        if d.sync() != ll.LL_OK:
             raise RuntimeError("sweep decode failed")
+    # statistics of one sweep (per launch: each decoder's stats are its last launch's)
+    agg = dict(joint_evals=0, predictor_rows=0, labels=0, joint_rounds=0, predictor_steps=0, groups=0)
+    chain_ms_floor = 0.0
+    per_launch = []
+    for k, ch in enumerate(chunks):
+        d = decs[k % nstreams]
+        d.launch(ch["enc"], ch["lengths"], streams[0], out=ch["out"])
+        st = d.stats(streams[0])
+        per_launch.append(st)
+        for key in agg:
+            agg[key] += st[key]
     # correctness of the sweep: every utterance of this shard equals its planted alignment
+    tok, ts, ln = out_tok[:n_loc].cpu(), out_ts[:n_loc].cpu(), out_len[:n_loc].cpu()
+    du = out_du[:n_loc].cpu() if tdt else None
     bad = 0
-    for ch in chunks:
-        hy = ch["dec"]
-        n = ch["ids"].numel()
-        tok, ts, ln = hy.tokens[:n].cpu(), hy.timestamps[:n].cpu(), hy.lengths_out[:n].cpu()
-        du = hy.durs[:n].cpu() if tdt else None
-        for i, u in enumerate(ch["ids"].cpu().tolist()):
-            k = int(ln[i])
-            got = (tok[i, :k].tolist(), ts[i, :k].tolist()) + ((du[i, :k].tolist(),) if tdt else ())
-            bad += got != tuple(planted[u])
+    for i, u in enumerate(ids.tolist()):
+        k = int(ln[i])
+        got = (tok[i, :k].tolist(), ts[i, :k].tolist()) + ((du[i, :k].tolist(),) if tdt else ())
+        bad += got != tuple(planted[u])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    kern = []
     with ClockSampler(local) as clk:
         for i in range(a.steps):
             flush.zero_()
             if world > 1:
                 dist.barrier()
             ev0[i].record(stream)
-            step()
+            step(timed=True)
             ev1[i].record(stream)
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()
+            kern.append([ev_k[k][0].elapsed_time(ev_k[k][1]) for k in range(len(chunks))])
+        t_end = time.perf_counter() + a.clock_window
+        while time.perf_counter() < t_end:
+            step()
+            torch.cuda.synchronize()
     ms = [ev0[i].elapsed_time(ev1[i]) for i in range(a.steps)]
     e2e_ms, d2h = [], 0
     for i in range(a.steps):
@@ -548,7 +684,7 @@ def run_sweep(a, rank, world, local, dev):
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-        d2h = sum(b.numel() * 4 for b in got) if got is not None else 0
+        d2h = got.numel() * 4 if got is not None else 0
     t_all = torch.tensor([sum(ms), sum(e2e_ms), float(bad)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
@@ -557,24 +693,54 @@ def run_sweep(a, rank, world, local, dev):
     n_utt = int(c["n_utt"])
     value = a.steps * audio_s / (tot_ms / 1e3)
     h2d = sum(ch["frames"].numel() * 2 + ch["lengths"].numel() * 4 for ch in chunks)
+    # roofline of the decode kernel on this rank: algorithmic FLOPs of every
+    # launch over that launch's duration (CUDA events on its stream), averaged
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("bf16_tflops", 1590.0)
+    kern_mean = [statistics.mean(kern[i][k] for i in range(a.steps)) for k in range(len(chunks))]
+    flops = []
+    for k, ch in enumerate(chunks):
+        _, a2, a3 = algorithmic_flops(spec, per_launch[k], ch["frames_n"])
+        flops.append(a2 + a3)
+    achieved = sum(flops) / (sum(kern_mean) / 1e3) / 1e12
+    clocks = clk.summary()
+    sm_mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    floor = sum(chain_floor_ms(spec, st["chain_rounds"], st["chain_pred_steps"], sm_mhz) for st in per_launch)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic",
         "config": {"workload": a.config, "family": "planted", "utterances": n_utt, "batch": c["batch"],
-                   "chunk": a.chunk, "frames": int(L_all.sum()), "audio_s_per_step": audio_s,
+                   "launch_batch": a.chunk, "streams": nstreams, "launches_per_rank": len(chunks),
+                   "frames": int(L_all.sum()), "audio_s_per_step": audio_s,
                    "l2": "flushed (512 MiB) between steps", "parallelism": f"LPT length-bucketed x{world}, NCCL gather"},
         "utterances_per_s": a.steps * n_utt / (tot_ms / 1e3),
         "e2e": {"value": a.steps * audio_s / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_tot / a.steps},
-        # per chunk: projection GEMM + decode + the two packing kernels of ll_gather_ragged (NCCL's own
-        # all-gather / send-recv kernels not counted); model tables prepared once before timing
-        "gpu_launches": a.steps * len(chunks) * 4,
+        # per launch: projection GEMM + decode; per step: the two packing kernels of ll_gather_ragged
+        # (NCCL's own all-gather / send-recv kernels not counted); model tables prepared once before timing
+        "gpu_launches": a.steps * (len(chunks) * 2 + 2),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "decode_kernel (rank 0, every launch)",
+                     "kernel_ms_sum": sum(kern_mean), "flops_per_step": sum(flops),
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback 1.59 PF"},
+        "chain_floor": {"ms": floor, "frac": floor / sum(kern_mean), "kernel_ms_sum": sum(kern_mean),
+                        "basis": "sum over launches of the per-launch dependency-chain floor (DESIGN.md §7)"},
+        "decode_stats": dict(agg, tokens_per_frame=agg["labels"] / max(1, sum(ch["frames_n"] for ch in chunks))),
         "hypotheses_equal_planted": bad_max == 0,
         "gathered_hypotheses_ok": gathered_ok,
     }
-    clocks = clk.summary()
+    if rank == 0 and not a.no_cpu_baseline:
+        sp, ws_, enc_s, len_s = sweep_sample(a.config, a.cpu_sample or 64)
+        v, dt, procs, nutt, audio = cpu_oracle_time(sp, ws_, enc_s, len_s, len(len_s), a.config)
+        line["cpu_baseline"] = dict({"value": v, "unit": UNIT, "cores": procs, "kind": "oracle",
+                                     "impl": "oracle/ Python + numpy float64, sequential greedy (Alg. 1), "
+                                             "one process per utterance",
+                                     "sample": f"utterances 0..{nutt - 1} of the sweep ({audio:.1f} audio-s), "
+                                               f"{dt:.1f} s wall"}, **cpu_info())
     if clocks:
+        clocks["window"] = f"the {a.steps} timed steps + identical untimed steps to >= {a.clock_window} s"
         line["clocks"] = clocks
     if rank == 0:
         print(json.dumps(line), flush=True)

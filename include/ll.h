@@ -142,6 +142,34 @@ ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B
                         void *workspace, size_t workspace_bytes, ll_stream stream);
 
 /*
+ * Greedy decoding with scores (BatchedHyps keeps "tokens,
+ * time-stamps, scores").  As ll_decode_rnnt / ll_decode_tdt, plus
+ *  out_scores  [B] f32 (DEVICE, non-NULL when B > 0): the greedy score of each
+ *              hypothesis = the sum over EVERY decision the method takes (blanks
+ *              included, reading A19 after SPEC.md:239, :266) of the decision's
+ *              log-probability log softmax(logits)[y]; for TDT plus the duration
+ *              log-probability log softmax(dur_logits)[d] (the pair's joint
+ *              log-probability, reading A26).
+ * The log-sum-exp over the V+1 (and |D|) logits is fused into the joint
+ * epilogue and combined across the cluster with the argmax keys; logits never
+ * reach HBM.  Hypotheses are identical to the calls without scores.  Per-row
+ * tick schedule only (ll_options.schedule = 0 returns LL_ERR_UNSUPPORTED).
+ */
+ll_status ll_decode_rnnt_scores(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                                const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                                int32_t blank_id, int32_t max_symbols,
+                                int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_lengths,
+                                int32_t out_capacity, float *out_scores,
+                                void *workspace, size_t workspace_bytes, ll_stream stream);
+ll_status ll_decode_tdt_scores(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                               const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                               int32_t blank_id, int32_t max_symbols,
+                               const int32_t *durations, int32_t num_durations,
+                               int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_durations,
+                               int32_t *out_lengths, int32_t out_capacity, float *out_scores,
+                               void *workspace, size_t workspace_bytes, ll_stream stream);
+
+/*
  * Frame-looping BASELINE (Alg. 2, "Batched Inference of Transducer",
  * PAPER.md:84-115) on the same kernels, for the paper's label- vs frame-looping
  * comparison.  Same arguments, ownership, errors and
@@ -195,7 +223,9 @@ const char *ll_status_string(ll_status status);
  * Alg. 1), [3] batched predictor steps, [4] predictor row evaluations,
  * [5] labels emitted, [6] groups decoded, [7] cluster size, [8] joint rows
  * computed (including speculative window frames), [9] window W, [10] rows
- * per group R, [11] reserved. */
+ * per group R, [11] the longest per-cluster chain, packed (rounds + steps) << 40
+ * | joint rounds << 20 | predictor steps of that cluster (each field saturates
+ * at 2^20 - 1): the critical path of the launch (bench.py's chain floor). */
 ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream);
 
 /*

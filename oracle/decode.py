@@ -28,7 +28,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .model import Transducer, argmax_lowest
+from .model import Transducer, argmax_lowest, log_prob
 
 
 @dataclasses.dataclass
@@ -39,13 +39,27 @@ class DecodeResult:
     joint_evals: int = 0          # joint evaluations of this utterance
     predictor_calls: int = 0      # predictor calls of this utterance (incl. SOS)
     trace: Optional[list] = None  # every decision (t, y[, d]) in order
+    score: float = 0.0            # greedy score: sum of log-probabilities of every decision (N2, A19)
 
 
 def _decide(model: Transducer, f_t, g):
+    y, d, _ = _decide_scored(model, f_t, g)
+    return y, d
+
+
+def _decide_scored(model: Transducer, f_t, g):
+    """(y, d, log-probability of the decision): token log-softmax at y, plus,
+    for TDT, the duration log-softmax at the chosen duration (the joint
+    probability of the (token, duration) pair; reading A19)."""
     logits, dl = model.joint(f_t, g)
     y = argmax_lowest(logits)
-    d = None if dl is None else model.durations[argmax_lowest(dl)]
-    return y, d
+    lp = log_prob(logits, y)
+    d = None
+    if dl is not None:
+        j = argmax_lowest(dl)
+        d = model.durations[j]
+        lp += log_prob(dl, j)
+    return y, d, lp
 
 
 def decode_sequential(model: Transducer, enc_row: np.ndarray, L: int, max_symbols: int,
@@ -65,8 +79,9 @@ def decode_sequential(model: Transducer, enc_row: np.ndarray, L: int, max_symbol
     res.predictor_calls = 1
     t, k = 0, 0
     while t < L:                                             # line 63
-        y, d = _decide(model, f[t], g)                       # lines 69-70
+        y, d, lp = _decide_scored(model, f[t], g)            # lines 69-70
         res.joint_evals += 1
+        res.score += lp                                      # every argmax step, blanks included
         if keep_trace:
             res.trace.append((t, y) if not tdt else (t, y, d))
         if y == model.blank:                                 # line 75-76: t = t + 1

@@ -26,6 +26,16 @@ def argmax_lowest(v: np.ndarray) -> int:
     return int(np.flatnonzero(v == m)[0])
 
 
+def log_prob(v: np.ndarray, i: int) -> float:
+    """log softmax(v)[i] = v[i] - log sum_j exp(v[j]) (the greedy score term of
+    one argmax step; BatchedHyps "scores", read per SPEC.md:239 /
+    :266 as the log-probability of every argmax step, blanks included).  The
+    max is subtracted before exp for range only (exact identity)."""
+    v = np.asarray(v, dtype=np.float64)
+    m = v.max()
+    return float(v[i] - (m + np.log(np.exp(v - m).sum())))
+
+
 def _sigmoid(x):
     return 1.0 / (1.0 + np.exp(-x))
 

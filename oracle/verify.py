@@ -25,7 +25,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .model import Transducer, argmax_lowest
+from .model import Transducer, argmax_lowest, log_prob
 
 
 @dataclasses.dataclass
@@ -34,6 +34,7 @@ class VerifyResult:
     decisions: int = 0
     near_ties: int = 0
     message: str = ""
+    score: float = 0.0   # float64 greedy score along the verified decisions (N2)
 
 
 def _accept(logits: np.ndarray, y: int, tol: float):
@@ -72,6 +73,8 @@ def verify_rnnt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
             acc, tie = _accept(logits, tokens[i], tol)
             r.decisions += 1
             r.near_ties += int(tie and acc)
+            if acc:
+                r.score += log_prob(logits, tokens[i])
             if not acc:
                 return VerifyResult(False, r.decisions, r.near_ties,
                                     f"label {tokens[i]} at t={t} (#{i}) rejected: gap "
@@ -85,6 +88,8 @@ def verify_rnnt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
             acc, tie = _accept(logits, model.blank, tol)
             r.decisions += 1
             r.near_ties += int(tie and acc)
+            if acc:
+                r.score += log_prob(logits, model.blank)
             if not acc:
                 return VerifyResult(False, r.decisions, r.near_ties,
                                     f"blank at t={t} rejected: gap "
@@ -114,13 +119,13 @@ def verify_tdt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
     nodes = [0]
     best = {"msg": "no acceptable path"}
 
-    def rec(i, t, k, st, g, dec_count, ties):
+    def rec(i, t, k, st, g, dec_count, ties, score):
         nodes[0] += 1
         if nodes[0] > max_nodes:
             return None
         if t >= L:
             if i == len(tokens):
-                return (dec_count, ties)
+                return (dec_count, ties, score)
             best["msg"] = f"utterance ended with {len(tokens) - i} labels left"
             return None
         logits, dl = model.joint(f[t], g)
@@ -142,7 +147,8 @@ def verify_tdt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
                 nt, nk = t + d, 0
             else:
                 nt, nk = (t + 1, 0) if k + 1 == m else (t, k + 1)
-            return rec(i + 1, nt, nk, st2, g2, dec_count + 1, ties + int(tie_y) + int(tie_d))
+            return rec(i + 1, nt, nk, st2, g2, dec_count + 1, ties + int(tie_y) + int(tie_d),
+                       score + log_prob(logits, y) + log_prob(dl, D.index(d)))
         if i < len(tokens) and timestamps[i] < t:
             best["msg"] = f"label #{i} stamped {timestamps[i]} was skipped over (t={t})"
             return None
@@ -156,12 +162,13 @@ def verify_tdt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
             acc_d, tie_d = _accept(dl, j, tol)
             if not acc_d:
                 continue
-            out = rec(i, t + max(D[j], 1), 0, st, g, dec_count + 1, ties + int(tie_b) + int(tie_d))
+            out = rec(i, t + max(D[j], 1), 0, st, g, dec_count + 1, ties + int(tie_b) + int(tie_d),
+                      score + log_prob(logits, model.blank) + log_prob(dl, j))
             if out is not None:
                 return out
         return None
 
-    out = rec(0, 0, 0, st0, g0, 0, 0)
+    out = rec(0, 0, 0, st0, g0, 0, 0, 0.0)
     if out is None:
         return VerifyResult(False, message=best["msg"] if nodes[0] <= max_nodes else "search budget exceeded")
-    return VerifyResult(True, out[0], out[1])
+    return VerifyResult(True, out[0], out[1], score=out[2])

@@ -27,7 +27,34 @@ __device__ __forceinline__ uint64_t pack_key(float v, int idx) {
 __device__ __forceinline__ int key_index(uint64_t key) {
   return (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull));
 }
+// the logit a key encodes (inverse of ordered_f32)
+__device__ __forceinline__ float key_value(uint64_t key) {
+  const uint32_t u = (uint32_t)(key >> 32);
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Log-sum-exp partials for the greedy scores (N2): (m, s) with s = sum exp(v - m)
+// over a subset of logits, packed in 64 bits (m in the low word).  Combining
+// is exact up to rounding and order-independent up to rounding; the kernels
+// always combine in a fixed order, so results are deterministic.  The empty
+// subset is (-inf, 0).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t lse_pack(float m, float s) {
+  return ((uint64_t)__float_as_uint(s) << 32) | __float_as_uint(m);
+}
+__device__ __forceinline__ float lse_m(uint64_t p) { return __uint_as_float((uint32_t)p); }
+__device__ __forceinline__ float lse_s(uint64_t p) { return __uint_as_float((uint32_t)(p >> 32)); }
+__device__ __forceinline__ uint64_t lse_empty() { return lse_pack(-INFINITY, 0.f); }
+__device__ __forceinline__ uint64_t lse_combine(uint64_t a, uint64_t b) {
+  const float ma = lse_m(a), mb = lse_m(b);
+  const float m = fmaxf(ma, mb);
+  if (m == -INFINITY) return lse_empty();
+  return lse_pack(m, lse_s(a) * __expf(ma - m) + lse_s(b) * __expf(mb - m));
+}
+// log sum exp of the subset
+__device__ __forceinline__ float lse_value(uint64_t p) { return lse_m(p) + __logf(lse_s(p)); }
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
   lo = __shfl_xor_sync(0xffffffffu, lo, m);

@@ -72,15 +72,20 @@ enum {
 // Shared-memory layout (identical on host and device).
 struct Layout {
   int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
+  int wks, pks;                  // u64 words per per-warp key entry / per cluster partial (scores: 4)
   size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, off_es, total;
 };
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ring: bf16 LSTM (producer warp + weight ring + shared-memory h); NS slots.
+// sc: greedy scores (N2): per-warp entries carry log-sum-exp partials (4 words),
+// TDT cluster partials too (token + duration partials: 4 words).
 __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, int V1, int nD, int R, int W,
-                                              int WF, int C, int NS) {
+                                              int WF, int C, int NS, int sc = 0) {
   Layout L;
+  L.wks = sc ? 4 : 2;
+  L.pks = (sc && nD > 0) ? 4 : 2;
   const int NT = (V1 + nD + 7) / 8;
   L.tiles_max = (NT + C - 1) / C;
   L.UPC = lstm ? P / C : 0;
@@ -107,8 +112,8 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.off_f = o;    o = align_up(o + (size_t)2 * R * WF * H * (bf ? 2 : 4), 128);
   L.off_g = o;    o = align_up(o + (size_t)R * H * 4, 128);
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * 4, 128);
-  L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 16, 128);
-  L.off_wkey = o; o = align_up(o + (size_t)L.NW * L.JR * 16, 128);
+  L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 8 * L.pks, 128);
+  L.off_wkey = o; o = align_up(o + (size_t)L.NW * L.JR * 8 * L.wks, 128);
   L.off_hs = o;   o = align_up(o + (size_t)(L.ring ? 2 * R * L.hstride : 0), 128);
   L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * P * 2, 128);
   L.off_es = o;   o = align_up(o + (size_t)(L.ring ? R * 4 * L.UPC * 4 : 0), 128);
@@ -137,6 +142,7 @@ struct DecodeParams {
   void *h;                       // f32 LSTM: [2][B][P]
   float *gglob;                  // f32 LSTM: [B][H]
   int *out_tokens, *out_timestamps, *out_durations, *out_lengths;
+  float *out_scores;             // greedy scores [B] (SC instantiations), else NULL
   int *status;                   // bit0 bad length, bit1 capacity
   int *group_counter;
   unsigned long long *stats;     // see ll.h ll_stats
@@ -158,6 +164,8 @@ struct RowState {
   int ctx[MAX_CTX][MAX_R];
   int active[MAX_R], scanning[MAX_R], found[MAX_R], needp[MAX_R];
   int fy[MAX_R], ft[MAX_R], fd[MAX_R];
+  float score[MAX_R];                    // greedy score of each slot (SC)
+  float lp[MAX_JR];                      // log-probability of each logical joint row's decision (SC)
   int fbase[2][MAX_R], fcnt[2][MAX_R];   // frames held in fbuf[X] for each slot
   int slist[MAX_R], plist[MAX_R];
   int llist[MAX_R], nload;               // per-row schedule: slots whose window must be (re)loaded
@@ -180,7 +188,8 @@ __device__ __forceinline__ void csync(int nthreads) {
 // HC / PC / CC: compile-time joint dim H, predictor dim P and cluster size
 // (0 = runtime).  The production shape (H = P = 640, 16-CTA clusters) is
 // instantiated with all three fixed so that loops unroll and addressing folds.
-template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0>
+// SC: 1 = greedy scores (N2): log-sum-exp partials ride along with the argmax keys.
+template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0, int SC = 0>
 struct Ctx {
   static constexpr bool BF = sizeof(T) == 2;
   const DecodeParams &p;
@@ -286,7 +295,10 @@ struct Ctx {
     else return d;
   }
   __device__ float *cs() const { return (float *)(sm + L.off_c); }
-  __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * 2; }
+  __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * pks(); }
+  // words per per-warp key entry / per cluster partial (compile-time unless SC with a runtime family)
+  __device__ __forceinline__ int wks() const { return SC ? 4 : 2; }
+  __device__ __forceinline__ int pks() const { return (SC && is_tdt()) ? 4 : 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
   __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * hstride(); }
   __device__ float *es() const { return (float *)(sm + L.off_es); }
@@ -532,21 +544,29 @@ struct Ctx {
         else joint_mma<1>(acc);
       }
       uint64_t tk[2][2], dk[2][2];
+      [[maybe_unused]] uint64_t tl[2][2], dl[2][2];   // SC: log-sum-exp partials (token, duration)
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           tk[mt][rr] = 0;
           dk[mt][rr] = 0;
+          [[maybe_unused]] float vv[2];
+          [[maybe_unused]] int kind[2];   // 0 none, 1 token, 2 duration
 #pragma unroll
           for (int e2 = 0; e2 < 2; ++e2) {
             const int e = rr * 2 + e2;
             const int lr = warp * 8 + 2 * q + e2;     // local vocab row
             const int v = tile0 * 8 + lr;
+            if constexpr (SC) kind[e2] = 0;
             if (warp < ntiles && v < NV) {
               const float val = (acc[mt][0][e] + acc[mt][1][e]) + bsl()[lr];
               if (v < V1) tk[mt][rr] = umax64(tk[mt][rr], pack_key(val, v));
               else dk[mt][rr] = umax64(dk[mt][rr], pack_key(val, v - V1));
+              if constexpr (SC) {
+                vv[e2] = val;
+                kind[e2] = v < V1 ? 1 : 2;
+              }
               const int jr = mt * 16 + g + rr * 8;
               if (logits != nullptr && mt < MT && jr < nrows_valid) logits[(size_t)(row_base + jr) * NV + v] = val;
             }
@@ -556,6 +576,28 @@ struct Ctx {
           if (is_tdt()) {
             dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 1));
             dk[mt][rr] = umax64(dk[mt][rr], shfl_xor_u64(dk[mt][rr], 2));
+          }
+          if constexpr (SC) {
+            // the warp's partial over its 8 vocabulary rows: the max is the key's
+            // value (exact), then the sum of exp(v - max) over the 4 lanes of the row
+            const float mt_ = tk[mt][rr] ? key_value(tk[mt][rr]) : -INFINITY;
+            float st_ = 0.f, sd_ = 0.f;
+            const float md_ = dk[mt][rr] ? key_value(dk[mt][rr]) : -INFINITY;
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+              if (kind[e2] == 1) st_ += __expf(vv[e2] - mt_);
+              if (kind[e2] == 2) sd_ += __expf(vv[e2] - md_);
+            }
+            st_ += __shfl_xor_sync(0xffffffffu, st_, 1);
+            st_ += __shfl_xor_sync(0xffffffffu, st_, 2);
+            tl[mt][rr] = mt_ == -INFINITY ? lse_empty() : lse_pack(mt_, st_);
+            if (is_tdt()) {
+              sd_ += __shfl_xor_sync(0xffffffffu, sd_, 1);
+              sd_ += __shfl_xor_sync(0xffffffffu, sd_, 2);
+              dl[mt][rr] = md_ == -INFINITY ? lse_empty() : lse_pack(md_, sd_);
+            } else {
+              dl[mt][rr] = lse_empty();
+            }
           }
         }
       if (q == 0) {
@@ -568,7 +610,14 @@ struct Ctx {
               uint4 e;
               e.x = (uint32_t)tk[mt][rr]; e.y = (uint32_t)(tk[mt][rr] >> 32);
               e.z = (uint32_t)dk[mt][rr]; e.w = (uint32_t)(dk[mt][rr] >> 32);
-              *reinterpret_cast<uint4 *>(wk + ((size_t)warp * L.JR + jr) * 2) = e;
+              uint64_t *dst = wk + ((size_t)warp * L.JR + jr) * wks();
+              *reinterpret_cast<uint4 *>(dst) = e;
+              if constexpr (SC) {
+                uint4 f;
+                f.x = (uint32_t)tl[mt][rr]; f.y = (uint32_t)(tl[mt][rr] >> 32);
+                f.z = (uint32_t)dl[mt][rr]; f.w = (uint32_t)(dl[mt][rr] >> 32);
+                *reinterpret_cast<uint4 *>(dst + 2) = f;
+              }
             }
           }
       }
@@ -576,6 +625,7 @@ struct Ctx {
       // fp32 SIMT: one warp per vocabulary row, lanes split K in a fixed order,
       // butterfly reduction; lane jr keeps the best key of joint row jr.
       uint64_t tkey = 0, dkey = 0;
+      [[maybe_unused]] uint64_t tlse = lse_empty(), dlse = lse_empty();   // SC
       const int nrows = ntiles * 8;
       const int zst = zstride() / 4;
       const float *z = (const float *)zs();
@@ -611,12 +661,20 @@ struct Ctx {
           const float val = mine + bsl()[lr];
           if (v < V1) tkey = umax64(tkey, pack_key(val, v));
           else dkey = umax64(dkey, pack_key(val, v - V1));
+          if constexpr (SC) {
+            if (v < V1) tlse = lse_combine(tlse, lse_pack(val, 1.f));
+            else dlse = lse_combine(dlse, lse_pack(val, 1.f));
+          }
           if (logits != nullptr && lane < nrows_valid) logits[(size_t)(row_base + lane) * NV + v] = val;
         }
       }
       if (lane < L.JR) {
-        wk[((size_t)warp * L.JR + lane) * 2 + 0] = tkey;
-        wk[((size_t)warp * L.JR + lane) * 2 + 1] = dkey;
+        wk[((size_t)warp * L.JR + lane) * wks() + 0] = tkey;
+        wk[((size_t)warp * L.JR + lane) * wks() + 1] = dkey;
+        if constexpr (SC) {
+          wk[((size_t)warp * L.JR + lane) * wks() + 2] = tlse;
+          wk[((size_t)warp * L.JR + lane) * wks() + 3] = dlse;
+        }
       }
     }
   }
@@ -628,31 +686,41 @@ struct Ctx {
   // of any other (it needs everyone's partials to leave a round).
   __device__ void exchange_keys() {
     const int nz = rs.nz;
-    if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par()), (uint32_t)(C * nz * 16));
+    if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par()), (uint32_t)(C * nz * 8 * pks()));
     sync();
     const uint64_t *wk = wkey();
     uint64_t *pt = part(par());
     if (tid < nz) {
       const int jr = tid;                       // compact joint row
       uint64_t tkey = 0, dkey = 0;
+      [[maybe_unused]] uint64_t tl = lse_empty(), dl = lse_empty();
 #pragma unroll
       for (int w = 0; w < MAX_NW; ++w) {
         if (w < NW) {
+          const uint64_t *e = wk + ((size_t)w * L.JR + jr) * wks();
           if (is_tdt()) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(wk + ((size_t)w * L.JR + jr) * 2);
+            const uint4 v = *reinterpret_cast<const uint4 *>(e);
             tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
             dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
           } else {   // RNN-T: the token key only
-            tkey = umax64(tkey, wk[((size_t)w * L.JR + jr) * 2]);
+            tkey = umax64(tkey, e[0]);
+          }
+          if constexpr (SC) {
+            tl = lse_combine(tl, e[2]);
+            if (is_tdt()) dl = lse_combine(dl, e[3]);
           }
         }
       }
-      const uint32_t slot = smem_u32(pt + ((size_t)rank * L.JR + jr) * 2);
+      const uint32_t slot = smem_u32(pt + ((size_t)rank * L.JR + jr) * pks());
       const uint32_t bb = smem_u32(bar(BAR_X + par()));
+      // partial: (token key, duration key) or, with scores, (token key, token lse)
+      // for RNN-T and (token key, duration key, token lse, duration lse) for TDT
+      const uint64_t second = (SC && !is_tdt()) ? tl : dkey;
 #pragma unroll 16
       for (int d = 0; d < C; ++d) {
         const int dst = (rank + d) % C;
-        st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, dkey, mapa_u32(bb, (uint32_t)dst));
+        st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, second, mapa_u32(bb, (uint32_t)dst));
+        if (SC && is_tdt()) st_async_u64x2(mapa_u32(slot + 16, (uint32_t)dst), tl, dl, mapa_u32(bb, (uint32_t)dst));
       }
     }
   }
@@ -668,7 +736,7 @@ struct Ctx {
 #pragma unroll
     for (int r = 0; r < MAX_C; ++r) {
       if (r < C) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + jr) * 2);
+        const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + jr) * pks());
         tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
         dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
       }
@@ -689,18 +757,30 @@ struct Ctx {
     int dec = 0;
     if (lane < nz) {
       uint64_t tkey = 0, dkey = 0;
+      [[maybe_unused]] uint64_t tl = lse_empty(), dl = lse_empty();
 #pragma unroll 16
       for (int r = 0; r < C; ++r) {
+        const uint64_t *e = pt + ((size_t)r * L.JR + lane) * pks();
         if (is_tdt()) {
-          const uint4 v = *reinterpret_cast<const uint4 *>(pt + ((size_t)r * L.JR + lane) * 2);
+          const uint4 v = *reinterpret_cast<const uint4 *>(e);
           tkey = umax64(tkey, ((uint64_t)v.y << 32) | v.x);
           dkey = umax64(dkey, ((uint64_t)v.w << 32) | v.z);
-        } else {     // RNN-T: the token key only
-          tkey = umax64(tkey, pt[((size_t)r * L.JR + lane) * 2]);
+          if constexpr (SC) {
+            tl = lse_combine(tl, e[2]);
+            dl = lse_combine(dl, e[3]);
+          }
+        } else {     // RNN-T: the token key only (+ its lse with scores)
+          tkey = umax64(tkey, e[0]);
+          if constexpr (SC) tl = lse_combine(tl, e[1]);
         }
       }
       dec = key_index(tkey) | ((is_tdt() ? key_index(dkey) : 0) << 24);
       rs.dec[rs.zdst[lane]] = dec;
+      if constexpr (SC) {   // log-probability of this row's decision (token [+ duration])
+        float lp = key_value(tkey) - lse_value(tl);
+        if (is_tdt()) lp += key_value(dkey) - lse_value(dl);
+        rs.lp[rs.zdst[lane]] = lp;
+      }
     }
     __syncwarp();
     return dec;   // lane k: decision of compact joint row k
@@ -786,6 +866,13 @@ struct Ctx {
     const int pos = found ? __ffs(m) - 1 : c;
     const int y = __shfl_sync(FULL, dec, found ? b0 + pos : 0) & 0xFFFFFF;
     const int used = scan ? (found ? pos + 1 : c) : 0;
+    if constexpr (SC) {   // greedy score: every decision used (blanks included)
+      float add = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < used) add += rs.lp[lane * p.W + j];
+      if (scan) rs.score[lane] += add;
+    }
     if (scan) {
       t += pos;
       // the per-frame label counter restarts whenever t advanced (reading A6/A14)
@@ -871,10 +958,12 @@ struct Ctx {
       (void)dec; (void)b0; (void)c;
       if (scan) {
         const int W = p.W;
+        [[maybe_unused]] float add = 0.f;
         while (pos < W && t + pos < Ls) {
           const int ee = rs.dec[lane * W + pos];
           const int yy = ee & 0xFFFFFF, dd = p.durations[ee >> 24];
           ++used;
+          if constexpr (SC) add += rs.lp[lane * W + pos];
           if (yy != p.blank) {
             found = true;
             y = yy;
@@ -883,6 +972,7 @@ struct Ctx {
           }
           pos += dd > 1 ? dd : 1;
         }
+        if constexpr (SC) rs.score[lane] += add;
       }
     } else {
       const unsigned nb = __ballot_sync(FULL, lane < rs.nz && (dec & 0xFFFFFF) != p.blank);
@@ -891,6 +981,13 @@ struct Ctx {
       pos = found ? __ffs(m) - 1 : c;
       y = __shfl_sync(FULL, dec, found ? b0 + pos : 0) & 0xFFFFFF;
       used = scan ? (found ? pos + 1 : c) : 0;
+      if constexpr (SC) {
+        float add = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < used) add += rs.lp[lane * p.W + j];
+        if (scan) rs.score[lane] += add;
+      }
     }
     if (scan) {
       t += pos;
@@ -1725,12 +1822,14 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // (the FC instantiations carry only the code of their model family).
 // DBG: 1 = the probe hook (ll.h ll_options): the same kernel also writes the
 // logits of every joint row and g after every predictor step (parity tests).
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0>
+// SC: 1 = greedy scores (N2), per-row tick schedule only.
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0,
+          int SC = 0>
 __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  Ctx<T, KR, HC, PC, CC, TM> cx(p, smem, rs, PRED == 0, s_bars);
+  Ctx<T, KR, HC, PC, CC, TM, SC> cx(p, smem, rs, PRED == 0, s_bars);
   const bool tdt = TM == 0 ? p.tdt != 0 : TM == 2;
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
@@ -1800,6 +1899,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         rs.needp[lane] = L > 0;
         rs.scanning[lane] = 0;
         rs.found[lane] = 0;
+        rs.score[lane] = 0.f;
       }
       if constexpr (PRED == 0) {
         // LSTM initial state h = c = 0 (reading A8)
@@ -2143,6 +2243,7 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
         int tot = 0;
         if (lane < R && b < p.B) {
           p.out_lengths[b] = rs.len[lane];
+          if constexpr (SC) p.out_scores[b] = rs.score[lane];
           tot = rs.len[lane];
         }
         for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
@@ -2164,6 +2265,12 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
       atomicAdd(p.stats + 5, (unsigned long long)s_cnt[SC_LABELS]);
       atomicAdd(p.stats + 6, (unsigned long long)s_cnt[SC_GROUPS]);
       atomicAdd(p.stats + 8, (unsigned long long)s_cnt[SC_ROWEVALS]);
+      // the longest dependent chain of one cluster (its joint rounds + predictor
+      // steps, over every group it decoded): the critical path of the launch
+      {
+        const unsigned long long r = min(s_cnt[SC_ROUNDS], 0xFFFFFu), pr = min(s_cnt[SC_PRED], 0xFFFFFu);
+        atomicMax(p.stats + 11, ((r + pr) << 40) | (r << 20) | pr);
+      }
       if (blockIdx.x == 0) {
         p.stats[7] = (unsigned long long)C;
         p.stats[9] = (unsigned long long)p.W;

@@ -125,7 +125,7 @@ static int pow2ceil(int x) {
 // nclusters: how many clusters of the chosen size can be resident (0: unknown,
 // assume 8).  R is chosen so that all groups of the batch run in one wave.
 bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf,
-                   int nclusters = 0) {
+                   int nclusters = 0, int sc = 0) {
   const int forceC = g_opt.cluster_size;
   const int forceR = g_opt.group_rows;
   const int forceW = g_opt.window;
@@ -169,7 +169,7 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
       for (; W >= 1; W >>= 1) {
         cf.C = C; cf.R = R; cf.W = W; cf.WF = W + (maxd > 1 ? maxd - 1 : 0);
         cf.NS = 0;
-        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0);
+        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0, sc);
         if (cf.L.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) return true;
         if (forceW) break;
       }
@@ -211,10 +211,11 @@ int max_clusters(int C, const Layout &L) {
   return n;
 }
 
-template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0>
+template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0,
+          int SC = 0>
 ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_groups, cudaStream_t st,
                         int &used_clusters) {
-  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, LM, TM, DBG>;
+  auto kern = decode_kernel<T, PRED, KR, HC, PC, CC, LM, TM, DBG, SC>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total) != cudaSuccess)
     return LL_ERR_CUDA;
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -349,8 +350,8 @@ ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw
 
 // Cluster size / group rows / window for a call: choose_config, then again
 // with the number of clusters that can actually be resident.
-bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf) {
-  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return false;
+bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf, int sc = 0) {
+  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, 0, sc)) return false;
   int ncl = 0;
   if (is_fc(bf, H, P, cf.C))
     ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1>(cf.C, cf.L)
@@ -361,7 +362,7 @@ bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
     ncl = lstm ? max_clusters<bf16, 0, KREG_SMALL>(cf.C, cf.L) : max_clusters<bf16, 1, KREG_SMALL>(cf.C, cf.L);
   else
     ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
-  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl));
+  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl, sc));
 }
 
 // ---------------------------------------------------------------------------
@@ -435,7 +436,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
                       int32_t blank_id, int32_t max_symbols, const int32_t *durations, int32_t nD,
                       int32_t *out_tokens, int32_t *out_timestamps, int32_t *out_durations,
                       int32_t *out_lengths, int32_t cap, void *workspace, size_t workspace_bytes,
-                      ll_stream stream) {
+                      ll_stream stream, float *out_scores = nullptr) {
   if (B < 0 || T_max < 0 || cap < 0) return LL_ERR_INVALID_ARGUMENT;
   if (!workspace || ((uintptr_t)workspace & 255)) return LL_ERR_INVALID_ARGUMENT;
   if (B > 0 && (!enc || !lengths || !out_tokens || !out_timestamps || !out_lengths))
@@ -457,8 +458,11 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   const int H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs, De = jn->enc_dim;
   int maxd = 1;
   for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
+  // greedy scores (N2): the per-row tick schedule's SC kernels
+  const int sc = out_scores != nullptr;
+  if (sc && (frame_looping || g_opt.schedule == 0 || g_opt.probe_logits)) return LL_ERR_UNSUPPORTED;
   Config cf;
-  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf)) return LL_ERR_UNSUPPORTED;
+  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf, sc)) return LL_ERR_UNSUPPORTED;
   if (frame_looping) {   // Alg. 2 evaluates one frame per joint call
     cf.W = 1;
     cf.WF = 1;
@@ -524,6 +528,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.out_tokens = out_tokens; p.out_timestamps = out_timestamps;
   p.out_durations = tdt ? out_durations : nullptr;
   p.out_lengths = out_lengths;
+  p.out_scores = out_scores;
   p.status = (int *)ws;
   p.group_counter = (int *)ws + 1;
   p.stats = (unsigned long long *)(ws + 64);
@@ -557,6 +562,24 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     else
       s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used)
                : launch_decode<float, 1, 1, 0, 0, 0, 3>(p, C, L, p.n_groups, st, used);
+  } else if (sc) {      // greedy scores: tick-schedule kernels with the score epilogue
+    if (is_fc(bf, H, P, C)) {
+      if (lstm)
+        s = tdt ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 2, 0, 1>(p, C, L, p.n_groups, st, used)
+                : launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1, 0, 1>(p, C, L, p.n_groups, st, used);
+      else
+        s = tdt ? launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 2, 0, 1>(p, C, L, p.n_groups, st, used)
+                : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 1, 0, 1>(p, C, L, p.n_groups, st, used);
+    } else if (bf && kreg_for(bf, H) == KREG) {
+      s = lstm ? launch_decode<bf16, 0, KREG, 0, 0, 0, 1, 0, 0, 1>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG, 0, 0, 0, 1, 0, 0, 1>(p, C, L, p.n_groups, st, used);
+    } else if (bf) {
+      s = lstm ? launch_decode<bf16, 0, KREG_SMALL, 0, 0, 0, 1, 0, 0, 1>(p, C, L, p.n_groups, st, used)
+               : launch_decode<bf16, 1, KREG_SMALL, 0, 0, 0, 1, 0, 0, 1>(p, C, L, p.n_groups, st, used);
+    } else {
+      s = lstm ? launch_decode<float, 0, 1, 0, 0, 0, 1, 0, 0, 1>(p, C, L, p.n_groups, st, used)
+               : launch_decode<float, 1, 1, 0, 0, 0, 1, 0, 0, 1>(p, C, L, p.n_groups, st, used);
+    }
   } else if (probe) {   // the production FC tick kernels + the probe hook (ll.h ll_options)
     if (lstm)
       s = tdt ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 2, 1>(p, C, L, p.n_groups, st, used)
@@ -653,6 +676,29 @@ ll_status ll_decode_rnnt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t 
   return decode_impl(false, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
                      workspace_bytes, stream);
+}
+
+ll_status ll_decode_rnnt_scores(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                                const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                                int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
+                                int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
+                                float *out_scores, void *workspace, size_t workspace_bytes, ll_stream stream) {
+  if (B > 0 && !out_scores) return LL_ERR_INVALID_ARGUMENT;
+  return decode_impl(false, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+                     nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
+                     workspace_bytes, stream, out_scores);
+}
+
+ll_status ll_decode_tdt_scores(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,
+                               const int32_t *lengths, const ll_predictor *pred, const ll_joint *joint,
+                               int32_t blank_id, int32_t max_symbols, const int32_t *durations,
+                               int32_t num_durations, int32_t *out_tokens, int32_t *out_timestamps,
+                               int32_t *out_durations, int32_t *out_lengths, int32_t out_capacity,
+                               float *out_scores, void *workspace, size_t workspace_bytes, ll_stream stream) {
+  if (B > 0 && !out_scores) return LL_ERR_INVALID_ARGUMENT;
+  return decode_impl(true, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
+                     durations, num_durations, out_tokens, out_timestamps, out_durations, out_lengths,
+                     out_capacity, workspace, workspace_bytes, stream, out_scores);
 }
 
 ll_status ll_decode_rnnt_frame_looping(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B, int32_t T_max,

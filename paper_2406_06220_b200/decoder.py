@@ -64,6 +64,7 @@ class DecodeOutput:
     timestamps: torch.Tensor    # [B, cap] int32
     durations: Optional[torch.Tensor]
     lengths: torch.Tensor       # [B] int32
+    scores: Optional[torch.Tensor] = None   # [B] f32 greedy scores (decoders built with scores=True)
 
     def hypotheses(self) -> List[tuple]:
         """Per-utterance python lists (copies to the host)."""
@@ -84,12 +85,15 @@ class LabelLoopingDecoder:
     """Owns the workspace and output buffers for batches up to (B_max, T_max)."""
 
     def __init__(self, model: Model, max_symbols: int, B_max: int, T_max: int, cap: Optional[int] = None,
-                 prec: int = ll.LL_PREC_FAST, frame_looping: bool = False):
+                 prec: int = ll.LL_PREC_FAST, frame_looping: bool = False, scores: bool = False):
         """frame_looping=True runs the Alg. 2 baseline (ll_decode_rnnt_frame_looping,
         RNN-T only) instead of label-looping."""
         if frame_looping and model.durations is not None:
             raise ValueError("frame-looping baseline: RNN-T only")
         self.frame_looping = bool(frame_looping)
+        if scores and frame_looping:
+            raise ValueError("greedy scores: label-looping only")
+        self.with_scores = bool(scores)
         self.model = model
         self.max_symbols = int(max_symbols)
         self.B_max, self.T_max = int(B_max), int(T_max)
@@ -108,6 +112,7 @@ class LabelLoopingDecoder:
         self.timestamps = torch.zeros_like(self.tokens)
         self.durs = torch.zeros_like(self.tokens) if nD else None
         self.lengths_out = torch.zeros(self.B_max, dtype=torch.int32, device=dev)
+        self.scores = torch.zeros(self.B_max, dtype=torch.float32, device=dev) if self.with_scores else None
 
     def release(self) -> None:
         """ll_release: drop the library's ll_prepare record of this workspace
@@ -132,22 +137,40 @@ class LabelLoopingDecoder:
         if s != ll.LL_OK:
             raise ll.LLError(s, "ll_prepare")
 
-    def launch(self, enc: torch.Tensor, lengths: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> int:
-        """Enqueue a decode of enc [B, T, D_e] (device, model dtype) with lengths [B] int32 (device)."""
+    def launch(self, enc: torch.Tensor, lengths: torch.Tensor, stream: Optional[torch.cuda.Stream] = None,
+               out: Optional[tuple] = None) -> int:
+        """Enqueue a decode of enc [B, T, D_e] (device, model dtype) with lengths [B] int32 (device).
+        out: optional (tokens, timestamps, durations or None, lengths) device int32 tensors of
+        [>= B, self.cap] / [>= B] to write instead of this decoder's own buffers (e.g. row
+        slices of one large buffer: the rows of a [N, cap] tensor are contiguous)."""
         m = self.model
         B, T = int(enc.shape[0]), int(enc.shape[1])
         assert B <= self.B_max and T <= self.T_max and enc.is_contiguous() and lengths.dtype == torch.int32
+        tok, ts, du, ln = out[:4] if out is not None else (self.tokens, self.timestamps, self.durs, self.lengths_out)
+        if out is not None:
+            assert tok.shape[1] == self.cap and ts.shape[1] == self.cap and tok.is_contiguous() and ts.is_contiguous()
         st = (stream or torch.cuda.current_stream()).cuda_stream
+        if self.with_scores:   # ll_decode_*_scores (N2)
+            sc = (out[4] if out is not None and len(out) > 4 else self.scores).data_ptr()
+            if m.durations is None:
+                return ll.ll_decode_rnnt_scores(enc.data_ptr(), m.dtype_code, self.prec, B, T, lengths.data_ptr(),
+                                                m.pred, m.joint, m.blank_id, self.max_symbols, tok.data_ptr(),
+                                                ts.data_ptr(), ln.data_ptr(), self.cap, sc, self.ws_ptr,
+                                                self.ws_bytes, st)
+            return ll.ll_decode_tdt_scores(enc.data_ptr(), m.dtype_code, self.prec, B, T, lengths.data_ptr(),
+                                           m.pred, m.joint, m.blank_id, self.max_symbols, m.durations,
+                                           m.num_durations, tok.data_ptr(), ts.data_ptr(),
+                                           None if du is None else du.data_ptr(), ln.data_ptr(), self.cap, sc,
+                                           self.ws_ptr, self.ws_bytes, st)
         if m.durations is None:
             fn = ll.ll_decode_rnnt_frame_looping if self.frame_looping else ll.ll_decode_rnnt
             return fn(enc.data_ptr(), m.dtype_code, self.prec, B, T, lengths.data_ptr(),
-                                     m.pred, m.joint, m.blank_id, self.max_symbols, self.tokens.data_ptr(),
-                                     self.timestamps.data_ptr(), self.lengths_out.data_ptr(), self.cap,
-                                     self.ws_ptr, self.ws_bytes, st)
+                      m.pred, m.joint, m.blank_id, self.max_symbols, tok.data_ptr(),
+                      ts.data_ptr(), ln.data_ptr(), self.cap, self.ws_ptr, self.ws_bytes, st)
         return ll.ll_decode_tdt(enc.data_ptr(), m.dtype_code, self.prec, B, T, lengths.data_ptr(), m.pred,
                                 m.joint, m.blank_id, self.max_symbols, m.durations, m.num_durations,
-                                self.tokens.data_ptr(), self.timestamps.data_ptr(), self.durs.data_ptr(),
-                                self.lengths_out.data_ptr(), self.cap, self.ws_ptr, self.ws_bytes, st)
+                                tok.data_ptr(), ts.data_ptr(), None if du is None else du.data_ptr(),
+                                ln.data_ptr(), self.cap, self.ws_ptr, self.ws_bytes, st)
 
     def decode(self, enc: torch.Tensor, lengths: torch.Tensor, stream=None, check: bool = True) -> DecodeOutput:
         B = int(enc.shape[0])
@@ -159,7 +182,8 @@ class LabelLoopingDecoder:
             if s != ll.LL_OK:
                 raise ll.LLError(s, "ll_sync")
         return DecodeOutput(self.tokens[:B], self.timestamps[:B],
-                            None if self.durs is None else self.durs[:B], self.lengths_out[:B])
+                            None if self.durs is None else self.durs[:B], self.lengths_out[:B],
+                            None if self.scores is None else self.scores[:B])
 
     def sync(self, stream=None) -> int:
         st = (stream or torch.cuda.current_stream()).cuda_stream
@@ -171,8 +195,11 @@ class LabelLoopingDecoder:
         if s != ll.LL_OK:
             raise ll.LLError(s, "ll_stats")
         keys = ["outer_steps", "joint_rounds", "joint_evals", "predictor_steps", "predictor_rows",
-                "labels", "groups", "cluster_size", "joint_rows_computed", "window", "group_rows", "reserved"]
-        return dict(zip(keys, v))
+                "labels", "groups", "cluster_size", "joint_rows_computed", "window", "group_rows", "chain"]
+        d = dict(zip(keys, v))
+        c = d.pop("chain")
+        d["chain_rounds"], d["chain_pred_steps"] = (c >> 20) & 0xFFFFF, c & 0xFFFFF
+        return d
 
 
 def debug_joint(model: Model, enc_rows: torch.Tensor, g_rows: torch.Tensor, want_logits: bool = True):

@@ -22,6 +22,7 @@ LL_PRED_LSTM, LL_PRED_STATELESS = 0, 1
 
 # Every symbol include/ll.h declares (checked by tests/test_abi.py).
 EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_rnnt_frame_looping", "ll_decode_tdt", "ll_prepare",
+            "ll_decode_rnnt_scores", "ll_decode_tdt_scores",
             "ll_sync",
             "ll_status_string",
             "ll_stats", "ll_debug_joint", "ll_set_timing_events", "ll_version", "ll_release", "ll_set_options",
@@ -88,6 +89,10 @@ def load_library() -> ctypes.CDLL:
                                   c_int32, POINTER(c_int32), c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_int32, c_void_p, c_size_t, c_void_p]
     lib.ll_decode_tdt.restype = c_int32
+    lib.ll_decode_rnnt_scores.argtypes = lib.ll_decode_rnnt.argtypes[:14] + [c_void_p] + lib.ll_decode_rnnt.argtypes[14:]
+    lib.ll_decode_rnnt_scores.restype = c_int32
+    lib.ll_decode_tdt_scores.argtypes = lib.ll_decode_tdt.argtypes[:17] + [c_void_p] + lib.ll_decode_tdt.argtypes[17:]
+    lib.ll_decode_tdt_scores.restype = c_int32
     lib.ll_prepare.argtypes = [P, J, c_int32, c_int32, c_int32, c_int32, POINTER(c_int32), c_int32, c_void_p,
                                c_size_t, c_void_p]
     lib.ll_prepare.restype = c_int32
@@ -143,6 +148,27 @@ def ll_decode_rnnt(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, m
                                              ctypes.byref(joint), blank_id, max_symbols, out_tokens,
                                              out_timestamps, out_lengths, out_capacity, workspace,
                                              workspace_bytes, stream))
+
+
+def ll_decode_rnnt_scores(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols, out_tokens,
+                          out_timestamps, out_lengths, out_capacity, out_scores, workspace, workspace_bytes,
+                          stream) -> int:
+    return int(load_library().ll_decode_rnnt_scores(enc, dtype, prec, B, T_max, lengths, ctypes.byref(pred),
+                                                    ctypes.byref(joint), blank_id, max_symbols, out_tokens,
+                                                    out_timestamps, out_lengths, out_capacity, out_scores,
+                                                    workspace, workspace_bytes, stream))
+
+
+def ll_decode_tdt_scores(enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols, durations,
+                         num_durations, out_tokens, out_timestamps, out_durations, out_lengths, out_capacity,
+                         out_scores, workspace, workspace_bytes, stream) -> int:
+    dur = None
+    if durations is not None:
+        dur = (c_int32 * max(1, len(durations)))(*[int(d) for d in durations])
+    return int(load_library().ll_decode_tdt_scores(enc, dtype, prec, B, T_max, lengths, ctypes.byref(pred),
+                                                   ctypes.byref(joint), blank_id, max_symbols, dur, num_durations,
+                                                   out_tokens, out_timestamps, out_durations, out_lengths,
+                                                   out_capacity, out_scores, workspace, workspace_bytes, stream))
 
 
 def ll_prepare(pred, joint, dtype, prec, B, T_max, durations, num_durations, workspace, workspace_bytes,

@@ -533,3 +533,78 @@ def test_config4_random_family_full_batch():
     decs = sum(r[1] for r in res)
     print(f"config 4 random family: {decs} decisions, {ties} near-ties, {st['labels']} labels")
     assert decs > c["B"] * 50
+
+
+# ------------------------------------------------------------------ greedy scores (N2)
+# ll_decode_*_scores: the fused log-sum-exp in the joint epilogue.  The float64
+# reference score is the verifier's, accumulated along the GPU's own decisions
+# (oracle/verify.py).  Bound per decision: the token (and duration) logit and
+# the log-sum-exp each within the north_star logit tolerance, so 2 x tol per
+# log-probability (4 x for TDT's two terms), plus fp32 accumulation.
+def _scored_decode(spec, w, enc, lengths, dtype):
+    model = gpu_model(spec, w, dtype)
+    B, T = enc.shape[0], enc.shape[1]
+    e = torch.from_numpy(np.ascontiguousarray(enc)).to("cuda", model.tdtype)
+    l = torch.from_numpy(np.asarray(lengths, dtype=np.int32)).cuda()
+    plain = LabelLoopingDecoder(model, spec.max_symbols, B, T).decode(e, l).hypotheses()
+    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, scores=True)
+    out = dec.decode(e, l)
+    return plain, out.hypotheses(), out.scores.cpu().numpy().astype(np.float64)
+
+
+def _check_scores(spec, w, enc, lengths, hyps, scores, tol_logit):
+    from oracle.verify import verify_rnnt, verify_tdt
+    o = Transducer.from_spec(spec, w)
+    checked = 0
+    for b in range(len(hyps)):
+        L = int(lengths[b])
+        h = hyps[b]
+        r = (verify_tdt(o, enc[b], L, spec.max_symbols, h[0], h[1], h[2]) if spec.is_tdt
+             else verify_rnnt(o, enc[b], L, spec.max_symbols, h[0], h[1]))
+        assert r.ok, r.message
+        if spec.is_tdt and r.near_ties:
+            continue   # the search may follow another acceptable blank duration than the kernel did
+        bound = r.decisions * (4 if spec.is_tdt else 2) * tol_logit + 1e-6 * abs(r.score) + 1e-5
+        assert abs(scores[b] - r.score) <= bound, (b, scores[b], r.score, bound)
+        checked += 1
+    return checked
+
+
+@pytest.mark.parametrize("dtype,tol", [("bf16", 2e-3), ("f32", 1e-5)])
+@pytest.mark.parametrize("cfg", ["tiny", "tiny-tdt"])
+def test_scores_tiny_random_family(dtype, tol, cfg):
+    c = synth.CONFIGS[cfg]
+    spec = c["spec"]
+    checked = 0
+    for seed in range(6):
+        for kind, ctx in [("stateless", 2), ("lstm", 1)]:
+            sp = synth.ModelSpec(spec.num_tokens, spec.enc_dim, spec.pred_dim, spec.joint_dim, kind, ctx,
+                                 spec.durations, spec.blank_id, spec.max_symbols)
+            w = synth.make_weights(sp, 1300 + seed, blank_bias=0.5)
+            enc, lengths = synth.make_inputs(2300 + seed, c["B"], c["T_max"], sp.enc_dim, c["len_lo"], c["len_hi"])
+            plain, hyps, scores = _scored_decode(sp, w, enc, lengths, dtype)
+            assert hyps == plain            # scores do not change the hypotheses
+            checked += _check_scores(sp, w, enc, lengths, hyps, scores, tol)
+    assert checked >= 30
+
+
+@pytest.mark.parametrize("tdt", [False, True])
+def test_scores_fc_random_family(tdt):
+    """Config (2)/(3) shapes (the FC score instantiations), random family."""
+    c = synth.CONFIGS["fc-tdt" if tdt else "fc-rnnt"]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 81, blank_bias=3.0 if not tdt else 1.0)
+    enc, lengths = synth.make_inputs(82, 16, 120, spec.enc_dim, 60, 120)
+    plain, hyps, scores = _scored_decode(spec, w, enc, lengths, "bf16")
+    assert hyps == plain
+    assert _check_scores(spec, w, enc, lengths, hyps, scores, 2e-3) >= 8
+
+
+def test_scores_cat_dog_closed_form():
+    """Fig. 2 table model: 7 decisions per utterance, each with logit 10 on the
+    chosen symbol and 0 on the other six: score = 7 (10 - log(e^10 + 6))."""
+    spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
+    for dtype in ("bf16", "f32"):
+        _, hyps, scores = _scored_decode(spec, w, enc, lengths, dtype)
+        expect = 7 * (10.0 - np.log(np.exp(10.0) + 6.0))
+        assert np.abs(scores - expect).max() < 1e-5, (scores, expect)

@@ -534,3 +534,64 @@ def test_verifier_tdt_label_duration_near_tie():
         # X@0 with d = 2 jumps to t = 2 (blank, d=1) -> end
         r = verify_tdt(model, enc[0], L, 3, [X], [0], [2], tol=NEAR)
         assert r.ok == ok, r.message
+
+
+# ---------------------------------------------------------------- greedy scores (N2)
+# BatchedHyps keeps "scores"; reading A19: the
+# greedy score of a hypothesis is the sum of the log-probabilities of EVERY
+# argmax step, blanks included (TDT: token and duration log-probabilities).
+
+def test_score_cat_dog_closed_form():
+    """Fig. 2 table model: every decision sees logit 10 on the chosen symbol and
+    0 on the other 6, so each step contributes 10 - log(e^10 + 6); CAT and DOG
+    take 7 decisions each (PAPER.md:172 alignments)."""
+    spec, w, enc, lengths, vocab = synth.cat_dog_fixture()
+    model = Transducer.from_spec(spec, w)
+    step = 10.0 - np.log(np.exp(10.0) + 6.0)
+    for b in range(2):
+        r = decode_sequential(model, enc[b], int(lengths[b]), spec.max_symbols)
+        assert r.joint_evals == 7
+        assert abs(r.score - 7 * step) < 1e-12
+        v = verify_rnnt(model, enc[b], int(lengths[b]), spec.max_symbols, r.tokens, r.timestamps, tol=0)
+        assert abs(v.score - r.score) < 1e-12
+
+
+@pytest.mark.parametrize("tdt", [False, True])
+def test_score_uniform_logits_closed_form(tdt):
+    """All-zero joint output weights: every logit ties, the lowest index (blank)
+    wins at every frame, so the score is -L (log(V+1) [+ log |D|])."""
+    durs = (0, 1, 2) if tdt else None
+    spec = synth.ModelSpec(9, 16, 16, 16, "lstm", 1, durs, 0, 3)
+    w = synth.make_weights(spec, 3)
+    w["w_out"] = np.zeros_like(w["w_out"])
+    w["b_out"] = np.zeros_like(w["b_out"])
+    if tdt:
+        w["w_dur"] = np.zeros_like(w["w_dur"])
+        w["b_dur"] = np.zeros_like(w["b_dur"])
+    model = Transducer.from_spec(spec, w)
+    enc, _ = synth.make_inputs(4, 1, 12, 16, 12, 12)
+    r = decode_sequential(model, enc[0], 12, 3)
+    assert r.tokens == [] and r.joint_evals == 12
+    expect = -12 * (np.log(9) + (np.log(3) if tdt else 0.0))
+    assert abs(r.score - expect) < 1e-12
+
+
+def test_score_verifier_matches_sequential_on_random_models():
+    """The teacher-forced verifier accumulates the same float64 score along the
+    oracle's own decisions as Alg. 1 does (RNN-T and TDT, random tiny models)."""
+    rng = np.random.default_rng(11)
+    n = 0
+    for _ in range(40):
+        tdt = bool(rng.random() < 0.5)
+        spec, model, enc, lengths = _random_case(rng, tdt)
+        for b in range(enc.shape[0]):
+            L = int(lengths[b])
+            r = decode_sequential(model, enc[b], L, spec.max_symbols)
+            if tdt:
+                v = verify_tdt(model, enc[b], L, spec.max_symbols, r.tokens, r.timestamps, r.durations, tol=0)
+            else:
+                v = verify_rnnt(model, enc[b], L, spec.max_symbols, r.tokens, r.timestamps, tol=0)
+            assert v.ok and abs(v.score - r.score) < 1e-9 * max(1.0, abs(r.score))
+            assert r.score <= 0.0
+            n += 1
+    assert n > 50

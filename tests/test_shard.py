@@ -137,3 +137,23 @@ def test_gather_ragged_world2_gloo(tdt):
     for p in procs:
         p.join(timeout=60)
     assert all(res), res
+
+
+def test_bench_gpus_spawns_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself with
+    2 ranks (torch.distributed.run, 127.0.0.1); the reference arm runs on rank 0
+    only and prints one JSON line with n_gpus 2, the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                          "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "tiny", "--steps", "1", "--warmup", "0", "--cpu-sample", "2"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["cpu_baseline"]["nproc"] >= 1
