@@ -75,7 +75,7 @@ def workload(cfg_name, seed, family="planted"):
             w, enc, lengths, _ = synth.make_planted_rnnt(spec, seed, c["B"], c["T_max"], c["len_lo"], c["len_hi"],
                                                          rho=c.get("rho", 0.28))
     else:
-        w = synth.make_weights(spec, seed, blank_bias=3.0 if spec.joint_dim > 64 else 0.5)
+        w = synth.make_weights(spec, seed, blank_bias=synth.random_family_blank_bias(spec))
         enc, lengths = synth.make_inputs(seed + 1, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     return spec, w, enc, lengths
 

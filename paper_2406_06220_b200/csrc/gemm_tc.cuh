@@ -27,7 +27,25 @@ struct TcGemmArgs {
   void *Y;
   int64_t ldy;
   int M, N, K;
+  // optional ragged rows (the encoder projection): row r = b * T + t is used only
+  // if t < lengths[b]; M tiles without a used row are skipped, unused rows of
+  // the other tiles are not stored (frames t >= lengths[b] are never read)
+  const int *lengths;
+  int T;
 };
+
+// whether any of the rows [m0, m0 + n) is used under the ragged-row rule (all are without lengths)
+__device__ __forceinline__ bool tile_has_rows(const TcGemmArgs &a, int m0, int n) {
+  if (!a.lengths) return true;
+  const int m1 = min(m0 + n, a.M);
+  for (int b = m0 / a.T; b * a.T < m1; ++b) {
+    const int t0 = max(m0 - b * a.T, 0);   // first row of utterance b inside the tile
+    int L = a.lengths[b];
+    if (L > a.T) L = a.T;
+    if (t0 < L) return true;
+  }
+  return false;
+}
 
 // UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row
 // core groups 1024 bytes apart (SBO), version 1 (sm_100).
@@ -64,6 +82,7 @@ __global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
   const int nk = a.K / TC_BK;
+  if (!tile_has_rows(a, m0, TC_BM)) return;   // padding frames only: nothing to compute
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
@@ -128,7 +147,12 @@ __global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__
     uint32_t r[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
     tmem_wait_ld();
-    if (row < a.M) {
+    bool used = row < a.M;
+    if (used && a.lengths) {
+      const int b = row / a.T;
+      used = row - b * a.T < a.lengths[b];
+    }
+    if (used) {
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {

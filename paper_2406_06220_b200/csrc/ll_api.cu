@@ -304,7 +304,8 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t rows, uint64_t col
 
 // tcgen05 GEMM (gemm_tc.cuh) when the shape fits its tiles; false = not taken.
 bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const void *bias, const void *bias2, void *Y,
-               int64_t ldy, int M, int N, int K, bool out_bf16, cudaStream_t st, ll_status &s) {
+               int64_t ldy, int M, int N, int K, bool out_bf16, cudaStream_t st, ll_status &s,
+               const int *lengths = nullptr, int T = 0) {
   if (g_opt.gemm_mma_sync) return false;
   if (K % TC_BK || N % TC_BN || (ldx * 2) % 16 || (ldw * 2) % 16 || ((uintptr_t)X & 15) || ((uintptr_t)W & 15))
     return false;
@@ -313,7 +314,7 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
   if (!make_map_bf16(&mx, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, TC_BM) ||
       !make_map_bf16(&mw, W, (uint64_t)N, (uint64_t)K, (uint64_t)ldw, TC_BN))
     return false;
-  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K};
+  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K, lengths, T};
   dim3 grid(N / TC_BN, (M + TC_BM - 1) / TC_BM);
   if (out_bf16) {
     cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
@@ -326,13 +327,14 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
   return true;
 }
 
+// lengths / T: ragged encoder rows (row b*T + t used iff t < lengths[b]); tcgen05 path only
 ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw, const void *bias,
                  const void *bias2, void *Y, int64_t ldy, int M, int N, int K, bool out_bf16,
-                 cudaStream_t st) {
+                 cudaStream_t st, const int *lengths = nullptr, int T = 0) {
   if (M <= 0 || N <= 0) return LL_OK;
   if (bf) {
     ll_status s;
-    if (linear_tc(X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K, out_bf16, st, s)) return s;
+    if (linear_tc(X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K, out_bf16, st, s, lengths, T)) return s;
   }
   LinearArgs a{X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K};
   if (bf) {
@@ -479,7 +481,9 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   if (B == 0) return LL_OK;
 
   // (1) encoder projection for all frames: f [B*T_max, H]
-  s = linear(bf, enc, De, jn->w_enc, De, jn->b_enc, nullptr, ws + w.f, H, B * T_max, H, De, bf, st);
+  // (frames t >= lengths[b] are never read: the tcgen05 GEMM skips tiles of
+  // padding frames; a length > T_max is clamped here and reported by the decode)
+  s = linear(bf, enc, De, jn->w_enc, De, jn->b_enc, nullptr, ws + w.f, H, B * T_max, H, De, bf, st, lengths, T_max);
   if (s != LL_OK) return s;
   // (2) model tables (weight-only; skipped if ll_prepare built exactly these
   // into this workspace)

@@ -473,6 +473,27 @@ CONFIGS = {
                            T_max=1500, len_lo=50, len_hi=1500),
 }
 
+def random_family_blank_bias(spec: ModelSpec) -> float:
+    """Blank bias of the RANDOM family at FastConformer scale (H = 640,
+    V+1 = 1025), calibrated on the float64 oracle (calibration batch: weights
+    seed 61, inputs seed 62, 3 x 60 frames; SURVEY.md §8(d) "blank bias
+    calibrated closed-loop"): the token rate is steep in the bias (RNN-T LSTM
+    0.25 -> 1.75, 0.30 -> 0.67, 0.35 -> 0.11 tokens/frame; bias >= 0.5 emits
+    nothing), so each family gets the bias that lands at ~0.3-0.7
+    tokens/frame, where labels, blanks and near-ties all occur.  Small models
+    keep 0.5."""
+    if spec.joint_dim <= 64:
+        return 0.5
+    if spec.is_tdt:
+        return 0.2          # 0.59 tokens/frame
+    if spec.pred_kind == "stateless":
+        return 0.28         # ~0.5 tokens/frame (context 2)
+    return 0.3              # 0.67 tokens/frame
+
+
+__all__.append("random_family_blank_bias")
+
+
 # (5) batch-sharded sweep: 8192 utterances with LibriSpeech-like lengths (seed
 # 2024, SURVEY.md §8(d)), FastConformer shapes, RNN-T and TDT; batches of 32.
 SWEEPS = {

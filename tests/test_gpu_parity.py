@@ -186,12 +186,15 @@ def test_fc_random_family_full_batch(tdt):
     the teacher-forced float64 verifier with the 1e-3 near-tie tolerance."""
     c = synth.CONFIGS["fc-tdt" if tdt else "fc-rnnt"]
     spec = c["spec"]
-    w = synth.make_weights(spec, 21, blank_bias=3.0 if not tdt else 1.0)
+    w = synth.make_weights(spec, 21, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(22, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     hyps, _ = gpu_decode(spec, w, enc, lengths, "bf16")
     ties, decs = verify_all(spec, w, enc, lengths, hyps)
+    labels = sum(len(h[0]) for h in hyps)
+    print(f"fc random family tdt={tdt}: {labels} labels, {decs} decisions, {ties} near-ties")
+    assert labels > 32 * 50            # the calibrated bias emits labels (not an all-blank run)
     assert decs > 32 * (60 if tdt else 200)
-    assert ties <= decs * 0.01
+    assert ties <= decs * 0.02
 
 
 def test_stateless_large_batch_config4_sampled():
@@ -247,7 +250,7 @@ def test_determinism_and_batch_composition():
     decodes identically alone and inside a permuted batch."""
     c = synth.CONFIGS["fc-rnnt"]
     spec = c["spec"]
-    w = synth.make_weights(spec, 31, blank_bias=3.0)
+    w = synth.make_weights(spec, 31, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(32, 20, 120, spec.enc_dim, 60, 120)
     model = gpu_model(spec, w)
     h1, _ = gpu_decode(spec, w, enc, lengths, model=model)
@@ -352,7 +355,7 @@ def test_schedules_identical(cfg):
     counts (the algorithmic decisions)."""
     c = synth.CONFIGS[cfg]
     spec = c["spec"]
-    w = synth.make_weights(spec, 41, blank_bias=3.0 if not spec.is_tdt else 1.0)
+    w = synth.make_weights(spec, 41, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(42, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     model = gpu_model(spec, w)
     out = {}
@@ -473,7 +476,7 @@ def test_production_kernel_logits_and_g(kind, tdt):
     durs = (0, 1, 2, 3, 4) if tdt else None
     De = 1024 if kind == "stateless" else 512
     spec = synth.ModelSpec(1025, De, 640, 640, kind, 2 if kind == "stateless" else 1, durs, 0, 10)
-    w = synth.make_weights(spec, 61, blank_bias=1.0 if tdt else 3.0)
+    w = synth.make_weights(spec, 61, blank_bias=synth.random_family_blank_bias(spec))
     B, T = 16, 80
     enc, lengths = synth.make_inputs(62, B, T, spec.enc_dim, 40, T)
     model = gpu_model(spec, w)
@@ -487,6 +490,7 @@ def test_production_kernel_logits_and_g(kind, tdt):
     fs = {b: o.enc_proj(enc[b][:int(lengths[b])]) for b in range(B)}
     st = dec.stats()
     assert len(jrows) == st["joint_rows_computed"] and len(grows) == st["predictor_rows"]
+    assert len(grows) > 10 * B          # labels were emitted: the recurrence is exercised
     lerr = 0.0
     for b, t, n, lg in jrows:
         assert 0 <= b < B and 0 <= t < lengths[b] and 0 <= n <= len(hyps[b][0])
@@ -502,36 +506,22 @@ def test_production_kernel_logits_and_g(kind, tdt):
     assert gerr < G_TOL, gerr
 
 
-_CFG4 = {}
-
-
-def _verify_rows(rows):
-    a = _CFG4   # inherited through fork (the encoder outputs are ~3 GB: never pickled)
-    return verify_all(a["spec"], a["w"], a["enc"], a["lengths"], a["hyps"], rows=rows)
-
-
 def test_config4_random_family_full_batch():
     """Config (4) in the launch configuration bench.py times (B=512, lengths
     50..1500, D_e=1024, stateless context 2, throughput mode: many waves of small
-    groups) on the RANDOM family (near-ties present): all 512 rows pass the
-    teacher-forced float64 verifier."""
-    import multiprocessing as mp
+    groups) on the RANDOM family (calibrated blank bias: labels, blanks and
+    near-ties): all 512 rows pass the teacher-forced float64 verifier."""
     c = synth.CONFIGS["stateless-b512"]
     spec = c["spec"]
-    w = synth.make_weights(spec, 71, blank_bias=3.0)
+    w = synth.make_weights(spec, 71, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(72, c["B"], c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     hyps, dec = gpu_decode(spec, w, enc, lengths, "bf16")
     st = dec.stats()
     # throughput mode: groups of <= 16 rows taken from the work counter in many waves
     assert st["group_rows"] <= 16 and st["groups"] >= c["B"] // 16
-    chunks = [list(range(i, c["B"], 32)) for i in range(32)]
-    _CFG4.update(spec=spec, w=w, enc=enc, lengths=lengths, hyps=hyps)
-    with mp.get_context("fork").Pool(min(32, mp.cpu_count())) as pool:
-        res = pool.map(_verify_rows, chunks)
-    _CFG4.clear()
-    ties = sum(r[0] for r in res)
-    decs = sum(r[1] for r in res)
+    ties, decs = verify_all(spec, w, enc, lengths, hyps)
     print(f"config 4 random family: {decs} decisions, {ties} near-ties, {st['labels']} labels")
+    assert st["labels"] > c["B"] * 50
     assert decs > c["B"] * 50
 
 
@@ -593,7 +583,7 @@ def test_scores_fc_random_family(tdt):
     """Config (2)/(3) shapes (the FC score instantiations), random family."""
     c = synth.CONFIGS["fc-tdt" if tdt else "fc-rnnt"]
     spec = c["spec"]
-    w = synth.make_weights(spec, 81, blank_bias=3.0 if not tdt else 1.0)
+    w = synth.make_weights(spec, 81, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(82, 16, 120, spec.enc_dim, 60, 120)
     plain, hyps, scores = _scored_decode(spec, w, enc, lengths, "bf16")
     assert hyps == plain
