@@ -35,6 +35,7 @@ class VerifyResult:
     near_ties: int = 0
     message: str = ""
     score: float = 0.0   # float64 greedy score along the verified decisions (N2)
+    path_scores: Optional[List[float]] = None   # TDT, all_paths=True: score of every acceptable path
 
 
 def _accept(logits: np.ndarray, y: int, tol: float):
@@ -101,7 +102,11 @@ def verify_rnnt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
 
 def verify_tdt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
                timestamps: List[int], durations: List[int], tol: float = 1e-3,
-               max_nodes: int = 100000) -> VerifyResult:
+               max_nodes: int = 100000, all_paths: bool = False) -> VerifyResult:
+    """all_paths: keep searching after the first acceptable decision path and
+    return the scores of all of them (`path_scores`): near-tie blank durations
+    are not visible in the outputs, so the path a decoder took (and hence its
+    greedy score, N2) is one of these."""
     import sys
     sys.setrecursionlimit(max(sys.getrecursionlimit(), 4 * (L + len(tokens)) + 1000))
     tokens = [int(x) for x in tokens]
@@ -125,6 +130,9 @@ def verify_tdt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
             return None
         if t >= L:
             if i == len(tokens):
+                if all_paths:
+                    found.append((dec_count, ties, score))
+                    return None
                 return (dec_count, ties, score)
             best["msg"] = f"utterance ended with {len(tokens) - i} labels left"
             return None
@@ -168,7 +176,11 @@ def verify_tdt(model: Transducer, enc_row, L: int, m: int, tokens: List[int],
                 return out
         return None
 
+    found = []
     out = rec(0, 0, 0, st0, g0, 0, 0, 0.0)
+    if all_paths and found:
+        out = found[0]
+        return VerifyResult(True, out[0], out[1], score=out[2], path_scores=[f[2] for f in found])
     if out is None:
         return VerifyResult(False, message=best["msg"] if nodes[0] <= max_nodes else "search budget exceeded")
     return VerifyResult(True, out[0], out[1], score=out[2])

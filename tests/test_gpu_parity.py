@@ -549,13 +549,16 @@ def _check_scores(spec, w, enc, lengths, hyps, scores, tol_logit):
     for b in range(len(hyps)):
         L = int(lengths[b])
         h = hyps[b]
-        r = (verify_tdt(o, enc[b], L, spec.max_symbols, h[0], h[1], h[2]) if spec.is_tdt
+        r = (verify_tdt(o, enc[b], L, spec.max_symbols, h[0], h[1], h[2], all_paths=True) if spec.is_tdt
              else verify_rnnt(o, enc[b], L, spec.max_symbols, h[0], h[1]))
         assert r.ok, r.message
-        if spec.is_tdt and r.near_ties:
-            continue   # the search may follow another acceptable blank duration than the kernel did
-        bound = r.decisions * (4 if spec.is_tdt else 2) * tol_logit + 1e-6 * abs(r.score) + 1e-5
-        assert abs(scores[b] - r.score) <= bound, (b, scores[b], r.score, bound)
+        # TDT: blank durations are not in the outputs, so the kernel's decision
+        # path is one of the acceptable paths (near-tie durations); its score
+        # must match that path's float64 score
+        cands = r.path_scores if spec.is_tdt else [r.score]
+        bound = (r.decisions + 2) * (4 if spec.is_tdt else 2) * tol_logit + 1e-6 * abs(r.score) + 1e-5
+        err = min(abs(scores[b] - c_) for c_ in cands)
+        assert err <= bound, (b, scores[b], cands, bound)
         checked += 1
     return checked
 

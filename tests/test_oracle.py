@@ -595,3 +595,20 @@ def test_score_verifier_matches_sequential_on_random_models():
             assert r.score <= 0.0
             n += 1
     assert n > 50
+
+
+def test_verifier_tdt_all_paths_scores():
+    """verify_tdt(all_paths=True) returns the score of every acceptable decision
+    path (its first entry is the path the plain search returns): with the
+    alternative blank duration at t = 0 5e-4 below the argmax, an all-blank
+    output is reachable through d = 1 or d = 2 at t = 0, and the two paths have
+    different float64 scores; at tol 0 only the argmax path remains."""
+    b = 0
+    D = [0, 1, 2]
+    steps = [(0, b, b, 1), (1, b, b, 2), (2, b, b, 1), (3, b, b, 1)]
+    spec, model, enc, L = _table(steps, 4, 4, durations=D, edits=[("dur", 2, 0, b, 10.0 - 5e-4)])
+    r = verify_tdt(model, enc[0], L, 3, [], [], [], tol=NEAR, all_paths=True)
+    assert r.ok and r.path_scores[0] == r.score and all(x < 0 for x in r.path_scores)
+    assert len({round(x, 9) for x in r.path_scores}) >= 2
+    r0 = verify_tdt(model, enc[0], L, 3, [], [], [], tol=0, all_paths=True)
+    assert r0.ok and len(r0.path_scores) == 1 and r0.score == r.score
