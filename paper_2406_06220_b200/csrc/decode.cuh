@@ -66,12 +66,45 @@ enum {
   BAR_FULL = 10,    // [NSMAX] weight ring: tile landed
   BAR_EMPTY = 10 + NSMAX,  // [NSMAX] weight ring: tile consumed
   BAR_E = 10 + 2 * NSMAX,  // E' slices of the predictor rows landed
-  NBARS = 11 + 2 * NSMAX
+  BAR_GQ = 11 + 2 * NSMAX,   // (TG) MMA warp: a gate batch is requested (consumer thread 0 arrives)
+  BAR_GATE = 12 + 2 * NSMAX, // (TG) gate batch complete (tcgen05.commit)
+  NBARS = 13 + 2 * NSMAX
 };
+
+// ---------------------------------------------------------------------------
+// TG: the FC LSTM instantiation (P = 640 in 16-CTA clusters: 40 units = 160
+// gate rows per CTA) computes the recurrent pre-activations W_hh h on the
+// 5th-generation tensor cores, in the BACKGROUND: W_hh h does not depend on
+// the next label (only E'[y] does, Alg. 3 line 6), so as soon as a predictor
+// step has produced h' a dedicated MMA warp issues tcgen05.mma (A = W_hh
+// resident in TMEM, B = h' in shared memory) for every slot of the group, and
+// the next predictor step only reads the result back.
+//   TMEM columns [0, 320):   gate rows 0..127 (units 0..31, row = 4 unit + gate),
+//                            lane = row, column j = K elements 2j, 2j+1
+//   TMEM columns [320, 400): gate rows 128..159 (units 32..39) K-folded: lanes
+//                            32j + r hold row 128 + r over K [160j, 160j + 160)
+//   TMEM columns [400, 408): D main  (M=128, N=8 slots)
+//   TMEM columns [408, 440): D fold  (M=128, N=32 = 4 K-quarters x 8 slots; the
+//                            diagonal blocks are the 4 partial sums)
+// h lives in shared memory as the MMA's B operand, K-major without swizzle:
+// 8-row x 16-byte core matrices, element (slot n, k) at
+//   (k / 160) * 2560 + ((k % 160) / 8) * 128 + n * 16 + (k % 8) * 2
+// so the main MMA reads it with LBO = 128 (next 8 K) and the fold MMA reads the
+// same bytes as a 32-row operand (row 8j + n = slot n's K-quarter j, SBO = 2560).
+// ---------------------------------------------------------------------------
+constexpr int TG_P = 640, TG_C = 16, TG_UPC = TG_P / TG_C;   // 40 units per CTA
+constexpr int TG_NH = 8;                                       // slots (B rows): R <= 8
+constexpr int TG_QB = (TG_P / 4 / 8) * 128;                    // bytes per K-quarter of h (2560)
+constexpr int TG_HBYTES = 4 * TG_QB;                           // h buffer (10240)
+constexpr uint32_t TG_COL_FOLD = TG_P / 2, TG_COL_DMAIN = TG_P / 2 + TG_P / 8, TG_COL_DFOLD = TG_COL_DMAIN + TG_NH;
+__host__ __device__ inline bool tg_shape(bool bf, bool lstm, int H, int P, int C) {
+  return bf && lstm && H == TG_P && P == TG_P && C == TG_C;
+}
 
 // Shared-memory layout (identical on host and device).
 struct Layout {
   int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
+  int tg, NTH;                   // TG (tcgen05 gate pre-activations + MMA warp), threads per CTA
   int wks, pks;                  // u64 words per per-warp key entry / per cluster partial (scores: 4)
   size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, off_es, total;
 };
@@ -92,6 +125,8 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.DPC = H / C;
   L.NW = bf ? MAX_NW : 8;          // bf16: one vocab tile per warp (<= MAX_NW tiles per CTA)
   L.ring = (bf && lstm) ? 1 : 0;   // bf16 LSTM: W_hh in TMEM, W_pred tiles resident in smem
+  L.tg = tg_shape(bf, lstm, H, P, C) ? 1 : 0;
+  L.NTH = L.NW * 32 + (L.tg ? 32 : 0);
   L.NS = L.ring ? L.DPC / 8 : 0;   // W_pred tiles of this CTA
   (void)NS;
   L.JR = R * W;
@@ -114,7 +149,7 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * 4, 128);
   L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 8 * L.pks, 128);
   L.off_wkey = o; o = align_up(o + (size_t)L.NW * L.JR * 8 * L.wks, 128);
-  L.off_hs = o;   o = align_up(o + (size_t)(L.ring ? 2 * R * L.hstride : 0), 128);
+  L.off_hs = o;   o = align_up(o + (size_t)(L.tg ? TG_HBYTES : L.ring ? 2 * R * L.hstride : 0), 128);
   L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * P * 2, 128);
   L.off_es = o;   o = align_up(o + (size_t)(L.ring ? R * 4 * L.UPC * 4 : 0), 128);
   L.total = o;
@@ -176,6 +211,7 @@ struct RowState {
   int grp[2];                            // group index broadcast (double-buffered)
   int ack[2];
   volatile int done;                     // consumers finished (producer exits)
+  volatile int mma_exit;                 // (TG) the MMA warp leaves its loop
   volatile unsigned tag[NSMAX];          // ring: index of the tile last issued into each slot
 };
 
@@ -192,6 +228,9 @@ __device__ __forceinline__ void csync(int nthreads) {
 template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0, int SC = 0>
 struct Ctx {
   static constexpr bool BF = sizeof(T) == 2;
+  // the FC LSTM shape: tcgen05 gate pre-activations (see TG_* above); only the
+  // LSTM member functions use it (the stateless FC kernel never issues a batch)
+  static constexpr bool TG = BF && HC == TG_P && PC == TG_P && CC == TG_C;
   const DecodeParams &p;
   const Layout &L;            // in the kernel parameters (constant bank; uniform, no registers)
   uint8_t *sm;
@@ -205,7 +244,8 @@ struct Ctx {
   // Barrier phase bookkeeping, replicated in every consumer thread and packed
   // into one register: bits 0-1 fph (BAR_F+X phase), 2-3 fpend (bulk copy into
   // fbuf[X] outstanding), 4-5 xph (BAR_X+par phase), 6 hph (BAR_H/G/E phase),
-  // 7 par (partial-key buffer parity).
+  // 7 par (partial-key buffer parity); TG: 8 gate batch pending, 9 BAR_GATE
+  // phase, 10 the gate pre-activations in TMEM are valid for this group.
   uint32_t phs;
   __device__ __forceinline__ uint32_t fph(int X) const { return (phs >> X) & 1u; }
   __device__ __forceinline__ uint32_t fpend(int X) const { return (phs >> (2 + X)) & 1u; }
@@ -304,6 +344,55 @@ struct Ctx {
   __device__ float *es() const { return (float *)(sm + L.off_es); }
   __device__ uint8_t *ringslot(int slot) const { return sm + L.off_ring + (size_t)slot * 8 * Pd() * 2; }
   __device__ void sync() const { csync(NCT); }
+
+  // ---- TG: gate pre-activation batches (MMA warp) ---------------------------
+  __device__ uint8_t *hbuf() const { return sm + L.off_hs; }
+  // byte offset of 16-byte chunk c (K elements 8c .. 8c+7) of slot n's h row
+  __device__ __forceinline__ static int hoff(int n, int c) { return (c / 20) * TG_QB + (c % 20) * 128 + n * 16; }
+  // every consumer thread: wait for the outstanding gate batch, if any
+  __device__ __forceinline__ void gate_wait() {
+    if constexpr (TG) {
+      if (phs & (1u << 8)) {
+        mbar_wait(bar(BAR_GATE), (phs >> 9) & 1u);
+        phs ^= 1u << 9;
+        phs &= ~(1u << 8);
+      }
+    }
+  }
+  // consumer thread 0 (after a CTA barrier that follows every thread's
+  // fence.proxy.async): request a gate batch over the current h buffer.
+  // Every consumer thread calls it (replicated bookkeeping).
+  __device__ __forceinline__ void gate_request() {
+    if (tid == 0) mbar_arrive(bar(BAR_GQ));
+    phs |= (1u << 8) | (1u << 10);
+  }
+  // The MMA warp (lane 0): for every request, D_main = W_hh[rows 0..127] h and
+  // D_fold = the K-quarter partials of rows 128..159, one tcgen05.commit.
+  __device__ void mma_warp_loop() {
+    if constexpr (TG) {
+      if (lane != 0) return;
+      constexpr uint32_t ID_MAIN = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TG_NH >> 3) << 17) | (8u << 24);
+      constexpr uint32_t ID_FOLD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(4 * TG_NH >> 3) << 17) | (8u << 24);
+      const uint32_t hb = smem_u32(hbuf());
+      for (uint32_t ph = 0;; ph ^= 1u) {
+        mbar_wait(bar(BAR_GQ), ph);
+        if (rs.mma_exit) break;
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TG_P / 16; ++kk) {   // K = 16 per MMA: h chunks 2kk, 2kk + 1
+          const int c = 2 * kk;
+          const uint64_t db = umma_desc_ns(hb + (uint32_t)((c / 20) * TG_QB + (c % 20) * 128), 128, 1024);
+          umma_ts(tmem + TG_COL_DMAIN, tmem + (uint32_t)(8 * kk), db, ID_MAIN, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < TG_P / 64; ++kk) {   // the 4 K-quarters side by side (32 B rows)
+          const uint64_t db = umma_desc_ns(hb + (uint32_t)(kk * 256), 128, TG_QB);
+          umma_ts(tmem + TG_COL_DFOLD, tmem + TG_COL_FOLD + (uint32_t)(8 * kk), db, ID_FOLD, kk > 0);
+        }
+        umma_commit(bar(BAR_GATE));
+      }
+    }
+  }
 
   __device__ void init_barriers() {
     if (tid == 0) {
@@ -685,6 +774,10 @@ struct Ctx {
   // double-buffered by round parity, and a CTA can be at most one round ahead
   // of any other (it needs everyone's partials to leave a round).
   __device__ void exchange_keys() {
+    // TG: the other CTAs write their next h' slices into this CTA's h buffer
+    // only after this round's partial keys arrive, so the gate batch reading
+    // the buffer completes first
+    gate_wait();
     const int nz = rs.nz;
     if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par()), (uint32_t)(C * nz * 8 * pks()));
     sync();
@@ -1248,6 +1341,40 @@ struct Ctx {
   // Kernel start: W_hh tiles of this CTA from the packed stream into TMEM,
   // W_pred tiles into shared memory (one bulk copy).
   __device__ void load_lstm_weights() {
+    if constexpr (TG) {
+      // W_hh rows of this CTA's 40 units into TMEM in the A-operand layout (TG_*
+      // above): warps 0-3 the main rows of lane quarter q = warp (unit 8q +
+      // lane/4, gate lane%4), warps 4-7 the K-quarter j = warp - 4 of the folded
+      // rows (unit 32 + lane/4, gate lane%4); one 32-bit column = 2 bf16 K elements
+      if (warp < 8) {
+        const int qd = warp & 3;
+        const bool fold = warp >= 4;
+        const int unit = (fold ? 32 : 8 * qd) + (lane >> 2), gate = lane & 3;
+        const bf16 *src = (const bf16 *)p.w_hh + ((size_t)gate * TG_P + u0 + unit) * TG_P + (fold ? (TG_P / 4) * qd : 0);
+        const uint32_t ta = tmem + ((uint32_t)(32 * qd) << 16) + (fold ? TG_COL_FOLD : 0u);
+        const int ncols = fold ? TG_P / 8 : TG_P / 2;
+        for (int c0 = 0; c0 < ncols; c0 += 16) {
+          uint32_t r[16];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint4 x = ldg128_nc(src + 2 * c0 + 8 * v);
+            r[4 * v] = x.x; r[4 * v + 1] = x.y; r[4 * v + 2] = x.z; r[4 * v + 3] = x.w;
+          }
+          tmem_st16(ta + (uint32_t)c0, r);
+        }
+      }
+      tmem_wait_st();
+      if (warp == 0) {   // W_pred tiles (the packed stream's tail) into shared memory
+        const int NG = ng(), NPT = npt();
+        const uint32_t bytes = (uint32_t)(NPT * 8 * TG_P * 2);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(bar(BAR_FULL), bytes);
+          bulk_g2s(ringslot(0), p.wst + ((size_t)rank * (NG + NPT) + NG) * 8 * TG_P, bytes, bar(BAR_FULL));
+        }
+        mbar_wait(bar(BAR_FULL), 0);
+      }
+      return;
+    }
     const int NG = ng(), NPT = npt(), KB = Pd() / 32;
     const int sw = ((g & 1) && (Pd() % 64) == 0) ? 4 : 0;
     for (int n = 2 * warp; n < NG; n += 2 * NW) {   // stream tiles n (half 0), n + 1 (half 1) = pair n / 2
@@ -1353,6 +1480,8 @@ struct Ctx {
   // 2t+1 of the resident smem copy, rows >= DPC read as zero), B = h' rows.
   // K blocks are split over the warps: warp w takes kb = w, w + NW, ... (and
   // warp 0 the 16-wide tail).
+  // hrow[nb]: the row's chunk-q address (hsrow + q * 16), or (TG) the h
+  // buffer + 16 * slot (chunk offsets from hoff).
   template <int NB>
   __device__ __forceinline__ void wpred_partial(float (&acc)[3][NB][4], const uint8_t *const *hrow) const {
     const int KB = Pd() / 32, NPT = npt();
@@ -1367,7 +1496,10 @@ struct Ctx {
       if (kb >= KB) break;
       uint4 x[NB];
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) x[nb] = lds128(hrow[nb] + kb * 64);
+      for (int nb = 0; nb < NB; ++nb) {
+        if constexpr (TG) x[nb] = lds128(hrow[nb] + hoff(0, 4 * kb + q));
+        else x[nb] = lds128(hrow[nb] + kb * 64);
+      }
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         if (2 * t < NPT) {
@@ -1484,7 +1616,8 @@ struct Ctx {
     for (int nb = 0; nb < NB; ++nb) {
       const int i = 8 * (nb0 + nb) + g;
       const int s = rs.plist[i < n ? i : 0];
-      hrow[nb] = hsrow(rs.hpar[s] ^ 1, s) + q * 16;
+      if constexpr (TG) hrow[nb] = hbuf() + 16 * s;
+      else hrow[nb] = hsrow(rs.hpar[s] ^ 1, s) + q * 16;
     }
     float acc[3][NB][4];
     wpred_partial<NB>(acc, hrow);
@@ -1528,6 +1661,79 @@ struct Ctx {
     // staged into shared memory by bulk copies that overlap the gate GEMM.
     // (the table's columns are CTA-major: one bulk copy per predictor row)
     if (!eprefetched && warp == NW - 1) issue_eprime(rs.plist, n);
+    if constexpr (TG) {
+      // W_hh h from the background gate batch (zero on the group's first step)
+      gate_wait();
+      tc_fence_after();
+      const bool dvalid = (phs >> 10) & 1u;
+      float *gb = reinterpret_cast<float *>(zs());   // [40 units][36]: gate g at 8g + slot (main units)
+      float *fb = gb + TG_UPC * 36;                  // [4 quarters][8 units][4 gates][8 slots] (fold partials)
+      if (warp < 8) {
+        uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const int qd = warp & 3;
+        if (dvalid) {
+          tmem_ld8(tmem + ((uint32_t)(32 * qd) << 16) + (warp < 4 ? TG_COL_DMAIN : TG_COL_DFOLD + 8u * qd), r);
+          tmem_wait_ld();
+        }
+        float *dst = warp < 4 ? gb + (8 * qd + (lane >> 2)) * 36 + (lane & 3) * 8 : fb + (qd * 32 + lane) * 8;
+        reinterpret_cast<float4 *>(dst)[0] = make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]),
+                                                         __uint_as_float(r[2]), __uint_as_float(r[3]));
+        reinterpret_cast<float4 *>(dst)[1] = make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]),
+                                                         __uint_as_float(r[6]), __uint_as_float(r[7]));
+      }
+      tc_fence_before();
+      mbar_wait(bar(BAR_E), hph());
+      sync();
+      tl_pred(1);
+      // cell update, one thread per (unit, slot): gates = E'[y] + W_hh h (the
+      // folded units sum their 4 K-quarter partials in a fixed order), PyTorch
+      // LSTM (reading A9): c' = s(f) c + s(i) tanh(g), h' = s(o) tanh(c')
+      {
+        const int ul = tid >> 3, s = tid & 7;
+        if (s < p.R && rs.needp[s]) {
+          float gt[4];
+          if (ul < 32) {
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) gt[gg] = gb[ul * 36 + gg * 8 + s];
+          } else {
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+              const int row = ((ul - 32) * 4 + gg) * 8 + s;
+              gt[gg] = ((fb[row] + fb[256 + row]) + fb[512 + row]) + fb[768 + row];
+            }
+          }
+          const float *ep = es() + (size_t)s * 4 * TG_UPC + ul;
+          float *cp = cs() + (size_t)s * TG_UPC + ul;
+          const float gi = gt[0] + ep[0], gf = gt[1] + ep[TG_UPC], gg = gt[2] + ep[2 * TG_UPC],
+                      go = gt[3] + ep[3 * TG_UPC];
+          const float cn = sigmoidf_(gf) * *cp + sigmoidf_(gi) * tanhf(gg);
+          *cp = cn;
+          const int k = u0 + ul;
+          *reinterpret_cast<bf16 *>(hbuf() + hoff(s, k >> 3) + (k & 7) * 2) = __float2bfloat16_rn(sigmoidf_(go) * tanhf(cn));
+        }
+      }
+      tl_pred(2);
+      sync();
+      tl_pred_bar(3);
+      // h' slices (this CTA's 5 chunks of every predicted row) to every other CTA
+      if (C > 1) {
+        const int total = n * 5 * (C - 1);
+        const uint32_t bb = smem_u32(bar(BAR_H));
+        for (int idx = tid; idx < total; idx += NCT) {
+          const int d = idx % (C - 1), rem = idx / (C - 1);
+          const int c = 5 * rank + rem % 5, s = rs.plist[rem / 5];
+          const uint8_t *src = hbuf() + hoff(s, c);
+          const uint4 v = *reinterpret_cast<const uint4 *>(src);
+          const uint32_t dst = (uint32_t)((rank + 1 + d) % C);
+          st_async_u64x2(mapa_u32(smem_u32(src), dst), ((uint64_t)v.y << 32) | v.x, ((uint64_t)v.w << 32) | v.z,
+                         mapa_u32(bb, dst));
+        }
+        mbar_wait(bar(BAR_H), hph());
+      }
+      // the h buffer (local writes + the other CTAs' st.async) -> async proxy
+      fence_proxy_async_smem();
+      tl_pred(4);
+    } else {
     {
       bool e_ready = false;
       for (int nb0 = 0; nb0 * 8 < n; nb0 += 2) {
@@ -1551,6 +1757,7 @@ struct Ctx {
       mbar_wait(bar(BAR_H), hph());
     }
     tl_pred(4);
+    }
     // (3) g = W_pred h' + b_pred for this CTA's output dims: K split over the
     // warps (partials in shared memory), then one thread per (row, 4 dims)
     // sums the partials in a fixed warp order, adds the bias, stores g locally
@@ -1562,6 +1769,9 @@ struct Ctx {
       if (nb0 == 0) tl_pred(9);
       sync();
       if (nb0 == 0) tl_pred_bar(10);
+      if constexpr (TG) {
+        if (nb0 == 0) gate_request();   // W_hh h' for the next step, in the background
+      }
       const int nrows = min(16, n - nb0 * 8);
       const int D4 = dpc() / 4;
       const float4 *wp = reinterpret_cast<const float4 *>(zs());
@@ -1601,7 +1811,7 @@ struct Ctx {
     // (4) the other CTAs' g slices
     if (C > 1) mbar_wait(bar(BAR_G), hph());
     phs ^= 1u << 6;
-    if (warp == 0 && lane < n) {
+    if (!TG && warp == 0 && lane < n) {
       const int s = rs.plist[lane];
       rs.hpar[s] ^= 1;
     }
@@ -1825,11 +2035,15 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // SC: 1 = greedy scores (N2), per-row tick schedule only.
 template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0,
           int SC = 0>
-__global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_constant__ DecodeParams p) {
+__global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && HC == TG_P && PC == TG_P && CC == TG_C ? 32 : 0), 1)
+    decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  Ctx<T, KR, HC, PC, CC, TM, SC> cx(p, smem, rs, PRED == 0, s_bars);
+  using CtxT = Ctx<T, KR, HC, PC, CC, TM, SC>;
+  CtxT cx(p, smem, rs, PRED == 0, s_bars);
+  // TG: an 11th warp issues the background gate batches (outside the consumer barrier)
+  constexpr bool MMAW = PRED == 0 && CtxT::TG;
   const bool tdt = TM == 0 ? p.tdt != 0 : TM == 2;
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
@@ -1851,11 +2065,14 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
     cx.load_lstm_weights();
     tc_fence_before();
   }
+  if (tid == 0) rs.mma_exit = 0;
   __syncthreads();
   if (C > 1) cluster_sync_all();  // barriers initialised cluster-wide before any st.async
   if constexpr (RING) tc_fence_after();
 
-  {
+  if (MMAW && warp == MAX_NW) {
+    cx.mma_warp_loop();
+  } else {
     int cur = 0;                  // f buffer of the current round
 #ifndef LL_DEBUG_TRACE
 #define LL_PHASE(k)
@@ -1904,7 +2121,14 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
       if constexpr (PRED == 0) {
         // LSTM initial state h = c = 0 (reading A8)
         for (int i = tid; i < R * cx.L.UPC; i += cx.NCT) cx.cs()[i] = 0.f;
-        if constexpr (RING) {
+        if constexpr (MMAW) {
+          // no gate batch may still read the h buffer; h = 0 means W_hh h = 0,
+          // so the first step skips the (not yet computed) pre-activations
+          cx.gate_wait();
+          cx.phs &= ~(1u << 10);
+          for (int i = tid; i < TG_HBYTES / 16; i += cx.NCT)
+            reinterpret_cast<uint4 *>(cx.hbuf())[i] = make_uint4(0, 0, 0, 0);
+        } else if constexpr (RING) {
           for (int i = tid; i < R * cx.Pd() / 8; i += cx.NCT) {
             const int s = i / (cx.Pd() / 8), c = i % (cx.Pd() / 8);
             *reinterpret_cast<uint4 *>(cx.hsrow(0, s) + c * 16) = make_uint4(0, 0, 0, 0);
@@ -2254,6 +2478,13 @@ __global__ void __launch_bounds__(MAX_NW * 32, 1) decode_kernel(const __grid_con
     // drain outstanding f bulk copies before the CTA exits
     if (cx.fpend(0)) cx.wait_f(0);
     if (cx.fpend(1)) cx.wait_f(1);
+    if constexpr (MMAW) {
+      cx.gate_wait();
+      if (tid == 0) {
+        rs.mma_exit = 1;
+        mbar_arrive(cx.bar(BAR_GQ));
+      }
+    }
     cx.sync();
 #undef LL_PHASE
     if (rank == 0 && tid == 0 && p.stats) {

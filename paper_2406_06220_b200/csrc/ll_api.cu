@@ -162,6 +162,7 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
     }
     for (int R = Rpref; R >= 1; --R) {
       if (forceR && R != forceR) continue;
+      if (tg_shape(bf, lstm, H, P, C) && R > TG_NH) continue;   // gate batch: one N=8 B operand
       int W = forceW ? forceW : MAX_JR / R;
       if (W > 8) W = 8;
       if (W < 1) W = 1;
@@ -198,7 +199,7 @@ int max_clusters(int C, const Layout &L) {
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(L.NW * 32);
+  cfg.blockDim = dim3(L.NTH);
   cfg.dynamicSmemBytes = L.total;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
@@ -226,7 +227,7 @@ ll_status launch_decode(const DecodeParams &p, int C, const Layout &L, int n_gro
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(L.NW * 32);
+  cfg.blockDim = dim3(L.NTH);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = st;
   cfg.attrs = attr;
@@ -258,7 +259,7 @@ ll_status launch_debug(const DecodeParams &p, int C, const Layout &L, int n_chun
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(L.NW * 32);
+  cfg.blockDim = dim3(L.NTH);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = st;
   cfg.attrs = attr;
