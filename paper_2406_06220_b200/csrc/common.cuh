@@ -275,6 +275,19 @@ __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t bdesc, 
       "r"(a), "l"(bdesc), "r"(idesc), "r"((uint32_t)acc)
       : "memory");
 }
+// D[tmem] (+)= A[smem] . B[smem]^T, kind::f16; issued by one thread.
+__device__ __forceinline__ void umma_ss(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"((uint32_t)acc)
+      : "memory");
+}
+// four 8x8 b16 matrices (8 rows x 16 bytes each; lane 8i + r gives the address of matrix i's row r)
+__device__ __forceinline__ void ldmatrix_x4(uint32_t saddr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(saddr));
+}
 // every prior tcgen05 op of this thread completes -> one arrive on `bar`
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))

@@ -38,6 +38,7 @@
 //       masked append into the caller's preallocated [B, cap] buffers, one lane
 //       per row (each row has one owner, no atomics).
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 
 namespace ll {
@@ -66,10 +67,13 @@ enum {
   BAR_FULL = 10,    // [NSMAX] weight ring: tile landed
   BAR_EMPTY = 10 + NSMAX,  // [NSMAX] weight ring: tile consumed
   BAR_E = 10 + 2 * NSMAX,  // E' slices of the predictor rows landed
-  BAR_GQ = 11 + 2 * NSMAX,   // (TG) MMA warp: a gate batch is requested (consumer thread 0 arrives)
+  BAR_GQ = 11 + 2 * NSMAX,   // (TJ) MMA warp: a command was posted (consumer thread 0 arrives)
   BAR_GATE = 12 + 2 * NSMAX, // (TG) gate batch complete (tcgen05.commit)
-  NBARS = 13 + 2 * NSMAX
+  BAR_MACK = 13 + 2 * NSMAX, // (TJ) MMA warp: command read (the command word may be reused)
+  BAR_JOINT = 14 + 2 * NSMAX,// (TJ) joint MMAs complete (tcgen05.commit)
+  NBARS = 15 + 2 * NSMAX
 };
+enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3 };
 
 // ---------------------------------------------------------------------------
 // TG: the FC LSTM instantiation (P = 640 in 16-CTA clusters: 40 units = 160
@@ -101,10 +105,46 @@ __host__ __device__ inline bool tg_shape(bool bf, bool lstm, int H, int P, int C
   return bf && lstm && H == TG_P && P == TG_P && C == TG_C;
 }
 
+// ---------------------------------------------------------------------------
+// TJ: the FC joint (H = 640 in 16-CTA clusters, LSTM or stateless) on tcgen05.
+// Each CTA owns 64 vocabulary rows (8 n8 tiles) on the tensor core plus at
+// most one extra tile (rows 1024.. when V+1+|D| > 1024) on mma.sync.  The
+// 64 x 640 weight slice is the A operand in shared memory, K-folded into
+// M = 128: A row r = 32 (v / 16) + 16 a + v % 16 holds vocabulary row v's
+// K-half a (320 elements); the z rows are the B operand with both K-halves
+// stacked along N (B row 32 a + k = joint row k's K-half a), so ONE 20-MMA
+// chain (M = 128, N = 64, K = 320) replaces a 40-MMA one: tcgen05.mma is
+// issue-bound at ~48 cycles per instruction for these small N
+// (tools/tc_probe2.cu), so the fold halves the joint's tensor-core time.  The
+// accumulator D'[r][32 a' + k] is useful where a' = a; TMEM lane quarter q
+// holds both halves of vocabulary rows 16q .. 16q + 15.
+//   A: K-major, no swizzle: row r, 16-byte chunk c (K' 8c .. 8c+7) at
+//      (r / 8) * 5120 + c * 128 + (r % 8) * 16                      (80 KB)
+//   z: row k, chunk c of 80 -> half a = c / 40 at
+//      a * 20480 + (k / 8) * 5120 + (c % 40) * 128 + (k % 8) * 16   (40 KB)
+//   f rows in shared memory with a 1296-byte stride (bank-conflict-free
+//   8-row x 16-byte reads in build_z), one bulk copy per frame.
+//   TMEM columns [440, 504): D' (after the TG gate columns).
+// ---------------------------------------------------------------------------
+constexpr int TJ_H = 640, TJ_C = 16;
+constexpr int TJ_FROW = TJ_H * 2 + 16;          // f row stride in shared memory (bytes)
+constexpr int TJ_GRP = (TJ_H / 2 / 8) * 128;    // bytes per 8-row group of one K-half (5120)
+constexpr int TJ_ZHALF = 4 * TJ_GRP;            // z: one K-half of 32 rows (20480)
+constexpr int TJ_ZBYTES = 2 * TJ_ZHALF;         // 40960
+constexpr int TJ_ABYTES = 16 * TJ_GRP;          // A: 128 rows (81920)
+constexpr int TJ_XROW = TJ_H * 2 + 16;          // extra tile weights: 8 rows, padded stride
+constexpr int TJ_NKW = 5;                       // per-CTA key partials: 4 lane quarters + the extra tile
+constexpr uint32_t TJ_COL_D = 440;
+__host__ __device__ inline bool tj_shape(bool bf, int H, int P, int C) {
+  return bf && H == TJ_H && P == TJ_H && C == TJ_C;
+}
+
 // Shared-memory layout (identical on host and device).
 struct Layout {
   int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
-  int tg, NTH;                   // TG (tcgen05 gate pre-activations + MMA warp), threads per CTA
+  int tg, tj, NTH;               // TG (tcgen05 gate pre-activations), TJ (tcgen05 joint + MMA warp), threads per CTA
+  size_t off_wa, off_wx;         // TJ: joint weight slice (A operand), extra tile weights
+  int fss;                       // TJ: f bytes per slot (WF padded rows, 128-byte aligned for the tensor copy)
   int wks, pks;                  // u64 words per per-warp key entry / per cluster partial (scores: 4)
   size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, off_es, total;
 };
@@ -114,8 +154,9 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // ring: bf16 LSTM (producer warp + weight ring + shared-memory h); NS slots.
 // sc: greedy scores (N2): per-warp entries carry log-sum-exp partials (4 words),
 // TDT cluster partials too (token + duration partials: 4 words).
+// allow_tj = false: a kernel without the TJ / TG paths (debug_joint_kernel).
 __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, int V1, int nD, int R, int W,
-                                              int WF, int C, int NS, int sc = 0) {
+                                              int WF, int C, int NS, int sc = 0, bool allow_tj = true) {
   Layout L;
   L.wks = sc ? 4 : 2;
   L.pks = (sc && nD > 0) ? 4 : 2;
@@ -125,9 +166,10 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.DPC = H / C;
   L.NW = bf ? MAX_NW : 8;          // bf16: one vocab tile per warp (<= MAX_NW tiles per CTA)
   L.ring = (bf && lstm) ? 1 : 0;   // bf16 LSTM: W_hh in TMEM, W_pred tiles resident in smem
-  L.tg = tg_shape(bf, lstm, H, P, C) ? 1 : 0;
-  L.NTH = L.NW * 32 + (L.tg ? 32 : 0);
-  L.NS = L.ring ? L.DPC / 8 : 0;   // W_pred tiles of this CTA
+  L.tg = (allow_tj && tg_shape(bf, lstm, H, P, C)) ? 1 : 0;
+  L.tj = (allow_tj && tj_shape(bf, H, P, C)) ? 1 : 0;
+  L.NTH = L.NW * 32 + (L.tj ? 32 : 0);
+  L.NS = (L.ring && !L.tj) ? L.DPC / 8 : 0;   // W_pred tiles of this CTA in smem (TJ: registers)
   (void)NS;
   L.JR = R * W;
   L.JRp = (L.JR + 15) / 16 * 16;
@@ -139,24 +181,33 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.off_b = o;    o = align_up(o + (size_t)L.tiles_max * 8 * 4, 128);
   L.off_z = o;    // joint operand rows; in the bf16 LSTM predictor: W_pred partials [NW][3][2][32] float4
   {
-    size_t zb = (size_t)L.JRp * L.zstride;
+    size_t zb = L.tj ? (size_t)TJ_ZBYTES : (size_t)L.JRp * L.zstride;
     const size_t wp = (size_t)L.NW * 3 * 2 * 32 * 16;
     if (L.ring && zb < wp) zb = wp;
     o = align_up(o + zb, 128);
   }
-  L.off_f = o;    o = align_up(o + (size_t)2 * R * WF * H * (bf ? 2 : 4), 128);
+  L.fss = (int)align_up((size_t)WF * TJ_FROW, 128);
+  L.off_f = o;    o = align_up(o + (L.tj ? (size_t)R * L.fss : (size_t)2 * R * WF * H * (bf ? 2 : 4)), 128);
   L.off_g = o;    o = align_up(o + (size_t)R * H * 4, 128);
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * 4, 128);
   L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 8 * L.pks, 128);
-  L.off_wkey = o; o = align_up(o + (size_t)L.NW * L.JR * 8 * L.wks, 128);
+  L.off_wkey = o; o = align_up(o + (size_t)(L.tj ? TJ_NKW : L.NW) * L.JR * 8 * L.wks, 128);
   L.off_hs = o;   o = align_up(o + (size_t)(L.tg ? TG_HBYTES : L.ring ? 2 * R * L.hstride : 0), 128);
   L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * P * 2, 128);
   L.off_es = o;   o = align_up(o + (size_t)(L.ring ? R * 4 * L.UPC * 4 : 0), 128);
+  L.off_wa = o;   o = align_up(o + (size_t)(L.tj ? TJ_ABYTES : 0), 128);
+  L.off_wx = o;   o = align_up(o + (size_t)(L.tj ? 8 * TJ_XROW : 0), 128);
   L.total = o;
   return L;
 }
 
 struct DecodeParams {
+  // TJ: f as a 3-D tensor {8 elements, 81 chunks, B*T_max frames} with chunk
+  // stride 16 B and frame stride 2H: a box of WF frames lands in shared memory
+  // as rows of 81 chunks = the 1296-byte padded f rows (the 81st chunk is the
+  // next frame's first, never read); fmap_ok = 0: one bulk copy per frame
+  alignas(64) CUtensorMap fmap;
+  int fmap_ok;
   Layout L;                      // shared-memory layout of the launch (read from the constant bank)
   int B, T_max, H, P, V1, nD;
   int blank, max_sym, tdt;
@@ -211,7 +262,7 @@ struct RowState {
   int grp[2];                            // group index broadcast (double-buffered)
   int ack[2];
   volatile int done;                     // consumers finished (producer exits)
-  volatile int mma_exit;                 // (TG) the MMA warp leaves its loop
+  volatile int mcmd;                     // (TJ) command word for the MMA warp (MCMD_*)
   volatile unsigned tag[NSMAX];          // ring: index of the tile last issued into each slot
 };
 
@@ -231,6 +282,8 @@ struct Ctx {
   // the FC LSTM shape: tcgen05 gate pre-activations (see TG_* above); only the
   // LSTM member functions use it (the stateless FC kernel never issues a batch)
   static constexpr bool TG = BF && HC == TG_P && PC == TG_P && CC == TG_C;
+  // the FC joint on tcgen05 (TJ_* above), LSTM and stateless FC kernels
+  static constexpr bool TJ = BF && HC == TJ_H && PC == TJ_H && CC == TJ_C;
   const DecodeParams &p;
   const Layout &L;            // in the kernel parameters (constant bank; uniform, no registers)
   uint8_t *sm;
@@ -245,8 +298,11 @@ struct Ctx {
   // into one register: bits 0-1 fph (BAR_F+X phase), 2-3 fpend (bulk copy into
   // fbuf[X] outstanding), 4-5 xph (BAR_X+par phase), 6 hph (BAR_H/G/E phase),
   // 7 par (partial-key buffer parity); TG: 8 gate batch pending, 9 BAR_GATE
-  // phase, 10 the gate pre-activations in TMEM are valid for this group.
+  // phase, 10 the gate pre-activations in TMEM are valid for this group;
+  // TJ: 11 BAR_JOINT phase.
   uint32_t phs;
+  uint32_t npost = 0;         // TJ, thread 0: commands posted to the MMA warp
+  uint4 wpr[2][3][2];         // TJ LSTM: this warp's W_pred fragments (K blocks warp, warp + 10)
   __device__ __forceinline__ uint32_t fph(int X) const { return (phs >> X) & 1u; }
   __device__ __forceinline__ uint32_t fpend(int X) const { return (phs >> (2 + X)) & 1u; }
   __device__ __forceinline__ uint32_t xph(int X) const { return (phs >> (4 + X)) & 1u; }
@@ -325,7 +381,11 @@ struct Ctx {
   __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
   __device__ uint8_t *zs() const { return sm + L.off_z; }
-  __device__ uint8_t *fbuf(int X) const { return sm + L.off_f + (size_t)X * p.R * p.WF * Hd() * sizeof(T); }
+  __device__ uint8_t *fbuf(int X) const {
+    if constexpr (TJ) return sm + L.off_f;   // one buffer (the bookkeeping of both halves is kept)
+    else return sm + L.off_f + (size_t)X * p.R * p.WF * Hd() * sizeof(T);
+  }
+
   __device__ float *gs() const { return (float *)(sm + L.off_g); }
   // bf16 path: g rows are stored as two planes, so that build_z's per-lane
   // 8-dim chunk c is two CONSECUTIVE float4s across lanes (conflict-free):
@@ -363,33 +423,56 @@ struct Ctx {
   // fence.proxy.async): request a gate batch over the current h buffer.
   // Every consumer thread calls it (replicated bookkeeping).
   __device__ __forceinline__ void gate_request() {
-    if (tid == 0) mbar_arrive(bar(BAR_GQ));
+    if (tid == 0) post(MCMD_GATES);
     phs |= (1u << 8) | (1u << 10);
   }
-  // The MMA warp (lane 0): for every request, D_main = W_hh[rows 0..127] h and
-  // D_fold = the K-quarter partials of rows 128..159, one tcgen05.commit.
+  // thread 0: hand a command to the MMA warp (after the previous one was read)
+  __device__ void post(int cmd) {
+    if (npost > 0) mbar_wait(bar(BAR_MACK), (npost - 1) & 1u);
+    rs.mcmd = cmd;
+    mbar_arrive(bar(BAR_GQ));
+    ++npost;
+  }
+  __device__ __forceinline__ uint32_t jph() const { return (phs >> 11) & 1u; }
+  // The MMA warp (lane 0) executes the posted commands in order:
+  //   MCMD_GATES: D_main = W_hh[rows 0..127] h, D_fold = the K-quarter partials
+  //               of rows 128..159 (TS mode, A in TMEM) -> BAR_GATE
+  //   MCMD_JOINT: D' = A(W_out slice, K-folded) . z^T (SS mode)  -> BAR_JOINT
   __device__ void mma_warp_loop() {
-    if constexpr (TG) {
+    if constexpr (TJ) {
       if (lane != 0) return;
       constexpr uint32_t ID_MAIN = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TG_NH >> 3) << 17) | (8u << 24);
       constexpr uint32_t ID_FOLD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(4 * TG_NH >> 3) << 17) | (8u << 24);
-      const uint32_t hb = smem_u32(hbuf());
+      constexpr uint32_t ID_J = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | (8u << 24);
+      const uint32_t hb = smem_u32(hbuf()), za = smem_u32(zs()), wa = smem_u32(sm + L.off_wa);
       for (uint32_t ph = 0;; ph ^= 1u) {
         mbar_wait(bar(BAR_GQ), ph);
-        if (rs.mma_exit) break;
+        const int cmd = rs.mcmd;
+        mbar_arrive(bar(BAR_MACK));
+        if (cmd == MCMD_EXIT) break;
         tc_fence_after();
+        if (cmd == MCMD_GATES) {
 #pragma unroll
-        for (int kk = 0; kk < TG_P / 16; ++kk) {   // K = 16 per MMA: h chunks 2kk, 2kk + 1
-          const int c = 2 * kk;
-          const uint64_t db = umma_desc_ns(hb + (uint32_t)((c / 20) * TG_QB + (c % 20) * 128), 128, 1024);
-          umma_ts(tmem + TG_COL_DMAIN, tmem + (uint32_t)(8 * kk), db, ID_MAIN, kk > 0);
-        }
+          for (int kk = 0; kk < TG_P / 16; ++kk) {   // K = 16 per MMA: h chunks 2kk, 2kk + 1
+            const int c = 2 * kk;
+            const uint64_t db = umma_desc_ns(hb + (uint32_t)((c / 20) * TG_QB + (c % 20) * 128), 128, 1024);
+            umma_ts(tmem + TG_COL_DMAIN, tmem + (uint32_t)(8 * kk), db, ID_MAIN, kk > 0);
+          }
 #pragma unroll
-        for (int kk = 0; kk < TG_P / 64; ++kk) {   // the 4 K-quarters side by side (32 B rows)
-          const uint64_t db = umma_desc_ns(hb + (uint32_t)(kk * 256), 128, TG_QB);
-          umma_ts(tmem + TG_COL_DFOLD, tmem + TG_COL_FOLD + (uint32_t)(8 * kk), db, ID_FOLD, kk > 0);
+          for (int kk = 0; kk < TG_P / 64; ++kk) {   // the 4 K-quarters side by side (32 B rows)
+            const uint64_t db = umma_desc_ns(hb + (uint32_t)(kk * 256), 128, TG_QB);
+            umma_ts(tmem + TG_COL_DFOLD, tmem + TG_COL_FOLD + (uint32_t)(8 * kk), db, ID_FOLD, kk > 0);
+          }
+          umma_commit(bar(BAR_GATE));
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < TJ_H / 32; ++kk) {   // K' = 320: A / B chunks 2kk, 2kk + 1
+            const uint64_t da = umma_desc_ns(wa + (uint32_t)(kk * 256), 128, TJ_GRP);
+            const uint64_t db = umma_desc_ns(za + (uint32_t)(kk * 256), 128, TJ_GRP);
+            umma_ss(tmem + TJ_COL_D, da, db, ID_J, kk > 0);
+          }
+          umma_commit(bar(BAR_JOINT));
         }
-        umma_commit(bar(BAR_GATE));
       }
     }
   }
@@ -416,7 +499,32 @@ struct Ctx {
         bv = v < V1 ? to_f32(((const T *)p.b_out)[v]) : to_f32(((const T *)p.b_dur)[v - V1]);
       bs[r] = bv;
     }
-    if constexpr (BF) {
+    if constexpr (TJ) {
+      // A operand: the first 8 tiles (64 rows), row r = 32 (vl / 16) + 16 a + vl % 16
+      // holds local row vl's K-half a; the 9th tile (if any) for mma.sync
+      const int nmain = ntiles < 8 ? ntiles * 8 : 64;
+      for (int i = tid; i < 128 * (TJ_H / 16); i += NCT) {
+        const int r = i / (TJ_H / 16), c = i % (TJ_H / 16);
+        const int vl = 16 * (r >> 5) + (r & 15), a = (r >> 4) & 1, v = tile0 * 8 + vl;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (vl < nmain && v < NV) {
+          const bf16 *src = v < V1 ? (const bf16 *)p.w_out + (size_t)v * TJ_H : (const bf16 *)p.w_dur + (size_t)(v - V1) * TJ_H;
+          x = ldg128_nc(src + a * (TJ_H / 2) + c * 8);
+        }
+        *reinterpret_cast<uint4 *>(sm + L.off_wa + (r >> 3) * TJ_GRP + c * 128 + (r & 7) * 16) = x;
+      }
+      for (int i = tid; i < 8 * (TJ_H / 8); i += NCT) {
+        const int r = i / (TJ_H / 8), c = i % (TJ_H / 8);
+        const int vl = 64 + r, v = tile0 * 8 + vl;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (vl < ntiles * 8 && v < NV) {
+          const bf16 *src = v < V1 ? (const bf16 *)p.w_out + (size_t)v * TJ_H : (const bf16 *)p.w_dur + (size_t)(v - V1) * TJ_H;
+          x = ldg128_nc(src + c * 8);
+        }
+        *reinterpret_cast<uint4 *>(sm + L.off_wx + r * TJ_XROW + c * 16) = x;
+      }
+      fence_proxy_async_smem();   // the A operand is read by the tensor core
+    } else if constexpr (BF) {
       const int KB = H / 32;
       const int v = tile0 * 8 + warp * 8 + g;
       const bool ok = warp < ntiles && v < NV;
@@ -445,6 +553,7 @@ struct Ctx {
   }
   __device__ void issue_f(int X, bool spec, const int *list = nullptr, int nlist = 0) {
     if (fpend(X)) wait_f(X);  // drain a stale speculative copy first
+    if (TJ && fpend(X ^ 1)) wait_f(X ^ 1);   // one buffer behind both halves
     const int n = list ? nlist : rs.nscan;
     const uint32_t frb = (uint32_t)(Hd() * sizeof(T));
     if (warp == iw) {
@@ -458,6 +567,7 @@ struct Ctx {
         if (cnt < 0) cnt = 0;
         bytes = (uint32_t)cnt * frb;
       }
+      if (TJ && p.fmap_ok && cnt > 0) bytes = (uint32_t)(p.WF * TJ_FROW);   // whole boxes
       uint32_t tot = bytes;
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       if (lane == 0) mbar_arrive_expect_tx(bar(BAR_F + X), tot);
@@ -467,7 +577,20 @@ struct Ctx {
         rs.fcnt[X][s] = cnt;
         if (cnt > 0) {
           const uint8_t *src = (const uint8_t *)p.f + ((size_t)rs.b[s] * p.T_max + base) * frb;
-          bulk_g2s(fbuf(X) + (size_t)s * p.WF * frb, src, bytes, bar(BAR_F + X));
+          if constexpr (TJ) {   // padded rows: one tensor copy per slot (else one bulk copy per frame)
+            if (p.fmap_ok) {
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                      smem_u32(fbuf(X) + (size_t)s * L.fss)),
+                  "l"(&p.fmap), "r"(0), "r"(0), "r"(rs.b[s] * p.T_max + base), "r"(smem_u32(bar(BAR_F + X)))
+                  : "memory");
+            } else {
+              for (int i = 0; i < cnt; ++i)
+                bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * TJ_FROW, src + (size_t)i * frb, frb, bar(BAR_F + X));
+            }
+          } else {
+            bulk_g2s(fbuf(X) + (size_t)s * p.WF * frb, src, bytes, bar(BAR_F + X));
+          }
         }
       }
       __syncwarp();   // reconverge before the caller's (aligned) CTA barrier
@@ -486,7 +609,7 @@ struct Ctx {
       const int s = rs.slist[lane / W], j = lane % W;
       const int fr = rs.t[s] + j - rs.fbase[X][s];
       live = rs.t[s] + j < rs.L[s] && fr >= 0 && fr < rs.fcnt[X][s];
-      src = (s * p.WF + fr) * Hd();
+      src = TJ ? (s * L.fss + fr * TJ_FROW) / 2 : (s * p.WF + fr) * Hd();
       dst = s * W + j;
     }
     const unsigned m = __ballot_sync(0xffffffffu, live);
@@ -512,6 +635,48 @@ struct Ctx {
   __device__ void build_z(int X) {
     const int H = Hd(), W = p.W;
     const int nz = rs.nz;
+    if constexpr (TJ) {
+      // warps 0-7: 8-row group G = warp % 4, K-half a = warp / 4; lane = (row r,
+      // chunk phase cq): 8 rows x 16 bytes per chunk (conflict-free stores)
+      const int G = warp & 3, a = warp >> 2;
+      if (warp < 8 && 8 * G < nz) {
+        const int r = lane & 7, cq = lane >> 3, k = 8 * G + r;
+        const bool live = k < nz;
+        const uint8_t *fr = fbuf(X) + (size_t)(live ? rs.zsrc[k] : 0) * 2;
+        const int s = live ? rs.zdst[k] / W : 0;
+        const float4 *gr0 = reinterpret_cast<const float4 *>(gs() + (size_t)s * TJ_H);   // plane 0
+        const float4 *gr1 = gr0 + TJ_H / 8;                                               // plane 1
+        uint8_t *zr = zs() + a * TJ_ZHALF + G * TJ_GRP + r * 16;
+#pragma unroll
+        for (int i0 = 0; i0 < 10; i0 += 5) {
+          uint4 fv[5];
+          float4 ga[5], gb[5];
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            const int c = 40 * a + 4 * (i0 + u) + cq;
+            fv[u] = lds128(fr + c * 16);
+            ga[u] = gr0[c];
+            gb[u] = gr1[c];
+          }
+          if (live) {
+#pragma unroll
+            for (int u = 0; u < 5; ++u) {
+              const uint4 f = fv[u];
+              const float4 g0 = ga[u], g1 = gb[u];
+              uint4 o;
+              o.x = pack_bf16x2(fmaxf(bf16_lo(f.x) + g0.x, 0.f), fmaxf(bf16_hi(f.x) + g0.y, 0.f));
+              o.y = pack_bf16x2(fmaxf(bf16_lo(f.y) + g0.z, 0.f), fmaxf(bf16_hi(f.y) + g0.w, 0.f));
+              o.z = pack_bf16x2(fmaxf(bf16_lo(f.z) + g1.x, 0.f), fmaxf(bf16_hi(f.z) + g1.y, 0.f));
+              o.w = pack_bf16x2(fmaxf(bf16_lo(f.w) + g1.z, 0.f), fmaxf(bf16_hi(f.w) + g1.w, 0.f));
+              *reinterpret_cast<uint4 *>(zr + (4 * (i0 + u) + cq) * 128) = o;
+            }
+          }
+        }
+      }
+      tl_round_(11);
+      fence_proxy_async_smem();   // z is read by the tensor core
+      return;
+    }
     if constexpr (BF) {
       // one joint row per warp pass, up to 3 16-byte chunks per lane (H <= 768):
       // all shared loads of the row are issued before any store (the compiler
@@ -617,7 +782,167 @@ struct Ctx {
     }
   }
 
+  // TJ butterfly: 32-lane keys/partials, lane l keeps column l after the 4 steps
+  // (xor 8, 4, 2, 1 inside each 16-lane half; lane l's half = column block l / 16).
+  template <int NK>
+  __device__ __forceinline__ static void bfly_max(uint64_t (&x)[NK], int lane) {
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {
+      const bool b = (lane & w) != 0;
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const uint64_t lo = x[i], hi = x[i + w];
+        const uint64_t r = shfl_xor_u64(b ? lo : hi, w);
+        x[i] = umax64(b ? hi : lo, r);
+      }
+    }
+  }
+  template <int NK>
+  __device__ __forceinline__ static void bfly_lse(uint64_t (&x)[NK], int lane) {
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {
+      const bool b = (lane & w) != 0;
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const uint64_t lo = x[i], hi = x[i + w];
+        const uint64_t r = shfl_xor_u64(b ? lo : hi, w);
+        x[i] = lse_combine(b ? hi : lo, r);
+      }
+    }
+  }
+  __device__ __forceinline__ int nkw() const {
+    if constexpr (TJ) return ntiles > 8 ? TJ_NKW : TJ_NKW - 1;
+    else return NW;
+  }
+
+  // TJ joint: the MMA warp runs D' = A . z^T (posted here); warps 0-3 read D'
+  // (lane quarter q = vocabulary rows 16q .. 16q + 15, both K-halves), warps
+  // 4-5 the extra tile on mma.sync; per-partial keys -> wkey[0..4][jr].
+  __device__ void joint_keys_tj(int nrows_valid, float *logits, int row_base) {
+    const int V1 = p.V1, NV = p.V1 + p.nD;
+    uint64_t *wk = wkey();
+    if (tid == 0) post(MCMD_JOINT);
+    if (warp < 4) {
+      mbar_wait(bar(BAR_JOINT), jph());
+      tl_round_(12);
+      tc_fence_after();
+      uint32_t lo[32], hi[32];
+      const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + TJ_COL_D;
+      tmem_ld32(ta, lo);
+      tmem_ld32(ta + 32, hi);
+      tmem_wait_ld();
+      const int a = lane >> 4, vl = 16 * warp + (lane & 15), v = tile0 * 8 + vl;
+      const int nmain = ntiles < 8 ? ntiles * 8 : 64;
+      const int kind = (vl < nmain && v < NV) ? (v < V1 ? 1 : 2) : 0;
+      const float bias = bsl()[vl];
+      const bool dmain = is_tdt() && tile0 * 8 + nmain > V1;   // duration rows among the main rows
+      // logits of joint rows k = 16a + j: K-half partials of lanes l and l ^ 16 (lo + hi)
+      uint64_t tk[16], dk[16];
+      [[maybe_unused]] uint64_t tl[16], dl[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t send = a ? hi[j] : lo[j + 16];
+        const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 16));
+        const float val = (a ? recv + __uint_as_float(hi[16 + j]) : __uint_as_float(lo[j]) + recv) + bias;
+        const int k = 16 * a + j;
+        if (logits != nullptr && kind && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v] = val;
+        tk[j] = kind == 1 ? pack_key(val, v) : 0ull;
+        dk[j] = kind == 2 ? pack_key(val, v - V1) : 0ull;
+        if constexpr (SC) {
+          tl[j] = kind == 1 ? lse_pack(val, 1.f) : lse_empty();
+          dl[j] = kind == 2 ? lse_pack(val, 1.f) : lse_empty();
+        }
+      }
+      bfly_max(tk, lane);
+      if (dmain) bfly_max(dk, lane);
+      if constexpr (SC) {
+        bfly_lse(tl, lane);
+        if (dmain) bfly_lse(dl, lane);
+      }
+      tl_round_(13);
+      if (lane < L.JR) {
+        uint64_t *dst = wk + ((size_t)warp * L.JR + lane) * wks();
+        uint4 e;
+        const uint64_t d0 = dmain ? dk[0] : 0ull;
+        e.x = (uint32_t)tk[0]; e.y = (uint32_t)(tk[0] >> 32); e.z = (uint32_t)d0; e.w = (uint32_t)(d0 >> 32);
+        *reinterpret_cast<uint4 *>(dst) = e;
+        if constexpr (SC) {
+          const uint64_t l0 = dmain ? dl[0] : lse_empty();
+          uint4 f;
+          f.x = (uint32_t)tl[0]; f.y = (uint32_t)(tl[0] >> 32); f.z = (uint32_t)l0; f.w = (uint32_t)(l0 >> 32);
+          *reinterpret_cast<uint4 *>(dst + 2) = f;
+        }
+      }
+    } else if ((warp == 4 || (warp == 5 && rs.nz > 16)) && ntiles > 8) {
+      // extra tile (local rows 64..71): z rows as the m16 A operand (ldmatrix from
+      // the B' layout), the 8 weight rows as the n8 B operand
+      const int m0 = 16 * (warp - 4);
+      const uint8_t *wx = sm + L.off_wx;
+      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      const int mi = lane >> 3, rr = lane & 7, kz = m0 + 8 * (mi & 1) + rr;
+      const uint32_t zb = smem_u32(zs()) + (uint32_t)((kz >> 3) * TJ_GRP + (kz & 7) * 16);
+#pragma unroll 8
+      for (int kk = 0; kk < TJ_H / 16; ++kk) {
+        const int c = 2 * kk + (mi >> 1);
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(zb + (uint32_t)((c / 40) * TJ_ZHALF + (c % 40) * 128), a0, a1, a2, a3);
+        const uint8_t *wr = wx + g * TJ_XROW + (16 * kk + 2 * q) * 2;
+        const uint32_t b0 = *reinterpret_cast<const uint32_t *>(wr), b1 = *reinterpret_cast<const uint32_t *>(wr + 16);
+        mma_bf16_16816(acc[kk & 1], a0, a1, a2, a3, b0, b1);
+      }
+      tl_round_(14);
+      uint64_t tk2[2] = {0, 0}, dk2[2] = {0, 0};
+      [[maybe_unused]] uint64_t tl2[2] = {lse_empty(), lse_empty()}, dl2[2] = {lse_empty(), lse_empty()};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int vl = 64 + 2 * q + (e & 1), v = tile0 * 8 + vl, hr = e >> 1;
+        if (vl < ntiles * 8 && v < NV) {
+          const float val = (acc[0][e] + acc[1][e]) + bsl()[vl];
+          const int k = m0 + g + 8 * hr;
+          if (logits != nullptr && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v] = val;
+          if (v < V1) tk2[hr] = umax64(tk2[hr], pack_key(val, v));
+          else dk2[hr] = umax64(dk2[hr], pack_key(val, v - V1));
+          if constexpr (SC) {
+            if (v < V1) tl2[hr] = lse_combine(tl2[hr], lse_pack(val, 1.f));
+            else dl2[hr] = lse_combine(dl2[hr], lse_pack(val, 1.f));
+          }
+        }
+      }
+#pragma unroll
+      for (int hr = 0; hr < 2; ++hr) {
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+          tk2[hr] = umax64(tk2[hr], shfl_xor_u64(tk2[hr], o));
+          dk2[hr] = umax64(dk2[hr], shfl_xor_u64(dk2[hr], o));
+          if constexpr (SC) {
+            tl2[hr] = lse_combine(tl2[hr], shfl_xor_u64(tl2[hr], o));
+            dl2[hr] = lse_combine(dl2[hr], shfl_xor_u64(dl2[hr], o));
+          }
+        }
+        const int k = m0 + g + 8 * hr;
+        if (q == 0 && k < L.JR) {
+          uint64_t *dst = wk + ((size_t)4 * L.JR + k) * wks();
+          uint4 e;
+          e.x = (uint32_t)tk2[hr]; e.y = (uint32_t)(tk2[hr] >> 32); e.z = (uint32_t)dk2[hr]; e.w = (uint32_t)(dk2[hr] >> 32);
+          *reinterpret_cast<uint4 *>(dst) = e;
+          if constexpr (SC) {
+            uint4 f;
+            f.x = (uint32_t)tl2[hr]; f.y = (uint32_t)(tl2[hr] >> 32); f.z = (uint32_t)dl2[hr]; f.w = (uint32_t)(dl2[hr] >> 32);
+            *reinterpret_cast<uint4 *>(dst + 2) = f;
+          }
+        }
+      }
+    }
+    tc_fence_before();   // D' reads ordered before the next joint (through the exchange barrier)
+    phs ^= 1u << 11;
+  }
+
   __device__ void joint_keys(int MT, int nrows_valid, float *logits, int row_base) {
+    if constexpr (TJ) {
+      (void)MT;
+      joint_keys_tj(nrows_valid, logits, row_base);
+      return;
+    }
     const int V1 = p.V1, NV = p.V1 + p.nD, H = Hd();
     uint64_t *wk = wkey();
     if constexpr (BF) {
@@ -787,9 +1112,10 @@ struct Ctx {
       const int jr = tid;                       // compact joint row
       uint64_t tkey = 0, dkey = 0;
       [[maybe_unused]] uint64_t tl = lse_empty(), dl = lse_empty();
+      const int nk = nkw();
 #pragma unroll
       for (int w = 0; w < MAX_NW; ++w) {
-        if (w < NW) {
+        if (w < nk) {
           const uint64_t *e = wk + ((size_t)w * L.JR + jr) * wks();
           if (is_tdt()) {
             const uint4 v = *reinterpret_cast<const uint4 *>(e);
@@ -1364,14 +1690,20 @@ struct Ctx {
         }
       }
       tmem_wait_st();
-      if (warp == 0) {   // W_pred tiles (the packed stream's tail) into shared memory
-        const int NG = ng(), NPT = npt();
-        const uint32_t bytes = (uint32_t)(NPT * 8 * TG_P * 2);
-        if (lane == 0) {
-          mbar_arrive_expect_tx(bar(BAR_FULL), bytes);
-          bulk_g2s(ringslot(0), p.wst + ((size_t)rank * (NG + NPT) + NG) * 8 * TG_P, bytes, bar(BAR_FULL));
-        }
-        mbar_wait(bar(BAR_FULL), 0);
+      // W_pred into registers: warp w's K blocks kb = w, w + 10 (16-byte chunk
+      // 4 kb + q) of rows 16t + g (tile 2t) and 16t + 8 + g (tile 2t + 1)
+      if (warp < NW) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const int row = 16 * t + 8 * hf + g, kb = warp + MAX_NW * i;
+              wpr[i][t][hf] = (row < TG_UPC && kb < TG_P / 32)
+                                  ? ldg128_nc((const bf16 *)p.w_pred + (size_t)(d0 + row) * TG_P + (4 * kb + q) * 8)
+                                  : make_uint4(0, 0, 0, 0);
+            }
       }
       return;
     }
@@ -1503,10 +1835,15 @@ struct Ctx {
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         if (2 * t < NPT) {
-          const uint32_t co = (uint32_t)(((kb * 4 + q) ^ sw) * 16);
-          const uint4 wa = lds128(ringslot(2 * t) + (size_t)g * Pd() * 2 + co);
-          const uint4 wb = 2 * t + 1 < NPT ? lds128(ringslot(2 * t + 1) + (size_t)g * Pd() * 2 + co)
-                                           : make_uint4(0, 0, 0, 0);
+          uint4 wa, wb;
+          if constexpr (TG) {
+            wa = wpr[i][t][0];
+            wb = wpr[i][t][1];
+          } else {
+            const uint32_t co = (uint32_t)(((kb * 4 + q) ^ sw) * 16);
+            wa = lds128(ringslot(2 * t) + (size_t)g * Pd() * 2 + co);
+            wb = 2 * t + 1 < NPT ? lds128(ringslot(2 * t + 1) + (size_t)g * Pd() * 2 + co) : make_uint4(0, 0, 0, 0);
+          }
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
             mma_bf16_16816(acc[t][nb], wa.x, wb.x, wa.y, wb.y, x[nb].x, x[nb].y);
@@ -2035,15 +2372,17 @@ __global__ void pack_lstm_stream(const bf16 *w_hh, const bf16 *w_pred, bf16 *wst
 // SC: 1 = greedy scores (N2), per-row tick schedule only.
 template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int LM = 0, int TM = 0, int DBG = 0,
           int SC = 0>
-__global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && HC == TG_P && PC == TG_P && CC == TG_C ? 32 : 0), 1)
+__global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H && PC == TJ_H && CC == TJ_C ? 32 : 0), 1)
     decode_kernel(const __grid_constant__ DecodeParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
   using CtxT = Ctx<T, KR, HC, PC, CC, TM, SC>;
   CtxT cx(p, smem, rs, PRED == 0, s_bars);
-  // TG: an 11th warp issues the background gate batches (outside the consumer barrier)
-  constexpr bool MMAW = PRED == 0 && CtxT::TG;
+  // TJ: an 11th warp issues the tcgen05 joint (and, LSTM, the background gate
+  // batches), outside the consumer barrier
+  constexpr bool MMAW = CtxT::TJ;
+  constexpr bool TGK = PRED == 0 && CtxT::TG;
   const bool tdt = TM == 0 ? p.tdt != 0 : TM == 2;
   const int C = cx.C, rank = cx.rank, tid = cx.tid, lane = cx.lane, warp = cx.warp;
   const int R = p.R;
@@ -2056,19 +2395,18 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && 
   __shared__ uint32_t s_tmem;
   cx.init_barriers();
   cx.load_weight_slice();
-  if constexpr (RING) {
+  if constexpr (RING || MMAW) {
     if (warp == 0) tmem_alloc(&s_tmem, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     cx.tmem = s_tmem;
-    cx.load_lstm_weights();
+    if constexpr (RING) cx.load_lstm_weights();
     tc_fence_before();
   }
-  if (tid == 0) rs.mma_exit = 0;
   __syncthreads();
   if (C > 1) cluster_sync_all();  // barriers initialised cluster-wide before any st.async
-  if constexpr (RING) tc_fence_after();
+  if constexpr (RING || MMAW) tc_fence_after();
 
   if (MMAW && warp == MAX_NW) {
     cx.mma_warp_loop();
@@ -2121,7 +2459,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && 
       if constexpr (PRED == 0) {
         // LSTM initial state h = c = 0 (reading A8)
         for (int i = tid; i < R * cx.L.UPC; i += cx.NCT) cx.cs()[i] = 0.f;
-        if constexpr (MMAW) {
+        if constexpr (TGK) {
           // no gate batch may still read the h buffer; h = 0 means W_hh h = 0,
           // so the first step skips the (not yet computed) pre-activations
           cx.gate_wait();
@@ -2289,6 +2627,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && 
             cx.build_z(cur);
             cx.tl_round_(2);
             cx.sync();
+            cx.tl_round_bar(15);
             if (p.spec_prefetch) {
               cx.issue_f(cur ^ 1, true);
               have_spec = true;
@@ -2480,10 +2819,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && 
     if (cx.fpend(1)) cx.wait_f(1);
     if constexpr (MMAW) {
       cx.gate_wait();
-      if (tid == 0) {
-        rs.mma_exit = 1;
-        mbar_arrive(cx.bar(BAR_GQ));
-      }
+      if (tid == 0) cx.post(MCMD_EXIT);
     }
     cx.sync();
 #undef LL_PHASE
@@ -2509,9 +2845,9 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && PRED == 0 && 
       }
     }
   }
-  if constexpr (RING) tc_fence_before();
+  if constexpr (RING || MMAW) tc_fence_before();
   __syncthreads();
-  if constexpr (RING) {
+  if constexpr (RING || MMAW) {
     tc_fence_after();
     if (warp == 0) tmem_dealloc(cx.tmem, 512);
   }

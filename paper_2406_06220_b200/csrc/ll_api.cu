@@ -54,7 +54,7 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
   w.wih = o;  // bf16 LSTM: W_ih and b_ih, b_hh with gate rows permuted CTA-major (E' table columns)
   if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + 4 * P * P * 2 + 2 * 4 * P * 2, 256);
   w.f = o;
-  o = align_up(o + (size_t)B * T * H * esize(dt), 256);
+  o = align_up(o + (size_t)B * T * H * esize(dt) + 256, 256);   // + slack: the padded f-row boxes read 16 B past a row
   w.h = o;
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + 2 * (size_t)B * P * esize(dt), 256);
   w.g = o;
@@ -167,7 +167,10 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
       if (W > 8) W = 8;
       if (W < 1) W = 1;
       if (R * W > MAX_JR) continue;
-      for (; W >= 1; W >>= 1) {
+      for (; W >= 1; W = tj_shape(bf, H, P, C) ? W - 1 : W >> 1) {
+        // TJ (tcgen05 joint, ~1K cycles per round whatever the row count):
+        // fewer rows per group with a real window beat one-frame rounds
+        if (tj_shape(bf, H, P, C) && !forceW && !forceR && W == 1 && R > 1) break;
         cf.C = C; cf.R = R; cf.W = W; cf.WF = W + (maxd > 1 ? maxd - 1 : 0);
         cf.NS = 0;
         cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0, sc);
@@ -300,6 +303,20 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t rows, uint64_t col
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TJ f boxes (DecodeParams::fmap): {8 elements, 81 chunks, frames}, chunk stride
+// 16 B, frame stride 2H; box {8, 81, WF} -> WF padded 1296-byte rows.
+bool make_fmap(CUtensorMap *m, const void *f, uint64_t frames, int H, int WF) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc || H != TJ_H || WF < 1 || WF > 255) return false;
+  const cuuint64_t dims[3] = {8, (cuuint64_t)(TJ_FROW / 16), frames};
+  const cuuint64_t strides[2] = {16, (cuuint64_t)H * 2};
+  const cuuint32_t box[3] = {8, (cuuint32_t)(TJ_FROW / 16), (cuuint32_t)WF};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(f), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -524,6 +541,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.sched = g_opt.schedule < 0 ? 1 : g_opt.schedule;
   p.lengths = lengths;
   p.f = ws + w.f;
+  if (L.tj && bf) p.fmap_ok = make_fmap(&p.fmap, ws + w.f, (uint64_t)B * T_max, H, cf.WF) ? 1 : 0;
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
   p.w_pred = jn->w_pred; p.b_pred = jn->b_pred; p.w_hh = lstm ? pr->w_hh : nullptr;
   p.tab = tab;
@@ -796,7 +814,7 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   Config cf;
   if (!choose_config(bf, false, H, joint->pred_dim, V1, num_durations, 1, 16 * 8, cf)) return LL_ERR_UNSUPPORTED;
   cf.R = 16; cf.W = 1; cf.WF = 1; cf.NS = 0;
-  cf.L = make_layout(bf, false, H, joint->pred_dim, V1, num_durations, 16, 1, 1, cf.C, 0);
+  cf.L = make_layout(bf, false, H, joint->pred_dim, V1, num_durations, 16, 1, 1, cf.C, 0, 0, false);
   const int C = cf.C, R = cf.R;
   const Layout &L = cf.L;
   cudaStream_t st = (cudaStream_t)stream;

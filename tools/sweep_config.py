@@ -11,7 +11,8 @@ dec = LabelLoopingDecoder(model, spec.max_symbols, enc.shape[0], enc.shape[1])
 e = torch.from_numpy(enc).to("cuda", torch.bfloat16); l = torch.from_numpy(lengths).cuda()
 ref = None
 from paper_2406_06220_b200 import ll
-for R, W in [(4, 8), (5, 6), (5, 4), (4, 4), (5, 2), (8, 4), (11, 2), (16, 2), (5, 1)]:
+PAIRS = [tuple(map(int, x.split("x"))) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [(4, 8), (5, 6), (5, 4), (4, 4), (5, 2), (8, 4), (11, 2), (16, 2), (5, 1)]
+for R, W in PAIRS:
     NS = 0
     ll.ll_set_options(ll.options(group_rows=R, window=W).opts)
     try:

@@ -19,7 +19,7 @@ ll.ll_set_options(ll.options(timeline=buf.data_ptr()).opts)   # this thread, for
 import bench
 from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "fc-rnnt"
+cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "fc-rnnt"
 spec, w, enc, lengths = bench.workload(cfg, 1000)
 model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16")
 dec = LabelLoopingDecoder(model, spec.max_symbols, enc.shape[0], enc.shape[1])
@@ -55,9 +55,16 @@ def report(area, name, order, labels):
         print(f"  {'(gap to next event)':28s} {np.median(gaps):8.0f} cyc median")
     return ev
 
-report(0, "joint rounds", list(range(11)),
-       ["", "wait_f/plan (+sync)", "build_z", "sync (bar)", "spec issue + joint", "exchange send",
-        "exchange wait", "resolve", "sync (bar)", "decide", "sync+reload (bar)"])
+if "--tj" in sys.argv:   # the tcgen05 joint: stamps 11 (build_z before its proxy fence), 12 (joint MMAs done)
+    report(0, "joint rounds", [0, 1, 11, 2, 15, 3, 12, 13, 4, 5, 6, 7, 8, 9, 10],
+           ["", "wait_f/plan (+sync)", "build_z", "proxy fence", "sync", "spec issue", "joint MMA (post..done)",
+            "epilogue TMEM+bfly (w0-3)", "epilogue end (all)", "exchange send", "exchange wait", "resolve", "sync (bar)",
+            "decide", "sync+reload (bar)"])
+    report(0, "extra tile (warps 4-5)", [3, 14], ["", "mma.sync chain"])
+else:
+    report(0, "joint rounds", list(range(11)),
+           ["", "wait_f/plan (+sync)", "build_z", "sync (bar)", "spec issue + joint", "exchange send",
+            "exchange wait", "resolve", "sync (bar)", "decide", "sync+reload (bar)"])
 report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 9, 10, 5, 6, 7],
        ["", "outer-step entry", "first gate tile", "rest tiles + E' wait", "sync (bar)", "h' exchange",
         "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)", "g exchange + sync"])
