@@ -35,7 +35,9 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     lib = LIB if not variant else os.path.join(HERE, f"libll_{variant}.so")
     if not force and os.path.exists(lib) and not any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS):
         return lib
-    defs = {"": [], "timeline": ["-DLL_TIMELINE"], "trace": ["-DLL_DEBUG_TRACE"]}[variant]
+    defs = {"": [], "timeline": ["-DLL_TIMELINE"], "trace": ["-DLL_DEBUG_TRACE"]}.get(variant)
+    if defs is None:   # experiment variants: "timeline_exp1" -> -DLL_TIMELINE -DLL_EXP1
+        defs = ["-DLL_" + v.upper() for v in variant.split("_")]
     tmp = f"{lib}.tmp{os.getpid()}"   # per process: concurrent ranks may build at once; os.replace is atomic
     cmd = [NVCC] + FLAGS + defs + ["-I", os.path.join(ROOT, "include"), "-o", tmp] + SOURCES
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -80,6 +80,15 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 }
 
 __device__ __forceinline__ uint4 lds128(const void *p) { return *reinterpret_cast<const uint4 *>(p); }
+// 32-bit shared-window addresses (no 64-bit generic address arithmetic)
+__device__ __forceinline__ uint4 lds128_u32(uint32_t a) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a) : "memory");
+  return r;
+}
+__device__ __forceinline__ void sts128_u32(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ uint2 lds64(const void *p) { return *reinterpret_cast<const uint2 *>(p); }
 __device__ __forceinline__ uint4 ldg128_cg(const void *p) {
   uint4 r;
@@ -260,6 +269,18 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint4 &v) {
                : "r"(taddr));
 }
 
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row
+// core groups 1024 bytes apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)(1) << 16;                         // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;      // stride byte offset
+  d |= (uint64_t)1 << 46;                           // version
+  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
+  return d;
+}
+
 // UMMA shared-memory descriptor, K-major operand WITHOUT swizzle: 8-row x
 // 16-byte core matrices (128 contiguous bytes), `lbo` bytes between core
 // matrices adjacent in K, `sbo` bytes between 8-row groups (sm_100 version 1).
@@ -301,6 +322,39 @@ __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// bf16x2(relu(lo), relu(hi)), round to nearest (the relu on the rounded value: identical)
+__device__ __forceinline__ uint32_t pack_relu_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// z = bf16(relu(f + g)) for 8 elements: f bf16x8, g as two float4 (elements 0-3, 4-7)
+__device__ __forceinline__ uint4 relu_add_bf16x8(uint4 f, float4 g0, float4 g1) {
+  uint4 o;
+  o.x = pack_relu_bf16x2(bf16_lo(f.x) + g0.x, bf16_hi(f.x) + g0.y);
+  o.y = pack_relu_bf16x2(bf16_lo(f.y) + g0.z, bf16_hi(f.y) + g0.w);
+  o.z = pack_relu_bf16x2(bf16_lo(f.z) + g1.x, bf16_hi(f.z) + g1.y);
+  o.w = pack_relu_bf16x2(bf16_lo(f.w) + g1.z, bf16_hi(f.w) + g1.w);
+  return o;
+}
+
+// as relu_add_bf16x8 with g as raw float4 words; the adds as FADD2 (f32x2)
+__device__ __forceinline__ uint32_t add_relu_pack(uint32_t fw, uint32_t g_lo, uint32_t g_hi) {
+  const uint64_t fv = ((uint64_t)(fw & 0xffff0000u) << 32) | (uint64_t)(fw << 16);
+  const uint64_t gv = ((uint64_t)g_hi << 32) | g_lo;
+  uint64_t sv;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(sv) : "l"(fv), "l"(gv));
+  return pack_relu_bf16x2(__uint_as_float((uint32_t)sv), __uint_as_float((uint32_t)(sv >> 32)));
+}
+__device__ __forceinline__ uint4 relu_add_bf16x8_2(uint4 f, uint4 g0, uint4 g1) {
+  uint4 o;
+  o.x = add_relu_pack(f.x, g0.x, g0.y);
+  o.y = add_relu_pack(f.y, g0.z, g0.w);
+  o.z = add_relu_pack(f.z, g1.x, g1.y);
+  o.w = add_relu_pack(f.w, g1.z, g1.w);
+  return o;
 }
 
 template <typename T> __device__ __forceinline__ float to_f32(T v);

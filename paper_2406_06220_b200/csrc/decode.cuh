@@ -71,7 +71,8 @@ enum {
   BAR_GATE = 12 + 2 * NSMAX, // (TG) gate batch complete (tcgen05.commit)
   BAR_MACK = 13 + 2 * NSMAX, // (TJ) MMA warp: command read (the command word may be reused)
   BAR_JOINT = 14 + 2 * NSMAX,// (TJ) joint MMAs complete (tcgen05.commit)
-  NBARS = 15 + 2 * NSMAX
+  BAR_SPEC = 15 + 2 * NSMAX, // (TJ) MMA warp: speculative copies issued, fbase / fcnt written
+  NBARS = 16 + 2 * NSMAX
 };
 enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3 };
 
@@ -120,8 +121,11 @@ __host__ __device__ inline bool tg_shape(bool bf, bool lstm, int H, int P, int C
 // holds both halves of vocabulary rows 16q .. 16q + 15.
 //   A: K-major, no swizzle: row r, 16-byte chunk c (K' 8c .. 8c+7) at
 //      (r / 8) * 5120 + c * 128 + (r % 8) * 16                      (80 KB)
-//   z: row k, chunk c of 80 -> half a = c / 40 at
-//      a * 20480 + (k / 8) * 5120 + (c % 40) * 128 + (k % 8) * 16   (40 KB)
+//   z: K-major, 128-byte swizzle (1024-byte aligned): row k, 16-byte chunk c
+//      of 80 (half a = c / 40, 64-element block kb = (c % 40) / 8, j = c % 8) at
+//      kb * 8192 + a * 4096 + (k / 8) * 1024 + (k % 8) * 128 + ((j ^ (k % 8)) * 16)
+//      so B row 32 a + k sits in 8-row group 4 a + k / 8 (SBO = 1024) and a
+//      warp storing 32 consecutive chunks of one row is bank-conflict free (40 KB)
 //   f rows in shared memory with a 1296-byte stride (bank-conflict-free
 //   8-row x 16-byte reads in build_z), one bulk copy per frame.
 //   TMEM columns [440, 504): D' (after the TG gate columns).
@@ -179,6 +183,7 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.hstride = (int)(align_up((size_t)P * 2, 128) + 64);
   size_t o = 0;
   L.off_b = o;    o = align_up(o + (size_t)L.tiles_max * 8 * 4, 128);
+  if (L.tj) o = align_up(o, 1024);   // the swizzled z operand: 1024-byte aligned (dynamic smem base is)
   L.off_z = o;    // joint operand rows; in the bf16 LSTM predictor: W_pred partials [NW][3][2][32] float4
   {
     size_t zb = L.tj ? (size_t)TJ_ZBYTES : (size_t)L.JRp * L.zstride;
@@ -292,6 +297,7 @@ struct Ctx {
   uint32_t tmem;              // TMEM base address (bf16 LSTM: W_hh tiles)
   int C, rank, tid, warp, lane, NW, NCT, g, q;
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
+  int vm0, nmain, vx0, nx;    // TJ: main rows [vm0, vm0 + nmain) (tensor core), extra rows [vx0, vx0 + nx) (CUDA cores)
   int u0, d0;                 // LSTM units / W_pred output dims owned
   int iw;                     // issuing warp for bulk copies (a warp without a joint tile if any)
   // Barrier phase bookkeeping, replicated in every consumer thread and packed
@@ -299,7 +305,7 @@ struct Ctx {
   // fbuf[X] outstanding), 4-5 xph (BAR_X+par phase), 6 hph (BAR_H/G/E phase),
   // 7 par (partial-key buffer parity); TG: 8 gate batch pending, 9 BAR_GATE
   // phase, 10 the gate pre-activations in TMEM are valid for this group;
-  // TJ: 11 BAR_JOINT phase.
+  // TJ: 11 BAR_JOINT phase, 12 BAR_SPEC phase, 13 speculative copies posted this round.
   uint32_t phs;
   uint32_t npost = 0;         // TJ, thread 0: commands posted to the MMA warp
   uint4 wpr[2][3][2];         // TJ LSTM: this warp's W_pred fragments (K blocks warp, warp + 10)
@@ -308,7 +314,10 @@ struct Ctx {
   __device__ __forceinline__ uint32_t xph(int X) const { return (phs >> (4 + X)) & 1u; }
   __device__ __forceinline__ uint32_t hph() const { return (phs >> 6) & 1u; }
   __device__ __forceinline__ int par() const { return (int)((phs >> 7) & 1u); }
-  __device__ __forceinline__ void flip_par() { phs ^= 1u << 7; }
+  __device__ __forceinline__ void flip_par() {
+    phs ^= 1u << 7;
+    if (phs & (1u << 13)) phs ^= (1u << 12) | (1u << 13);   // BAR_SPEC consumed (warp 0) this round
+  }
   unsigned long long ntile_c; // weight-ring tiles consumed so far (replicated)
   // optional timeline (debug builds with -DLL_TIMELINE, buffer from
   // LL_TIMELINE_PTR): clock64 of every warp at phase boundaries of the first
@@ -358,6 +367,13 @@ struct Ctx {
     const int base = NT / C, rem = NT % C;
     ntiles = base + (rank < rem ? 1 : 0);
     tile0 = rank * base + (rank < rem ? rank : rem);
+    if constexpr (TJ) {   // 64 rows per CTA on the tensor core; the rest (<= 8 per CTA) spread over the CTAs
+      const int NV = p.V1 + p.nD, nxr = NV > 64 * TJ_C ? (NV - 64 * TJ_C + TJ_C - 1) / TJ_C : 0;
+      vm0 = 64 * rank;
+      nmain = min(max(NV - vm0, 0), 64);
+      vx0 = 64 * TJ_C + nxr * rank;
+      nx = min(max(NV - vx0, 0), nxr);
+    }
     u0 = rank * upc();
     d0 = rank * dpc();
     iw = (BF && L.tiles_max < NW) ? NW - 1 : 0;
@@ -381,6 +397,11 @@ struct Ctx {
   __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
   __device__ uint8_t *zs() const { return sm + L.off_z; }
+  // TJ: byte offset of row k's 16-byte chunk c in the swizzled z operand
+  __device__ __forceinline__ static int zoff(int k, int c) {
+    const int a = c >= 40 ? 1 : 0, cc = c - 40 * a;
+    return (cc >> 3) * 8192 + a * 4096 + (k >> 3) * 1024 + (k & 7) * 128 + (((cc & 7) ^ (k & 7)) << 4);
+  }
   __device__ uint8_t *fbuf(int X) const {
     if constexpr (TJ) return sm + L.off_f;   // one buffer (the bookkeeping of both halves is kept)
     else return sm + L.off_f + (size_t)X * p.R * p.WF * Hd() * sizeof(T);
@@ -440,18 +461,18 @@ struct Ctx {
   //   MCMD_JOINT: D' = A(W_out slice, K-folded) . z^T (SS mode)  -> BAR_JOINT
   __device__ void mma_warp_loop() {
     if constexpr (TJ) {
-      if (lane != 0) return;
       constexpr uint32_t ID_MAIN = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TG_NH >> 3) << 17) | (8u << 24);
       constexpr uint32_t ID_FOLD = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(4 * TG_NH >> 3) << 17) | (8u << 24);
       constexpr uint32_t ID_J = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | (8u << 24);
       const uint32_t hb = smem_u32(hbuf()), za = smem_u32(zs()), wa = smem_u32(sm + L.off_wa);
       for (uint32_t ph = 0;; ph ^= 1u) {
         mbar_wait(bar(BAR_GQ), ph);
-        const int cmd = rs.mcmd;
-        mbar_arrive(bar(BAR_MACK));
+        const int word = rs.mcmd, cmd = word & 0xFF;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(BAR_MACK));
         if (cmd == MCMD_EXIT) break;
         tc_fence_after();
-        if (cmd == MCMD_GATES) {
+        if (lane == 0 && cmd == MCMD_GATES) {
 #pragma unroll
           for (int kk = 0; kk < TG_P / 16; ++kk) {   // K = 16 per MMA: h chunks 2kk, 2kk + 1
             const int c = 2 * kk;
@@ -464,14 +485,20 @@ struct Ctx {
             umma_ts(tmem + TG_COL_DFOLD, tmem + TG_COL_FOLD + (uint32_t)(8 * kk), db, ID_FOLD, kk > 0);
           }
           umma_commit(bar(BAR_GATE));
-        } else {
+        } else if (lane == 0) {
 #pragma unroll
           for (int kk = 0; kk < TJ_H / 32; ++kk) {   // K' = 320: A / B chunks 2kk, 2kk + 1
             const uint64_t da = umma_desc_ns(wa + (uint32_t)(kk * 256), 128, TJ_GRP);
-            const uint64_t db = umma_desc_ns(za + (uint32_t)(kk * 256), 128, TJ_GRP);
+            const uint64_t db = umma_desc_sw128(za + (uint32_t)((kk >> 2) * 8192 + (kk & 3) * 32));
             umma_ss(tmem + TJ_COL_D, da, db, ID_J, kk > 0);
           }
           umma_commit(bar(BAR_JOINT));
+        }
+        __syncwarp();
+        if (cmd == MCMD_JOINT && (word & 0x100)) {   // next windows, while the MMAs run
+          spec_copies((word >> 9) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(BAR_SPEC));
         }
       }
     }
@@ -492,6 +519,15 @@ struct Ctx {
     const int nrows = L.tiles_max * 8;
     const int V1 = p.V1, NV = p.V1 + p.nD, H = Hd();
     float *bs = bsl();
+    if constexpr (TJ) {   // bias: [0, 64) main rows, [64, 64 + nx) extra rows
+      for (int r = tid; r < 72; r += NCT) {
+        const int v = r < 64 ? vm0 + r : vx0 + (r - 64);
+        float bv = 0.f;
+        if (r < 64 ? r < nmain : r - 64 < nx)
+          bv = v < V1 ? to_f32(((const T *)p.b_out)[v]) : to_f32(((const T *)p.b_dur)[v - V1]);
+        bs[r] = bv;
+      }
+    } else
     for (int r = tid; r < nrows; r += NCT) {
       const int v = tile0 * 8 + r;
       float bv = 0.f;
@@ -502,10 +538,9 @@ struct Ctx {
     if constexpr (TJ) {
       // A operand: the first 8 tiles (64 rows), row r = 32 (vl / 16) + 16 a + vl % 16
       // holds local row vl's K-half a; the 9th tile (if any) for mma.sync
-      const int nmain = ntiles < 8 ? ntiles * 8 : 64;
       for (int i = tid; i < 128 * (TJ_H / 16); i += NCT) {
         const int r = i / (TJ_H / 16), c = i % (TJ_H / 16);
-        const int vl = 16 * (r >> 5) + (r & 15), a = (r >> 4) & 1, v = tile0 * 8 + vl;
+        const int vl = 16 * (r >> 5) + (r & 15), a = (r >> 4) & 1, v = vm0 + vl;
         uint4 x = make_uint4(0, 0, 0, 0);
         if (vl < nmain && v < NV) {
           const bf16 *src = v < V1 ? (const bf16 *)p.w_out + (size_t)v * TJ_H : (const bf16 *)p.w_dur + (size_t)(v - V1) * TJ_H;
@@ -515,9 +550,9 @@ struct Ctx {
       }
       for (int i = tid; i < 8 * (TJ_H / 8); i += NCT) {
         const int r = i / (TJ_H / 8), c = i % (TJ_H / 8);
-        const int vl = 64 + r, v = tile0 * 8 + vl;
+        const int v = vx0 + r;
         uint4 x = make_uint4(0, 0, 0, 0);
-        if (vl < ntiles * 8 && v < NV) {
+        if (r < nx) {
           const bf16 *src = v < V1 ? (const bf16 *)p.w_out + (size_t)v * TJ_H : (const bf16 *)p.w_dur + (size_t)(v - V1) * TJ_H;
           x = ldg128_nc(src + c * 8);
         }
@@ -551,6 +586,58 @@ struct Ctx {
     phs ^= 1u << X;
     phs &= ~(1u << (2 + X));
   }
+  // Speculative next windows (every scanning row keeps scanning): frames
+  // t + W .. into fbuf[X].  TJ: the MMA warp issues the copies right after the
+  // joint MMAs (the command posted by joint_keys carries X); every consumer
+  // thread records the pending copy here.
+  int spec_x = -1;
+  __device__ void spec_issue(int X) {
+    if constexpr (TJ) {
+      if (fpend(X)) wait_f(X);
+      if (fpend(X ^ 1)) wait_f(X ^ 1);
+      spec_x = X;
+      phs |= (1u << (2 + X)) | (1u << 13);
+    } else {
+      issue_f(X, true);
+    }
+  }
+  // MMA warp (all lanes): the copies of a posted speculative request; lane =
+  // scanning slot.  fbase / fcnt are written before the (releasing) expect_tx
+  // arrive, so a consumer that waited on BAR_F + X sees them.
+  __device__ void spec_copies(int X) {
+    const int n = rs.nscan;
+    uint32_t bytes = 0;
+    int s = 0, base = 0, cnt = 0;
+    if (lane < n) {
+      s = rs.slist[lane];
+      base = rs.t[s] + p.W;
+      cnt = rs.L[s] - base;
+      if (cnt > p.WF) cnt = p.WF;
+      if (cnt < 0) cnt = 0;
+      rs.fbase[X][s] = base;
+      rs.fcnt[X][s] = cnt;
+      bytes = cnt > 0 ? (p.fmap_ok ? (uint32_t)(p.WF * TJ_FROW) : (uint32_t)(cnt * TJ_H * 2)) : 0u;
+    }
+    uint32_t tot = bytes;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(bar(BAR_F + X), tot);
+    __syncwarp();
+    if (lane < n && cnt > 0) {
+      if (p.fmap_ok) {
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                smem_u32(fbuf(X) + (size_t)s * L.fss)),
+            "l"(&p.fmap), "r"(0), "r"(0), "r"(rs.b[s] * p.T_max + base), "r"(smem_u32(bar(BAR_F + X)))
+            : "memory");
+      } else {
+        const uint8_t *src = (const uint8_t *)p.f + ((size_t)rs.b[s] * p.T_max + base) * (TJ_H * 2);
+        for (int i = 0; i < cnt; ++i)
+          bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * TJ_FROW, src + (size_t)i * TJ_H * 2, TJ_H * 2, bar(BAR_F + X));
+      }
+    }
+  }
+
   __device__ void issue_f(int X, bool spec, const int *list = nullptr, int nlist = 0) {
     if (fpend(X)) wait_f(X);  // drain a stale speculative copy first
     if (TJ && fpend(X ^ 1)) wait_f(X ^ 1);   // one buffer behind both halves
@@ -636,40 +723,39 @@ struct Ctx {
     const int H = Hd(), W = p.W;
     const int nz = rs.nz;
     if constexpr (TJ) {
-      // warps 0-7: 8-row group G = warp % 4, K-half a = warp / 4; lane = (row r,
-      // chunk phase cq): 8 rows x 16 bytes per chunk (conflict-free stores)
-      const int G = warp & 3, a = warp >> 2;
-      if (warp < 8 && 8 * G < nz) {
-        const int r = lane & 7, cq = lane >> 3, k = 8 * G + r;
-        const bool live = k < nz;
-        const uint8_t *fr = fbuf(X) + (size_t)(live ? rs.zsrc[k] : 0) * 2;
-        const int s = live ? rs.zdst[k] / W : 0;
-        const float4 *gr0 = reinterpret_cast<const float4 *>(gs() + (size_t)s * TJ_H);   // plane 0
-        const float4 *gr1 = gr0 + TJ_H / 8;                                               // plane 1
-        uint8_t *zr = zs() + a * TJ_ZHALF + G * TJ_GRP + r * 16;
+      // work unit = (scanning slot, 16-chunk block b): lane = (row parity h =
+      // lane / 16, chunk 16b + lane % 16): g once, then window rows h, h + 2, ..
+      // (compact rows zbeg + j).  Units are dealt to warps so that the four
+      // sub-partitions (3, 3, 2, 2 consumer warps) get equal shares.
+      (void)nz;
+      constexpr int NBLK = TJ_H / 8 / 16;   // 5
+      const int nu = rs.nscan * NBLK;
+      const int pos = (int)((0x9832761054ull >> (4 * warp)) & 0xF);   // warps 2,3,6,7,0,1,4,5,8,9 -> 0..9
+      const int h = lane >> 4, c = (lane & 15);
+      const uint32_t fb = smem_u32(fbuf(X)), zb = smem_u32(zs()), gb = smem_u32(gs());
+      for (int u = pos; u < nu; u += NW) {
+        const int s = rs.slist[u / NBLK], cc = 16 * (u % NBLK) + c;
+        const int kb0 = rs.zbeg[s], cnt = rs.zcnt[s];
+        // per-lane part of the swizzled z address of chunk cc, and its 16-byte slot j
+        const int a = cc >= 40 ? 1 : 0, c40 = cc - 40 * a;
+        const uint32_t zl = zb + (uint32_t)((c40 >> 3) * 8192 + a * 4096);
+        const uint32_t jx = (uint32_t)((c40 & 7) << 4);
+        const uint4 g0 = lds128_u32(gb + (uint32_t)(s * TJ_H * 4 + cc * 16));
+        const uint4 g1 = lds128_u32(gb + (uint32_t)(s * TJ_H * 4 + TJ_H * 2 + cc * 16));
+        uint4 f[4];
+        int kk[4];
 #pragma unroll
-        for (int i0 = 0; i0 < 10; i0 += 5) {
-          uint4 fv[5];
-          float4 ga[5], gb[5];
+        for (int i = 0; i < 4; ++i) {
+          const int j = h + 2 * i;
+          kk[i] = kb0 + j;
+          if (j < cnt) f[i] = lds128_u32(fb + (uint32_t)(rs.zsrc[kb0 + j] * 2 + cc * 16));
+        }
 #pragma unroll
-          for (int u = 0; u < 5; ++u) {
-            const int c = 40 * a + 4 * (i0 + u) + cq;
-            fv[u] = lds128(fr + c * 16);
-            ga[u] = gr0[c];
-            gb[u] = gr1[c];
-          }
-          if (live) {
-#pragma unroll
-            for (int u = 0; u < 5; ++u) {
-              const uint4 f = fv[u];
-              const float4 g0 = ga[u], g1 = gb[u];
-              uint4 o;
-              o.x = pack_bf16x2(fmaxf(bf16_lo(f.x) + g0.x, 0.f), fmaxf(bf16_hi(f.x) + g0.y, 0.f));
-              o.y = pack_bf16x2(fmaxf(bf16_lo(f.y) + g0.z, 0.f), fmaxf(bf16_hi(f.y) + g0.w, 0.f));
-              o.z = pack_bf16x2(fmaxf(bf16_lo(f.z) + g1.x, 0.f), fmaxf(bf16_hi(f.z) + g1.y, 0.f));
-              o.w = pack_bf16x2(fmaxf(bf16_lo(f.w) + g1.z, 0.f), fmaxf(bf16_hi(f.w) + g1.w, 0.f));
-              *reinterpret_cast<uint4 *>(zr + (4 * (i0 + u) + cq) * 128) = o;
-            }
+        for (int i = 0; i < 4; ++i) {
+          if (h + 2 * i < cnt) {
+            const int k = kk[i], r = k & 7;
+            const uint32_t za = zl + (uint32_t)((k >> 3) * 1024 + r * 128) + (jx ^ (uint32_t)(r << 4));
+            sts128_u32(za, relu_add_bf16x8_2(f[i], g0, g1));
           }
         }
       }
@@ -810,8 +896,38 @@ struct Ctx {
       }
     }
   }
+  template <int NK>
+  __device__ __forceinline__ static void bfly8_max(uint64_t (&x)[NK], int lane) {
+#pragma unroll
+    for (int w = 4; w >= 1; w >>= 1) {
+      const bool b = (lane & w) != 0;
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const uint64_t lo = x[i], hi = x[i + w];
+        const uint64_t r = shfl_xor_u64(b ? lo : hi, w);
+        x[i] = umax64(b ? hi : lo, r);
+      }
+    }
+    x[0] = umax64(x[0], shfl_xor_u64(x[0], 8));
+  }
+  template <int NK>
+  __device__ __forceinline__ static void bfly8_lse(uint64_t (&x)[NK], int lane) {
+#pragma unroll
+    for (int w = 4; w >= 1; w >>= 1) {
+      const bool b = (lane & w) != 0;
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const uint64_t lo = x[i], hi = x[i + w];
+        const uint64_t r = shfl_xor_u64(b ? lo : hi, w);
+        x[i] = lse_combine(b ? hi : lo, r);
+      }
+    }
+    // the two 8-lane groups, combined in a fixed (group 0, group 1) order on both sides
+    const uint64_t o = shfl_xor_u64(x[0], 8);
+    x[0] = (lane & 8) ? lse_combine(o, x[0]) : lse_combine(x[0], o);
+  }
   __device__ __forceinline__ int nkw() const {
-    if constexpr (TJ) return ntiles > 8 ? TJ_NKW : TJ_NKW - 1;
+    if constexpr (TJ) return nx > 0 ? TJ_NKW : TJ_NKW - 1;
     else return NW;
   }
 
@@ -821,89 +937,41 @@ struct Ctx {
   __device__ void joint_keys_tj(int nrows_valid, float *logits, int row_base) {
     const int V1 = p.V1, NV = p.V1 + p.nD;
     uint64_t *wk = wkey();
-    if (tid == 0) post(MCMD_JOINT);
-    if (warp < 4) {
+    if (tid == 0) post(MCMD_JOINT | (spec_x >= 0 ? 0x100 | (spec_x << 9) : 0));
+    spec_x = -1;
+    // extra rows (<= 8 per CTA, rows vx0 ..): after the MMAs (the tensor pipe and
+    // shared memory are busy with them until then), warps 8 and 9 take joint
+    // rows 0-15 / 16-31 on mma.sync: z rows as the m16 A operand (ldmatrix from
+    // the swizzled z), the extra weight rows as the n8 B operand, 4 chains
+    if ((warp == 8 || (warp == 9 && rs.nz > 16)) && nx > 0) {
+      const int m0 = 16 * (warp - 8);
       mbar_wait(bar(BAR_JOINT), jph());
-      tl_round_(12);
-      tc_fence_after();
-      uint32_t lo[32], hi[32];
-      const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + TJ_COL_D;
-      tmem_ld32(ta, lo);
-      tmem_ld32(ta + 32, hi);
-      tmem_wait_ld();
-      const int a = lane >> 4, vl = 16 * warp + (lane & 15), v = tile0 * 8 + vl;
-      const int nmain = ntiles < 8 ? ntiles * 8 : 64;
-      const int kind = (vl < nmain && v < NV) ? (v < V1 ? 1 : 2) : 0;
-      const float bias = bsl()[vl];
-      const bool dmain = is_tdt() && tile0 * 8 + nmain > V1;   // duration rows among the main rows
-      // logits of joint rows k = 16a + j: K-half partials of lanes l and l ^ 16 (lo + hi)
-      uint64_t tk[16], dk[16];
-      [[maybe_unused]] uint64_t tl[16], dl[16];
+      float acc[4][4];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t send = a ? hi[j] : lo[j + 16];
-        const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 16));
-        const float val = (a ? recv + __uint_as_float(hi[16 + j]) : __uint_as_float(lo[j]) + recv) + bias;
-        const int k = 16 * a + j;
-        if (logits != nullptr && kind && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v] = val;
-        tk[j] = kind == 1 ? pack_key(val, v) : 0ull;
-        dk[j] = kind == 2 ? pack_key(val, v - V1) : 0ull;
-        if constexpr (SC) {
-          tl[j] = kind == 1 ? lse_pack(val, 1.f) : lse_empty();
-          dl[j] = kind == 2 ? lse_pack(val, 1.f) : lse_empty();
-        }
-      }
-      bfly_max(tk, lane);
-      if (dmain) bfly_max(dk, lane);
-      if constexpr (SC) {
-        bfly_lse(tl, lane);
-        if (dmain) bfly_lse(dl, lane);
-      }
-      tl_round_(13);
-      if (lane < L.JR) {
-        uint64_t *dst = wk + ((size_t)warp * L.JR + lane) * wks();
-        uint4 e;
-        const uint64_t d0 = dmain ? dk[0] : 0ull;
-        e.x = (uint32_t)tk[0]; e.y = (uint32_t)(tk[0] >> 32); e.z = (uint32_t)d0; e.w = (uint32_t)(d0 >> 32);
-        *reinterpret_cast<uint4 *>(dst) = e;
-        if constexpr (SC) {
-          const uint64_t l0 = dmain ? dl[0] : lse_empty();
-          uint4 f;
-          f.x = (uint32_t)tl[0]; f.y = (uint32_t)(tl[0] >> 32); f.z = (uint32_t)l0; f.w = (uint32_t)(l0 >> 32);
-          *reinterpret_cast<uint4 *>(dst + 2) = f;
-        }
-      }
-    } else if ((warp == 4 || (warp == 5 && rs.nz > 16)) && ntiles > 8) {
-      // extra tile (local rows 64..71): z rows as the m16 A operand (ldmatrix from
-      // the B' layout), the 8 weight rows as the n8 B operand
-      const int m0 = 16 * (warp - 4);
-      const uint8_t *wx = sm + L.off_wx;
-      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
       const int mi = lane >> 3, rr = lane & 7, kz = m0 + 8 * (mi & 1) + rr;
-      const uint32_t zb = smem_u32(zs()) + (uint32_t)((kz >> 3) * TJ_GRP + (kz & 7) * 16);
+      const uint32_t zb = smem_u32(zs()), wb = smem_u32(sm + L.off_wx) + (uint32_t)(g * TJ_XROW + 4 * q);
 #pragma unroll 8
       for (int kk = 0; kk < TJ_H / 16; ++kk) {
         const int c = 2 * kk + (mi >> 1);
-        uint32_t a0, a1, a2, a3;
-        ldmatrix_x4(zb + (uint32_t)((c / 40) * TJ_ZHALF + (c % 40) * 128), a0, a1, a2, a3);
-        const uint8_t *wr = wx + g * TJ_XROW + (16 * kk + 2 * q) * 2;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t *>(wr), b1 = *reinterpret_cast<const uint32_t *>(wr + 16);
-        mma_bf16_16816(acc[kk & 1], a0, a1, a2, a3, b0, b1);
+        uint32_t a0, a1, a2, a3, b0, b1;
+        ldmatrix_x4(zb + (uint32_t)zoff(kz, c), a0, a1, a2, a3);
+        asm volatile("ld.shared.u32 %0, [%2];\n ld.shared.u32 %1, [%2 + 16];" : "=r"(b0), "=r"(b1) : "r"(wb + (uint32_t)(32 * kk)));
+        mma_bf16_16816(acc[kk & 3], a0, a1, a2, a3, b0, b1);
       }
-      tl_round_(14);
       uint64_t tk2[2] = {0, 0}, dk2[2] = {0, 0};
       [[maybe_unused]] uint64_t tl2[2] = {lse_empty(), lse_empty()}, dl2[2] = {lse_empty(), lse_empty()};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int vl = 64 + 2 * q + (e & 1), v = tile0 * 8 + vl, hr = e >> 1;
-        if (vl < ntiles * 8 && v < NV) {
-          const float val = (acc[0][e] + acc[1][e]) + bsl()[vl];
+        const int i = 2 * q + (e & 1), v2 = vx0 + i, hr = e >> 1;
+        if (i < nx) {
+          const float val = ((acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e])) + bsl()[64 + i];
           const int k = m0 + g + 8 * hr;
-          if (logits != nullptr && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v] = val;
-          if (v < V1) tk2[hr] = umax64(tk2[hr], pack_key(val, v));
-          else dk2[hr] = umax64(dk2[hr], pack_key(val, v - V1));
+          if (logits != nullptr && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v2] = val;
+          if (v2 < V1) tk2[hr] = umax64(tk2[hr], pack_key(val, v2));
+          else dk2[hr] = umax64(dk2[hr], pack_key(val, v2 - V1));
           if constexpr (SC) {
-            if (v < V1) tl2[hr] = lse_combine(tl2[hr], lse_pack(val, 1.f));
+            if (v2 < V1) tl2[hr] = lse_combine(tl2[hr], lse_pack(val, 1.f));
             else dl2[hr] = lse_combine(dl2[hr], lse_pack(val, 1.f));
           }
         }
@@ -914,14 +982,15 @@ struct Ctx {
         for (int o = 1; o <= 2; o <<= 1) {
           tk2[hr] = umax64(tk2[hr], shfl_xor_u64(tk2[hr], o));
           dk2[hr] = umax64(dk2[hr], shfl_xor_u64(dk2[hr], o));
-          if constexpr (SC) {
-            tl2[hr] = lse_combine(tl2[hr], shfl_xor_u64(tl2[hr], o));
-            dl2[hr] = lse_combine(dl2[hr], shfl_xor_u64(dl2[hr], o));
+          if constexpr (SC) {   // fixed order: the lower lane's subset first
+            const uint64_t ot = shfl_xor_u64(tl2[hr], o), od = shfl_xor_u64(dl2[hr], o);
+            tl2[hr] = (lane & o) ? lse_combine(ot, tl2[hr]) : lse_combine(tl2[hr], ot);
+            dl2[hr] = (lane & o) ? lse_combine(od, dl2[hr]) : lse_combine(dl2[hr], od);
           }
         }
         const int k = m0 + g + 8 * hr;
         if (q == 0 && k < L.JR) {
-          uint64_t *dst = wk + ((size_t)4 * L.JR + k) * wks();
+          uint64_t *dst = wk + ((size_t)4 * L.JR + k) * wks();   // partial 4: the extra rows
           uint4 e;
           e.x = (uint32_t)tk2[hr]; e.y = (uint32_t)(tk2[hr] >> 32); e.z = (uint32_t)dk2[hr]; e.w = (uint32_t)(dk2[hr] >> 32);
           *reinterpret_cast<uint4 *>(dst) = e;
@@ -930,6 +999,63 @@ struct Ctx {
             f.x = (uint32_t)tl2[hr]; f.y = (uint32_t)(tl2[hr] >> 32); f.z = (uint32_t)dl2[hr]; f.w = (uint32_t)(dl2[hr] >> 32);
             *reinterpret_cast<uint4 *>(dst + 2) = f;
           }
+        }
+      }
+    }
+    if (warp < 8) {
+      // warp w: lane quarter q = w % 4 (vocabulary rows 16q .. 16q + 15, both
+      // K-halves), joint-row half h = w / 4 (rows 16h .. 16h + 15)
+      const int qd = warp & 3, h = warp >> 2;
+      mbar_wait(bar(BAR_JOINT), jph());
+      tl_round_(12);
+      tc_fence_after();
+      uint32_t lo[16], hi[16];
+      const uint32_t ta = tmem + ((uint32_t)(32 * qd) << 16) + TJ_COL_D + 16u * h;
+      tmem_ld16(ta, lo);
+      tmem_ld16(ta + 32, hi);
+      tmem_wait_ld();
+      const int a = lane >> 4, vl = 16 * qd + (lane & 15), v = vm0 + vl;
+      const int kind = vl < nmain ? (v < V1 ? 1 : 2) : 0;
+      const float bias = bsl()[vl];
+      const bool dmain = is_tdt() && vm0 + nmain > V1;   // duration rows among the main rows
+      // joint rows k = 16h + 8a + i (i < 8): K-half partials of lanes l, l ^ 16 (lo + hi)
+      uint64_t tk[8], dk[8];
+      [[maybe_unused]] uint64_t tl[8], dl[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t send = a ? hi[i] : lo[i + 8];
+        const float recv = __uint_as_float(__shfl_xor_sync(0xffffffffu, send, 16));
+        const float val = (a ? recv + __uint_as_float(hi[i + 8]) : __uint_as_float(lo[i]) + recv) + bias;
+        const int k = 16 * h + 8 * a + i;
+        if (logits != nullptr && kind && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v] = val;
+        tk[i] = kind == 1 ? pack_key(val, v) : 0ull;
+        dk[i] = kind == 2 ? pack_key(val, v - V1) : 0ull;
+        if constexpr (SC) {
+          tl[i] = kind == 1 ? lse_pack(val, 1.f) : lse_empty();
+          dl[i] = kind == 2 ? lse_pack(val, 1.f) : lse_empty();
+        }
+      }
+      // 8 columns over the 16 lanes of the half: xor 4, 2, 1 keep one column
+      // (l & 7), xor 8 merges the two 8-lane groups
+      bfly8_max(tk, lane);
+      if (dmain) bfly8_max(dk, lane);
+      if constexpr (SC) {
+        bfly8_lse(tl, lane);
+        if (dmain) bfly8_lse(dl, lane);
+      }
+      tl_round_(13);
+      const int kc = 16 * h + 8 * a + (lane & 7);
+      if ((lane & 8) == 0 && kc < L.JR) {
+        uint64_t *dst = wk + ((size_t)qd * L.JR + kc) * wks();
+        uint4 e;
+        const uint64_t d0 = dmain ? dk[0] : 0ull;
+        e.x = (uint32_t)tk[0]; e.y = (uint32_t)(tk[0] >> 32); e.z = (uint32_t)d0; e.w = (uint32_t)(d0 >> 32);
+        *reinterpret_cast<uint4 *>(dst) = e;
+        if constexpr (SC) {
+          const uint64_t l0 = dmain ? dl[0] : lse_empty();
+          uint4 f;
+          f.x = (uint32_t)tl[0]; f.y = (uint32_t)(tl[0] >> 32); f.z = (uint32_t)l0; f.w = (uint32_t)(l0 >> 32);
+          *reinterpret_cast<uint4 *>(dst + 2) = f;
         }
       }
     }
@@ -1171,6 +1297,9 @@ struct Ctx {
   // PAPER.md:213).  decide() also rebuilds the scanning list and checks the
   // speculative window.
   __device__ int resolve_rows_w0() {
+    // TJ: the MMA warp read this round's row state for the speculative copies
+    // and wrote their fbase / fcnt: done before warp 0 changes / reads them
+    if (TJ && (phs & (1u << 13))) mbar_wait(bar(BAR_SPEC), (phs >> 12) & 1u);
     const uint64_t *pt = part(par());
     const int nz = rs.nz;
     int dec = 0;
@@ -2374,7 +2503,7 @@ template <typename T, int PRED, int KR, int HC = 0, int PC = 0, int CC = 0, int 
           int SC = 0>
 __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H && PC == TJ_H && CC == TJ_C ? 32 : 0), 1)
     decode_kernel(const __grid_constant__ DecodeParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
   using CtxT = Ctx<T, KR, HC, PC, CC, TM, SC>;
@@ -2391,6 +2520,14 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
   __shared__ unsigned s_cnt[SC_N];
   if (tid < SC_N) s_cnt[tid] = 0;
   const bool t0 = tid == 0;
+  if constexpr (MMAW) {   // the swizzled operands need a 1024-byte aligned base (uniform: every CTA alike)
+    if (smem_u32(smem) & 1023u) {
+      if (tid == 0 && rank == 0) atomicOr(p.status, 4);
+      return;
+    }
+    if (warp == MAX_NW - 1 && lane == 0 && p.fmap_ok)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.fmap) : "memory");
+  }
 
   __shared__ uint32_t s_tmem;
   cx.init_barriers();
@@ -2624,12 +2761,17 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             cx.plan_z(cur);
             cx.sync();
             cx.tl_round_bar(1);
+#ifdef LL_EXP1
+            cx.gate_wait();   // experiment: no gate batch in flight during build_z
+            cx.sync();
+            cx.tl_round_bar(1);
+#endif
             cx.build_z(cur);
             cx.tl_round_(2);
             cx.sync();
             cx.tl_round_bar(15);
             if (p.spec_prefetch) {
-              cx.issue_f(cur ^ 1, true);
+              cx.spec_issue(cur ^ 1);
               have_spec = true;
             }
             cx.tl_round_bar(3);
@@ -2716,7 +2858,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
           cx.tl_round_(2);
           cx.sync();
           // speculative: a row whose window is all blank needs the next window
-          if (p.spec_prefetch) cx.issue_f(cur ^ 1, true);
+          if (p.spec_prefetch) cx.spec_issue(cur ^ 1);
           LL_PHASE(2);
           cx.tl_round_bar(3);
           cx.joint_keys((rs.nz + 15) / 16, 0, nullptr, 0);

@@ -47,18 +47,6 @@ __device__ __forceinline__ bool tile_has_rows(const TcGemmArgs &a, int m0, int n
   return false;
 }
 
-// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row
-// core groups 1024 bytes apart (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
-  d |= (uint64_t)(1) << 16;                         // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;      // stride byte offset
-  d |= (uint64_t)1 << 46;                           // version
-  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
-  return d;
-}
-
 // Instruction descriptor: D fp32, A/B bf16, both K-major, N = 128, M = 128.
 constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
                               ((uint32_t)(TC_BM >> 4) << 24);

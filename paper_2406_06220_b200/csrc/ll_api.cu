@@ -778,6 +778,7 @@ ll_status ll_sync(void *workspace, ll_stream stream) {
   if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return LL_ERR_CUDA;
   int status = 0;
   if (cudaMemcpy(&status, workspace, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return LL_ERR_CUDA;
+  if (status & 4) return LL_ERR_CUDA;        // internal: misaligned shared-memory operand base
   if (status & 2) return LL_ERR_CAPACITY;
   if (status & 1) return LL_ERR_INVALID_ARGUMENT;
   return LL_OK;

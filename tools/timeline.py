@@ -12,7 +12,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2406_06220_b200 import build as llbuild
 from paper_2406_06220_b200 import ll
-ll.LIB_PATH = llbuild.build(variant="timeline")   # timeline hooks compiled in
+_exp = [a[2:] for a in sys.argv if a.startswith("--exp")]   # --exp1 -> variant timeline_exp1 (-DLL_EXP1)
+ll.LIB_PATH = llbuild.build(variant="timeline" + "".join("_" + e for e in _exp))   # timeline hooks compiled in
 TL_N, TL_PH, NW = 128, 16, 10
 buf = torch.zeros(2 * TL_N * TL_PH * NW, dtype=torch.int64, device="cuda")
 ll.ll_set_options(ll.options(timeline=buf.data_ptr()).opts)   # this thread, for every decode below
@@ -60,7 +61,7 @@ if "--tj" in sys.argv:   # the tcgen05 joint: stamps 11 (build_z before its prox
            ["", "wait_f/plan (+sync)", "build_z", "proxy fence", "sync", "spec issue", "joint MMA (post..done)",
             "epilogue TMEM+bfly (w0-3)", "epilogue end (all)", "exchange send", "exchange wait", "resolve", "sync (bar)",
             "decide", "sync+reload (bar)"])
-    report(0, "extra tile (warps 4-5)", [3, 14], ["", "mma.sync chain"])
+    
 else:
     report(0, "joint rounds", list(range(11)),
            ["", "wait_f/plan (+sync)", "build_z", "sync (bar)", "spec issue + joint", "exchange send",
