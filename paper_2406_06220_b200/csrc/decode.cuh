@@ -182,7 +182,7 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.zstride = bf ? (int)(align_up((size_t)K * 2, 128) + 64) : K * 4;
   L.hstride = (int)(align_up((size_t)P * 2, 128) + 64);
   size_t o = 0;
-  L.off_b = o;    o = align_up(o + (size_t)L.tiles_max * 8 * 4, 128);
+  L.off_b = o;    o = align_up(o + (size_t)(L.tiles_max * 8 + 48) * 4, 128);   // joint bias slice (+ TG: b_pred slice at 72)
   if (L.tj) o = align_up(o, 1024);   // the swizzled z operand: 1024-byte aligned (dynamic smem base is)
   L.off_z = o;    // joint operand rows; in the bf16 LSTM predictor: W_pred partials [NW][3][2][32] float4
   {
@@ -519,7 +519,9 @@ struct Ctx {
     const int nrows = L.tiles_max * 8;
     const int V1 = p.V1, NV = p.V1 + p.nD, H = Hd();
     float *bs = bsl();
-    if constexpr (TJ) {   // bias: [0, 64) main rows, [64, 64 + nx) extra rows
+    if constexpr (TJ) {   // bias: [0, 64) main rows, [64, 64 + nx) extra rows; [72, 72 + 40) b_pred slice (LSTM)
+      if (p.b_pred != nullptr && p.w_hh != nullptr)
+        for (int r = tid; r < TG_UPC; r += NCT) bs[72 + r] = to_f32(((const T *)p.b_pred)[d0 + r]);
       for (int r = tid; r < 72; r += NCT) {
         const int v = r < 64 ? vm0 + r : vx0 + (r - 64);
         float bv = 0.f;
@@ -714,6 +716,33 @@ struct Ctx {
       rs.zcnt[s] = __popc((m >> b0) & ((1u << W) - 1u));
     }
     if (lane == 0) rs.nz = __popc(m);
+  }
+
+  // TJ tick schedule (warp 0, lane = slot): the next round's plan, made when
+  // the round's decisions are taken.  Every row that scans in the next round
+  // has its window at base = t (a continuing row's speculative window starts
+  // at t, every other row is reloaded at t), so frame j of slot s is f row j of
+  // its fbuf slot: the plan depends only on (t, L) per slot.
+  __device__ void plan_next_tj(bool scan_next, int t, int Ls) {
+    const int W = p.W;
+    int cnt = 0;
+    if (scan_next) cnt = min(W, Ls - t);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int beg = incl - cnt;
+    if (lane < p.R) {
+      rs.zbeg[lane] = beg;
+      rs.zcnt[lane] = cnt;
+    }
+    for (int j = 0; j < cnt; ++j) {
+      rs.zsrc[beg + j] = (lane * L.fss + j * TJ_FROW) / 2;
+      rs.zdst[beg + j] = lane * W + j;
+    }
+    if (lane == 31) rs.nz = incl;
   }
 
   // z[jr] = ReLU(f[b_s, t_s + j] + g_s) for the live joint rows.  Other joint
@@ -1476,6 +1505,7 @@ struct Ctx {
       rs.ready = ms == 0u;
       *algevals += (unsigned)tot;
     }
+    if constexpr (TJ) plan_next_tj(inr && act && (scan || needp), t, Ls);
     __syncwarp();
     if (eprime && mp != 0u) issue_eprime(rs.plist, __popc(mp));
   }
@@ -1597,6 +1627,7 @@ struct Ctx {
       rs.ready = ms == 0u;
       *algevals += (unsigned)tot;
     }
+    if constexpr (TJ) plan_next_tj(inr && act && (scan || needp), t, Ls);
     __syncwarp();
     if (eprime && mp != 0u) issue_eprime(rs.plist, __popc(mp));
   }
@@ -2087,6 +2118,17 @@ struct Ctx {
     }
     float acc[3][NB][4];
     wpred_partial<NB>(acc, hrow);
+    if constexpr (TG) {   // (NB = 1) partials as P[warp][row i][dim d] (row stride 44: conflict-free)
+      float *P = reinterpret_cast<float *>(zs()) + warp * 8 * 44;
+#pragma unroll
+      for (int t = 0; t < 3; ++t)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int d = 16 * t + g + 8 * (e >> 1), i = 2 * q + (e & 1);
+          if (d < TG_UPC) P[i * 44 + d] = acc[t][0][e];
+        }
+      return;
+    }
     float4 *wp = reinterpret_cast<float4 *>(zs());
 #pragma unroll
     for (int t = 0; t < 3; ++t)
@@ -2241,6 +2283,33 @@ struct Ctx {
       const int nrows = min(16, n - nb0 * 8);
       const int D4 = dpc() / 4;
       const float4 *wp = reinterpret_cast<const float4 *>(zs());
+      if constexpr (TG) {   // one thread per (row, 4 dims): 10 float4 partials in a fixed warp order
+        if (tid < nrows * D4) {
+          const int i = tid / D4, d = (tid % D4) * 4;
+          const float *P = reinterpret_cast<const float *>(zs()) + i * 44 + d;
+          float4 pw[MAX_NW];
+#pragma unroll
+          for (int w = 0; w < MAX_NW; ++w) pw[w] = *reinterpret_cast<const float4 *>(P + w * 8 * 44);
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int w = 0; w < MAX_NW; ++w) {
+            acc.x += pw[w].x; acc.y += pw[w].y; acc.z += pw[w].z; acc.w += pw[w].w;
+          }
+          const float4 bp = *reinterpret_cast<const float4 *>(bsl() + 72 + d);   // b_pred slice (smem)
+          const float o0 = acc.x + bp.x, o1 = acc.y + bp.y, o2 = acc.z + bp.z, o3 = acc.w + bp.w;
+          const int s = rs.plist[i];
+          float *dst = gs() + (size_t)s * H + goff(d0 + d);
+          *reinterpret_cast<float4 *>(dst) = make_float4(o0, o1, o2, o3);
+          const uint64_t lo = ((uint64_t)__float_as_uint(o1) << 32) | __float_as_uint(o0);
+          const uint64_t hi2 = ((uint64_t)__float_as_uint(o3) << 32) | __float_as_uint(o2);
+          const uint32_t la = smem_u32(dst);
+#pragma unroll 16
+          for (int c = 1; c < C; ++c) {
+            const uint32_t dr = (uint32_t)((rank + c) % C);
+            st_async_u64x2(mapa_u32(la, dr), lo, hi2, mapa_u32(bg, dr));
+          }
+        }
+      } else
       for (int idx = tid; idx < nrows * D4; idx += NCT) {
         const int ii = idx / D4, d = (idx % D4) * 4;    // row within the pass, first of 4 dims
         const int i = nb0 * 8 + ii, nb = ii >> 3, il = ii & 7;
@@ -2688,6 +2757,9 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
         if constexpr (RING) {          // SOS inputs of the first predictor step
           if (warp == 0 && rs.npred > 0) cx.issue_eprime(rs.plist, rs.npred);
         }
+        if constexpr (CtxT::TJ) {      // the first round's plan (every active row scans from t = 0)
+          if (warp == 0) cx.plan_next_tj(lane < R && rs.active[lane], 0, lane < R ? rs.L[lane] : 0);
+        }
         cx.sync();
         bool have_spec = false;        // fbuf[cur ^ 1] holds the previous tick's speculative windows
         [[maybe_unused]] int dbg_l = 0, dbg_gr = 0;   // probe rows written by this cluster
@@ -2758,8 +2830,10 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
           if (rs.nscan > 0) {
             // (3) one joint round (Alg. 3 lines 7-19 over a W-frame window)
             cx.tl_round_(0);
-            cx.plan_z(cur);
-            cx.sync();
+            if constexpr (!CtxT::TJ) {   // TJ: planned with the previous decisions (plan_next_tj)
+              cx.plan_z(cur);
+              cx.sync();
+            }
             cx.tl_round_bar(1);
 #ifdef LL_EXP1
             cx.gate_wait();   // experiment: no gate batch in flight during build_z
