@@ -363,5 +363,7 @@ template <> __device__ __forceinline__ float to_f32<bf16>(bf16 v) { return __bfl
 
 // logistic: fast reciprocal (MUFU.RCP), no IEEE-division slow path; relative error ~1e-7
 __device__ __forceinline__ float sigmoidf_(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+// tanh x = 2 s(2x) - 1: absolute error ~1e-7 (a MUFU.EX2 + MUFU.RCP; tanhf is a longer sequence)
+__device__ __forceinline__ float tanhf_(float x) { return 2.0f * sigmoidf_(2.0f * x) - 1.0f; }
 
 }  // namespace ll

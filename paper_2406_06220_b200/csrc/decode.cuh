@@ -74,7 +74,7 @@ enum {
   BAR_SPEC = 15 + 2 * NSMAX, // (TJ) MMA warp: speculative copies issued, fbase / fcnt written
   NBARS = 16 + 2 * NSMAX
 };
-enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3 };
+enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3, MCMD_FLOAD = 4 };
 
 // ---------------------------------------------------------------------------
 // TG: the FC LSTM instantiation (P = 640 in 16-CTA clusters: 40 units = 160
@@ -485,7 +485,7 @@ struct Ctx {
             umma_ts(tmem + TG_COL_DFOLD, tmem + TG_COL_FOLD + (uint32_t)(8 * kk), db, ID_FOLD, kk > 0);
           }
           umma_commit(bar(BAR_GATE));
-        } else if (lane == 0) {
+        } else if (lane == 0 && cmd == MCMD_JOINT) {
 #pragma unroll
           for (int kk = 0; kk < TJ_H / 32; ++kk) {   // K' = 320: A / B chunks 2kk, 2kk + 1
             const uint64_t da = umma_desc_ns(wa + (uint32_t)(kk * 256), 128, TJ_GRP);
@@ -495,6 +495,7 @@ struct Ctx {
           umma_commit(bar(BAR_JOINT));
         }
         __syncwarp();
+        if (cmd == MCMD_FLOAD) spec_copies((word >> 9) & 1, true);
         if (cmd == MCMD_JOINT && (word & 0x100)) {   // next windows, while the MMAs run
           spec_copies((word >> 9) & 1);
           __syncwarp();
@@ -606,13 +607,14 @@ struct Ctx {
   // MMA warp (all lanes): the copies of a posted speculative request; lane =
   // scanning slot.  fbase / fcnt are written before the (releasing) expect_tx
   // arrive, so a consumer that waited on BAR_F + X sees them.
-  __device__ void spec_copies(int X) {
-    const int n = rs.nscan;
+  // (also the reloads at a tick's start: list = llist, base = t)
+  __device__ void spec_copies(int X, bool reload = false) {
+    const int n = reload ? rs.nload : rs.nscan;
     uint32_t bytes = 0;
     int s = 0, base = 0, cnt = 0;
     if (lane < n) {
-      s = rs.slist[lane];
-      base = rs.t[s] + p.W;
+      s = reload ? rs.llist[lane] : rs.slist[lane];
+      base = rs.t[s] + (reload ? 0 : p.W);
       cnt = rs.L[s] - base;
       if (cnt > p.WF) cnt = p.WF;
       if (cnt < 0) cnt = 0;
@@ -638,6 +640,15 @@ struct Ctx {
           bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * TJ_FROW, src + (size_t)i * TJ_H * 2, TJ_H * 2, bar(BAR_F + X));
       }
     }
+  }
+
+  // TJ tick start: the windows of rs.llist into fbuf[X], issued by the MMA warp
+  // (after every reader of fbuf is done: the caller's barrier)
+  __device__ void reload_f(int X) {
+    if (fpend(X)) wait_f(X);
+    if (fpend(X ^ 1)) wait_f(X ^ 1);
+    if (tid == 0) post(MCMD_FLOAD | (X << 9));
+    phs |= 1u << (2 + X);
   }
 
   __device__ void issue_f(int X, bool spec, const int *list = nullptr, int nlist = 0) {
@@ -2214,10 +2225,10 @@ struct Ctx {
           float *cp = cs() + (size_t)s * TG_UPC + ul;
           const float gi = gt[0] + ep[0], gf = gt[1] + ep[TG_UPC], gg = gt[2] + ep[2 * TG_UPC],
                       go = gt[3] + ep[3 * TG_UPC];
-          const float cn = sigmoidf_(gf) * *cp + sigmoidf_(gi) * tanhf(gg);
+          const float cn = sigmoidf_(gf) * *cp + sigmoidf_(gi) * tanhf_(gg);
           *cp = cn;
           const int k = u0 + ul;
-          *reinterpret_cast<bf16 *>(hbuf() + hoff(s, k >> 3) + (k & 7) * 2) = __float2bfloat16_rn(sigmoidf_(go) * tanhf(cn));
+          *reinterpret_cast<bf16 *>(hbuf() + hoff(s, k >> 3) + (k & 7) * 2) = __float2bfloat16_rn(sigmoidf_(go) * tanhf_(cn));
         }
       }
       tl_pred(2);
@@ -2765,6 +2776,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
         [[maybe_unused]] int dbg_l = 0, dbg_gr = 0;   // probe rows written by this cluster
         while (rs.nactive > 0) {
           if (t0) s_cnt[SC_OUTER]++;
+          cx.tl_pred(11);
           if (have_spec) {
             cx.wait_f(cur ^ 1);
             cur ^= 1;
@@ -2784,7 +2796,11 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             if (lane == 0) rs.nload = __popc(ml);
           }
           cx.sync();
-          if (rs.nload > 0) cx.issue_f(cur, false, rs.llist, rs.nload);
+          cx.tl_pred_bar(12);
+          if (rs.nload > 0) {
+            if constexpr (CtxT::TJ) cx.reload_f(cur);   // the MMA warp issues the copies
+            else cx.issue_f(cur, false, rs.llist, rs.nload);
+          }
           cx.tl_pred_bar(8);
           // (2) predictor (Alg. 3 line 6) for the rows that found a label
           if (rs.npred > 0) {
@@ -2825,6 +2841,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             cx.template rebuild_lists<false>();   // after the predictor's / round's barriers
           }
           if (cx.fpend(cur)) cx.wait_f(cur);
+          cx.tl_pred(13);
           cx.sync();
           have_spec = false;
           if (rs.nscan > 0) {

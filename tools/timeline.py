@@ -66,6 +66,11 @@ else:
     report(0, "joint rounds", list(range(11)),
            ["", "wait_f/plan (+sync)", "build_z", "sync (bar)", "spec issue + joint", "exchange send",
             "exchange wait", "resolve", "sync (bar)", "decide", "sync+reload (bar)"])
+if "--tj" in sys.argv:
+    report(1, "tick (predictor + the windows around it)", [11, 12, 8, 0, 1, 2, 3, 4, 9, 10, 5, 6, 7, 13],
+           ["", "spec wait + window plan + sync", "reload issue", "outer-step entry", "gate read + E' wait", "cell update",
+            "sync (bar)", "h' exchange", "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)",
+            "g exchange + sync", "lists + reload wait"])
 report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 9, 10, 5, 6, 7],
        ["", "outer-step entry", "first gate tile", "rest tiles + E' wait", "sync (bar)", "h' exchange",
         "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)", "g exchange + sync"])
