@@ -198,6 +198,10 @@ __device__ __forceinline__ void st_async_u64x2(uint32_t raddr, uint64_t a, uint6
                "l"(a), "l"(b), "r"(rbar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_u64(uint32_t raddr, uint64_t a, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(a), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

@@ -164,6 +164,7 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   Layout L;
   L.wks = sc ? 4 : 2;
   L.pks = (sc && nD > 0) ? 4 : 2;
+  if (allow_tj && tj_shape(bf, H, P, C) && !sc && nD == 0) L.pks = 1;   // TJ RNN-T: the token key alone
   const int NT = (V1 + nD + 7) / 8;
   L.tiles_max = (NT + C - 1) / C;
   L.UPC = lstm ? P / C : 0;
@@ -419,7 +420,7 @@ struct Ctx {
   __device__ uint64_t *part(int pr) const { return (uint64_t *)(sm + L.off_part) + (size_t)pr * C * L.JR * pks(); }
   // words per per-warp key entry / per cluster partial (compile-time unless SC with a runtime family)
   __device__ __forceinline__ int wks() const { return SC ? 4 : 2; }
-  __device__ __forceinline__ int pks() const { return (SC && is_tdt()) ? 4 : 2; }
+  __device__ __forceinline__ int pks() const { return (SC && is_tdt()) ? 4 : (TJ && !SC && !is_tdt()) ? 1 : 2; }
   __device__ uint64_t *wkey() const { return (uint64_t *)(sm + L.off_wkey); }
   __device__ uint8_t *hsrow(int hp, int s) const { return sm + L.off_hs + ((size_t)hp * p.R + s) * hstride(); }
   __device__ float *es() const { return (float *)(sm + L.off_es); }
@@ -1304,7 +1305,8 @@ struct Ctx {
 #pragma unroll 16
       for (int d = 0; d < C; ++d) {
         const int dst = (rank + d) % C;
-        st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, second, mapa_u32(bb, (uint32_t)dst));
+        if (TJ && !SC && !is_tdt()) st_async_u64(mapa_u32(slot, (uint32_t)dst), tkey, mapa_u32(bb, (uint32_t)dst));
+        else st_async_u64x2(mapa_u32(slot, (uint32_t)dst), tkey, second, mapa_u32(bb, (uint32_t)dst));
         if (SC && is_tdt()) st_async_u64x2(mapa_u32(slot + 16, (uint32_t)dst), tl, dl, mapa_u32(bb, (uint32_t)dst));
       }
     }
@@ -1448,6 +1450,7 @@ struct Ctx {
       act = rs.active[lane]; scan = rs.scanning[lane]; needp = rs.needp[lane];
       b0 = rs.zbeg[lane]; c = rs.zcnt[lane];
     }
+    [[maybe_unused]] const int t_round = t;   // window base of this round (TJ: the speculative next window starts at t_round + W)
     // decisions of the window (Alg. 3 lines 9-11 / 15-19): first non-blank frame
     const unsigned m = scan ? (nb >> b0) & ((1u << c) - 1u) : 0u;   // c <= W <= 8
     const bool found = m != 0u;
@@ -1516,7 +1519,15 @@ struct Ctx {
       rs.ready = ms == 0u;
       *algevals += (unsigned)tot;
     }
-    if constexpr (TJ) plan_next_tj(inr && act && (scan || needp), t, Ls);
+    if constexpr (TJ) {
+      plan_next_tj(inr && act && (scan || needp), t, Ls);
+      // the next tick's reloads: rows that found a label, and scanning rows whose
+      // speculative window (t_round + W) does not start at their new t (TDT jumps)
+      const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + p.W)));
+      const unsigned ml = __ballot_sync(FULL, ld);
+      if (ld) rs.llist[__popc(ml & below)] = lane;
+      if (lane == 0) rs.nload = __popc(ml);
+    }
     __syncwarp();
     if (eprime && mp != 0u) issue_eprime(rs.plist, __popc(mp));
   }
@@ -1540,6 +1551,7 @@ struct Ctx {
       act = rs.active[lane]; scan = rs.scanning[lane]; needp = rs.needp[lane];
       b0 = rs.zbeg[lane]; c = rs.zcnt[lane];
     }
+    [[maybe_unused]] const int t_round = t;   // window base of this round (TJ: the speculative next window starts at t_round + W)
     // decisions of the window (Alg. 3 lines 9-11 / 15-19): first non-blank frame
     bool found = false;
     int pos = 0, y = 0, d = 0, used = 0;
@@ -1638,7 +1650,15 @@ struct Ctx {
       rs.ready = ms == 0u;
       *algevals += (unsigned)tot;
     }
-    if constexpr (TJ) plan_next_tj(inr && act && (scan || needp), t, Ls);
+    if constexpr (TJ) {
+      plan_next_tj(inr && act && (scan || needp), t, Ls);
+      // the next tick's reloads: rows that found a label, and scanning rows whose
+      // speculative window (t_round + W) does not start at their new t (TDT jumps)
+      const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + p.W)));
+      const unsigned ml = __ballot_sync(FULL, ld);
+      if (ld) rs.llist[__popc(ml & below)] = lane;
+      if (lane == 0) rs.nload = __popc(ml);
+    }
     __syncwarp();
     if (eprime && mp != 0u) issue_eprime(rs.plist, __popc(mp));
   }
@@ -2768,8 +2788,14 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
         if constexpr (RING) {          // SOS inputs of the first predictor step
           if (warp == 0 && rs.npred > 0) cx.issue_eprime(rs.plist, rs.npred);
         }
-        if constexpr (CtxT::TJ) {      // the first round's plan (every active row scans from t = 0)
-          if (warp == 0) cx.plan_next_tj(lane < R && rs.active[lane], 0, lane < R ? rs.L[lane] : 0);
+        if constexpr (CtxT::TJ) {      // the first round's plan and windows (every active row scans from t = 0)
+          if (warp == 0) {
+            const bool act0 = lane < R && rs.active[lane];
+            cx.plan_next_tj(act0, 0, lane < R ? rs.L[lane] : 0);
+            const unsigned ml = __ballot_sync(0xffffffffu, act0);
+            if (act0) rs.llist[__popc(ml & ((1u << lane) - 1u))] = lane;
+            if (lane == 0) rs.nload = __popc(ml);
+          }
         }
         cx.sync();
         bool have_spec = false;        // fbuf[cur ^ 1] holds the previous tick's speculative windows
@@ -2783,7 +2809,9 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
           }
           // (1) windows: a continuing row whose speculative window starts at its t
           // reuses it; every other row about to scan gets a fresh window
-          if (warp == 0) {
+          // (TJ: the reload list was made with the decisions, finish_round*)
+          if (CtxT::TJ && rs.nload > 0) cx.reload_f(cur);
+          if (!CtxT::TJ && warp == 0) {
             bool ld = false;
             if (lane < R) {
               const int s = lane;
@@ -2795,11 +2823,10 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             if (ld) rs.llist[__popc(ml & ((1u << lane) - 1u))] = lane;
             if (lane == 0) rs.nload = __popc(ml);
           }
-          cx.sync();
-          cx.tl_pred_bar(12);
-          if (rs.nload > 0) {
-            if constexpr (CtxT::TJ) cx.reload_f(cur);   // the MMA warp issues the copies
-            else cx.issue_f(cur, false, rs.llist, rs.nload);
+          if constexpr (!CtxT::TJ) {
+            cx.sync();
+            cx.tl_pred_bar(12);
+            if (rs.nload > 0) cx.issue_f(cur, false, rs.llist, rs.nload);
           }
           cx.tl_pred_bar(8);
           // (2) predictor (Alg. 3 line 6) for the rows that found a label
