@@ -92,15 +92,17 @@ enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3, MCMD_FLOAD = 4 };
 //   TMEM columns [408, 440): D fold  (M=128, N=32 = 4 K-quarters x 8 slots; the
 //                            diagonal blocks are the 4 partial sums)
 // h lives in shared memory as the MMA's B operand, K-major without swizzle:
-// 8-row x 16-byte core matrices, element (slot n, k) at
-//   (k / 160) * 2560 + ((k % 160) / 8) * 128 + n * 16 + (k % 8) * 2
-// so the main MMA reads it with LBO = 128 (next 8 K) and the fold MMA reads the
-// same bytes as a 32-row operand (row 8j + n = slot n's K-quarter j, SBO = 2560).
+// 8-row x 16-byte core matrices 144 bytes apart (128 + 16 of padding, so the
+// mma.sync W_pred step's 16-byte loads of 4 consecutive chunks hit different
+// banks), element (slot n, k) at (k / 8) * 144 + n * 16 + (k % 8) * 2:
+// the main MMA reads it with LBO = 144 (next 8 K) and the fold MMA reads the
+// same bytes as a 32-row operand (row 8j + n = slot n's K-quarter j, SBO = 2880).
 // ---------------------------------------------------------------------------
 constexpr int TG_P = 640, TG_C = 16, TG_UPC = TG_P / TG_C;   // 40 units per CTA
 constexpr int TG_NH = 8;                                       // slots (B rows): R <= 8
-constexpr int TG_QB = (TG_P / 4 / 8) * 128;                    // bytes per K-quarter of h (2560)
-constexpr int TG_HBYTES = 4 * TG_QB;                           // h buffer (10240)
+constexpr int TG_CM = 144;                                     // h: core-matrix (8 rows x 16 B) stride, padded
+constexpr int TG_QB = (TG_P / 4 / 8) * TG_CM;                  // bytes per K-quarter of h (2880)
+constexpr int TG_HBYTES = 4 * TG_QB;                           // h buffer (11520)
 constexpr uint32_t TG_COL_FOLD = TG_P / 2, TG_COL_DMAIN = TG_P / 2 + TG_P / 8, TG_COL_DFOLD = TG_COL_DMAIN + TG_NH;
 __host__ __device__ inline bool tg_shape(bool bf, bool lstm, int H, int P, int C) {
   return bf && lstm && H == TG_P && P == TG_P && C == TG_C;
@@ -430,7 +432,7 @@ struct Ctx {
   // ---- TG: gate pre-activation batches (MMA warp) ---------------------------
   __device__ uint8_t *hbuf() const { return sm + L.off_hs; }
   // byte offset of 16-byte chunk c (K elements 8c .. 8c+7) of slot n's h row
-  __device__ __forceinline__ static int hoff(int n, int c) { return (c / 20) * TG_QB + (c % 20) * 128 + n * 16; }
+  __device__ __forceinline__ static int hoff(int n, int c) { return c * TG_CM + n * 16; }
   // every consumer thread: wait for the outstanding gate batch, if any
   __device__ __forceinline__ void gate_wait() {
     if constexpr (TG) {
@@ -477,12 +479,12 @@ struct Ctx {
 #pragma unroll
           for (int kk = 0; kk < TG_P / 16; ++kk) {   // K = 16 per MMA: h chunks 2kk, 2kk + 1
             const int c = 2 * kk;
-            const uint64_t db = umma_desc_ns(hb + (uint32_t)((c / 20) * TG_QB + (c % 20) * 128), 128, 1024);
+            const uint64_t db = umma_desc_ns(hb + (uint32_t)(c * TG_CM), TG_CM, 1024);
             umma_ts(tmem + TG_COL_DMAIN, tmem + (uint32_t)(8 * kk), db, ID_MAIN, kk > 0);
           }
 #pragma unroll
           for (int kk = 0; kk < TG_P / 64; ++kk) {   // the 4 K-quarters side by side (32 B rows)
-            const uint64_t db = umma_desc_ns(hb + (uint32_t)(kk * 256), 128, TG_QB);
+            const uint64_t db = umma_desc_ns(hb + (uint32_t)(kk * 2 * TG_CM), TG_CM, TG_QB);
             umma_ts(tmem + TG_COL_DFOLD, tmem + TG_COL_FOLD + (uint32_t)(8 * kk), db, ID_FOLD, kk > 0);
           }
           umma_commit(bar(BAR_GATE));

@@ -1,10 +1,9 @@
 // gemm_tc.cuh -- Y[M,N] = X[M,K] . W[N,K]^T + bias[N] (+ bias2[N]) on the
 // 5th-generation tensor cores (sm_100a): TMA (cp.async.bulk.tensor, 128-byte
-// swizzle) stages 128x64 tiles of X and W through a 4-stage shared-memory ring,
-// ONE thread issues tcgen05.mma (kind::f16, M=128, N=128, K=16, fp32
-// accumulator in TMEM) and tcgen05.commit releases each stage; four warps read
-// the accumulator back with tcgen05.ld (lane = output row) for the epilogue
-// (bias, conversion, store).
+// swizzle) stages 128x64 tiles of X and W through a 4-stage shared-memory ring;
+// a producer warp, an MMA warp (tcgen05.mma kind::f16, M=128, N=128, K=16,
+// fp32 accumulators in TMEM, double-buffered) and four epilogue warps
+// (tcgen05.ld, bias, conversion, store) run as a persistent pipeline.
 //
 // Used for the throughput-bound projections of PAPER.md §3.4 (:216-222): the
 // encoder projection f = W_enc enc + b_enc over all B*T_max frames (Alg. 3
@@ -59,117 +58,153 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
+// Persistent, warp-specialized: grid = number of SMs (one CTA each); CTA b
+// takes output tiles b, b + gridDim.x, ... (tile = (m-tile, n-tile), n fastest;
+// tiles of padding frames only are skipped by every role alike).
+//   warp 0:    TMA producer (lane 0): A/B 128x64 k-blocks into a TC_STAGES ring
+//   warp 1:    MMA issuer (lane 0): tcgen05.mma into one of TWO TMEM
+//              accumulators (128 columns each), tcgen05.commit per k-block
+//              (frees the stage) and per tile (accumulator full)
+//   warps 2-5: epilogue (TMEM lane quarter = warp % 4): accumulator -> bias ->
+//              global, then release the accumulator, so the MMAs of tile i+1
+//              overlap the epilogue of tile i.
+constexpr int TC_THREADS = 192;
+__device__ __forceinline__ void tile_mn(const TcGemmArgs &a, int tile, int &m0, int &n0) {
+  const int nt = a.N / TC_BN;
+  m0 = (tile / nt) * TC_BM;
+  n0 = (tile % nt) * TC_BN;
+}
+
 template <typename OutT>
-__global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
-                                                         const __grid_constant__ CUtensorMap map_w,
-                                                         const __grid_constant__ TcGemmArgs a) {
+__global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
+                                                                const __grid_constant__ CUtensorMap map_w,
+                                                                const __grid_constant__ TcGemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // SW128 atoms: 1024-B aligned
-  __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], done;
+  __shared__ __align__(8) uint64_t full[TC_STAGES], empty[TC_STAGES], acc_full[2], acc_empty[2];
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
   const int nk = a.K / TC_BK;
-  if (!tile_has_rows(a, m0, TC_BM)) return;   // padding frames only: nothing to compute
+  const int ntiles = ((a.M + TC_BM - 1) / TC_BM) * (a.N / TC_BN);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);   // one arrive per epilogue warp
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&s_tmem, TC_BN);   // 128 fp32 columns: the 128x128 accumulator
+  if (warp == 1) tmem_alloc(&s_tmem, 2 * TC_BN);   // two 128x128 fp32 accumulators
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
 
-  if (threadIdx.x == 0) {
-    // producer (TMA) and MMA issuer in one thread: stage kb is loaded
-    // TC_STAGES - 1 steps ahead of the MMAs that consume it
-    for (int it = 0; it < nk + TC_STAGES - 1; ++it) {
-      if (it < nk) {
-        const int s = it % TC_STAGES;
-        if (it >= TC_STAGES) mbar_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
-        uint8_t *sa = smem + s * (TC_TILE_A + TC_TILE_B), *sb = sa + TC_TILE_A;
-        mbar_arrive_expect_tx(&full[s], TC_TILE_A + TC_TILE_B);
-        tma_load_2d(sa, &map_x, it * TC_BK, m0, &full[s]);
-        tma_load_2d(sb, &map_w, it * TC_BK, n0, &full[s]);
+  if (warp == 0) {
+    if (lane == 0) {   // producer
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int m0, n0;
+        tile_mn(a, tile, m0, n0);
+        if (!tile_has_rows(a, m0, TC_BM)) continue;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % TC_STAGES;
+          if (it >= TC_STAGES) mbar_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
+          uint8_t *sa = smem + s * (TC_TILE_A + TC_TILE_B), *sb = sa + TC_TILE_A;
+          mbar_arrive_expect_tx(&full[s], TC_TILE_A + TC_TILE_B);
+          tma_load_2d(sa, &map_x, kb * TC_BK, m0, &full[s]);
+          tma_load_2d(sb, &map_w, kb * TC_BK, n0, &full[s]);
+        }
       }
-      const int kc = it - (TC_STAGES - 1);
-      if (kc >= 0) {
-        const int s = kc % TC_STAGES;
-        mbar_wait(&full[s], (kc / TC_STAGES) & 1);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // MMA issuer
+      int it = 0, t = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int m0, n0;
+        tile_mn(a, tile, m0, n0);
+        if (!tile_has_rows(a, m0, TC_BM)) continue;
+        const int ab = t & 1;
+        if (t >= 2) mbar_wait(&acc_empty[ab], ((t >> 1) - 1) & 1);   // the epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * (TC_TILE_A + TC_TILE_B)), sb = sa + TC_TILE_A;
+        const uint32_t acc = tmem + (uint32_t)(ab * TC_BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % TC_STAGES;
+          mbar_wait(&full[s], (it / TC_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * (TC_TILE_A + TC_TILE_B)), sb = sa + TC_TILE_A;
 #pragma unroll
-        for (int k = 0; k < TC_BK / 16; ++k) {   // K = 16 per MMA: +32 bytes inside the swizzle atom
-          const uint64_t da = umma_desc_sw128(sa + k * 32), db = umma_desc_sw128(sb + k * 32);
-          const uint32_t acc = (kc > 0 || k > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-              " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(TC_IDESC), "r"(acc)
-              : "memory");
+          for (int k = 0; k < TC_BK / 16; ++k)   // K = 16 per MMA: +32 bytes inside the swizzle atom
+            umma_ss(acc, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), TC_IDESC, kb > 0 || k > 0);
+          umma_commit(&empty[s]);   // the stage is free once these MMAs have read it
         }
-        // the stage is free once these MMAs have read it
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(&empty[s]))
-                     : "memory");
+        umma_commit(&acc_full[ab]);
+        ++t;
       }
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(&done))
-                 : "memory");
-  }
-  __syncwarp();
-  // epilogue: warp w owns accumulator rows 32w..32w+31 (TMEM lane = row)
-  mbar_wait(&done, 0);
-  tc_fence_after();
-  const int row = m0 + warp * 32 + lane;
-  const bf16 *bias = (const bf16 *)a.bias, *bias2 = (const bf16 *)a.bias2;
+  } else {
+    // epilogue: warp w reads accumulator rows 32 (w % 4) .. + 31 (TMEM lane = row)
+    const int qd = warp & 3;
+    const bf16 *bias = (const bf16 *)a.bias, *bias2 = (const bf16 *)a.bias2;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int m0, n0;
+      tile_mn(a, tile, m0, n0);
+      if (!tile_has_rows(a, m0, TC_BM)) continue;
+      const int ab = t & 1;
+      mbar_wait(&acc_full[ab], (t >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + qd * 32 + lane;
+      bool used = row < a.M;
+      if (used && a.lengths) {
+        const int b = row / a.T;
+        used = row - b * a.T < a.lengths[b];
+      }
 #pragma unroll 1
-  for (int c0 = 0; c0 < TC_BN; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
-    tmem_wait_ld();
-    bool used = row < a.M;
-    if (used && a.lengths) {
-      const int b = row / a.T;
-      used = row - b * a.T < a.lengths[b];
-    }
-    if (used) {
-      float v[32];
+      for (int c0 = 0; c0 < TC_BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * TC_BN + c0), r);
+        tmem_wait_ld();
+        if (used) {
+          float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = n0 + c0 + j;
-        float x = __uint_as_float(r[j]);
-        if (bias) x += __bfloat162float(bias[n]);
-        if (bias2) x += __bfloat162float(bias2[n]);
-        v[j] = x;
-      }
-      OutT *y = (OutT *)a.Y + (int64_t)row * a.ldy + n0 + c0;
-      if constexpr (sizeof(OutT) == 2) {
+          for (int j = 0; j < 32; ++j) {
+            const int n = n0 + c0 + j;
+            float x = __uint_as_float(r[j]);
+            if (bias) x += __bfloat162float(bias[n]);
+            if (bias2) x += __bfloat162float(bias2[n]);
+            v[j] = x;
+          }
+          OutT *y = (OutT *)a.Y + (int64_t)row * a.ldy + n0 + c0;
+          if constexpr (sizeof(OutT) == 2) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 o;
-          o.x = pack_bf16x2(v[j], v[j + 1]);
-          o.y = pack_bf16x2(v[j + 2], v[j + 3]);
-          o.z = pack_bf16x2(v[j + 4], v[j + 5]);
-          o.w = pack_bf16x2(v[j + 6], v[j + 7]);
-          *reinterpret_cast<uint4 *>(y + j) = o;
+            for (int j = 0; j < 32; j += 8) {
+              uint4 o;
+              o.x = pack_bf16x2(v[j], v[j + 1]);
+              o.y = pack_bf16x2(v[j + 2], v[j + 3]);
+              o.z = pack_bf16x2(v[j + 4], v[j + 5]);
+              o.w = pack_bf16x2(v[j + 6], v[j + 7]);
+              *reinterpret_cast<uint4 *>(y + j) = o;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4 *>(y + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          }
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4 *>(y + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      ++t;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, TC_BN);
+  if (warp == 1) tmem_dealloc(tmem, 2 * TC_BN);
 }
 
 }  // namespace ll

@@ -333,14 +333,22 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
       !make_map_bf16(&mw, W, (uint64_t)N, (uint64_t)K, (uint64_t)ldw, TC_BN))
     return false;
   TcGemmArgs a{bias, bias2, Y, ldy, M, N, K, lengths, T};
-  dim3 grid(N / TC_BN, (M + TC_BM - 1) / TC_BM);
-  if (out_bf16) {
-    cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-    gemm_tc_kernel<bf16><<<grid, 128, TC_SMEM, st>>>(mx, mw, a);
-  } else {
-    cudaFuncSetAttribute(gemm_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-    gemm_tc_kernel<float><<<grid, 128, TC_SMEM, st>>>(mx, mw, a);
+  static int nsm = 0, attr_done = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm < 1) nsm = 1;
   }
+  if (!attr_done) {   // once per process (not on every call)
+    cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    attr_done = 1;
+  }
+  const int ntiles = ((M + TC_BM - 1) / TC_BM) * (N / TC_BN);
+  dim3 grid(std::min(ntiles, nsm));
+  if (out_bf16) gemm_tc_kernel<bf16><<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, a);
+  else gemm_tc_kernel<float><<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, a);
   s = cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
   return true;
 }

@@ -2,7 +2,7 @@
 # Round evidence for profiles/ (GPU box): bench lines, ncu launch list, one
 # ncu --set full capture of the decode kernel, per-warp timeline.
 #   tools/collect_profiles.sh <tag>      -> gpurun_out/<tag>_*
-t=${1:-r01}
+t=${1:-r02}
 o=gpurun_out
 for c in fc-rnnt fc-tdt stateless-b512; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > $o/${t}_bench_$c.json 2> $o/${t}_bench_$c.err
@@ -23,4 +23,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $o/${t}_launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:decode_kernel -s 2 -c 1 \
   -o $o/${t}_decode python tools/one_decode.py fc-rnnt 3 > $o/${t}_ncu.log 2>&1
-timeout 300 python tools/timeline.py fc-rnnt > $o/${t}_timeline.txt 2>&1
+timeout 300 python tools/timeline.py fc-rnnt --tj > $o/${t}_timeline.txt 2>&1; timeout 300 python tools/timeline.py fc-tdt --tj >> $o/${t}_timeline.txt 2>&1

@@ -16,6 +16,11 @@ KEYS = [
     "l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "sm__icc_request_hit_rate.pct",
     "launch__registers_per_thread", "launch__block_size", "launch__grid_size", "launch__cluster_dim_x",
     "launch__shared_mem_per_block_dynamic",
+    # tcgen05: tensor-memory / tensor-core shared-memory traffic and pipes
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+    "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
 ]
 STALL = "smsp__pcsamp_warps_issue_stalled_"
 
