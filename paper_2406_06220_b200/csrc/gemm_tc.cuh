@@ -16,9 +16,11 @@
 
 namespace ll {
 
-constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 64, TC_STAGES = 4;
+// Output tiles are 128 x 256 (the last tile of a row 128 x (N % 256)): the
+// wider B tile halves the operand bytes staged per MMA cycle against 128 x 128.
+constexpr int TC_BM = 128, TC_BN = 256, TC_BNQ = 128, TC_BK = 64, TC_STAGES = 4;   // N % TC_BNQ == 0
 constexpr int TC_TILE_A = TC_BM * TC_BK * 2;   // 16 KB
-constexpr int TC_TILE_B = TC_BN * TC_BK * 2;   // 16 KB
+constexpr int TC_TILE_B = TC_BN * TC_BK * 2;   // 32 KB (rows past N are zero-filled by the TMA)
 constexpr int TC_SMEM = TC_STAGES * (TC_TILE_A + TC_TILE_B) + 1024;   // + alignment slack
 
 struct TcGemmArgs {
@@ -31,6 +33,7 @@ struct TcGemmArgs {
   // the other tiles are not stored (frames t >= lengths[b] are never read)
   const int *lengths;
   int T;
+  int bn;   // output tile width: TC_BN (256) or TC_BNQ (128, small problems: more tiles than SMs)
 };
 
 // whether any of the rows [m0, m0 + n) is used under the ragged-row rule (all are without lengths)
@@ -46,9 +49,10 @@ __device__ __forceinline__ bool tile_has_rows(const TcGemmArgs &a, int m0, int n
   return false;
 }
 
-// Instruction descriptor: D fp32, A/B bf16, both K-major, N = 128, M = 128.
-constexpr uint32_t TC_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
-                              ((uint32_t)(TC_BM >> 4) << 24);
+// Instruction descriptor: D fp32, A/B bf16, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t tc_idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
   asm volatile(
@@ -69,10 +73,11 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 //              global, then release the accumulator, so the MMAs of tile i+1
 //              overlap the epilogue of tile i.
 constexpr int TC_THREADS = 192;
-__device__ __forceinline__ void tile_mn(const TcGemmArgs &a, int tile, int &m0, int &n0) {
-  const int nt = a.N / TC_BN;
+__device__ __forceinline__ void tile_mn(const TcGemmArgs &a, int tile, int &m0, int &n0, int &nw) {
+  const int nt = (a.N + a.bn - 1) / a.bn;
   m0 = (tile / nt) * TC_BM;
-  n0 = (tile % nt) * TC_BN;
+  n0 = (tile % nt) * a.bn;
+  nw = min(a.bn, a.N - n0);
 }
 
 template <typename OutT>
@@ -85,7 +90,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = a.K / TC_BK;
-  const int ntiles = ((a.M + TC_BM - 1) / TC_BM) * (a.N / TC_BN);
+  const int ntiles = ((a.M + TC_BM - 1) / TC_BM) * ((a.N + a.bn - 1) / a.bn);
+  const uint32_t stage_tx = (uint32_t)(TC_TILE_A + a.bn * TC_BK * 2);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
@@ -98,7 +104,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(&s_tmem, 2 * TC_BN);   // two 128x128 fp32 accumulators
+  if (warp == 1) tmem_alloc(&s_tmem, 2 * TC_BN);   // two 128x256 fp32 accumulators (all 512 columns)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -108,14 +114,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     if (lane == 0) {   // producer
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int m0, n0;
-        tile_mn(a, tile, m0, n0);
+        int m0, n0, nw;
+        tile_mn(a, tile, m0, n0, nw);
         if (!tile_has_rows(a, m0, TC_BM)) continue;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % TC_STAGES;
           if (it >= TC_STAGES) mbar_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
           uint8_t *sa = smem + s * (TC_TILE_A + TC_TILE_B), *sb = sa + TC_TILE_A;
-          mbar_arrive_expect_tx(&full[s], TC_TILE_A + TC_TILE_B);
+          mbar_arrive_expect_tx(&full[s], stage_tx);
           tma_load_2d(sa, &map_x, kb * TC_BK, m0, &full[s]);
           tma_load_2d(sb, &map_w, kb * TC_BK, n0, &full[s]);
         }
@@ -125,8 +131,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     if (lane == 0) {   // MMA issuer
       int it = 0, t = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int m0, n0;
-        tile_mn(a, tile, m0, n0);
+        int m0, n0, nw;
+        tile_mn(a, tile, m0, n0, nw);
         if (!tile_has_rows(a, m0, TC_BM)) continue;
         const int ab = t & 1;
         if (t >= 2) mbar_wait(&acc_empty[ab], ((t >> 1) - 1) & 1);   // the epilogue drained this accumulator
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
           const uint32_t sa = smem_u32(smem + s * (TC_TILE_A + TC_TILE_B)), sb = sa + TC_TILE_A;
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k)   // K = 16 per MMA: +32 bytes inside the swizzle atom
-            umma_ss(acc, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), TC_IDESC, kb > 0 || k > 0);
+            umma_ss(acc, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32), tc_idesc(nw), kb > 0 || k > 0);
           umma_commit(&empty[s]);   // the stage is free once these MMAs have read it
         }
         umma_commit(&acc_full[ab]);
@@ -152,8 +158,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     const bf16 *bias = (const bf16 *)a.bias, *bias2 = (const bf16 *)a.bias2;
     int t = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      int m0, n0;
-      tile_mn(a, tile, m0, n0);
+      int m0, n0, nw;
+      tile_mn(a, tile, m0, n0, nw);
       if (!tile_has_rows(a, m0, TC_BM)) continue;
       const int ab = t & 1;
       mbar_wait(&acc_full[ab], (t >> 1) & 1);
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
         used = row - b * a.T < a.lengths[b];
       }
 #pragma unroll 1
-      for (int c0 = 0; c0 < TC_BN; c0 += 32) {
+      for (int c0 = 0; c0 < nw; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * TC_BN + c0), r);
         tmem_wait_ld();

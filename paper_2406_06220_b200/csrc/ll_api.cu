@@ -325,14 +325,9 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
                int64_t ldy, int M, int N, int K, bool out_bf16, cudaStream_t st, ll_status &s,
                const int *lengths = nullptr, int T = 0) {
   if (g_opt.gemm_mma_sync) return false;
-  if (K % TC_BK || N % TC_BN || (ldx * 2) % 16 || (ldw * 2) % 16 || ((uintptr_t)X & 15) || ((uintptr_t)W & 15))
+  if (K % TC_BK || N % TC_BNQ || (ldx * 2) % 16 || (ldw * 2) % 16 || ((uintptr_t)X & 15) || ((uintptr_t)W & 15))
     return false;
   if ((out_bf16 && (ldy * 2) % 16) || (!out_bf16 && (ldy * 4) % 16) || ((uintptr_t)Y & 15)) return false;
-  CUtensorMap mx, mw;
-  if (!make_map_bf16(&mx, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, TC_BM) ||
-      !make_map_bf16(&mw, W, (uint64_t)N, (uint64_t)K, (uint64_t)ldw, TC_BN))
-    return false;
-  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K, lengths, T};
   static int nsm = 0, attr_done = 0;
   if (!nsm) {
     int dev = 0;
@@ -340,12 +335,20 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm < 1) nsm = 1;
   }
+  // 128 x 256 tiles, unless that leaves fewer than two tiles per SM (then 128 x 128)
+  const int mt = (M + TC_BM - 1) / TC_BM;
+  const int bn = mt * ((N + TC_BN - 1) / TC_BN) >= 2 * nsm ? TC_BN : TC_BNQ;
+  CUtensorMap mx, mw;
+  if (!make_map_bf16(&mx, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, TC_BM) ||
+      !make_map_bf16(&mw, W, (uint64_t)N, (uint64_t)K, (uint64_t)ldw, (uint32_t)bn))
+    return false;
+  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K, lengths, T, bn};
   if (!attr_done) {   // once per process (not on every call)
     cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     attr_done = 1;
   }
-  const int ntiles = ((M + TC_BM - 1) / TC_BM) * (N / TC_BN);
+  const int ntiles = mt * ((N + bn - 1) / bn);
   dim3 grid(std::min(ntiles, nsm));
   if (out_bf16) gemm_tc_kernel<bf16><<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, a);
   else gemm_tc_kernel<float><<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, a);
