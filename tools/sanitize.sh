@@ -1,13 +1,13 @@
 #!/bin/bash
-# compute-sanitizer memcheck / synccheck / racecheck over tools/sanitize_run.py
+# compute-sanitizer memcheck / synccheck / racecheck / initcheck over tools/sanitize_run.py
 # (every kernel family, small shapes); summaries to gpurun_out/sanitizer.txt.
 set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 out=gpurun_out/sanitizer.txt
 : > "$out"
-for t in memcheck synccheck racecheck; do
-  timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_run.py \
+for t in memcheck synccheck racecheck initcheck; do
+  timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_run.py \
     > gpurun_out/san_$t.txt 2>&1
   rc=$?
   {

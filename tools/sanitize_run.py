@@ -35,7 +35,7 @@ def run_tiny(cfg):
     print(cfg, "rows", len(out.hypotheses()), flush=True)
 
 
-def run_planted(cfg, B, frame_looping=False, gather=False):
+def run_planted(cfg, B, frame_looping=False, gather=False, scores=False):
     c = synth.CONFIGS[cfg]
     spec = c["spec"]
     w, codes = synth.planted_weights(spec, 1000)
@@ -48,7 +48,7 @@ def run_planted(cfg, B, frame_looping=False, gather=False):
         enc[i, :e.shape[0]] = e
         planted.append(pl)
     model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16")
-    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, frame_looping=frame_looping)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, frame_looping=frame_looping, scores=scores)
     lengths = torch.from_numpy(L.astype(np.int32)).cuda()
     out = dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), lengths)
     hy = out.hypotheses()
@@ -77,6 +77,8 @@ if __name__ == "__main__":
     run_planted("fc-tdt", 6, gather=True)
     run_planted("fc-rnnt", 4, frame_looping=True)
     run_planted("stateless-b512", 20)
+    run_planted("fc-rnnt", 6, scores=True)   # greedy scores (N2): the SC kernels
+    run_planted("fc-tdt", 6, scores=True)
     with ll.options(schedule=0):   # the paper's batched outer loop (Alg. 3 as listed)
         run_tiny("tiny")
         run_planted("fc-rnnt", 6)
