@@ -236,8 +236,11 @@ ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream);
  *  out_logits      [n, V+1+num_durations] fp32 or NULL (token logits then duration logits)
  *  out_argmax      [n] int32 (lowest index among ties)
  *  out_dur_argmax  [n] int32 or NULL (TDT)
- * Uses the same cluster kernel code path (weights slicing, tensor-core joint,
- * fused argmax, cross-CTA reduction) as the decoders.
+ * Runs the generic cluster kernel's joint (register-resident weight slices,
+ * mma.sync, fused argmax, cross-CTA reduction: the path of every shape other
+ * than the FastConformer one).  The production FastConformer kernels (tcgen05
+ * joint, background recurrent GEMM) are checked through ll_options.probe_*,
+ * which makes the decode kernel itself write its logits and g.
  */
 ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, const ll_joint *joint,
                          ll_dtype dtype, ll_prec prec, int32_t num_durations,

@@ -813,6 +813,10 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   ll_status s = check_model(nullptr, joint, dtype, prec, num_durations, false);
   if (s != LL_OK) return s;
   if (n > 0 && (!enc_rows || !g_rows || !out_argmax)) return LL_ERR_INVALID_ARGUMENT;
+  {   // this call overwrites the workspace with its own layout: drop any prepared tables
+    std::lock_guard<std::mutex> lk(g_prep_mu);
+    g_prepared.erase(workspace);
+  }
   ll_predictor dummy = {};
   dummy.kind = LL_PRED_STATELESS;
   dummy.context = 1;
