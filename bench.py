@@ -436,6 +436,28 @@ def main():
     h2d = enc_h.numel() * enc_h.element_size() + len_h.numel() * 4
     d2h = sum(t.numel() * 4 for t in outs[0])
 
+    # single-call latency: the same public call with nothing overlapped -- H2D of
+    # the inputs, the decode, D2H of the hypotheses, back to back on one stream
+    def single_calls(n):
+        for _ in range(n):
+            bufs[0][0].copy_(enc_h, non_blocking=True)
+            bufs[0][1].copy_(len_h, non_blocking=True)
+            flush.zero_()
+            st = decs[0].launch(bufs[0][0], bufs[0][1], stream)
+            if st != ll.LL_OK:
+                raise ll.LLError(st, "decode")
+            for h, d in zip(outs[0], (decs[0].tokens, decs[0].timestamps, decs[0].lengths_out)):
+                h.copy_(d, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        single_calls(2)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        single_calls(a.steps)
+        e1.record(stream)
+    e1.synchronize()
+    single_ms = e0.elapsed_time(e1) / a.steps
+
     # whole-job aggregate: the audio / utterances of ALL ranks over the max-over-ranks time
     audio_s = float(len_np.sum()) * frame_s_of(a.config)
     t_all = torch.tensor([tot_ms, sum(e2e_ms)], dtype=torch.float64, device=dev)
@@ -483,7 +505,9 @@ def main():
         "utterances_per_s": utt_s,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms_max / a.steps,
-                "mode": "serving loop: step i+1's H2D overlaps step i's decode (H2D / D2H streams, 2 workspaces)"},
+                "mode": "serving loop: step i+1's H2D overlaps step i's decode (H2D / D2H streams, 2 workspaces)",
+                "single_call": {"ms": single_ms, "value": audio_s / (single_ms / 1e3), "unit": UNIT,
+                                "mode": "one call at a time: H2D, decode, D2H back to back on one stream (latency)"}},
         "gpu_launches": a.steps * 2,   # encoder projection GEMM + decode kernel (tables prepared once)
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "decode_kernel",
