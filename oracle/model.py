@@ -57,6 +57,7 @@ class Transducer:
         self.H = self.w["w_out"].shape[1]
         if pred_kind == "lstm":
             self.P = self.w["w_hh"].shape[1]
+            self.layers = 1 + (self.w["w_ih_rest"].shape[0] if "w_ih_rest" in self.w else 0)
         else:
             self.P = self.context * self.w["embedding"].shape[2]
 
@@ -74,23 +75,33 @@ class Transducer:
     def pred_init(self):
         """predictor.init_state() (Alg. 1 line 3): zeros / context of blanks (A8)."""
         if self.kind == "lstm":
-            return (np.zeros(self.P), np.zeros(self.P))
+            return (np.zeros((self.layers, self.P)), np.zeros((self.layers, self.P)))
         return tuple([self.blank] * self.context)
 
     def pred_step(self, state, label: int):
         """dec, new_state = predictor(state, label) (Alg. 1 line 65/67)."""
         if self.kind == "lstm":
-            h, c = state
+            # a stack of `layers` cells (PyTorch nn.LSTM, num_layers = L; reading
+            # A9): layer 0 reads the embedding, layer l the new h of layer l-1
+            hs, cs = state
             x = self.w["embedding"][label]
-            gates = (self.w["w_ih"] @ x + self.w["b_ih"]) + (self.w["w_hh"] @ h + self.w["b_hh"])
             P = self.P
-            i = _sigmoid(gates[0:P])
-            f = _sigmoid(gates[P:2 * P])
-            g = np.tanh(gates[2 * P:3 * P])
-            o = _sigmoid(gates[3 * P:4 * P])
-            c2 = f * c + i * g
-            h2 = o * np.tanh(c2)
-            return h2, (h2, c2)
+            h_new, c_new = np.empty_like(hs), np.empty_like(cs)
+            for layer in range(self.layers):
+                if layer == 0:
+                    w_ih, w_hh, b_ih, b_hh = self.w["w_ih"], self.w["w_hh"], self.w["b_ih"], self.w["b_hh"]
+                else:
+                    w_ih, w_hh = self.w["w_ih_rest"][layer - 1], self.w["w_hh_rest"][layer - 1]
+                    b_ih, b_hh = self.w["b_ih_rest"][layer - 1], self.w["b_hh_rest"][layer - 1]
+                gates = (w_ih @ x + b_ih) + (w_hh @ hs[layer] + b_hh)
+                i = _sigmoid(gates[0:P])
+                f = _sigmoid(gates[P:2 * P])
+                g = np.tanh(gates[2 * P:3 * P])
+                o = _sigmoid(gates[3 * P:4 * P])
+                c_new[layer] = f * cs[layer] + i * g
+                h_new[layer] = o * np.tanh(c_new[layer])
+                x = h_new[layer]
+            return h_new[-1], (h_new, c_new)
         new_state = (int(label),) + tuple(state[:-1])
         dec = np.concatenate([self.w["embedding"][k][new_state[k]] for k in range(self.context)])
         return dec, new_state

@@ -55,6 +55,7 @@ class ModelSpec:
     durations: Optional[Sequence[int]] = None  # TDT duration set D (None: RNN-T)
     blank_id: int = 0
     max_symbols: int = 10
+    num_layers: int = 1        # LSTM layers ("more layers"; layers >= 2: *_rest arrays)
 
     @property
     def is_tdt(self) -> bool:
@@ -68,7 +69,8 @@ def _uniform(rng, shape, fan_in):
 def make_weights(spec: ModelSpec, seed: int = 0, blank_bias: float = 0.0) -> Dict[str, np.ndarray]:
     """Random-init weights in ABI layout, bf16-rounded, as float32 arrays.
 
-    LSTM: embedding [V+1,P], w_ih/w_hh [4P,P] (gate rows i,f,g,o), b_ih/b_hh [4P].
+    LSTM: embedding [V+1,P], w_ih/w_hh [4P,P] (gate rows i,f,g,o), b_ih/b_hh [4P];
+    layers 2..L (spec.num_layers > 1): w_ih_rest/w_hh_rest [L-1,4P,P], b_ih_rest/b_hh_rest [L-1,4P].
     Stateless: embedding [c, V+1, P/c].  Joint: w_enc [H,D_e], b_enc [H],
     w_pred [H,P], b_pred [H], w_out [V+1,H], b_out [V+1]; TDT w_dur [|D|,H], b_dur [|D|].
     `blank_bias` is added to b_out[blank] before rounding.
@@ -99,6 +101,12 @@ def make_weights(spec: ModelSpec, seed: int = 0, blank_bias: float = 0.0) -> Dic
         nd = len(spec.durations)
         w["w_dur"] = _uniform(rng, (nd, H), H)
         w["b_dur"] = _uniform(rng, (nd,), H)
+    if spec.pred_kind == "lstm" and spec.num_layers > 1:   # drawn last: 1-layer weights unchanged per seed
+        Lr = spec.num_layers - 1
+        w["w_ih_rest"] = _uniform(rng, (Lr, 4 * P, P), P)
+        w["w_hh_rest"] = _uniform(rng, (Lr, 4 * P, P), P)
+        w["b_ih_rest"] = _uniform(rng, (Lr, 4 * P), P)
+        w["b_hh_rest"] = _uniform(rng, (Lr, 4 * P), P)
     return {k: bf16_round(v) for k, v in w.items()}
 
 

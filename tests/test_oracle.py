@@ -176,7 +176,60 @@ def test_lstm_step_matches_torch_lstmcell():
         with torch.no_grad():
             h, c = cell(x, (h, c))
         np.testing.assert_allclose(dec, h[0].numpy(), rtol=0, atol=1e-14)
-        np.testing.assert_allclose(st[1], c[0].numpy(), rtol=0, atol=1e-14)
+        np.testing.assert_allclose(st[1][0], c[0].numpy(), rtol=0, atol=1e-14)   # layer 0 cell state
+
+
+def test_multilayer_lstm_matches_torch_lstm():
+    """N4 ("more layers"): the L-layer predictor equals
+    torch.nn.LSTM(num_layers=L) in float64 (layer l reads the new h of layer
+    l-1), and its first layer is the 1-layer model of the same seed."""
+    P, L = 12, 3
+    spec = synth.ModelSpec(7, 8, P, 8, "lstm", 1, None, 0, 3, num_layers=L)
+    w = synth.make_weights(spec, 21)
+    model = Transducer.from_spec(spec, w)
+    w1 = synth.make_weights(synth.ModelSpec(7, 8, P, 8, "lstm", 1, None, 0, 3), 21)
+    assert all(np.array_equal(w[k], w1[k]) for k in w1)   # extra layers drawn last
+    lstm = torch.nn.LSTM(P, P, num_layers=L).double()
+    with torch.no_grad():
+        for layer in range(L):
+            sfx = "" if layer == 0 else "_rest"
+            pick = (lambda a: a) if layer == 0 else (lambda a, l=layer: a[l - 1])
+            getattr(lstm, f"weight_ih_l{layer}").copy_(torch.from_numpy(pick(w["w_ih" + sfx]).astype(np.float64)))
+            getattr(lstm, f"weight_hh_l{layer}").copy_(torch.from_numpy(pick(w["w_hh" + sfx]).astype(np.float64)))
+            getattr(lstm, f"bias_ih_l{layer}").copy_(torch.from_numpy(pick(w["b_ih" + sfx]).astype(np.float64)))
+            getattr(lstm, f"bias_hh_l{layer}").copy_(torch.from_numpy(pick(w["b_hh" + sfx]).astype(np.float64)))
+    st = model.pred_init()
+    hc = (torch.zeros(L, 1, P, dtype=torch.float64), torch.zeros(L, 1, P, dtype=torch.float64))
+    for y in [0, 3, 5, 1, 6, 2]:
+        dec, st = model.pred_step(st, y)
+        x = torch.from_numpy(w["embedding"][y].astype(np.float64))[None, None]
+        with torch.no_grad():
+            out, hc = lstm(x, hc)
+        np.testing.assert_allclose(dec, out[0, 0].numpy(), rtol=0, atol=1e-13)
+        np.testing.assert_allclose(st[0], hc[0][:, 0].numpy(), rtol=0, atol=1e-13)
+        np.testing.assert_allclose(st[1], hc[1][:, 0].numpy(), rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("tdt", [False, True])
+def test_multilayer_label_looping_equals_sequential(tdt):
+    """Alg. 3 == Alg. 1 with a 2-layer LSTM predictor on 60 seeded tiny configs."""
+    rng = np.random.default_rng(77 + tdt)
+    labels = 0
+    for _ in range(60):
+        T = int(rng.integers(1, 12))
+        B = int(rng.integers(1, 4))
+        spec = synth.ModelSpec(int(rng.integers(3, 8)), 6, 8, 8, "lstm", 1, [0, 1, 2, 3] if tdt else None, 0,
+                               int(rng.integers(1, 4)), num_layers=2)
+        model = Transducer.from_spec(spec, synth.make_weights(spec, int(rng.integers(1 << 30)),
+                                                              blank_bias=float(rng.uniform(-0.5, 1.0))))
+        enc = rng.normal(size=(B, T, 6))
+        lengths = rng.integers(0, T + 1, size=B)
+        lab, _ = decode_label_looping(model, enc, lengths, spec.max_symbols)
+        for b in range(B):
+            r = decode_sequential(model, enc[b], int(lengths[b]), spec.max_symbols)
+            assert (lab[b].tokens, lab[b].timestamps, lab[b].durations) == (r.tokens, r.timestamps, r.durations)
+            labels += len(r.tokens)
+    assert labels > 100
 
 
 def test_projections_and_joint_match_torch_linear():
