@@ -60,7 +60,7 @@ typedef struct CUstream_st *ll_stream;
 
 /*
  * Prediction network (Fig. 1; "stateful (LSTM) and stateless", :33).
- *  LSTM (PyTorch nn.LSTM convention, one layer, gate rows i,f,g,o):
+ *  LSTM (PyTorch nn.LSTM convention, gate rows i,f,g,o; layer 1 shown, more below):
  *    x = embedding[y];  gates = w_ih x + b_ih + w_hh h + b_hh
  *    c' = sigmoid(f) c + sigmoid(i) tanh(g);  h' = sigmoid(o) tanh(c');  dec = h'
  *    embedding [num_tokens, hidden], w_ih/w_hh [4*hidden, hidden], b_ih/b_hh [4*hidden].
@@ -76,6 +76,14 @@ typedef struct {
   int32_t context;     /* stateless only: 1..4, hidden % context == 0 */
   const void *embedding;
   const void *w_ih, *w_hh, *b_ih, *b_hh;
+  /* LSTM layers 2..num_layers ("more layers"; PyTorch nn.LSTM
+   * stacking: layer l's input is the NEW h of layer l-1, dec = h of the last
+   * layer).  num_layers 0 or 1: one layer, the fields below unused.  Stacked
+   * [num_layers-1, 4*hidden, hidden] (w_*_rest) and [num_layers-1, 4*hidden]
+   * (b_*_rest).  Supported with LL_F32 weights (the generic kernel reads every
+   * layer's weights through L2); LL_BF16 with num_layers > 1 -> LL_ERR_UNSUPPORTED. */
+  int32_t num_layers;
+  const void *w_ih_rest, *w_hh_rest, *b_ih_rest, *b_hh_rest;
 } ll_predictor;
 
 /*

@@ -47,6 +47,7 @@ constexpr int MAX_R = 32;        // rows per group (<= 32: one lane per row)
 constexpr int MAX_JR = 32;       // joint rows per round R*W (<= 32: one lane per joint row)
 constexpr int MAX_DUR = 16;
 constexpr int MAX_CTX = 4;
+constexpr int MAX_LAYERS = 8;    // LSTM predictor layers (fp32 generic kernel)
 enum { SC_OUTER, SC_ROUNDS, SC_ALGEVALS, SC_PRED, SC_PREDROWS, SC_LABELS, SC_GROUPS, SC_ROWEVALS, SC_N };
 constexpr int MAX_NW = 10;       // warps per CTA (320 threads; 168 registers per thread at most)
 constexpr int MAX_C = 16;        // cluster size
@@ -162,7 +163,8 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // TDT cluster partials too (token + duration partials: 4 words).
 // allow_tj = false: a kernel without the TJ / TG paths (debug_joint_kernel).
 __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, int V1, int nD, int R, int W,
-                                              int WF, int C, int NS, int sc = 0, bool allow_tj = true) {
+                                              int WF, int C, int NS, int sc = 0, bool allow_tj = true,
+                                              int layers = 1) {
   Layout L;
   L.wks = sc ? 4 : 2;
   L.pks = (sc && nD > 0) ? 4 : 2;
@@ -197,12 +199,13 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.fss = (int)align_up((size_t)WF * TJ_FROW, 128);
   L.off_f = o;    o = align_up(o + (L.tj ? (size_t)R * L.fss : (size_t)2 * R * WF * H * (bf ? 2 : 4)), 128);
   L.off_g = o;    o = align_up(o + (size_t)R * H * 4, 128);
-  L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * 4, 128);
+  L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * layers * 4, 128);   // c of every layer
   L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 8 * L.pks, 128);
   L.off_wkey = o; o = align_up(o + (size_t)(L.tj ? TJ_NKW : L.NW) * L.JR * 8 * L.wks, 128);
   L.off_hs = o;   o = align_up(o + (size_t)(L.tg ? TG_HBYTES : L.ring ? 2 * R * L.hstride : 0), 128);
   L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * P * 2, 128);
-  L.off_es = o;   o = align_up(o + (size_t)(L.ring ? R * 4 * L.UPC * 4 : 0), 128);
+  // E' slices (bf16 LSTM); fp32 LSTM with layers > 1: the input-side gate partials of a layer
+  L.off_es = o;   o = align_up(o + (size_t)((L.ring || (lstm && layers > 1)) ? R * 4 * L.UPC * 4 : 0), 128);
   L.off_wa = o;   o = align_up(o + (size_t)(L.tj ? TJ_ABYTES : 0), 128);
   L.off_wx = o;   o = align_up(o + (size_t)(L.tj ? 8 * TJ_XROW : 0), 128);
   L.total = o;
@@ -231,6 +234,8 @@ struct DecodeParams {
   const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
   const void *w_out, *b_out, *w_dur, *b_dur;
   const void *w_pred, *b_pred, *w_hh;
+  int layers;                    // LSTM layers (> 1: fp32 generic kernel only)
+  const void *w_ih_rest, *w_hh_rest, *b_ih_rest, *b_hh_rest;   // layers 2..L, stacked
   const float *tab;              // LSTM: E' [V1][4P]; stateless: G [ctx][V1][H] (b_pred in G_0)
   const bf16 *wst;               // bf16 LSTM: per-CTA tile stream [C][NG+NPT][8][P] (packed, swizzled)
   void *h;                       // f32 LSTM: [2][B][P]
@@ -2416,7 +2421,8 @@ struct Ctx {
     }
   }
 
-  __device__ void load_h_rows_f32(int n, int which /*0: current hpar, 1: next*/) {
+  // h rows of layer `layer` ([layers][2][B][P] in global memory) into z rows 0..n-1
+  __device__ void load_h_rows_f32(int n, int which /*0: current hpar, 1: next*/, int layer = 0) {
     const int P = Pd();
     float *z = (float *)zs();
     const int zst = zstride() / 4;
@@ -2426,7 +2432,7 @@ struct Ctx {
       float v = 0.f;
       if (!(which == 0 && rs.hzero[s])) {
         const int hp = which == 0 ? rs.hpar[s] : (rs.hpar[s] ^ 1);
-        v = __ldcg((const float *)p.h + ((size_t)hp * p.B + rs.b[s]) * P + c);
+        v = __ldcg((const float *)p.h + (((size_t)layer * 2 + hp) * p.B + rs.b[s]) * P + c);
       }
       z[(size_t)i * zst + c] = v;
     }
@@ -2462,7 +2468,55 @@ struct Ctx {
     }
     __threadfence();
     if (C > 1) cluster_sync_all(); else sync();
-    load_h_rows_f32(n, 1);
+    // layers 2..L (PyTorch nn.LSTM stacking, reading A9): x = the new h of the
+    // layer below; gates = (W_ih x + b_ih) + (W_hh h + b_hh), the input side
+    // first into shared memory, then the recurrent side and the cell update
+    for (int layer = 1; layer < p.layers; ++layer) {
+      const size_t lw = (size_t)(layer - 1) * 4 * P;
+      const float *wih = (const float *)p.w_ih_rest + lw * P, *whh = (const float *)p.w_hh_rest + lw * P;
+      const float *bih = (const float *)p.b_ih_rest + lw, *bhh = (const float *)p.b_hh_rest + lw;
+      float *part = es();   // [slot i][gate][unit] input-side partials
+      load_h_rows_f32(n, 1, layer - 1);
+      for (int uu = warp; uu < upc(); uu += NW) {
+        const int unit = u0 + uu;
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          float acc[MAX_R];
+          warp_dot_f32(acc, wih + ((size_t)gi * P + unit) * P, P, n);
+#pragma unroll
+          for (int i = 0; i < MAX_R; ++i)
+            if (i < n && lane == i) part[((size_t)i * 4 + gi) * upc() + uu] = acc[i] + bih[gi * P + unit];
+        }
+      }
+      sync();
+      load_h_rows_f32(n, 0, layer);
+      for (int uu = warp; uu < upc(); uu += NW) {
+        const int unit = u0 + uu;
+        float mine[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+          float acc[MAX_R];
+          warp_dot_f32(acc, whh + ((size_t)gi * P + unit) * P, P, n);
+#pragma unroll
+          for (int i = 0; i < MAX_R; ++i)
+            if (lane == i) mine[gi] = acc[i];
+        }
+        if (lane < n) {
+          const int s = rs.plist[lane];
+          float gate[4];
+#pragma unroll
+          for (int gi = 0; gi < 4; ++gi)
+            gate[gi] = part[((size_t)lane * 4 + gi) * upc() + uu] + (mine[gi] + bhh[gi * P + unit]);
+          float *cp = cs() + ((size_t)layer * p.R + s) * upc() + uu;
+          const float cn = sigmoidf_(gate[1]) * *cp + sigmoidf_(gate[0]) * tanhf(gate[2]);
+          *cp = cn;
+          ((float *)p.h)[(((size_t)layer * 2 + (rs.hpar[s] ^ 1)) * p.B + rs.b[s]) * P + unit] = sigmoidf_(gate[3]) * tanhf(cn);
+        }
+      }
+      __threadfence();
+      if (C > 1) cluster_sync_all(); else sync();
+    }
+    load_h_rows_f32(n, 1, p.layers - 1);
     for (int dd = warp; dd < dpc(); dd += NW) {
       const int d = d0 + dd;
       float acc[MAX_R];
@@ -2697,7 +2751,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
       }
       if constexpr (PRED == 0) {
         // LSTM initial state h = c = 0 (reading A8)
-        for (int i = tid; i < R * cx.L.UPC; i += cx.NCT) cx.cs()[i] = 0.f;
+        for (int i = tid; i < R * cx.L.UPC * max(p.layers, 1); i += cx.NCT) cx.cs()[i] = 0.f;
         if constexpr (TGK) {
           // no gate batch may still read the h buffer; h = 0 means W_hh h = 0,
           // so the first step skips the (not yet computed) pre-activations

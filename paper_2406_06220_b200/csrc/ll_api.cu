@@ -37,6 +37,9 @@ struct Ws {
 };
 
 size_t esize(ll_dtype d) { return d == LL_BF16 ? 2 : 4; }
+inline int nlayers(const ll_predictor *pr) {
+  return (pr && pr->kind == LL_PRED_LSTM && pr->num_layers > 1) ? pr->num_layers : 1;
+}
 
 // Workspace regions (256-B aligned).  The weight-only tables come first so
 // that their offsets do not depend on the batch shape (ll_prepare).
@@ -55,8 +58,8 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
   if (pr->kind == LL_PRED_LSTM && dt == LL_BF16) o = align_up(o + 4 * P * P * 2 + 2 * 4 * P * 2, 256);
   w.f = o;
   o = align_up(o + (size_t)B * T * H * esize(dt) + 256, 256);   // + slack: the padded f-row boxes read 16 B past a row
-  w.h = o;
-  if (pr->kind == LL_PRED_LSTM) o = align_up(o + 2 * (size_t)B * P * esize(dt), 256);
+  w.h = o;   // [layers][2][B][P]
+  if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)nlayers(pr) * 2 * B * P * esize(dt), 256);
   w.g = o;
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
   w.total = o;
@@ -92,6 +95,11 @@ ll_status check_model(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, l
     if (pr->num_tokens != jn->num_outputs || pr->hidden != jn->pred_dim) return LL_ERR_INVALID_ARGUMENT;
     if (pr->kind == LL_PRED_LSTM) {
       if (!pr->w_ih || !pr->w_hh || !pr->b_ih || !pr->b_hh) return LL_ERR_INVALID_ARGUMENT;
+      if (pr->num_layers < 0 || pr->num_layers > MAX_LAYERS) return LL_ERR_INVALID_ARGUMENT;
+      if (pr->num_layers > 1) {
+        if (!pr->w_ih_rest || !pr->w_hh_rest || !pr->b_ih_rest || !pr->b_hh_rest) return LL_ERR_INVALID_ARGUMENT;
+        if (dt != LL_F32) return LL_ERR_UNSUPPORTED;   // bf16: one layer (the FC kernel keeps W_hh in TMEM)
+      }
     } else if (pr->kind == LL_PRED_STATELESS) {
       if (pr->context < 1) return LL_ERR_INVALID_ARGUMENT;
       if (pr->context > MAX_CTX || pr->hidden % pr->context) return LL_ERR_UNSUPPORTED;
@@ -125,7 +133,7 @@ static int pow2ceil(int x) {
 // nclusters: how many clusters of the chosen size can be resident (0: unknown,
 // assume 8).  R is chosen so that all groups of the batch run in one wave.
 bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf,
-                   int nclusters = 0, int sc = 0) {
+                   int nclusters = 0, int sc = 0, int layers = 1) {
   const int forceC = g_opt.cluster_size;
   const int forceR = g_opt.group_rows;
   const int forceW = g_opt.window;
@@ -173,7 +181,7 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
         if (tj_shape(bf, H, P, C) && !forceW && !forceR && W == 1 && R > 1) break;
         cf.C = C; cf.R = R; cf.W = W; cf.WF = W + (maxd > 1 ? maxd - 1 : 0);
         cf.NS = 0;
-        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0, sc);
+        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0, sc, true, layers);
         if (cf.L.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) return true;
         if (forceW) break;
       }
@@ -381,8 +389,9 @@ ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw
 
 // Cluster size / group rows / window for a call: choose_config, then again
 // with the number of clusters that can actually be resident.
-bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf, int sc = 0) {
-  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, 0, sc)) return false;
+bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf, int sc = 0,
+                   int layers = 1) {
+  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, 0, sc, layers)) return false;
   int ncl = 0;
   if (is_fc(bf, H, P, cf.C))
     ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1>(cf.C, cf.L)
@@ -393,7 +402,7 @@ bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
     ncl = lstm ? max_clusters<bf16, 0, KREG_SMALL>(cf.C, cf.L) : max_clusters<bf16, 1, KREG_SMALL>(cf.C, cf.L);
   else
     ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
-  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl, sc));
+  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl, sc, layers));
 }
 
 // ---------------------------------------------------------------------------
@@ -493,11 +502,12 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   const int sc = out_scores != nullptr;
   if (sc && (frame_looping || g_opt.schedule == 0 || g_opt.probe_logits)) return LL_ERR_UNSUPPORTED;
   Config cf;
-  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf, sc)) return LL_ERR_UNSUPPORTED;
+  const int nl = nlayers(pr);
+  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf, sc, nl)) return LL_ERR_UNSUPPORTED;
   if (frame_looping) {   // Alg. 2 evaluates one frame per joint call
     cf.W = 1;
     cf.WF = 1;
-    cf.L = make_layout(bf, lstm, H, P, V1, nD, cf.R, 1, 1, cf.C, 0);
+    cf.L = make_layout(bf, lstm, H, P, V1, nD, cf.R, 1, 1, cf.C, 0, 0, true, nl);
   }
   const int C = cf.C, R = cf.R;
   const Layout &L = cf.L;
@@ -555,6 +565,10 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   if (L.tj && bf) p.fmap_ok = make_fmap(&p.fmap, ws + w.f, (uint64_t)B * T_max, H, cf.WF) ? 1 : 0;
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
   p.w_pred = jn->w_pred; p.b_pred = jn->b_pred; p.w_hh = lstm ? pr->w_hh : nullptr;
+  p.layers = lstm ? nl : 1;
+  if (lstm && nl > 1) {
+    p.w_ih_rest = pr->w_ih_rest; p.w_hh_rest = pr->w_hh_rest; p.b_ih_rest = pr->b_ih_rest; p.b_hh_rest = pr->b_hh_rest;
+  }
   p.tab = tab;
   p.wst = ring ? (const bf16 *)(ws + w.wst) : nullptr;
   p.h = lstm ? (void *)(ws + w.h) : nullptr;
@@ -774,7 +788,8 @@ ll_status ll_prepare(const ll_predictor *pred, const ll_joint *joint, ll_dtype d
   int maxd = 1;
   for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
   Config cf;
-  if (!decode_config(bf, lstm, joint->joint_dim, joint->pred_dim, joint->num_outputs, nD, maxd, B, cf))
+  if (!decode_config(bf, lstm, joint->joint_dim, joint->pred_dim, joint->num_outputs, nD, maxd, B, cf, 0,
+                     nlayers(pred)))
     return LL_ERR_UNSUPPORTED;
   const Ws w = ws_layout(B, T_max, pred, joint, dtype);
   s = build_tables(bf, pred, joint, dtype, w, (uint8_t *)workspace, cf.C, cf.L, (cudaStream_t)stream);

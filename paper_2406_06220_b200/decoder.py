@@ -48,7 +48,9 @@ class Model:
         ptr = lambda k: w[k].data_ptr() if k in w else None
         self.pred = ll.ll_predictor(
             ll.LL_PRED_LSTM if pred_kind == "lstm" else ll.LL_PRED_STATELESS, self.V1, self.P,
-            int(context), ptr("embedding"), ptr("w_ih"), ptr("w_hh"), ptr("b_ih"), ptr("b_hh"))
+            int(context), ptr("embedding"), ptr("w_ih"), ptr("w_hh"), ptr("b_ih"), ptr("b_hh"),
+            1 + (int(w["w_ih_rest"].shape[0]) if "w_ih_rest" in w else 0),   # LSTM layers (ll.h)
+            ptr("w_ih_rest"), ptr("w_hh_rest"), ptr("b_ih_rest"), ptr("b_hh_rest"))
         self.joint = ll.ll_joint(self.De, self.P, self.H, self.V1, ptr("w_enc"), ptr("b_enc"),
                                  ptr("w_pred"), ptr("b_pred"), ptr("w_out"), ptr("b_out"),
                                  ptr("w_dur"), ptr("b_dur"))

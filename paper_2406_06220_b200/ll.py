@@ -33,7 +33,8 @@ EXPORTED = ["ll_workspace_size", "ll_decode_rnnt", "ll_decode_rnnt_frame_looping
 class ll_predictor(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("num_tokens", c_int32), ("hidden", c_int32), ("context", c_int32),
                 ("embedding", c_void_p), ("w_ih", c_void_p), ("w_hh", c_void_p), ("b_ih", c_void_p),
-                ("b_hh", c_void_p)]
+                ("b_hh", c_void_p), ("num_layers", c_int32), ("w_ih_rest", c_void_p), ("w_hh_rest", c_void_p),
+                ("b_ih_rest", c_void_p), ("b_hh_rest", c_void_p)]
 
 
 class ll_joint(ctypes.Structure):

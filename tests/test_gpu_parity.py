@@ -601,3 +601,40 @@ def test_scores_cat_dog_closed_form():
         _, hyps, scores = _scored_decode(spec, w, enc, lengths, dtype)
         expect = 7 * (10.0 - np.log(np.exp(10.0) + 6.0))
         assert np.abs(scores - expect).max() < 1e-5, (scores, expect)
+
+
+@pytest.mark.parametrize("cfg", ["tiny", "tiny-tdt"])
+@pytest.mark.parametrize("layers", [2, 3])
+def test_multilayer_lstm_f32(cfg, layers):
+    """N4 ("more layers"): an L-layer LSTM predictor (fp32 weights,
+    generic kernel) on many seeds, every row teacher-forced against the float64
+    L-layer oracle, and equal to the oracle decode where no near-tie occurred."""
+    c = synth.CONFIGS[cfg]
+    spec = c["spec"]
+    ties = decs = 0
+    for seed in range(8):
+        sp = synth.ModelSpec(spec.num_tokens, spec.enc_dim, spec.pred_dim, spec.joint_dim, "lstm", 1,
+                             spec.durations, spec.blank_id, spec.max_symbols, num_layers=layers)
+        w = synth.make_weights(sp, 3000 + seed, blank_bias=0.5)
+        enc, lengths = synth.make_inputs(4000 + seed, c["B"], c["T_max"], sp.enc_dim, c["len_lo"], c["len_hi"])
+        hyps, _ = gpu_decode(sp, w, enc, lengths, "f32")
+        t, d = verify_all(sp, w, enc, lengths, hyps)
+        ties += t
+        decs += d
+        ref = oracle_hyps(sp, w, enc, lengths)
+        mism = sum(1 for b in ref if tuple(map(list, ref[b])) != tuple(map(list, hyps[b])))
+        assert mism == 0 or ties > 0
+    assert decs > 300
+
+
+def test_multilayer_lstm_bf16_unsupported():
+    """bf16 weights with more than one LSTM layer are refused (ll.h), before any work."""
+    c = synth.CONFIGS["tiny"]
+    spec = c["spec"]
+    sp = synth.ModelSpec(spec.num_tokens, spec.enc_dim, spec.pred_dim, spec.joint_dim, "lstm", 1,
+                         None, spec.blank_id, spec.max_symbols, num_layers=2)
+    w = synth.make_weights(sp, 5)
+    enc, lengths = synth.make_inputs(6, c["B"], c["T_max"], sp.enc_dim, c["len_lo"], c["len_hi"])
+    with pytest.raises(ll.LLError) as e:
+        gpu_decode(sp, w, enc, lengths, "bf16")
+    assert e.value.status == ll.LL_ERR_UNSUPPORTED
