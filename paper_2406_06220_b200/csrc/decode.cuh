@@ -10,33 +10,41 @@
 //
 //   outer step (label loop, Alg. 3 line 5):
 //     predictor phase (Alg. 3 line 6) for rows that found a label and are still
-//       active.  LSTM (bf16): gates = E'[y] + W_hh h on tensor cores; this CTA's
-//       W_hh slice is resident in TMEM for the whole kernel (loaded once, read
-//       with tcgen05.ld as the m16 A operand of mma.sync) and its W_pred slice
-//       is resident in shared memory; E'[y] slices arrive by bulk copies; gate
-//       nonlinearities + cell update fused in the epilogue (c stays in its
-//       owner CTA); h' and g = W_pred h' + b_pred slices are exchanged between
-//       the CTAs with st.async + mbarriers (no global memory, no cluster
-//       barrier).  Stateless: g = sum_k G_k[ctx_k] (precomputed tables).
+//       active.  FastConformer shape (TG, see TG_* below): gates = E'[y] + W_hh h
+//       where W_hh h was computed in the BACKGROUND on tcgen05 (A = this CTA's
+//       W_hh slice, resident in TMEM) as soon as h was known -- it does not
+//       depend on the label; the cell update reads it back from TMEM.  h' and
+//       g = W_pred h' + b_pred (W_pred in registers, mma.sync, K split over the
+//       warps) slices are exchanged between the CTAs with st.async + mbarriers
+//       (no global memory, no cluster barrier).  Other shapes: the gate GEMM on
+//       mma.sync with W_hh read from TMEM (tcgen05.ld), or fp32 SIMT with the
+//       weights read through L2 (any number of LSTM layers).  Stateless:
+//       g = sum_k G_k[ctx_k] (precomputed tables).
 //     scan (frame loop, Alg. 3 lines 7-19) in ROUNDS.  While a row scans, its
 //       predictor output g is fixed, so the joint at frames t..t+W-1 does not
 //       depend on the blank decisions between them: a round evaluates a W-frame
 //       window of every scanning row at once and then applies the decisions in
 //       frame order (first non-blank wins; TDT follows the duration chain).
 //       This is an exact reordering of the inner loop.
-//       Per round:
-//         z = ReLU(f[b, t..t+W-1] + g_b)                     (bf16, shared memory)
-//         joint GEMM [R*W x H] x [H x slice of V+1(+|D|)]    (mma.sync; the CTA's
-//           weight slice lives in REGISTERS for the whole kernel)
-//         argmax fused in the epilogue (packed 64-bit keys, warp shuffles),
+//       Per round (FastConformer shape, TJ, see TJ_* below):
+//         z = ReLU(f[b, t..t+W-1] + g_b)            (bf16, the swizzled B operand)
+//         joint GEMM on tcgen05: this CTA's 64 vocabulary rows K-folded into an
+//           M = 128 A operand (shared memory), z rows as N, D' in TMEM; the
+//           <= 8 extra rows of the CTA on mma.sync
+//         argmax fused in the TMEM epilogue (packed 64-bit keys, butterfly),
 //         per-CTA partial keys st.async'ed to every CTA of the cluster,
 //         mbarrier completion, every CTA reduces the C partials and applies the
 //         same rules -> replicated row state.
-//       f rows arrive by bulk copies; the next window is prefetched
+//       (Other shapes: the joint weight slice in registers, mma.sync.)
+//       f windows arrive by tensor / bulk copies; the next window is prefetched
 //       speculatively (assuming the row keeps scanning).
 //     append + time rules + guard (BatchedHyps add_results):
 //       masked append into the caller's preallocated [B, cap] buffers, one lane
 //       per row (each row has one owner, no atomics).
+//
+// Warps: 10 consumer warps run the control loop; in the TJ instantiations an
+// 11th "MMA warp" sleeps on an mbarrier and executes the commands consumer
+// thread 0 posts (tcgen05 gate batches, the joint MMAs, the f window copies).
 #pragma once
 #include <cuda.h>
 #include "common.cuh"
@@ -53,7 +61,6 @@ constexpr int MAX_NW = 10;       // warps per CTA (320 threads; 168 registers pe
 constexpr int MAX_C = 16;        // cluster size
 constexpr int KREG = 20;         // 32-wide K blocks of the joint weight slice held in registers (H <= 656)
 constexpr int KREG_SMALL = 4;    // small-H instantiation (H <= 144): no register budget lost to padding
-constexpr int NSMAX = 8;         // weight-ring slots
 constexpr int TL_N = 128;        // timeline: rounds / predictor steps recorded
 constexpr int TL_PH = 16;        // timeline: phase slots per event
 
@@ -65,15 +72,14 @@ enum {
   BAR_ACK = 6,      // [2] (rank 0) acknowledgements of the group index
   BAR_H = 8,        // h' slices arriving
   BAR_G = 9,        // g slices arriving
-  BAR_FULL = 10,    // [NSMAX] weight ring: tile landed
-  BAR_EMPTY = 10 + NSMAX,  // [NSMAX] weight ring: tile consumed
-  BAR_E = 10 + 2 * NSMAX,  // E' slices of the predictor rows landed
-  BAR_GQ = 11 + 2 * NSMAX,   // (TJ) MMA warp: a command was posted (consumer thread 0 arrives)
-  BAR_GATE = 12 + 2 * NSMAX, // (TG) gate batch complete (tcgen05.commit)
-  BAR_MACK = 13 + 2 * NSMAX, // (TJ) MMA warp: command read (the command word may be reused)
-  BAR_JOINT = 14 + 2 * NSMAX,// (TJ) joint MMAs complete (tcgen05.commit)
-  BAR_SPEC = 15 + 2 * NSMAX, // (TJ) MMA warp: speculative copies issued, fbase / fcnt written
-  NBARS = 16 + 2 * NSMAX
+  BAR_FULL = 10,    // W_pred tiles landed (generic bf16 LSTM, kernel start)
+  BAR_E = 11,       // E' slices of the predictor rows landed
+  BAR_GQ = 12,      // (TJ) MMA warp: a command was posted (consumer thread 0 arrives)
+  BAR_GATE = 13,    // (TG) gate batch complete (tcgen05.commit)
+  BAR_MACK = 14,    // (TJ) MMA warp: command read (the command word may be reused)
+  BAR_JOINT = 15,   // (TJ) joint MMAs complete (tcgen05.commit)
+  BAR_SPEC = 16,    // (TJ) MMA warp: speculative copies issued, fbase / fcnt written
+  NBARS = 17
 };
 enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3, MCMD_FLOAD = 4 };
 
@@ -274,9 +280,7 @@ struct RowState {
   int nscan, npred, nactive, nz, ready;
   int grp[2];                            // group index broadcast (double-buffered)
   int ack[2];
-  volatile int done;                     // consumers finished (producer exits)
   volatile int mcmd;                     // (TJ) command word for the MMA warp (MCMD_*)
-  volatile unsigned tag[NSMAX];          // ring: index of the tile last issued into each slot
 };
 
 // Consumer-only CTA barrier (named barrier 1): the producer warp never joins.
