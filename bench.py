@@ -60,6 +60,11 @@ def parse():
                     help="time the Alg. 2 frame-looping baseline (ll_decode_rnnt_frame_looping) instead")
     ap.add_argument("--schedule", default="ticks", choices=["ticks", "batched"],
                     help="label-looping schedule: per-row ticks (default) or the batched outer loop of Alg. 3 as listed")
+    ap.add_argument("--projections", default="precompute", choices=["precompute", "on-the-fly"],
+                    help="joint input projections precomputed (default, PAPER.md §3.4) or applied at every joint "
+                         "evaluation (the ablation arm of Table 3; ll_options.projections = 1)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="decode only the first B utterances of the config's batch (Table 3's batch sizes 1 / 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0: auto)")
     return ap.parse_args()
@@ -310,8 +315,10 @@ def main():
     from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
     llbuild.build()
-    if a.schedule == "batched":     # the paper's batched outer loop (Alg. 3 as listed), this thread
-        if ll.ll_set_options(ll.options(schedule=0).opts) != ll.LL_OK:
+    if a.schedule == "batched" or a.projections == "on-the-fly":   # ll_options of this thread
+        o = ll.options(schedule=0 if a.schedule == "batched" else -1,
+                       projections=1 if a.projections == "on-the-fly" else 0).opts
+        if ll.ll_set_options(o) != ll.LL_OK:
             raise RuntimeError("ll_set_options")
     torch.cuda.set_device(local)
     if world > 1:
@@ -322,6 +329,8 @@ def main():
 
     # weak scaling: every rank decodes its own batch (seed 1000 + rank)
     spec, w, enc_np, len_np = workload(a.config, 1000 + rank, a.family)
+    if a.batch > 0:   # the first B utterances of the seeded batch
+        enc_np, len_np = enc_np[:a.batch].copy(), len_np[:a.batch].copy()
     B, T = enc_np.shape[0], enc_np.shape[1]
     model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16", device=f"cuda:{local}")
     dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, frame_looping=a.frame_looping)
@@ -480,6 +489,8 @@ def main():
     if os.path.exists(pk_path):
         peaks = json.load(open(pk_path))
     peak = peaks.get("bf16_tflops", 1590.0)
+    if a.projections == "on-the-fly":   # the decode kernel also does the projections (a1 is counted once)
+        a2 += a1
     achieved = (a2 + a3) / (kern_mean / 1e3) / 1e12
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -499,6 +510,9 @@ def main():
                    "algorithm": "frame-looping (Alg. 2 baseline)" if a.frame_looping else
                    ("label-looping (Alg. 3), batched outer loop" if a.schedule == "batched"
                     else "label-looping (Alg. 3), per-row ticks"),
+                   "projections": a.projections + (" (W_enc, W_pred applied at every joint evaluation, inside "
+                                                   "the decode kernel; no f)" if a.projections == "on-the-fly" else
+                                                   " (encoder GEMM over all frames + g once per predictor step)"),
                    "frames": int(len_np.sum()), "audio_s_per_step": audio_s, "l2": "flushed (512 MiB) between steps",
                    "model_tables": "prepared once per model (ll_prepare), outside the step",
                    "parallelism": f"utterance-sharded x{world} (each rank its own B={B} batch)"},
@@ -508,7 +522,8 @@ def main():
                 "mode": "serving loop: step i+1's H2D overlaps step i's decode (H2D / D2H streams, 2 workspaces)",
                 "single_call": {"ms": single_ms, "value": audio_s / (single_ms / 1e3), "unit": UNIT,
                                 "mode": "one call at a time: H2D, decode, D2H back to back on one stream (latency)"}},
-        "gpu_launches": a.steps * 2,   # encoder projection GEMM + decode kernel (tables prepared once)
+        # encoder projection GEMM + decode kernel (tables prepared once); on the fly: the decode kernel only
+        "gpu_launches": a.steps * (1 if a.projections == "on-the-fly" else 2),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "decode_kernel",
                      "kernel_ms": kern_mean, "kernel_share_of_step": kern_mean / (tot_ms_max / a.steps),

@@ -308,6 +308,19 @@ ll_status ll_release(void *workspace);
  *    probe_counts  DEVICE i32 [probe_regions][2]: logit rows, g rows written
  *                  (values > probe_rows mean the region was truncated)
  *  Set probe_logits = NULL to disable the probe.
+ *
+ *  projections    0 (default): the joint's input projections are precomputed
+ *                 (encoder: one GEMM over all frames before the decode, Alg. 3
+ *                 line 2; predictor: once per predictor step, line 6 --
+ *                 PAPER.md §3.4 :216-222).  1: ON THE FLY -- the ablation arm of
+ *                 the paper's Table 3: the decode kernel reads
+ *                 the encoder rows themselves and applies W_enc and W_pred (+ both
+ *                 biases) at every joint evaluation; no f is stored.  Supported
+ *                 for bf16, 1-layer LSTM predictors of the FastConformer shape
+ *                 (H = P = 640), D_e a multiple of 32 and <= 1024, the per-row
+ *                 tick schedule, no scores / probe, RNN-T and TDT (label-looping);
+ *                 anything else returns LL_ERR_UNSUPPORTED.  Same hypotheses up
+ *                 to near-ties (f is not rounded to bf16 on this path).
  */
 typedef struct {
   int32_t cluster_size, group_rows, window, max_clusters;
@@ -320,6 +333,7 @@ typedef struct {
   int32_t *probe_gmeta;
   int32_t *probe_counts;
   int32_t probe_rows, probe_regions;
+  int32_t projections;
 } ll_options;
 
 ll_status ll_set_options(const ll_options *options);

@@ -79,7 +79,8 @@ enum {
   BAR_MACK = 14,    // (TJ) MMA warp: command read (the command word may be reused)
   BAR_JOINT = 15,   // (TJ) joint MMAs complete (tcgen05.commit)
   BAR_SPEC = 16,    // (TJ) MMA warp: speculative copies issued, fbase / fcnt written
-  NBARS = 17
+  BAR_Z = 17,       // (OTF) z slices of the other CTAs arriving (st.async)
+  NBARS = 18
 };
 enum { MCMD_GATES = 1, MCMD_JOINT = 2, MCMD_EXIT = 3, MCMD_FLOAD = 4 };
 
@@ -152,12 +153,35 @@ __host__ __device__ inline bool tj_shape(bool bf, int H, int P, int C) {
   return bf && H == TJ_H && P == TJ_H && C == TJ_C;
 }
 
+// ---------------------------------------------------------------------------
+// OTF: on-the-fly projections (the "w/o precomputation" arm of the paper's
+// Table 3; §3.4 :216-222 is the precompute it ablates).  The
+// FC LSTM tick kernel (LM = 4) reads ENCODER rows instead of precomputed f rows
+// and applies both joint input projections at every joint evaluation:
+//   z[k] = bf16(ReLU(W_enc e[b, t] + b_enc + W_pred h_s + b_pred))
+// for the live joint rows k of a round, distributed by output dims: each CTA
+// computes its 40 dims (mma.sync, K = D_e + P split over the 10 consumer warps;
+// W_pred fragments in registers as in the precompute kernel, W_enc fragments
+// read through L2 every round) and st.async's the 16-byte z chunks into the
+// swizzled z operand of every CTA of the cluster (BAR_Z), so no f or g is
+// stored.  The predictor step produces h' only.
+//   encoder rows in shared memory: stride 2 D_e + 16 bytes (one bulk copy per
+//   frame; conflict-free 8-row x 16-byte B-fragment loads)
+//   K-split partials [10 warps][16 rows][44] f32 in the g region (OTF_PART)
+// ---------------------------------------------------------------------------
+constexpr int OTF_ROWS = 16;                                   // joint rows per projection pass
+constexpr int OTF_PS = 44;                                     // partial row stride (floats, conflict-free)
+constexpr int OTF_PART = MAX_NW * OTF_ROWS * OTF_PS * 4;       // 28160 bytes
+constexpr int OTF_MAX_DE = 1024;
+__host__ __device__ inline int otf_row(int De) { return 2 * De + 16; }
+
 // Shared-memory layout (identical on host and device).
 struct Layout {
   int zstride, hstride, tiles_max, UPC, DPC, NW, JR, JRp, ring, NS;
   int tg, tj, NTH;               // TG (tcgen05 gate pre-activations), TJ (tcgen05 joint + MMA warp), threads per CTA
   size_t off_wa, off_wx;         // TJ: joint weight slice (A operand), extra tile weights
   int fss;                       // TJ: f bytes per slot (WF padded rows, 128-byte aligned for the tensor copy)
+  int otf;                       // on-the-fly projections (OTF_*): encoder rows of D_e = otf elements, else 0
   int wks, pks;                  // u64 words per per-warp key entry / per cluster partial (scores: 4)
   size_t off_b, off_z, off_f, off_g, off_c, off_part, off_wkey, off_hs, off_ring, off_es, total;
 };
@@ -170,8 +194,9 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // allow_tj = false: a kernel without the TJ / TG paths (debug_joint_kernel).
 __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, int V1, int nD, int R, int W,
                                               int WF, int C, int NS, int sc = 0, bool allow_tj = true,
-                                              int layers = 1) {
+                                              int layers = 1, int otf_de = 0) {
   Layout L;
+  L.otf = otf_de;
   L.wks = sc ? 4 : 2;
   L.pks = (sc && nD > 0) ? 4 : 2;
   if (allow_tj && tj_shape(bf, H, P, C) && !sc && nD == 0) L.pks = 1;   // TJ RNN-T: the token key alone
@@ -202,9 +227,12 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
     if (L.ring && zb < wp) zb = wp;
     o = align_up(o + zb, 128);
   }
-  L.fss = (int)align_up((size_t)WF * TJ_FROW, 128);
+  L.fss = (int)align_up((size_t)WF * (otf_de ? otf_row(otf_de) : TJ_FROW), 128);
   L.off_f = o;    o = align_up(o + (L.tj ? (size_t)R * L.fss : (size_t)2 * R * WF * H * (bf ? 2 : 4)), 128);
-  L.off_g = o;    o = align_up(o + (size_t)R * H * 4, 128);
+  {   // OTF: g is not kept; the region holds the projection's K-split partials
+    const size_t gb = (size_t)R * H * 4, pb = otf_de ? (size_t)OTF_PART : 0;
+    L.off_g = o;  o = align_up(o + (gb > pb ? gb : pb), 128);
+  }
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * layers * 4, 128);   // c of every layer
   L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 8 * L.pks, 128);
   L.off_wkey = o; o = align_up(o + (size_t)(L.tj ? TJ_NKW : L.NW) * L.JR * 8 * L.wks, 128);
@@ -262,6 +290,9 @@ struct DecodeParams {
   float *dbg_logits;
   int *dbg_argmax, *dbg_dargmax;
   int dbg_n;
+  // OTF (LM = 4): p.f points at the ENCODER output [B, T_max, De] (bf16)
+  int De;
+  const void *w_enc, *b_enc;
 };
 
 struct RowState {
@@ -293,7 +324,8 @@ __device__ __forceinline__ void csync(int nthreads) {
 // (0 = runtime).  The production shape (H = P = 640, 16-CTA clusters) is
 // instantiated with all three fixed so that loops unroll and addressing folds.
 // SC: 1 = greedy scores (N2): log-sum-exp partials ride along with the argmax keys.
-template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0, int SC = 0>
+// OTF: 1 = on-the-fly projections (OTF_* above; FC LSTM tick kernel only).
+template <typename T, int KR, int HC = 0, int PC = 0, int CC = 0, int TM = 0, int SC = 0, int OTF = 0>
 struct Ctx {
   static constexpr bool BF = sizeof(T) == 2;
   // the FC LSTM shape: tcgen05 gate pre-activations (see TG_* above); only the
@@ -414,6 +446,10 @@ struct Ctx {
     const int a = c >= 40 ? 1 : 0, cc = c - 40 * a;
     return (cc >> 3) * 8192 + a * 4096 + (k >> 3) * 1024 + (k & 7) * 128 + (((cc & 7) ^ (k & 7)) << 4);
   }
+  // TJ window rows: bytes per source row (f, or the encoder row under OTF) and
+  // the padded row stride in shared memory
+  __device__ __forceinline__ int frow_src() const { return OTF ? p.De * 2 : TJ_H * 2; }
+  __device__ __forceinline__ int frow_smem() const { return OTF ? otf_row(p.De) : TJ_FROW; }
   __device__ uint8_t *fbuf(int X) const {
     if constexpr (TJ) return sm + L.off_f;   // one buffer (the bookkeeping of both halves is kept)
     else return sm + L.off_f + (size_t)X * p.R * p.WF * Hd() * sizeof(T);
@@ -533,8 +569,9 @@ struct Ctx {
     const int V1 = p.V1, NV = p.V1 + p.nD, H = Hd();
     float *bs = bsl();
     if constexpr (TJ) {   // bias: [0, 64) main rows, [64, 64 + nx) extra rows; [72, 72 + 40) b_pred slice (LSTM)
-      if (p.b_pred != nullptr && p.w_hh != nullptr)
-        for (int r = tid; r < TG_UPC; r += NCT) bs[72 + r] = to_f32(((const T *)p.b_pred)[d0 + r]);
+      if (p.b_pred != nullptr && p.w_hh != nullptr)   // OTF: b_pred + b_enc (both projections per round)
+        for (int r = tid; r < TG_UPC; r += NCT)
+          bs[72 + r] = to_f32(((const T *)p.b_pred)[d0 + r]) + (OTF ? to_f32(((const T *)p.b_enc)[d0 + r]) : 0.f);
       for (int r = tid; r < 72; r += NCT) {
         const int v = r < 64 ? vm0 + r : vx0 + (r - 64);
         float bv = 0.f;
@@ -632,7 +669,7 @@ struct Ctx {
       if (cnt < 0) cnt = 0;
       rs.fbase[X][s] = base;
       rs.fcnt[X][s] = cnt;
-      bytes = cnt > 0 ? (p.fmap_ok ? (uint32_t)(p.WF * TJ_FROW) : (uint32_t)(cnt * TJ_H * 2)) : 0u;
+      bytes = cnt > 0 ? (p.fmap_ok ? (uint32_t)(p.WF * TJ_FROW) : (uint32_t)(cnt * frow_src())) : 0u;
     }
     uint32_t tot = bytes;
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
@@ -647,9 +684,10 @@ struct Ctx {
             "l"(&p.fmap), "r"(0), "r"(0), "r"(rs.b[s] * p.T_max + base), "r"(smem_u32(bar(BAR_F + X)))
             : "memory");
       } else {
-        const uint8_t *src = (const uint8_t *)p.f + ((size_t)rs.b[s] * p.T_max + base) * (TJ_H * 2);
+        const int rb = frow_src(), rst = frow_smem();
+        const uint8_t *src = (const uint8_t *)p.f + ((size_t)rs.b[s] * p.T_max + base) * rb;
         for (int i = 0; i < cnt; ++i)
-          bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * TJ_FROW, src + (size_t)i * TJ_H * 2, TJ_H * 2, bar(BAR_F + X));
+          bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * rst, src + (size_t)i * rb, rb, bar(BAR_F + X));
       }
     }
   }
@@ -667,7 +705,7 @@ struct Ctx {
     if (fpend(X)) wait_f(X);  // drain a stale speculative copy first
     if (TJ && fpend(X ^ 1)) wait_f(X ^ 1);   // one buffer behind both halves
     const int n = list ? nlist : rs.nscan;
-    const uint32_t frb = (uint32_t)(Hd() * sizeof(T));
+    const uint32_t frb = TJ ? (uint32_t)frow_src() : (uint32_t)(Hd() * sizeof(T));
     if (warp == iw) {
       uint32_t bytes = 0;
       int s = 0, base = 0, cnt = 0;
@@ -698,7 +736,7 @@ struct Ctx {
                   : "memory");
             } else {
               for (int i = 0; i < cnt; ++i)
-                bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * TJ_FROW, src + (size_t)i * frb, frb, bar(BAR_F + X));
+                bulk_g2s(fbuf(X) + (size_t)s * L.fss + (size_t)i * frow_smem(), src + (size_t)i * frb, frb, bar(BAR_F + X));
             }
           } else {
             bulk_g2s(fbuf(X) + (size_t)s * p.WF * frb, src, bytes, bar(BAR_F + X));
@@ -721,7 +759,7 @@ struct Ctx {
       const int s = rs.slist[lane / W], j = lane % W;
       const int fr = rs.t[s] + j - rs.fbase[X][s];
       live = rs.t[s] + j < rs.L[s] && fr >= 0 && fr < rs.fcnt[X][s];
-      src = TJ ? (s * L.fss + fr * TJ_FROW) / 2 : (s * p.WF + fr) * Hd();
+      src = TJ ? (s * L.fss + fr * frow_smem()) / 2 : (s * p.WF + fr) * Hd();
       dst = s * W + j;
     }
     const unsigned m = __ballot_sync(0xffffffffu, live);
@@ -762,7 +800,7 @@ struct Ctx {
       rs.zcnt[lane] = cnt;
     }
     for (int j = 0; j < cnt; ++j) {
-      rs.zsrc[beg + j] = (lane * L.fss + j * TJ_FROW) / 2;
+      rs.zsrc[beg + j] = (lane * L.fss + j * frow_smem()) / 2;
       rs.zdst[beg + j] = lane * W + j;
     }
     if (lane == 31) rs.nz = incl;
@@ -864,6 +902,154 @@ struct Ctx {
                               fmaxf(fv.w + gv.w, 0.f));
         }
       }
+    }
+  }
+
+  // OTF (replaces build_z): the round's z rows with both projections applied
+  // now (OTF_* above).  Per pass of 16 joint rows, warp w sums its K blocks --
+  // h' (kb = w, w + 10: W_pred fragments in registers, h' of the row's slot from
+  // the h buffer) and the encoder row (kb = w, w + 10, .. < D_e / 32: W_enc
+  // fragments through L2) -- for the CTA's 40 output dims (3 m16 tiles, rows
+  // 40..47 zero) x 2 n8 tiles, as partials P[w][row][dim]; one thread per
+  // (row, 16-byte chunk) then sums the 10 partials in warp order, adds
+  // b_enc + b_pred, applies ReLU, rounds to bf16 and stores the chunk into its
+  // own z and every other CTA's z (st.async, tx on BAR_Z).  Remote writes are
+  // safe: a CTA projects round r + 1 only after every CTA's round-r keys, which
+  // each CTA sends after its joint MMAs (the readers of z) completed; the gate
+  // scratch in z (predictor step) is read before the h' slices that another
+  // CTA waits for are sent.
+  __device__ __forceinline__ uint32_t zph() const { return (phs >> 14) & 1u; }
+  __device__ void project_z(int X) {
+    if constexpr (OTF) {
+      constexpr int CPC = TJ_H / 8 / TJ_C;   // 16-byte z chunks per CTA (5)
+      const int nz = rs.nz, KBE = p.De / 32;
+      if (tid == 0) mbar_arrive_expect_tx(bar(BAR_Z), (uint32_t)((C - 1) * nz * CPC * 16));
+      const uint32_t fb = smem_u32(fbuf(X)), hb = smem_u32(hbuf()), zb = smem_u32(zs()), bz = smem_u32(bar(BAR_Z));
+      float *P = gs();
+      const bf16 *we = (const bf16 *)p.w_enc;
+      for (int k0 = 0; k0 < nz; k0 += OTF_ROWS) {
+        float acc[3][2][4];
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) acc[t][nb][0] = acc[t][nb][1] = acc[t][nb][2] = acc[t][nb][3] = 0.f;
+        uint32_t er[2], hr[2];
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          int k = k0 + 8 * nb + g;
+          if (k >= nz) k = nz - 1;   // rows past nz: any valid row (outputs never stored)
+          er[nb] = fb + (uint32_t)(rs.zsrc[k] * 2);
+          hr[nb] = hb + (uint32_t)(16 * (rs.zdst[k] / p.W));
+        }
+        const int nbn = (nz - k0) > 8 ? 2 : 1;
+        // W_enc fragments of this warp's first two encoder K blocks: issued
+        // first, so their L2 latency overlaps the h' part (register weights)
+        constexpr int NEI = (OTF_MAX_DE / 32 + MAX_NW - 1) / MAX_NW;
+        uint4 wa[2][3], wb[2][3];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int kb = warp + MAX_NW * i;
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int r0 = 16 * t + g, r1 = r0 + 8;
+            const bf16 *src = we + (size_t)(d0 + r0) * p.De + (4 * kb + q) * 8;
+            wa[i][t] = (kb < KBE && r0 < TG_UPC) ? ldg128_nc(src) : make_uint4(0, 0, 0, 0);
+            wb[i][t] = (kb < KBE && r1 < TG_UPC) ? ldg128_nc(src + (size_t)8 * p.De) : make_uint4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {   // h' . W_pred^T (registers)
+          const int kb = warp + MAX_NW * i;
+          if (kb < TG_P / 32) {
+            uint4 x[2];
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+              if (nb < nbn) x[nb] = lds128_u32(hr[nb] + (uint32_t)hoff(0, 4 * kb + q));
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              const uint4 ua = wpr[i][t][0], ub = wpr[i][t][1];
+#pragma unroll
+              for (int nb = 0; nb < 2; ++nb)
+                if (nb < nbn) {
+                  mma_bf16_16816(acc[t][nb], ua.x, ub.x, ua.y, ub.y, x[nb].x, x[nb].y);
+                  mma_bf16_16816(acc[t][nb], ua.z, ub.z, ua.w, ub.w, x[nb].z, x[nb].w);
+                }
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < NEI; ++i) {   // e . W_enc^T (L2)
+          const int kb = warp + MAX_NW * i;
+          if (kb < KBE) {
+            uint4 ua[3], ub[3], x[2];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              if (i < 2) {
+                ua[t] = wa[i][t];
+                ub[t] = wb[i][t];
+              } else {
+                const int r0 = 16 * t + g, r1 = r0 + 8;
+                const bf16 *src = we + (size_t)(d0 + r0) * p.De + (4 * kb + q) * 8;
+                ua[t] = r0 < TG_UPC ? ldg128_nc(src) : make_uint4(0, 0, 0, 0);
+                ub[t] = r1 < TG_UPC ? ldg128_nc(src + (size_t)8 * p.De) : make_uint4(0, 0, 0, 0);
+              }
+            }
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb)
+              if (nb < nbn) x[nb] = lds128_u32(er[nb] + (uint32_t)((4 * kb + q) * 16));
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+              for (int nb = 0; nb < 2; ++nb)
+                if (nb < nbn) {
+                  mma_bf16_16816(acc[t][nb], ua[t].x, ub[t].x, ua[t].y, ub[t].y, x[nb].x, x[nb].y);
+                  mma_bf16_16816(acc[t][nb], ua[t].z, ub[t].z, ua[t].w, ub[t].w, x[nb].z, x[nb].w);
+                }
+          }
+        }
+        // partials: acc[t][nb][e] = (dim 16t + g + 8(e >> 1), row 8nb + 2q + (e & 1))
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int d = 16 * t + g + 8 * (e >> 1), i = 8 * nb + 2 * q + (e & 1);
+              if (d < TG_UPC && nb < nbn) P[(warp * OTF_ROWS + i) * OTF_PS + d] = acc[t][nb][e];
+            }
+        sync();
+        if (tid < OTF_ROWS * CPC) {
+          const int i = tid / CPC, c = tid % CPC, k = k0 + i;
+          if (k < nz) {
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
+#pragma unroll
+            for (int w = 0; w < MAX_NW; ++w) {   // fixed warp order
+              const float4 a = *reinterpret_cast<const float4 *>(P + (w * OTF_ROWS + i) * OTF_PS + 8 * c);
+              const float4 b = *reinterpret_cast<const float4 *>(P + (w * OTF_ROWS + i) * OTF_PS + 8 * c + 4);
+              s0.x += a.x; s0.y += a.y; s0.z += a.z; s0.w += a.w;
+              s1.x += b.x; s1.y += b.y; s1.z += b.z; s1.w += b.w;
+            }
+            const float *bp = bsl() + 72 + 8 * c;   // b_enc + b_pred slice
+            uint4 o;
+            o.x = pack_relu_bf16x2(s0.x + bp[0], s0.y + bp[1]);
+            o.y = pack_relu_bf16x2(s0.z + bp[2], s0.w + bp[3]);
+            o.z = pack_relu_bf16x2(s1.x + bp[4], s1.y + bp[5]);
+            o.w = pack_relu_bf16x2(s1.z + bp[6], s1.w + bp[7]);
+            const uint32_t za = zb + (uint32_t)zoff(k, CPC * rank + c);
+            sts128_u32(za, o);
+            const uint64_t lo = ((uint64_t)o.y << 32) | o.x, hi = ((uint64_t)o.w << 32) | o.z;
+#pragma unroll 16
+            for (int cc = 1; cc < C; ++cc) {
+              const uint32_t dr = (uint32_t)((rank + cc) % C);
+              st_async_u64x2(mapa_u32(za, dr), lo, hi, mapa_u32(bz, dr));
+            }
+          }
+        }
+        sync();   // P is reused by the next pass
+      }
+      mbar_wait(bar(BAR_Z), zph());
+      phs ^= 1u << 14;
+      fence_proxy_async_smem();   // z (local stores + the other CTAs' st.async) is read by the tensor core
     }
   }
 
@@ -2204,7 +2390,7 @@ struct Ctx {
     // arm the h' / g exchange barriers for this step (tx from the other CTAs)
     if (tid == 0 && C > 1) {
       mbar_arrive_expect_tx(bar(BAR_H), (uint32_t)((C - 1) * n * upc() * 2));
-      mbar_arrive_expect_tx(bar(BAR_G), (uint32_t)((C - 1) * n * dpc() * 4));
+      if (!OTF) mbar_arrive_expect_tx(bar(BAR_G), (uint32_t)((C - 1) * n * dpc() * 4));
     }
     // (1) gates = E'[y] + W_hh h; fused cell update for this CTA's units.
     // E'[y_i] slices of this CTA's units (4 gates x UPC floats per row) are
@@ -2307,6 +2493,13 @@ struct Ctx {
       mbar_wait(bar(BAR_H), hph());
     }
     tl_pred(4);
+    }
+    if constexpr (OTF) {   // no g: the rounds apply W_pred themselves (project_z)
+      sync();              // h' complete in every thread's view (fence.proxy.async above)
+      gate_request();      // W_hh h' for the next step, in the background
+      phs ^= 1u << 6;
+      tl_next_step();
+      return;
     }
     // (3) g = W_pred h' + b_pred for this CTA's output dims: K split over the
     // warps (partials in shared memory), then one thread per (row, 4 dims)
@@ -2666,7 +2859,11 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ RowState rs;
   __shared__ __align__(8) uint64_t s_bars[NBARS];
-  using CtxT = Ctx<T, KR, HC, PC, CC, TM, SC>;
+  // LM: 0 runtime schedule (p.sched), 1 per-row ticks, 2 Alg. 3 batched outer
+  // loop, 3 frame-looping baseline (Alg. 2), 4 per-row ticks with on-the-fly
+  // projections (OTF, FC LSTM only)
+  using CtxT = Ctx<T, KR, HC, PC, CC, TM, SC, (LM == 4 ? 1 : 0)>;
+  static_assert(LM != 4 || (PRED == 0 && CtxT::TG && SC == 0 && DBG == 0), "OTF: the FC LSTM tick kernel only");
   CtxT cx(p, smem, rs, PRED == 0, s_bars);
   // TJ: an 11th warp issues the tcgen05 joint (and, LSTM, the background gate
   // batches), outside the consumer barrier
@@ -2837,7 +3034,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
       // in the previous tick, then one joint round for every row that scans
       // (continuing rows and the rows just updated).  A row never waits for the
       // other rows of its group to find their labels.
-      if (LM == 1 || (LM == 0 && p.sched == 1)) {
+      if (LM == 1 || LM == 4 || (LM == 0 && p.sched == 1)) {
         if (warp == 0 && lane < R) {
           rs.scanning[lane] = 0;
           rs.found[lane] = 0;
@@ -2944,7 +3141,8 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             cx.sync();
             cx.tl_round_bar(1);
 #endif
-            cx.build_z(cur);
+            if constexpr (LM == 4) cx.project_z(cur);
+            else cx.build_z(cur);
             cx.tl_round_(2);
             cx.sync();
             cx.tl_round_bar(15);

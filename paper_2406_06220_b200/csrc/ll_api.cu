@@ -133,7 +133,7 @@ static int pow2ceil(int x) {
 // nclusters: how many clusters of the chosen size can be resident (0: unknown,
 // assume 8).  R is chosen so that all groups of the batch run in one wave.
 bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf,
-                   int nclusters = 0, int sc = 0, int layers = 1) {
+                   int nclusters = 0, int sc = 0, int layers = 1, int otf_de = 0) {
   const int forceC = g_opt.cluster_size;
   const int forceR = g_opt.group_rows;
   const int forceW = g_opt.window;
@@ -181,7 +181,8 @@ bool choose_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
         if (tj_shape(bf, H, P, C) && !forceW && !forceR && W == 1 && R > 1) break;
         cf.C = C; cf.R = R; cf.W = W; cf.WF = W + (maxd > 1 ? maxd - 1 : 0);
         cf.NS = 0;
-        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0, sc, true, layers);
+        cf.L = make_layout(bf, lstm, H, P, V1, nD, R, W, cf.WF, C, 0, sc, true, layers,
+                           otf_de && tg_shape(bf, lstm, H, P, C) ? otf_de : 0);
         if (cf.L.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) return true;
         if (forceW) break;
       }
@@ -390,10 +391,12 @@ ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw
 // Cluster size / group rows / window for a call: choose_config, then again
 // with the number of clusters that can actually be resident.
 bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, int B, Config &cf, int sc = 0,
-                   int layers = 1) {
-  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, 0, sc, layers)) return false;
+                   int layers = 1, int otf_de = 0) {
+  if (!choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, 0, sc, layers, otf_de)) return false;
   int ncl = 0;
-  if (is_fc(bf, H, P, cf.C))
+  if (otf_de && cf.L.otf)
+    ncl = max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, 4, 1>(cf.C, cf.L);
+  else if (is_fc(bf, H, P, cf.C))
     ncl = lstm ? max_clusters<bf16, 0, KREG, FC_H, FC_P, FC_C, 1, 1>(cf.C, cf.L)
                : max_clusters<bf16, 1, KREG, FC_H, FC_P, FC_C, 1, 1>(cf.C, cf.L);
   else if (bf && kreg_for(bf, H) == KREG)
@@ -402,7 +405,7 @@ bool decode_config(bool bf, bool lstm, int H, int P, int V1, int nD, int maxd, i
     ncl = lstm ? max_clusters<bf16, 0, KREG_SMALL>(cf.C, cf.L) : max_clusters<bf16, 1, KREG_SMALL>(cf.C, cf.L);
   else
     ncl = lstm ? max_clusters<float, 0, 1>(cf.C, cf.L) : max_clusters<float, 1, 1>(cf.C, cf.L);
-  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl, sc, layers));
+  return !(ncl > 0 && !choose_config(bf, lstm, H, P, V1, nD, maxd, B, cf, ncl, sc, layers, otf_de));
 }
 
 // ---------------------------------------------------------------------------
@@ -503,7 +506,13 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   if (sc && (frame_looping || g_opt.schedule == 0 || g_opt.probe_logits)) return LL_ERR_UNSUPPORTED;
   Config cf;
   const int nl = nlayers(pr);
-  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf, sc, nl)) return LL_ERR_UNSUPPORTED;
+  // on-the-fly projections (ll_options.projections = 1; Table 3's ablation arm)
+  const bool otf = g_opt.projections == 1;
+  if (otf && (!bf || !lstm || nl != 1 || frame_looping || sc || g_opt.probe_logits || g_opt.schedule == 0 ||
+              H != FC_H || P != FC_P || De % 32 || De > OTF_MAX_DE))
+    return LL_ERR_UNSUPPORTED;
+  if (!decode_config(bf, lstm, H, P, V1, nD, maxd, B, cf, sc, nl, otf ? De : 0)) return LL_ERR_UNSUPPORTED;
+  if (otf && !cf.L.otf) return LL_ERR_UNSUPPORTED;   // not the FC cluster shape
   if (frame_looping) {   // Alg. 2 evaluates one frame per joint call
     cf.W = 1;
     cf.WF = 1;
@@ -522,8 +531,11 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   // (1) encoder projection for all frames: f [B*T_max, H]
   // (frames t >= lengths[b] are never read: the tcgen05 GEMM skips tiles of
   // padding frames; a length > T_max is clamped here and reported by the decode)
-  s = linear(bf, enc, De, jn->w_enc, De, jn->b_enc, nullptr, ws + w.f, H, B * T_max, H, De, bf, st, lengths, T_max);
-  if (s != LL_OK) return s;
+  // -- not under OTF: the decode kernel projects the encoder rows it evaluates
+  if (!otf) {
+    s = linear(bf, enc, De, jn->w_enc, De, jn->b_enc, nullptr, ws + w.f, H, B * T_max, H, De, bf, st, lengths, T_max);
+    if (s != LL_OK) return s;
+  }
   // (2) model tables (weight-only; skipped if ll_prepare built exactly these
   // into this workspace)
   float *tab = (float *)(ws + w.tab);
@@ -561,8 +573,13 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.frame_looping = frame_looping ? 1 : 0;
   p.sched = g_opt.schedule < 0 ? 1 : g_opt.schedule;
   p.lengths = lengths;
-  p.f = ws + w.f;
-  if (L.tj && bf) p.fmap_ok = make_fmap(&p.fmap, ws + w.f, (uint64_t)B * T_max, H, cf.WF) ? 1 : 0;
+  p.f = otf ? enc : (const void *)(ws + w.f);
+  if (L.tj && bf && !otf) p.fmap_ok = make_fmap(&p.fmap, ws + w.f, (uint64_t)B * T_max, H, cf.WF) ? 1 : 0;
+  if (otf) {   // encoder rows by one bulk copy per frame (fmap_ok = 0)
+    p.De = De;
+    p.w_enc = jn->w_enc;
+    p.b_enc = jn->b_enc;
+  }
   p.w_out = jn->w_out; p.b_out = jn->b_out; p.w_dur = jn->w_dur; p.b_dur = jn->b_dur;
   p.w_pred = jn->w_pred; p.b_pred = jn->b_pred; p.w_hh = lstm ? pr->w_hh : nullptr;
   p.layers = lstm ? nl : 1;
@@ -597,7 +614,10 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   }
   int used = 0;
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
-  if (frame_looping) {   // Alg. 2 baseline instantiations
+  if (otf) {             // on-the-fly projections (Table 3's ablation arm)
+    s = tdt ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 4, 2>(p, C, L, p.n_groups, st, used)
+            : launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 4, 1>(p, C, L, p.n_groups, st, used);
+  } else if (frame_looping) {   // Alg. 2 baseline instantiations
     if (is_fc(bf, H, P, C))
       s = lstm ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 3, 1>(p, C, L, p.n_groups, st, used)
                : launch_decode<bf16, 1, KREG, FC_H, FC_P, FC_C, 3, 1>(p, C, L, p.n_groups, st, used);
@@ -689,7 +709,8 @@ ll_status ll_set_options(const ll_options *o) {
   }
   if (o->cluster_size < 0 || o->cluster_size > MAX_C || o->group_rows < 0 || o->group_rows > MAX_R ||
       o->window < 0 || o->window > 8 || o->max_clusters < 0 || o->schedule < -1 || o->schedule > 1 ||
-      o->spec_prefetch < -1 || o->spec_prefetch > 1 || o->probe_rows < 0 || o->probe_regions < 0)
+      o->spec_prefetch < -1 || o->spec_prefetch > 1 || o->probe_rows < 0 || o->probe_regions < 0 ||
+      o->projections < 0 || o->projections > 1)
     return LL_ERR_INVALID_ARGUMENT;
   g_opt = *o;
   return LL_OK;

@@ -160,12 +160,15 @@ def test_options_validation_and_release(lib):
     ll_release of an unknown / NULL workspace is a no-op."""
     assert ll.ll_set_options(None) == ll.LL_OK
     for bad in [dict(window=9), dict(group_rows=33), dict(cluster_size=17), dict(schedule=2),
-                dict(spec_prefetch=-2), dict(max_clusters=-1), dict(probe_rows=-1)]:
+                dict(spec_prefetch=-2), dict(max_clusters=-1), dict(probe_rows=-1), dict(projections=2),
+                dict(projections=-1)]:
         o = ll.default_options()
         for k, v in bad.items():
             setattr(o, k, v)
         assert ll.ll_set_options(o) == ll.LL_ERR_INVALID_ARGUMENT, bad
     with ll.options(window=2, group_rows=4, schedule=0):
+        pass
+    with ll.options(projections=1):   # on-the-fly projections (Table 3's ablation arm)
         pass
     assert ll.ll_set_options(None) == ll.LL_OK
     assert ll.ll_release(None) == ll.LL_OK
