@@ -49,8 +49,17 @@ enum {
 typedef enum { LL_BF16 = 0, LL_F32 = 1 } ll_dtype;
 
 /* LL_PREC_FAST: bf16 tensor-core contractions with fp32 accumulation; the
- * projected encoder rows f are stored in bf16.  (LL_F32 inputs are always
- * computed in fp32.)  LL_PREC_EXACT is reserved (returns LL_ERR_UNSUPPORTED). */
+ * projected encoder rows f, the recurrent operand h and the joint operand z are
+ * rounded to bf16.  (LL_F32 inputs are always computed in fp32.)
+ * LL_PREC_EXACT with LL_BF16 inputs: the call computes the SAME model in fp32
+ * (f, g, h, c, z never rounded to bf16; the fp32 tolerance class of north_star,
+ * 1e-5 on the logits): fp32 copies of the bf16 values (exact: every bf16 value
+ * is an fp32 value) are made behind the fp32 call's workspace and the fp32
+ * kernels run on them; ll_workspace_size includes the copies (weights + the
+ * encoder output); slower than FAST; model tables are rebuilt on every call
+ * (ll_prepare records nothing).  LL_PREC_EXACT with LL_F32 inputs = LL_PREC_FAST.
+ * Not combinable with ll_options.projections = 1 or the probe
+ * (LL_ERR_UNSUPPORTED). */
 typedef enum { LL_PREC_FAST = 0, LL_PREC_EXACT = 1 } ll_prec;
 
 typedef enum { LL_PRED_LSTM = 0, LL_PRED_STATELESS = 1 } ll_pred_kind;
@@ -80,8 +89,9 @@ typedef struct {
    * stacking: layer l's input is the NEW h of layer l-1, dec = h of the last
    * layer).  num_layers 0 or 1: one layer, the fields below unused.  Stacked
    * [num_layers-1, 4*hidden, hidden] (w_*_rest) and [num_layers-1, 4*hidden]
-   * (b_*_rest).  Supported with LL_F32 weights (the generic kernel reads every
-   * layer's weights through L2); LL_BF16 with num_layers > 1 -> LL_ERR_UNSUPPORTED. */
+   * (b_*_rest).  Computed by the fp32 generic kernel (every layer's weights
+   * read through L2); LL_BF16 weights with num_layers > 1 are widened to fp32
+   * as under LL_PREC_EXACT (the bf16 FC kernel keeps ONE layer's W_hh in TMEM). */
   int32_t num_layers;
   const void *w_ih_rest, *w_hh_rest, *b_ih_rest, *b_hh_rest;
 } ll_predictor;

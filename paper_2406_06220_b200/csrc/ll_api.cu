@@ -96,10 +96,8 @@ ll_status check_model(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, l
     if (pr->kind == LL_PRED_LSTM) {
       if (!pr->w_ih || !pr->w_hh || !pr->b_ih || !pr->b_hh) return LL_ERR_INVALID_ARGUMENT;
       if (pr->num_layers < 0 || pr->num_layers > MAX_LAYERS) return LL_ERR_INVALID_ARGUMENT;
-      if (pr->num_layers > 1) {
-        if (!pr->w_ih_rest || !pr->w_hh_rest || !pr->b_ih_rest || !pr->b_hh_rest) return LL_ERR_INVALID_ARGUMENT;
-        if (dt != LL_F32) return LL_ERR_UNSUPPORTED;   // bf16: one layer (the FC kernel keeps W_hh in TMEM)
-      }
+      if (pr->num_layers > 1 && (!pr->w_ih_rest || !pr->w_hh_rest || !pr->b_ih_rest || !pr->b_hh_rest))
+        return LL_ERR_INVALID_ARGUMENT;   // bf16 with > 1 layer: widened to fp32 (see widened() below)
     } else if (pr->kind == LL_PRED_STATELESS) {
       if (pr->context < 1) return LL_ERR_INVALID_ARGUMENT;
       if (pr->context > MAX_CTX || pr->hidden % pr->context) return LL_ERR_UNSUPPORTED;
@@ -107,7 +105,6 @@ ll_status check_model(const ll_predictor *pr, const ll_joint *jn, ll_dtype dt, l
       return LL_ERR_INVALID_ARGUMENT;
     }
   }
-  if (prec == LL_PREC_EXACT) return LL_ERR_UNSUPPORTED;
   if (jn->enc_dim % 16 || jn->pred_dim % 16 || jn->joint_dim % 16) return LL_ERR_UNSUPPORTED;
   if (need_pred && pr->kind == LL_PRED_STATELESS && (jn->pred_dim / pr->context) % 8)
     return LL_ERR_UNSUPPORTED;
@@ -474,6 +471,107 @@ ll_status build_tables(bool bf, const ll_predictor *pr, const ll_joint *jn, ll_d
   return LL_OK;
 }
 
+// ---------------------------------------------------------------------------
+// LL_PREC_EXACT with bf16 inputs, and bf16 LSTM predictors of more than one
+// layer: the call runs the fp32 kernels on fp32 copies of the bf16 values.
+// Every bf16 value is an fp32 value, so this is the same model computed with
+// fp32 f, g, h, c and z (the fp32 tolerance class, 1e-5 on the logits) instead
+// of bf16-rounded f / h / z.  The copies (one widening kernel per array) sit
+// BEHIND the fp32 call's own workspace, whose header (status, stats) stays at
+// the front for ll_sync / ll_stats.  The model tables are rebuilt on every
+// such call (ll_prepare records nothing for them).
+// ---------------------------------------------------------------------------
+__global__ void widen_bf16_kernel(const bf16 *src, float *dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
+inline bool widened(const ll_predictor *pr, ll_dtype dt, ll_prec prec) {
+  return dt == LL_BF16 && (prec == LL_PREC_EXACT || (pr && nlayers(pr) > 1));
+}
+
+struct WideArr {
+  const void *src;
+  const void **dst;   // the pointer field of the fp32 copy of the model struct
+  size_t n;
+};
+
+// The weight arrays of (pr, jn) in a fixed order (NULL fields skipped); the
+// destinations are the matching fields of pr32 / jn32 (pr may be NULL).
+int wide_arrays(const ll_predictor *pr, const ll_joint *jn, int nD, ll_predictor *pr32, ll_joint *jn32,
+                WideArr *a) {
+  const size_t H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs, De = jn->enc_dim;
+  int k = 0;
+  auto add = [&](const void *src, const void **dst, size_t n) {
+    if (src) a[k++] = WideArr{src, dst, n};
+  };
+  add(jn->w_enc, &jn32->w_enc, H * De);
+  add(jn->b_enc, &jn32->b_enc, H);
+  add(jn->w_pred, &jn32->w_pred, H * P);
+  add(jn->b_pred, &jn32->b_pred, H);
+  add(jn->w_out, &jn32->w_out, V1 * H);
+  add(jn->b_out, &jn32->b_out, V1);
+  if (nD > 0) {
+    add(jn->w_dur, &jn32->w_dur, (size_t)nD * H);
+    add(jn->b_dur, &jn32->b_dur, (size_t)nD);
+  }
+  if (pr) {
+    add(pr->embedding, &pr32->embedding, V1 * P);   // LSTM [V1, P]; stateless [ctx][V1, P / ctx]
+    if (pr->kind == LL_PRED_LSTM) {
+      const size_t Lr = (size_t)nlayers(pr) - 1;
+      add(pr->w_ih, &pr32->w_ih, 4 * P * P);
+      add(pr->w_hh, &pr32->w_hh, 4 * P * P);
+      add(pr->b_ih, &pr32->b_ih, 4 * P);
+      add(pr->b_hh, &pr32->b_hh, 4 * P);
+      if (Lr > 0) {
+        add(pr->w_ih_rest, &pr32->w_ih_rest, Lr * 4 * P * P);
+        add(pr->w_hh_rest, &pr32->w_hh_rest, Lr * 4 * P * P);
+        add(pr->b_ih_rest, &pr32->b_ih_rest, Lr * 4 * P);
+        add(pr->b_hh_rest, &pr32->b_hh_rest, Lr * 4 * P);
+      }
+    }
+  }
+  return k;
+}
+constexpr int MAX_WIDE = 24;
+
+// bytes of the fp32 copies: the weights + the encoder rows [B, T, D_e]
+size_t wide_bytes(int B, int T, const ll_predictor *pr, const ll_joint *jn, int nD) {
+  ll_predictor p2 = pr ? *pr : ll_predictor{};
+  ll_joint j2 = *jn;
+  WideArr a[MAX_WIDE];
+  const int na = wide_arrays(pr, jn, nD, pr ? &p2 : nullptr, &j2, a);
+  size_t o = 0;
+  for (int i = 0; i < na; ++i) o = align_up(o + a[i].n * 4, 256);
+  return align_up(o + (size_t)B * T * jn->enc_dim * 4, 256);
+}
+
+// Widen into ws (256-aligned): fills pr32 / jn32 (copies of pr / jn with the
+// fp32 pointers) and returns the fp32 encoder rows.
+float *widen_all(const void *enc, size_t enc_n, const ll_predictor *pr, const ll_joint *jn, int nD,
+                 ll_predictor *pr32, ll_joint *jn32, uint8_t *ws, cudaStream_t st, ll_status &s) {
+  if (pr) *pr32 = *pr;
+  *jn32 = *jn;
+  WideArr a[MAX_WIDE];
+  const int na = wide_arrays(pr, jn, nD, pr32, jn32, a);
+  size_t o = 0;
+  auto widen = [&](const void *src, float *dst, size_t n) {
+    if (n == 0) return;
+    const int blocks = (int)std::min<size_t>((n + 255) / 256, 4096);
+    widen_bf16_kernel<<<blocks, 256, 0, st>>>((const bf16 *)src, dst, n);
+  };
+  for (int i = 0; i < na; ++i) {
+    float *d = (float *)(ws + o);
+    *a[i].dst = d;
+    widen(a[i].src, d, a[i].n);
+    o = align_up(o + a[i].n * 4, 256);
+  }
+  float *enc32 = (float *)(ws + o);
+  widen(enc, enc32, enc_n);
+  s = cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
+  return enc32;
+}
+
 ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt, ll_prec prec, int32_t B, int32_t T_max,
                       const int32_t *lengths, const ll_predictor *pr, const ll_joint *jn,
                       int32_t blank_id, int32_t max_symbols, const int32_t *durations, int32_t nD,
@@ -501,6 +599,25 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   const int H = jn->joint_dim, P = jn->pred_dim, V1 = jn->num_outputs, De = jn->enc_dim;
   int maxd = 1;
   for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
+  if (widened(pr, dt, prec)) {   // fp32 kernels on fp32 copies (see widened() above)
+    if (g_opt.projections == 1 || g_opt.probe_logits) return LL_ERR_UNSUPPORTED;   // bf16 FC kernels only
+    {
+      Config c32;
+      if (!decode_config(false, lstm, H, P, V1, nD, maxd, B, c32, out_scores != nullptr, nlayers(pr)))
+        return LL_ERR_UNSUPPORTED;
+    }
+    const size_t inner = align_up(ws_layout(B, T_max, pr, jn, LL_F32).total, 256);
+    ll_predictor pr32;
+    ll_joint jn32;
+    ll_status ws_s = LL_OK;
+    float *enc32 = widen_all(enc, (size_t)B * T_max * De, pr, jn, nD, &pr32, &jn32, (uint8_t *)workspace + inner,
+                             (cudaStream_t)stream, ws_s);
+    if (ws_s != LL_OK) return ws_s;
+    ll_release(workspace);   // the fp32 tables are rebuilt from the fresh copies
+    return decode_impl(tdt, frame_looping, enc32, LL_F32, LL_PREC_FAST, B, T_max, lengths, &pr32, &jn32, blank_id,
+                       max_symbols, durations, nD, out_tokens, out_timestamps, out_durations, out_lengths, cap,
+                       workspace, inner, stream, out_scores);
+  }
   // greedy scores (N2): the per-row tick schedule's SC kernels
   const int sc = out_scores != nullptr;
   if (sc && (frame_looping || g_opt.schedule == 0 || g_opt.probe_logits)) return LL_ERR_UNSUPPORTED;
@@ -734,6 +851,9 @@ size_t ll_workspace_size(int32_t B, int32_t T_max, const ll_predictor *pred, con
   if (check_model(pred, joint, dtype, prec, num_durations, false) == LL_ERR_INVALID_ARGUMENT) return 0;
   if (pred->kind != LL_PRED_LSTM && pred->kind != LL_PRED_STATELESS) return 0;
   if (pred->kind == LL_PRED_STATELESS && pred->context < 1) return 0;
+  if (widened(pred, dtype, prec))   // the fp32 call's workspace, then the fp32 copies
+    return align_up(ws_layout(B, T_max, pred, joint, LL_F32).total, 256) +
+           wide_bytes(B, T_max, pred, joint, num_durations > 0 ? num_durations : 0);
   return ws_layout(B, T_max, pred, joint, dtype).total;
 }
 
@@ -805,6 +925,7 @@ ll_status ll_prepare(const ll_predictor *pred, const ll_joint *joint, ll_dtype d
   ll_status s = check_model(pred, joint, dtype, prec, nD, true);
   if (s != LL_OK) return s;
   if (workspace_bytes < ll_workspace_size(B, T_max, pred, joint, dtype, prec, nD)) return LL_ERR_WORKSPACE;
+  if (widened(pred, dtype, prec)) return LL_OK;   // tables rebuilt by every such decode (no record)
   const bool bf = dtype == LL_BF16, lstm = pred->kind == LL_PRED_LSTM;
   int maxd = 1;
   for (int i = 0; i < nD; ++i) maxd = durations[i] > maxd ? durations[i] : maxd;
@@ -861,6 +982,17 @@ ll_status ll_debug_joint(const void *enc_rows, const float *g_rows, int32_t n, c
   if (workspace_bytes < ll_workspace_size(n, 1, &dummy, joint, dtype, prec, num_durations))
     return LL_ERR_WORKSPACE;
   ll_release(workspace);   // its f rows overwrite the region prepared tables would occupy
+  if (dtype == LL_BF16 && prec == LL_PREC_EXACT) {   // the fp32 joint on fp32 copies (see widened())
+    if (n == 0) return LL_OK;
+    const size_t inner = align_up(ws_layout(n, 1, &dummy, joint, LL_F32).total, 256);
+    ll_joint jn32;
+    ll_status ws_s = LL_OK;
+    float *rows32 = widen_all(enc_rows, (size_t)n * joint->enc_dim, nullptr, joint, num_durations, nullptr, &jn32,
+                              (uint8_t *)workspace + inner, (cudaStream_t)stream, ws_s);
+    if (ws_s != LL_OK) return ws_s;
+    return ll_debug_joint(rows32, g_rows, n, &jn32, LL_F32, LL_PREC_FAST, num_durations, out_logits, out_argmax,
+                          out_dur_argmax, workspace, inner, stream);
+  }
   const bool bf = dtype == LL_BF16;
   const int H = joint->joint_dim, V1 = joint->num_outputs, De = joint->enc_dim;
   Config cf;

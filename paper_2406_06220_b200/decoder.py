@@ -204,12 +204,13 @@ class LabelLoopingDecoder:
         return d
 
 
-def debug_joint(model: Model, enc_rows: torch.Tensor, g_rows: torch.Tensor, want_logits: bool = True):
+def debug_joint(model: Model, enc_rows: torch.Tensor, g_rows: torch.Tensor, want_logits: bool = True,
+                prec: int = ll.LL_PREC_FAST):
     """ll_debug_joint on n rows: returns (logits [n, V+1+|D|] or None, argmax [n], dur_argmax [n] or None)."""
     n = int(enc_rows.shape[0])
     nD = model.num_durations
     pred = ll.ll_predictor(ll.LL_PRED_STATELESS, model.V1, model.P, 1, None, None, None, None, None)
-    ws_bytes = ll.ll_workspace_size(n, 1, pred, model.joint, model.dtype_code, ll.LL_PREC_FAST, nD)
+    ws_bytes = ll.ll_workspace_size(n, 1, pred, model.joint, model.dtype_code, prec, nD)
     ws = torch.empty(ws_bytes + 256, dtype=torch.uint8, device=model.device)
     ws_ptr = (ws.data_ptr() + 255) // 256 * 256
     logits = torch.empty(n, model.V1 + nD, dtype=torch.float32, device=model.device) if want_logits else None
@@ -217,7 +218,7 @@ def debug_joint(model: Model, enc_rows: torch.Tensor, g_rows: torch.Tensor, want
     dam = torch.empty(n, dtype=torch.int32, device=model.device) if nD else None
     st = torch.cuda.current_stream().cuda_stream
     s = ll.ll_debug_joint(enc_rows.data_ptr(), g_rows.data_ptr(), n, model.joint, model.dtype_code,
-                          ll.LL_PREC_FAST, nD, logits.data_ptr() if logits is not None else None,
+                          prec, nD, logits.data_ptr() if logits is not None else None,
                           am.data_ptr(), dam.data_ptr() if dam is not None else None, ws_ptr, ws_bytes, st)
     if s != ll.LL_OK:
         raise ll.LLError(s, "ll_debug_joint")

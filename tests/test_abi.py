@@ -76,11 +76,28 @@ def test_workspace_size(lib):
     (dict(ws=0x100010), ll.LL_ERR_INVALID_ARGUMENT),      # not 256-byte aligned
     (dict(ws_bytes=1024), ll.LL_ERR_WORKSPACE),
     (dict(dtype=5), ll.LL_ERR_INVALID_ARGUMENT),
-    (dict(prec=ll.LL_PREC_EXACT), ll.LL_ERR_UNSUPPORTED),
+    (dict(prec=7), ll.LL_ERR_INVALID_ARGUMENT),
 ])
 def test_rnnt_validation(lib, kw, status):
     pred, joint = _model()
     assert _rnnt(pred, joint, **kw) == status
+
+
+def test_exact_workspace(lib):
+    """LL_PREC_EXACT with bf16 inputs (ll.h): the fp32 call's workspace plus fp32
+    copies of every weight and of the encoder output; too small -> LL_ERR_WORKSPACE
+    before anything is enqueued."""
+    pred, joint = _model()
+    fast = ll.ll_workspace_size(32, 275, pred, joint, ll.LL_BF16, ll.LL_PREC_FAST, 0)
+    exact = ll.ll_workspace_size(32, 275, pred, joint, ll.LL_BF16, ll.LL_PREC_EXACT, 0)
+    f32 = ll.ll_workspace_size(32, 275, pred, joint, ll.LL_F32, ll.LL_PREC_FAST, 0)
+    V1, P, H, De = 1025, 640, 640, 512
+    weights = (H * De + H + H * P + H + V1 * H + V1 + V1 * P + 2 * 4 * P * P + 2 * 4 * P) * 4
+    assert exact >= f32 + weights + 32 * 275 * De * 4
+    assert exact < f32 + weights + 32 * 275 * De * 4 + 24 * 256 + 512
+    assert ll.ll_workspace_size(32, 275, pred, joint, ll.LL_F32, ll.LL_PREC_EXACT, 0) == f32
+    assert _rnnt(pred, joint, prec=ll.LL_PREC_EXACT, ws_bytes=fast) == ll.LL_ERR_WORKSPACE
+    assert _rnnt(pred, joint, prec=ll.LL_PREC_EXACT, ws_bytes=exact - 1) == ll.LL_ERR_WORKSPACE
 
 
 def test_model_validation(lib):

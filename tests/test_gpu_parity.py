@@ -625,16 +625,3 @@ def test_multilayer_lstm_f32(cfg, layers):
         mism = sum(1 for b in ref if tuple(map(list, ref[b])) != tuple(map(list, hyps[b])))
         assert mism == 0 or ties > 0
     assert decs > 300
-
-
-def test_multilayer_lstm_bf16_unsupported():
-    """bf16 weights with more than one LSTM layer are refused (ll.h), before any work."""
-    c = synth.CONFIGS["tiny"]
-    spec = c["spec"]
-    sp = synth.ModelSpec(spec.num_tokens, spec.enc_dim, spec.pred_dim, spec.joint_dim, "lstm", 1,
-                         None, spec.blank_id, spec.max_symbols, num_layers=2)
-    w = synth.make_weights(sp, 5)
-    enc, lengths = synth.make_inputs(6, c["B"], c["T_max"], sp.enc_dim, c["len_lo"], c["len_hi"])
-    with pytest.raises(ll.LLError) as e:
-        gpu_decode(sp, w, enc, lengths, "bf16")
-    assert e.value.status == ll.LL_ERR_UNSUPPORTED
