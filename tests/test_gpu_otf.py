@@ -82,16 +82,18 @@ def test_otf_table3_batch_sizes(B):
 
 
 def test_otf_determinism():
-    """Bit-identical repeat runs (fixed reduction orders) and batch-composition
-    independence (a row decodes the same alone and inside the batch)."""
+    """Bit-identical repeat runs (fixed reduction orders; 11 runs) and
+    batch-composition independence (a row decodes the same alone and inside the
+    batch)."""
     c = synth.CONFIGS["fc-rnnt"]
     spec = c["spec"]
     w = synth.make_weights(spec, 51, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(52, 12, c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     model = gpu_model(spec, w)
     a, _ = _decode(spec, w, enc, lengths, model)
-    b, _ = _decode(spec, w, enc, lengths, model)
-    assert a == b
+    for _ in range(10):   # a race on the cross-CTA z exchange would show as run-to-run differences
+        b, _ = _decode(spec, w, enc, lengths, model)
+        assert a == b
     one, _ = _decode(spec, w, enc[5:6], lengths[5:6], model)
     assert one[0] == a[5]
 

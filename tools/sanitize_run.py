@@ -7,8 +7,9 @@ Covers: the generic cluster kernel (tiny RNN-T / TDT, stateless), the
 FastConformer-shape kernels (LSTM predictor with W_hh in TMEM, tcgen05 GEMM
 projections, tick schedule; RNN-T and TDT, planted family so every row emits
 labels), the stateless FC-shape kernel, the frame-looping baseline, the
-batched Alg. 3 schedule (ll_options.schedule = 0) and the native ragged gather (world
-size 1).  Each decode's hypotheses are compared
+batched Alg. 3 schedule (ll_options.schedule = 0), the on-the-fly projection
+kernels (ll_options.projections = 1), LL_PREC_EXACT (widening + fp32 kernels)
+and the native ragged gather (world size 1).  Each decode's hypotheses are compared
 with the planted alignment / checked for well-formedness; the point of the run
 is the sanitizer's report."""
 import os
@@ -35,7 +36,7 @@ def run_tiny(cfg):
     print(cfg, "rows", len(out.hypotheses()), flush=True)
 
 
-def run_planted(cfg, B, frame_looping=False, gather=False, scores=False):
+def run_planted(cfg, B, frame_looping=False, gather=False, scores=False, prec=ll.LL_PREC_FAST):
     c = synth.CONFIGS[cfg]
     spec = c["spec"]
     w, codes = synth.planted_weights(spec, 1000)
@@ -48,7 +49,7 @@ def run_planted(cfg, B, frame_looping=False, gather=False, scores=False):
         enc[i, :e.shape[0]] = e
         planted.append(pl)
     model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16")
-    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, frame_looping=frame_looping, scores=scores)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, B, T, frame_looping=frame_looping, scores=scores, prec=prec)
     lengths = torch.from_numpy(L.astype(np.int32)).cuda()
     out = dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), lengths)
     hy = out.hypotheses()
@@ -83,5 +84,9 @@ if __name__ == "__main__":
         run_tiny("tiny")
         run_planted("fc-rnnt", 6)
         run_planted("fc-tdt", 6)
+    with ll.options(projections=1):   # on-the-fly projections (Table 3 arm): the LM = 4 kernels
+        run_planted("fc-rnnt", 6)
+        run_planted("fc-tdt", 6)
+    run_planted("fc-rnnt", 3, prec=ll.LL_PREC_EXACT)   # widening kernels + the fp32 kernels
     torch.cuda.synchronize()
     print("sanitize_run done", flush=True)
