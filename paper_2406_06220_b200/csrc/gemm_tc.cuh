@@ -28,26 +28,46 @@ struct TcGemmArgs {
   void *Y;
   int64_t ldy;
   int M, N, K;
-  // optional ragged rows (the encoder projection): row r = b * T + t is used only
-  // if t < lengths[b]; M tiles without a used row are skipped, unused rows of
-  // the other tiles are not stored (frames t >= lengths[b] are never read)
+  // Rows are Bu SEGMENTS of T rows (row r = b * T + t; without lengths: one
+  // segment, T = M).  Optional ragged rows (the encoder projection): row
+  // b * T + t is used only if t < lengths[b].  M tiles never straddle a
+  // segment (X is read as a 3-D tensor {K, T, Bu}, rows past T zero-filled)
+  // and only the tiles of used rows exist: ceil(min(lengths[b], T) / 128) per
+  // segment, dealt round-robin to the persistent CTAs, so padding frames cost
+  // neither MMAs nor load imbalance (frames t >= lengths[b] are never read).
   const int *lengths;
-  int T;
+  int T, Bu;
   int bn;   // output tile width: TC_BN (256) or TC_BNQ (128, small problems: more tiles than SMs)
 };
 
-// whether any of the rows [m0, m0 + n) is used under the ragged-row rule (all are without lengths)
-__device__ __forceinline__ bool tile_has_rows(const TcGemmArgs &a, int m0, int n) {
-  if (!a.lengths) return true;
-  const int m1 = min(m0 + n, a.M);
-  for (int b = m0 / a.T; b * a.T < m1; ++b) {
-    const int t0 = max(m0 - b * a.T, 0);   // first row of utterance b inside the tile
-    int L = a.lengths[b];
-    if (L > a.T) L = a.T;
-    if (t0 < L) return true;
+// Walks the segments' M tiles in order (tile index mi -> segment b, first row
+// t0); every role of a CTA walks the same sequence.
+struct TileCursor {
+  int b = 0, cum = 0, cb = 0, L = 0;   // segment b: used rows L, its first tile index cum, tile count cb
+  __device__ __forceinline__ void load(const TcGemmArgs &a) {
+    L = 0;
+    if (b < a.Bu) {
+      L = a.lengths ? a.lengths[b] : a.T;
+      L = L < 0 ? 0 : (L > a.T ? a.T : L);
+    }
+    cb = (L + TC_BM - 1) / TC_BM;
   }
-  return false;
-}
+  __device__ __forceinline__ void init(const TcGemmArgs &a) {
+    b = 0;
+    cum = 0;
+    load(a);
+  }
+  // position on tile index mi (non-decreasing across calls); false past the end
+  __device__ __forceinline__ bool seek(const TcGemmArgs &a, int mi) {
+    while (b < a.Bu && mi >= cum + cb) {
+      cum += cb;
+      ++b;
+      load(a);
+    }
+    return b < a.Bu;
+  }
+  __device__ __forceinline__ int t0(int mi) const { return (mi - cum) * TC_BM; }
+};
 
 // Instruction descriptor: D fp32, A/B bf16, both K-major, M = 128, N = n.
 __host__ __device__ constexpr uint32_t tc_idesc(int n) {
@@ -61,10 +81,17 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 
-// Persistent, warp-specialized: grid = number of SMs (one CTA each); CTA b
-// takes output tiles b, b + gridDim.x, ... (tile = (m-tile, n-tile), n fastest;
-// tiles of padding frames only are skipped by every role alike).
+// Persistent, warp-specialized: grid = number of SMs (one CTA each); CTA c
+// takes output tiles c, c + gridDim.x, ... of the used tiles (tile = (m-tile,
+// n-tile), n fastest; TileCursor maps m-tile indices to segments).
 //   warp 0:    TMA producer (lane 0): A/B 128x64 k-blocks into a TC_STAGES ring
 //   warp 1:    MMA issuer (lane 0): tcgen05.mma into one of TWO TMEM
 //              accumulators (128 columns each), tcgen05.commit per k-block
@@ -73,12 +100,6 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 //              global, then release the accumulator, so the MMAs of tile i+1
 //              overlap the epilogue of tile i.
 constexpr int TC_THREADS = 192;
-__device__ __forceinline__ void tile_mn(const TcGemmArgs &a, int tile, int &m0, int &n0, int &nw) {
-  const int nt = (a.N + a.bn - 1) / a.bn;
-  m0 = (tile / nt) * TC_BM;
-  n0 = (tile % nt) * a.bn;
-  nw = min(a.bn, a.N - n0);
-}
 
 template <typename OutT>
 __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap map_x,
@@ -90,7 +111,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = a.K / TC_BK;
-  const int ntiles = ((a.M + TC_BM - 1) / TC_BM) * ((a.N + a.bn - 1) / a.bn);
+  const int nt = (a.N + a.bn - 1) / a.bn;
   const uint32_t stage_tx = (uint32_t)(TC_TILE_A + a.bn * TC_BK * 2);
 
   if (threadIdx.x == 0) {
@@ -113,16 +134,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   if (warp == 0) {
     if (lane == 0) {   // producer
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int m0, n0, nw;
-        tile_mn(a, tile, m0, n0, nw);
-        if (!tile_has_rows(a, m0, TC_BM)) continue;
+      TileCursor cur;
+      cur.init(a);
+      for (int tile = blockIdx.x;; tile += gridDim.x) {
+        const int mi = tile / nt, n0 = (tile % nt) * a.bn;
+        if (!cur.seek(a, mi)) break;
+        const int t0 = cur.t0(mi);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % TC_STAGES;
           if (it >= TC_STAGES) mbar_wait(&empty[s], ((it / TC_STAGES) - 1) & 1);
           uint8_t *sa = smem + s * (TC_TILE_A + TC_TILE_B), *sb = sa + TC_TILE_A;
           mbar_arrive_expect_tx(&full[s], stage_tx);
-          tma_load_2d(sa, &map_x, kb * TC_BK, m0, &full[s]);
+          tma_load_3d(sa, &map_x, kb * TC_BK, t0, cur.b, &full[s]);
           tma_load_2d(sb, &map_w, kb * TC_BK, n0, &full[s]);
         }
       }
@@ -130,10 +153,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
   } else if (warp == 1) {
     if (lane == 0) {   // MMA issuer
       int it = 0, t = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int m0, n0, nw;
-        tile_mn(a, tile, m0, n0, nw);
-        if (!tile_has_rows(a, m0, TC_BM)) continue;
+      TileCursor cur;
+      cur.init(a);
+      for (int tile = blockIdx.x;; tile += gridDim.x) {
+        const int mi = tile / nt, n0 = (tile % nt) * a.bn, nw = min(a.bn, a.N - n0);
+        if (!cur.seek(a, mi)) break;
         const int ab = t & 1;
         if (t >= 2) mbar_wait(&acc_empty[ab], ((t >> 1) - 1) & 1);   // the epilogue drained this accumulator
         tc_fence_after();
@@ -157,19 +181,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gemm_tc_kernel(const __grid_con
     const int qd = warp & 3;
     const bf16 *bias = (const bf16 *)a.bias, *bias2 = (const bf16 *)a.bias2;
     int t = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      int m0, n0, nw;
-      tile_mn(a, tile, m0, n0, nw);
-      if (!tile_has_rows(a, m0, TC_BM)) continue;
+    TileCursor cur;
+    cur.init(a);
+    for (int tile = blockIdx.x;; tile += gridDim.x) {
+      const int mi = tile / nt, n0 = (tile % nt) * a.bn, nw = min(a.bn, a.N - n0);
+      if (!cur.seek(a, mi)) break;
       const int ab = t & 1;
       mbar_wait(&acc_full[ab], (t >> 1) & 1);
       tc_fence_after();
-      const int row = m0 + qd * 32 + lane;
-      bool used = row < a.M;
-      if (used && a.lengths) {
-        const int b = row / a.T;
-        used = row - b * a.T < a.lengths[b];
-      }
+      const int tr = cur.t0(mi) + qd * 32 + lane;   // row within segment cur.b
+      const bool used = tr < cur.L;
+      const int64_t row = (int64_t)cur.b * a.T + tr;
 #pragma unroll 1
       for (int c0 = 0; c0 < nw; c0 += 32) {
         uint32_t r[32];

@@ -312,6 +312,22 @@ bool make_map_bf16(CUtensorMap *m, const void *base, uint64_t rows, uint64_t col
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D bf16 tensor map over Bu segments of T rows of a row-major matrix with
+// leading dimension ld (elements), segment stride T * ld: 64-column x box_rows x
+// 1 boxes, 128-byte swizzle; rows past T in a segment are zero-filled.
+bool make_map3_bf16(CUtensorMap *m, const void *base, uint64_t T, uint64_t Bu, uint64_t cols, uint64_t ld,
+                    uint32_t box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {cols, T, Bu};
+  const cuuint64_t strides[2] = {ld * 2, T * ld * 2};
+  const cuuint32_t box[3] = {TC_BK, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // TJ f boxes (DecodeParams::fmap): {8 elements, 81 chunks, frames}, chunk stride
 // 16 B, frame stride 2H; box {8, 81, WF} -> WF padded 1296-byte rows.
 bool make_fmap(CUtensorMap *m, const void *f, uint64_t frames, int H, int WF) {
@@ -341,14 +357,18 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm < 1) nsm = 1;
   }
-  // 128 x 256 tiles, unless that leaves fewer than two tiles per SM (then 128 x 128)
-  const int mt = (M + TC_BM - 1) / TC_BM;
+  // rows as segments: the encoder frames of each utterance (lengths), else one segment
+  if (lengths && (T < 1 || M % T)) return false;
+  const int Tseg = lengths ? T : M, Bu = lengths ? M / T : 1;
+  // 128 x 256 tiles, unless that leaves fewer than two tiles per SM (then 128 x 128);
+  // mt: M tiles at full lengths (an upper bound of the used ones)
+  const int mt = Bu * ((Tseg + TC_BM - 1) / TC_BM);
   const int bn = mt * ((N + TC_BN - 1) / TC_BN) >= 2 * nsm ? TC_BN : TC_BNQ;
   CUtensorMap mx, mw;
-  if (!make_map_bf16(&mx, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, TC_BM) ||
+  if (!make_map3_bf16(&mx, X, (uint64_t)Tseg, (uint64_t)Bu, (uint64_t)K, (uint64_t)ldx, TC_BM) ||
       !make_map_bf16(&mw, W, (uint64_t)N, (uint64_t)K, (uint64_t)ldw, (uint32_t)bn))
     return false;
-  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K, lengths, T, bn};
+  TcGemmArgs a{bias, bias2, Y, ldy, M, N, K, lengths, Tseg, Bu, bn};
   if (!attr_done) {   // once per process (not on every call)
     cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
