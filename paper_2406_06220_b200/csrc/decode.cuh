@@ -381,12 +381,17 @@ struct Ctx {
     }
   }
   __device__ void tl_init() { tl = (p.prof != nullptr && blockIdx.x == 0) ? p.prof : nullptr; }
+  // warp 0's sub-phases of a round's finish (phase slot 14, "warp" column k)
+  __device__ void tl_sub(int k) const {
+    if (tl != nullptr && tl_round < TL_N && lane == 0) tl[((size_t)tl_round * TL_PH + 14) * MAX_NW + k] = clock64();
+  }
   __device__ void tl_next_round() { ++tl_round; }
   __device__ void tl_next_step() { ++tl_step; }
 #else
   __device__ __forceinline__ void tl_stamp(int, int, int) const {}
   __device__ __forceinline__ void tl_stamp_bar(int, int, int) const {}
   __device__ __forceinline__ void tl_init() {}
+  __device__ __forceinline__ void tl_sub(int) const {}
   __device__ __forceinline__ void tl_next_round() {}
   __device__ __forceinline__ void tl_next_step() {}
   static constexpr int tl_round = 0, tl_step = 0;
@@ -437,6 +442,13 @@ struct Ctx {
   __device__ __forceinline__ int upc() const { return (PC && CC) ? PC / CC : L.UPC; }
   __device__ __forceinline__ int dpc() const { return (HC && CC) ? HC / CC : L.DPC; }
   __device__ __forceinline__ bool is_tdt() const { return TM == 0 ? p.tdt != 0 : TM == 2; }
+  // TJ RNN-T tick kernels without scores / probe / OTF: the decisions are read
+  // from warp 0's registers (finish_round_rnnt) and z rows from (slot, frame),
+  // so the compact-row tables (zsrc / zdst) and the per-row decision array are
+  // not written
+  __device__ __forceinline__ bool lean() const {
+    return TJ && !is_tdt() && !SC && !OTF && p.sched == 1 && !p.frame_looping && p.probe_logits == nullptr;
+  }
   __device__ __forceinline__ int Pd() const { return PC ? PC : p.P; }
   __device__ uint64_t *bar(int i) const { return bars + i; }
   __device__ float *bsl() const { return (float *)(sm + L.off_b); }
@@ -788,28 +800,33 @@ struct Ctx {
     const int W = p.W;
     int cnt = 0;
     if (scan_next) cnt = min(W, Ls - t);
-    int incl = cnt;
-#pragma unroll
+    int incl = cnt;   // inclusive scan over the slots (cnt = 0 on lanes >= R)
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
+      if (2 * o >= p.R) break;   // uniform: lanes < R hold their full prefix sums
     }
+    const int total = __shfl_sync(0xffffffffu, incl, p.R - 1);
     const int beg = incl - cnt;
     if (lane < p.R) {
       rs.zbeg[lane] = beg;
       rs.zcnt[lane] = cnt;
     }
-    for (int j = 0; j < cnt; ++j) {
-      rs.zsrc[beg + j] = (lane * L.fss + j * frow_smem()) / 2;
-      rs.zdst[beg + j] = lane * W + j;
+    if (!lean()) {
+      for (int j = 0; j < cnt; ++j) {
+        rs.zsrc[beg + j] = (lane * L.fss + j * frow_smem()) / 2;
+        rs.zdst[beg + j] = lane * W + j;
+      }
     }
-    if (lane == 31) rs.nz = incl;
+    if (lane == 0) rs.nz = total;
   }
 
   // z[jr] = ReLU(f[b_s, t_s + j] + g_s) for the live joint rows.  Other joint
   // rows keep stale values: an MMA output row depends only on its own A row
   // and those rows are never read.  Warp per joint row, 8 columns per lane.
-  __device__ void build_z(int X) {
+  // tick: the TJ tick schedule's plan (plan_next_tj), where compact row zbeg[s] + j
+  // is frame j of slot s's window, row j of its f buffer slot
+  __device__ void build_z(int X, bool tick = false) {
     const int H = Hd(), W = p.W;
     const int nz = rs.nz;
     if constexpr (TJ) {
@@ -838,7 +855,9 @@ struct Ctx {
         for (int i = 0; i < 4; ++i) {
           const int j = h + 2 * i;
           kk[i] = kb0 + j;
-          if (j < cnt) f[i] = lds128_u32(fb + (uint32_t)(rs.zsrc[kb0 + j] * 2 + cc * 16));
+          if (j < cnt)
+            f[i] = lds128_u32(fb + (tick ? (uint32_t)(s * L.fss + j * frow_smem())
+                                         : (uint32_t)(rs.zsrc[kb0 + j] * 2)) + (uint32_t)(cc * 16));
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1562,7 +1581,7 @@ struct Ctx {
         }
       }
       dec = key_index(tkey) | ((is_tdt() ? key_index(dkey) : 0) << 24);
-      rs.dec[rs.zdst[lane]] = dec;
+      if (!lean()) rs.dec[rs.zdst[lane]] = dec;
       if constexpr (SC) {   // log-probability of this row's decision (token [+ duration])
         float lp = key_value(tkey) - lse_value(tl);
         if (is_tdt()) lp += key_value(dkey) - lse_value(dl);
@@ -1647,6 +1666,7 @@ struct Ctx {
       act = rs.active[lane]; scan = rs.scanning[lane]; needp = rs.needp[lane];
       b0 = rs.zbeg[lane]; c = rs.zcnt[lane];
     }
+    tl_sub(1);
     [[maybe_unused]] const int t_round = t;   // window base of this round (TJ: the speculative next window starts at t_round + W)
     // decisions of the window (Alg. 3 lines 9-11 / 15-19): first non-blank frame
     const unsigned m = scan ? (nb >> b0) & ((1u << c) - 1u) : 0u;   // c <= W <= 8
@@ -1701,6 +1721,7 @@ struct Ctx {
         rs.ctx[0][lane] = y;
       }
     }
+    tl_sub(2);
     // compacted lists (ascending slot order) and counters
     const unsigned ms = __ballot_sync(FULL, inr && scan);
     const unsigned mp = __ballot_sync(FULL, inr && needp);
@@ -1716,8 +1737,10 @@ struct Ctx {
       rs.ready = ms == 0u;
       *algevals += (unsigned)tot;
     }
+    tl_sub(3);
     if constexpr (TJ) {
       plan_next_tj(inr && act && (scan || needp), t, Ls);
+      tl_sub(4);
       // the next tick's reloads: rows that found a label, and scanning rows whose
       // speculative window (t_round + W) does not start at their new t (TDT jumps)
       const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + p.W)));
@@ -1726,7 +1749,16 @@ struct Ctx {
       if (lane == 0) rs.nload = __popc(ml);
     }
     __syncwarp();
-    if (eprime && mp != 0u) issue_eprime(rs.plist, __popc(mp));
+    tl_sub(5);
+    if (eprime && mp != 0u) {   // the next predictor's E'[y] slices, from the lanes' registers
+      const uint32_t segb = (uint32_t)(4 * upc() * 4);
+      if (lane == 0) mbar_arrive_expect_tx(bar(BAR_E), (uint32_t)__popc(mp) * segb);
+      __syncwarp();
+      if (inr && needp)
+        bulk_g2s(es() + (size_t)lane * 4 * upc(), p.tab + (size_t)y * 4 * Pd() + (size_t)rank * 4 * upc(), segb,
+                 bar(BAR_E));
+    }
+    tl_sub(6);
   }
 
   // Tick schedule: decide / decide_rnnt (Xnext = -1) + append_found +
@@ -1828,7 +1860,8 @@ struct Ctx {
       if (found) {
         rs.last[lane] = y;
 #pragma unroll
-        for (int cc = MAX_CTX - 1; cc > 0; --cc) rs.ctx[cc][lane] = rs.ctx[cc - 1][lane];
+        for (int cc = MAX_CTX - 1; cc > 0; --cc)
+          if (cc < p.context) rs.ctx[cc][lane] = rs.ctx[cc - 1][lane];   // stateless context > 1 only
         rs.ctx[0][lane] = y;
       }
     }
@@ -2954,12 +2987,14 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
         // LSTM initial state h = c = 0 (reading A8)
         for (int i = tid; i < R * cx.L.UPC * max(p.layers, 1); i += cx.NCT) cx.cs()[i] = 0.f;
         if constexpr (TGK) {
-          // no gate batch may still read the h buffer; h = 0 means W_hh h = 0,
-          // so the first step skips the (not yet computed) pre-activations
+          // h = 0 means W_hh h = 0: the group's first step skips the
+          // pre-activations (bit 10 cleared) and writes h' of every active
+          // slot.  The h buffer is NOT zeroed here: the other CTAs may already
+          // be st.async'ing this group's first h' slices into it (they only
+          // wait for the group index), and no reader uses an inactive slot's
+          // h (its gate / W_pred columns are never read)
           cx.gate_wait();
           cx.phs &= ~(1u << 10);
-          for (int i = tid; i < TG_HBYTES / 16; i += cx.NCT)
-            reinterpret_cast<uint4 *>(cx.hbuf())[i] = make_uint4(0, 0, 0, 0);
         } else if constexpr (RING) {
           for (int i = tid; i < R * cx.Pd() / 8; i += cx.NCT) {
             const int s = i / (cx.Pd() / 8), c = i % (cx.Pd() / 8);
@@ -3142,7 +3177,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             cx.tl_round_bar(1);
 #endif
             if constexpr (LM == 4) cx.project_z(cur);
-            else cx.build_z(cur);
+            else cx.build_z(cur, CtxT::TJ);
             cx.tl_round_(2);
             cx.sync();
             cx.tl_round_bar(15);

@@ -71,6 +71,17 @@ if "--tj" in sys.argv:
            ["", "spec wait + window plan + sync", "reload issue", "outer-step entry", "gate read + E' wait", "cell update",
             "sync (bar)", "h' exchange", "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)",
             "g exchange + sync", "lists + reload wait"])
+if "--sub" in sys.argv:   # warp 0's finish_round_rnnt sub-phases (slot 14, columns 1..6)
+    x = tl[0]
+    ev = [i for i in range(TL_N) if x[i, 8, 0] > 0 and all(x[i, 14, k] > 0 for k in range(1, 7))]
+    labs = ["load state + decisions", "append + state store", "lists + counters", "plan_next_tj", "reload list", "E' issue"]
+    prev = [x[i, 8, 0] for i in ev]
+    print(f"\nfinish_round_rnnt sub-phases ({len(ev)} rounds)")
+    for k in range(1, 7):
+        cur = [x[i, 14, k] for i in ev]
+        print(f"  {labs[k - 1]:28s} {np.mean(np.array(cur) - np.array(prev)):8.0f} cyc")
+        prev = cur
+    print(f"  {'to stamp 9':28s} {np.mean([x[i, 9, 0] - x[i, 14, 6] for i in ev]):8.0f} cyc")
 report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 9, 10, 5, 6, 7],
        ["", "outer-step entry", "first gate tile", "rest tiles + E' wait", "sync (bar)", "h' exchange",
         "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)", "g exchange + sync"])
