@@ -317,6 +317,9 @@ ll_status ll_release(void *workspace);
  *                  predictor has consumed = hypothesis length, 0, 0)
  *    probe_counts  DEVICE i32 [probe_regions][2]: logit rows, g rows written
  *                  (values > probe_rows mean the region was truncated)
+ *    probe_stall   cycles that the odd ranks of every cluster spin before each
+ *                  group's initialisation (test hook: skews the CTAs of a cluster
+ *                  at group starts, to stress the cross-CTA exchanges); 0 = off
  *  Set probe_logits = NULL to disable the probe.
  *
  *  projections    0 (default): the joint's input projections are precomputed
@@ -344,6 +347,7 @@ typedef struct {
   int32_t *probe_counts;
   int32_t probe_rows, probe_regions;
   int32_t projections;
+  int32_t probe_stall;
 } ll_options;
 
 ll_status ll_set_options(const ll_options *options);

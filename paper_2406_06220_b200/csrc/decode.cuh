@@ -285,6 +285,7 @@ struct DecodeParams {
   float *probe_logits, *probe_g;
   int *probe_lmeta, *probe_gmeta, *probe_counts;
   int probe_rows, probe_regions;
+  int probe_stall;               // probe kernels: cycles odd ranks spin before each group's init
   // ll_debug_joint mode
   const float *dbg_g;
   float *dbg_logits;
@@ -2982,6 +2983,13 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
         rs.scanning[lane] = 0;
         rs.found[lane] = 0;
         rs.score[lane] = 0.f;
+      }
+      if constexpr (DBG != 0) {   // test hook: skew the cluster's CTAs at group starts
+        if (p.probe_stall > 0 && (rank & 1)) {
+          const long long c0 = clock64();
+          while (clock64() - c0 < p.probe_stall) {
+          }
+        }
       }
       if constexpr (PRED == 0) {
         // LSTM initial state h = c = 0 (reading A8)

@@ -747,6 +747,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     p.probe_logits = g_opt.probe_logits; p.probe_lmeta = g_opt.probe_lmeta;
     p.probe_g = g_opt.probe_g; p.probe_gmeta = g_opt.probe_gmeta; p.probe_counts = g_opt.probe_counts;
     p.probe_rows = g_opt.probe_rows; p.probe_regions = g_opt.probe_regions;
+    p.probe_stall = g_opt.probe_stall;
     if (cudaMemsetAsync(p.probe_counts, 0, sizeof(int) * 2 * p.probe_regions, st) != cudaSuccess) return LL_ERR_CUDA;
   }
   int used = 0;
@@ -847,7 +848,7 @@ ll_status ll_set_options(const ll_options *o) {
   if (o->cluster_size < 0 || o->cluster_size > MAX_C || o->group_rows < 0 || o->group_rows > MAX_R ||
       o->window < 0 || o->window > 8 || o->max_clusters < 0 || o->schedule < -1 || o->schedule > 1 ||
       o->spec_prefetch < -1 || o->spec_prefetch > 1 || o->probe_rows < 0 || o->probe_regions < 0 ||
-      o->projections < 0 || o->projections > 1)
+      o->projections < 0 || o->projections > 1 || o->probe_stall < 0)
     return LL_ERR_INVALID_ARGUMENT;
   g_opt = *o;
   return LL_OK;

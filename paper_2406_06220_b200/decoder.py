@@ -227,11 +227,12 @@ def debug_joint(model: Model, enc_rows: torch.Tensor, g_rows: torch.Tensor, want
 
 
 def probe_decode(dec: "LabelLoopingDecoder", enc: torch.Tensor, lengths: torch.Tensor, rows: int = 8192,
-                 regions: int = 8):
+                 regions: int = 8, **opts):
     """Decode through the production FastConformer kernel instantiation with its
     probe hook (ll.h ll_options): returns (DecodeOutput, joint rows, g rows) where
     joint rows = list of (b, t, n_labels, logits [V+1+|D|]) and g rows = list of
-    (b, n_labels, g [H]) as numpy arrays (parity tests only)."""
+    (b, n_labels, g [H]) as numpy arrays (parity tests only).  opts: further
+    ll_options fields (e.g. group_rows)."""
     m = dec.model
     NV = m.V1 + m.num_durations
     dev = m.device
@@ -242,7 +243,7 @@ def probe_decode(dec: "LabelLoopingDecoder", enc: torch.Tensor, lengths: torch.T
     cnt = torch.zeros(regions, 2, dtype=torch.int32, device=dev)
     with ll.options(probe_logits=pl.data_ptr(), probe_lmeta=lm.data_ptr(), probe_g=pg.data_ptr(),
                     probe_gmeta=gm.data_ptr(), probe_counts=cnt.data_ptr(), probe_rows=rows,
-                    probe_regions=regions):
+                    probe_regions=regions, **opts):
         out = dec.decode(enc, lengths)
     torch.cuda.synchronize()
     cnt = cnt.cpu().numpy()

@@ -506,6 +506,33 @@ def test_production_kernel_logits_and_g(kind, tdt):
     assert gerr < G_TOL, gerr
 
 
+def test_group_start_h_exchange_race_regression():
+    """Regression (round 2): a CTA used to zero its h buffer when it took the
+    next group while faster CTAs of its cluster could already have st.async'ed
+    that group's first h' slices into it -> wrong g on the first predictor step
+    of a group.  Many short groups (2 rows each, short utterances) make group
+    starts frequent, and the probe's stall hook delays the odd ranks of each
+    cluster at every group start (the race window wide open); the production
+    kernel's g after EVERY predictor step must match float64."""
+    from paper_2406_06220_b200.decoder import probe_decode
+    spec = synth.ModelSpec(1025, 512, 640, 640, "lstm", 1, None, 0, 10)
+    w = synth.make_weights(spec, 71, blank_bias=synth.random_family_blank_bias(spec))
+    B, T = 40, 24
+    enc, lengths = synth.make_inputs(72, B, T, spec.enc_dim, 6, T)
+    model = gpu_model(spec, w)
+    o = Transducer.from_spec(spec, w)
+    for _ in range(3):
+        dec = LabelLoopingDecoder(model, spec.max_symbols, B, T)
+        out, jrows, grows = probe_decode(dec, torch.from_numpy(enc).to("cuda", torch.bfloat16),
+                                         torch.from_numpy(lengths).cuda(), regions=4, group_rows=2,
+                                         probe_stall=20000)
+        hyps = out.hypotheses()
+        gseq = {b: _oracle_g_sequence(o, hyps[b][0]) for b in range(B)}
+        assert dec.stats()["groups"] == B // 2
+        gerr = max(float(np.abs(g.astype(np.float64) - gseq[b][n]).max()) for b, n, g in grows)
+        assert gerr < G_TOL, gerr
+
+
 def test_config4_random_family_full_batch():
     """Config (4) in the launch configuration bench.py times (B=512, lengths
     50..1500, D_e=1024, stateless context 2, throughput mode: many waves of small
