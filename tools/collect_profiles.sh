@@ -17,8 +17,11 @@ for c in fc-rnnt fc-tdt; do
     > $o/${t}_bench_${c}_alg3-batched.json 2> $o/${t}_bench_${c}_alg3-batched.err
 done
 for c in sweep-rnnt sweep-tdt; do
-  timeout 900 python bench.py --config $c --steps 3 --warmup 1 --no-cpu-baseline > $o/${t}_bench_$c.json 2> $o/${t}_bench_$c.err
+  timeout 900 python bench.py --config $c --steps 3 --warmup 3 > $o/${t}_bench_$c.json 2> $o/${t}_bench_$c.err
 done
+# the sweep as B=32 launches (the metric's batch) on 4 concurrent streams
+timeout 900 python bench.py --config sweep-rnnt --chunk 32 --streams 4 --steps 3 --warmup 3 --no-cpu-baseline \
+  > $o/${t}_bench_sweep-rnnt_b32x4.json 2> $o/${t}_bench_sweep-rnnt_b32x4.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/${t}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $o/${t}_launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:decode_kernel -s 2 -c 1 \

@@ -16,6 +16,7 @@ ROWS = [
     ("stateless-b512", "stateless-b512 (config 4)"),
     ("sweep-rnnt", "sweep-rnnt (config 5, 8192 utt)"),
     ("sweep-tdt", "sweep-tdt (config 5, 8192 utt)"),
+    ("sweep-rnnt_b32x4", "sweep-rnnt as B=32 launches on 4 streams"),
     ("fc-rnnt-4x", "fc-rnnt-4x (4× subsampling, 40 ms frames, T ≈ 500)"),
     ("fc-rnnt_alg3-batched", "fc-rnnt, Alg. 3 batched outer loop (--schedule batched)"),
     ("fc-tdt_alg3-batched", "fc-tdt, Alg. 3 batched outer loop"),
