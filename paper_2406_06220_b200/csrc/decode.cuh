@@ -1195,6 +1195,13 @@ struct Ctx {
   __device__ void joint_keys_tj(int nrows_valid, float *logits, int row_base) {
     const int V1 = p.V1, NV = p.V1 + p.nD;
     uint64_t *wk = wkey();
+#ifdef LL_TIMELINE
+    if (tid == 0 && tl != nullptr && tl_round < TL_N) {   // is the background gate batch still running?
+      const bool pend = (phs & (1u << 8)) && !mbar_test_wait(smem_u32(bar(BAR_GATE)), (phs >> 9) & 1u);
+      tl[((size_t)tl_round * TL_PH + 14) * MAX_NW + 7] = pend ? 2 : 1;
+      tl[((size_t)tl_round * TL_PH + 14) * MAX_NW + 8] = clock64();
+    }
+#endif
     if (tid == 0) post(MCMD_JOINT | (spec_x >= 0 ? 0x100 | (spec_x << 9) : 0));
     spec_x = -1;
     // extra rows (<= 8 per CTA, rows vx0 ..): after the MMAs (the tensor pipe and
@@ -1486,7 +1493,13 @@ struct Ctx {
     // TG: the other CTAs write their next h' slices into this CTA's h buffer
     // only after this round's partial keys arrive, so the gate batch reading
     // the buffer completes first
+#ifdef LL_TIMELINE
+    const bool gpend = (phs & (1u << 8)) != 0;
+#endif
     gate_wait();
+#ifdef LL_TIMELINE
+    if (tid == 0 && tl != nullptr && tl_round < TL_N && gpend) tl[((size_t)tl_round * TL_PH + 14) * MAX_NW + 9] = clock64();
+#endif
     const int nz = rs.nz;
     if (tid == 0) mbar_arrive_expect_tx(bar(BAR_X + par()), (uint32_t)(C * nz * 8 * pks()));
     sync();

@@ -22,12 +22,21 @@ from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
 cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "fc-rnnt"
 spec, w, enc, lengths = bench.workload(cfg, 1000)
+if "--sorted" in sys.argv:   # longest utterances first: cluster 0 (block 0) decodes the critical group
+    order = np.argsort(-lengths, kind="stable")
+    enc, lengths = np.ascontiguousarray(enc[order]), np.ascontiguousarray(lengths[order])
 model = Model(w, spec.pred_kind, spec.context, spec.blank_id, spec.durations, "bf16")
 dec = LabelLoopingDecoder(model, spec.max_symbols, enc.shape[0], enc.shape[1])
 e = torch.from_numpy(enc).to("cuda", torch.bfloat16); l = torch.from_numpy(lengths).cuda()
+import time
 for _ in range(3):
     buf.zero_()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
     dec.decode(e, l)
+    ev1.record()
+    torch.cuda.synchronize()
+print("decode ms (timeline build):", round(ev0.elapsed_time(ev1), 4))
 torch.cuda.synchronize()
 print(cfg, dec.stats())
 tl = buf.cpu().numpy().reshape(2, TL_N, TL_PH, NW).astype(np.float64)
@@ -82,6 +91,14 @@ if "--sub" in sys.argv:   # warp 0's finish_round_rnnt sub-phases (slot 14, colu
         print(f"  {labs[k - 1]:28s} {np.mean(np.array(cur) - np.array(prev)):8.0f} cyc")
         prev = cur
     print(f"  {'to stamp 9':28s} {np.mean([x[i, 9, 0] - x[i, 14, 6] for i in ev]):8.0f} cyc")
+if "--gate" in sys.argv:   # background gate batch vs the joint post (slot 14: col 7 pending flag, 8 post time, 9 gate done)
+    x = tl[0]
+    ev = [i for i in range(TL_N) if x[i, 14, 7] > 0]
+    pend = [i for i in ev if x[i, 14, 7] == 2]
+    print(f"\ngate batch still running at the joint post: {len(pend)} of {len(ev)} rounds")
+    lag = [x[i, 14, 9] - x[i, 14, 8] for i in pend if x[i, 14, 9] > 0]
+    if lag:
+        print(f"  gate done after the post by {np.mean(lag):.0f} cyc on average (max {np.max(lag):.0f})")
 report(1, "predictor steps", [8, 0, 1, 2, 3, 4, 9, 10, 5, 6, 7],
        ["", "outer-step entry", "first gate tile", "rest tiles + E' wait", "sync (bar)", "h' exchange",
         "W_pred partial MMA", "sync (bar)", "W_pred reduce + g bcast", "sync (bar)", "g exchange + sync"])
