@@ -65,6 +65,9 @@ def parse():
                          "evaluation (the ablation arm of Table 3; ll_options.projections = 1)")
     ap.add_argument("--batch", type=int, default=0,
                     help="decode only the first B utterances of the config's batch (Table 3's batch sizes 1 / 4)")
+    ap.add_argument("--no-group-plan", action="store_true",
+                    help="equal groups of consecutive utterances (ll_options.group_plan = 0) instead of the "
+                         "length-sorted unequal groups")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0: auto)")
     return ap.parse_args()
@@ -315,9 +318,10 @@ def main():
     from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
     llbuild.build()
-    if a.schedule == "batched" or a.projections == "on-the-fly":   # ll_options of this thread
+    if a.schedule == "batched" or a.projections == "on-the-fly" or a.no_group_plan:   # ll_options of this thread
         o = ll.options(schedule=0 if a.schedule == "batched" else -1,
-                       projections=1 if a.projections == "on-the-fly" else 0).opts
+                       projections=1 if a.projections == "on-the-fly" else 0,
+                       group_plan=0 if a.no_group_plan else -1).opts
         if ll.ll_set_options(o) != ll.LL_OK:
             raise RuntimeError("ll_set_options")
     torch.cuda.set_device(local)

@@ -297,6 +297,10 @@ ll_status ll_release(void *workspace);
  *  schedule       -1 default (per-row ticks), 0 the batched outer loop of
  *                 Alg. 3 as listed, 1 per-row ticks.
  *  spec_prefetch  -1 default (on), 0 off, 1 on: speculative next-window copies.
+ *  group_plan     -1 default (on), 0 off, 1 on: length-sorted unequal groups for
+ *                 one-wave RNN-T decodes of the FastConformer shape (B <= 32):
+ *                 the groups with a spare slot hold the longest utterances and
+ *                 take a wider window; hypotheses are the same.
  *  gemm_mma_sync  1: encoder projection on the mma.sync GEMM instead of tcgen05.
  *  timeline       DEVICE u64 buffer for the per-warp timeline (libll_timeline
  *                 builds only; ignored by libll.so).
@@ -348,6 +352,7 @@ typedef struct {
   int32_t probe_rows, probe_regions;
   int32_t projections;
   int32_t probe_stall;
+  int32_t group_plan;
 } ll_options;
 
 ll_status ll_set_options(const ll_options *options);

@@ -194,7 +194,7 @@ __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a -
 // allow_tj = false: a kernel without the TJ / TG paths (debug_joint_kernel).
 __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, int V1, int nD, int R, int W,
                                               int WF, int C, int NS, int sc = 0, bool allow_tj = true,
-                                              int layers = 1, int otf_de = 0) {
+                                              int layers = 1, int otf_de = 0, int jr_min = 0) {
   Layout L;
   L.otf = otf_de;
   L.wks = sc ? 4 : 2;
@@ -211,7 +211,7 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   L.NTH = L.NW * 32 + (L.tj ? 32 : 0);
   L.NS = (L.ring && !L.tj) ? L.DPC / 8 : 0;   // W_pred tiles of this CTA in smem (TJ: registers)
   (void)NS;
-  L.JR = R * W;
+  L.JR = R * W > jr_min ? R * W : jr_min;   // jr_min: unequal groups (a smaller group's wider window)
   L.JRp = (L.JR + 15) / 16 * 16;
   if (L.JRp < R) L.JRp = (R + 15) / 16 * 16;
   const int K = H > P ? H : P;
@@ -291,6 +291,10 @@ struct DecodeParams {
   float *dbg_logits;
   int *dbg_argmax, *dbg_dargmax;
   int dbg_n;
+  // length-sorted unequal groups (RNN-T FC tick kernels, one wave, B <= 32):
+  // groups g < gp_small hold gp_rsmall utterances with a gp_wsmall-frame
+  // window, the others R with W; utterances dealt by (length desc, index)
+  int gp_small, gp_rsmall, gp_wsmall;
   // OTF (LM = 4): p.f points at the ENCODER output [B, T_max, De] (bf16)
   int De;
   const void *w_enc, *b_enc;
@@ -310,6 +314,7 @@ struct RowState {
   int dec[MAX_JR];                        // per joint row: token | dur_index << 24
   int zbeg[MAX_R], zcnt[MAX_R];          // per slot: first compact joint row of its window, live rows
   int nscan, npred, nactive, nz, ready;
+  int wg;                                // window of the current group (p.W, or gp_wsmall)
   int grp[2];                            // group index broadcast (double-buffered)
   int ack[2];
   volatile int mcmd;                     // (TJ) command word for the MMA warp (MCMD_*)
@@ -676,7 +681,7 @@ struct Ctx {
     int s = 0, base = 0, cnt = 0;
     if (lane < n) {
       s = reload ? rs.llist[lane] : rs.slist[lane];
-      base = rs.t[s] + (reload ? 0 : p.W);
+      base = rs.t[s] + (reload ? 0 : rs.wg);
       cnt = rs.L[s] - base;
       if (cnt > p.WF) cnt = p.WF;
       if (cnt < 0) cnt = 0;
@@ -798,7 +803,7 @@ struct Ctx {
   // at t, every other row is reloaded at t), so frame j of slot s is f row j of
   // its fbuf slot: the plan depends only on (t, L) per slot.
   __device__ void plan_next_tj(bool scan_next, int t, int Ls) {
-    const int W = p.W;
+    const int W = rs.wg;
     int cnt = 0;
     if (scan_next) cnt = min(W, Ls - t);
     int incl = cnt;   // inclusive scan over the slots (cnt = 0 on lanes >= R)
@@ -1757,7 +1762,7 @@ struct Ctx {
       tl_sub(4);
       // the next tick's reloads: rows that found a label, and scanning rows whose
       // speculative window (t_round + W) does not start at their new t (TDT jumps)
-      const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + p.W)));
+      const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + rs.wg)));
       const unsigned ml = __ballot_sync(FULL, ld);
       if (ld) rs.llist[__popc(ml & below)] = lane;
       if (lane == 0) rs.nload = __popc(ml);
@@ -1898,7 +1903,7 @@ struct Ctx {
       plan_next_tj(inr && act && (scan || needp), t, Ls);
       // the next tick's reloads: rows that found a label, and scanning rows whose
       // speculative window (t_round + W) does not start at their new t (TDT jumps)
-      const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + p.W)));
+      const bool ld = inr && act && (needp || (scan && !(p.spec_prefetch && t == t_round + rs.wg)));
       const unsigned ml = __ballot_sync(FULL, ld);
       if (ld) rs.llist[__popc(ml & below)] = lane;
       if (lane == 0) rs.nload = __popc(ml);
@@ -2975,8 +2980,34 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
       if (grp >= p.n_groups) break;
       if (t0) s_cnt[SC_GROUPS]++;
       // ---- group init (warp 0: lane = row slot) -----------------------------
+      int gb = grp * R + lane, gsize = R;   // this slot's utterance, the group's size
+      if (warp == 0) {
+        if (p.gp_small > 0) {
+          // unequal groups: utterance i (lane i, B <= 32) ranked by (length desc, i)
+          int Li = 0;
+          if (lane < p.B) {
+            Li = p.lengths[lane];
+            if (Li < 0 || Li > p.T_max) Li = 0;
+          }
+          int rk = 0;
+          for (int j = 0; j < p.B; ++j) {
+            const int Lj = __shfl_sync(0xffffffffu, Li, j);
+            rk += (Lj > Li || (Lj == Li && j < lane)) ? 1 : 0;
+          }
+          const int xs = p.gp_small, rsz = p.gp_rsmall;
+          const int start = grp < xs ? grp * rsz : xs * rsz + (grp - xs) * R;
+          gsize = grp < xs ? rsz : R;
+          if (lane < p.B && rk >= start && rk < start + gsize) rs.zsrc[rk - start] = lane;   // scratch
+          __syncwarp();
+          gb = lane < gsize ? rs.zsrc[lane] : p.B;
+          __syncwarp();
+          if (lane == 0) rs.wg = grp < xs ? p.gp_wsmall : p.W;
+        } else if (lane == 0) {
+          rs.wg = p.W;
+        }
+      }
       if (warp == 0 && lane < R) {
-        const int b = grp * R + lane;
+        const int b = lane < gsize ? gb : p.B;
         int L = 0;
         if (b < p.B) {
           L = p.lengths[b];
@@ -2985,7 +3016,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
             L = 0;
           }
         }
-        rs.b[lane] = b < p.B ? b : 0;
+        rs.b[lane] = b < p.B ? b : p.B;   // p.B: no utterance in this slot (never addressed: L = 0)
         rs.L[lane] = L;
         rs.t[lane] = 0; rs.k[lane] = 0; rs.len[lane] = 0;
         rs.last[lane] = p.blank;
@@ -3376,9 +3407,9 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
       }
       // ---- group done: lengths, statistics -----------------------------------
       if (rank == 0 && warp == 0) {
-        const int b = grp * R + lane;
+        const int b = lane < R ? rs.b[lane] : p.B;   // the slot's utterance (unequal groups: length-sorted)
         int tot = 0;
-        if (lane < R && b < p.B) {
+        if (b < p.B) {
           p.out_lengths[b] = rs.len[lane];
           if constexpr (SC) p.out_scores[b] = rs.score[lane];
           tot = rs.len[lane];

@@ -75,6 +75,7 @@ ll_options default_options() {
   memset(&o, 0, sizeof(o));
   o.schedule = -1;
   o.spec_prefetch = -1;
+  o.group_plan = -1;
   return o;
 }
 thread_local ll_options g_opt = default_options();
@@ -655,6 +656,28 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     cf.WF = 1;
     cf.L = make_layout(bf, lstm, H, P, V1, nD, cf.R, 1, 1, cf.C, 0, 0, true, nl);
   }
+  // Length-sorted unequal groups: a one-wave RNN-T FC tick
+  // decode of n groups of R rows has n R - B spare slots; making those groups
+  // one row smaller lets them take wider windows, and the longest utterances
+  // (dealt by length) go there -- the critical group needs fewer ticks
+  int gp_small = 0, gp_rsmall = 0, gp_wsmall = 0;
+  if (g_opt.group_plan != 0 && !tdt && !sc && !frame_looping && !g_opt.probe_logits && !otf && bf &&
+      is_fc(bf, H, P, cf.C) && !g_opt.group_rows && !g_opt.window && (g_opt.schedule < 0 || g_opt.schedule == 1) &&
+      B <= 32 && cf.R >= 3) {
+    const int ng = (B + cf.R - 1) / cf.R, xs = ng * cf.R - B, rsm = cf.R - 1;
+    int wsm = MAX_JR / rsm;
+    if (wsm > 8) wsm = 8;
+    if (xs > 0 && xs < ng && wsm > cf.W) {
+      const Layout L2 = make_layout(bf, lstm, H, P, V1, nD, cf.R, cf.W, wsm, cf.C, 0, 0, true, nl, 0, rsm * wsm);
+      if (L2.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) {
+        cf.L = L2;
+        cf.WF = wsm;
+        gp_small = xs;
+        gp_rsmall = rsm;
+        gp_wsmall = wsm;
+      }
+    }
+  }
   const int C = cf.C, R = cf.R;
   const Layout &L = cf.L;
 
@@ -707,6 +730,9 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.cap = cap;
   p.L = L;
   p.spec_prefetch = frame_looping ? 0 : (g_opt.spec_prefetch < 0 ? 1 : g_opt.spec_prefetch);
+  p.gp_small = gp_small;
+  p.gp_rsmall = gp_rsmall;
+  p.gp_wsmall = gp_wsmall;
   p.frame_looping = frame_looping ? 1 : 0;
   p.sched = g_opt.schedule < 0 ? 1 : g_opt.schedule;
   p.lengths = lengths;
@@ -848,7 +874,8 @@ ll_status ll_set_options(const ll_options *o) {
   if (o->cluster_size < 0 || o->cluster_size > MAX_C || o->group_rows < 0 || o->group_rows > MAX_R ||
       o->window < 0 || o->window > 8 || o->max_clusters < 0 || o->schedule < -1 || o->schedule > 1 ||
       o->spec_prefetch < -1 || o->spec_prefetch > 1 || o->probe_rows < 0 || o->probe_regions < 0 ||
-      o->projections < 0 || o->projections > 1 || o->probe_stall < 0)
+      o->projections < 0 || o->projections > 1 || o->probe_stall < 0 || o->group_plan < -1 ||
+      o->group_plan > 1)
     return LL_ERR_INVALID_ARGUMENT;
   g_opt = *o;
   return LL_OK;

@@ -50,13 +50,15 @@ class ll_options(ctypes.Structure):
                 ("gemm_mma_sync", c_int32), ("timeline", c_void_p), ("trace", c_void_p),
                 ("probe_logits", c_void_p), ("probe_lmeta", c_void_p), ("probe_g", c_void_p),
                 ("probe_gmeta", c_void_p), ("probe_counts", c_void_p), ("probe_rows", c_int32),
-                ("probe_regions", c_int32), ("projections", c_int32), ("probe_stall", c_int32)]
+                ("probe_regions", c_int32), ("projections", c_int32), ("probe_stall", c_int32),
+                ("group_plan", c_int32)]
 
 
 def default_options() -> ll_options:
     o = ll_options()
     o.schedule = -1
     o.spec_prefetch = -1
+    o.group_plan = -1
     return o
 
 

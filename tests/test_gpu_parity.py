@@ -652,3 +652,31 @@ def test_multilayer_lstm_f32(cfg, layers):
         mism = sum(1 for b in ref if tuple(map(list, ref[b])) != tuple(map(list, hyps[b])))
         assert mism == 0 or ties > 0
     assert decs > 300
+
+
+@pytest.mark.parametrize("B", [32, 30, 29])
+def test_group_plan_equals_equal_groups(B):
+    """Length-sorted unequal groups (ll_options.group_plan, default on for
+    one-wave FC RNN-T decodes): hypotheses identical to equal groups of
+    consecutive utterances (utterances are independent), every
+    output length written (buffers pre-filled with garbage), a zero-length
+    utterance included; every row verified against float64."""
+    c = synth.CONFIGS["fc-rnnt"]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 91 + B, blank_bias=synth.random_family_blank_bias(spec))
+    enc, lengths = synth.make_inputs(92 + B, B, c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
+    lengths[B // 2] = 0
+    model = gpu_model(spec, w)
+    out = {}
+    for plan in (0, -1):
+        dec = LabelLoopingDecoder(model, spec.max_symbols, B, c["T_max"])
+        dec.lengths_out.fill_(-7)
+        dec.tokens.fill_(-7)
+        with ll.options(group_plan=plan):
+            o = dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), torch.from_numpy(lengths).cuda())
+        assert int(o.lengths.min()) >= 0
+        out[plan] = (o.hypotheses(), dec.stats())
+    assert out[0][0] == out[-1][0]
+    assert out[-1][0][B // 2] == ([], [])
+    assert out[0][1]["joint_evals"] == out[-1][1]["joint_evals"]
+    verify_all(spec, w, enc, lengths, out[-1][0])
