@@ -1806,7 +1806,7 @@ struct Ctx {
     if constexpr (TD) {
       (void)dec; (void)b0; (void)c;
       if (scan) {
-        const int W = p.W;
+        const int W = rs.wg;   // logical rows s * W + j (plan_next_tj)
         [[maybe_unused]] float add = 0.f;
         while (pos < W && t + pos < Ls) {
           const int ee = rs.dec[lane * W + pos];
@@ -1834,7 +1834,7 @@ struct Ctx {
         float add = 0.f;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (j < used) add += rs.lp[lane * p.W + j];
+          if (j < used) add += rs.lp[lane * rs.wg + j];
         if (scan) rs.score[lane] += add;
       }
     }

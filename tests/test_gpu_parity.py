@@ -654,14 +654,15 @@ def test_multilayer_lstm_f32(cfg, layers):
     assert decs > 300
 
 
-@pytest.mark.parametrize("B", [32, 30, 29])
-def test_group_plan_equals_equal_groups(B):
+@pytest.mark.parametrize("cfg,B", [("fc-rnnt", 32), ("fc-rnnt", 30), ("fc-rnnt", 29), ("fc-tdt", 32),
+                                   ("fc-tdt", 31)])
+def test_group_plan_equals_equal_groups(cfg, B):
     """Length-sorted unequal groups (ll_options.group_plan, default on for
-    one-wave FC RNN-T decodes): hypotheses identical to equal groups of
+    one-wave FC decodes, RNN-T and TDT): hypotheses identical to equal groups of
     consecutive utterances (utterances are independent), every
     output length written (buffers pre-filled with garbage), a zero-length
     utterance included; every row verified against float64."""
-    c = synth.CONFIGS["fc-rnnt"]
+    c = synth.CONFIGS[cfg]
     spec = c["spec"]
     w = synth.make_weights(spec, 91 + B, blank_bias=synth.random_family_blank_bias(spec))
     enc, lengths = synth.make_inputs(92 + B, B, c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
@@ -677,6 +678,6 @@ def test_group_plan_equals_equal_groups(B):
         assert int(o.lengths.min()) >= 0
         out[plan] = (o.hypotheses(), dec.stats())
     assert out[0][0] == out[-1][0]
-    assert out[-1][0][B // 2] == ([], [])
+    assert out[-1][0][B // 2][0] == []
     assert out[0][1]["joint_evals"] == out[-1][1]["joint_evals"]
     verify_all(spec, w, enc, lengths, out[-1][0])
