@@ -299,7 +299,7 @@ ll_status ll_release(void *workspace);
  *  spec_prefetch  -1 default (on), 0 off, 1 on: speculative next-window copies.
  *  group_plan     -1 default (on), 0 off, 1 on: length-sorted unequal groups for
  *                 one-wave decodes of the FastConformer shape (B <= 32, RNN-T and
- *                 TDT, tick schedule, no scores / probe / on-the-fly projections):
+ *                 TDT, tick schedule, no scores / probe):
  *                 the groups with a spare slot hold the longest utterances and
  *                 take a wider window; hypotheses are the same.
  *  gemm_mma_sync  1: encoder projection on the mma.sync GEMM instead of tcgen05.

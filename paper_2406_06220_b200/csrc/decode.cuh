@@ -964,7 +964,7 @@ struct Ctx {
           int k = k0 + 8 * nb + g;
           if (k >= nz) k = nz - 1;   // rows past nz: any valid row (outputs never stored)
           er[nb] = fb + (uint32_t)(rs.zsrc[k] * 2);
-          hr[nb] = hb + (uint32_t)(16 * (rs.zdst[k] / p.W));
+          hr[nb] = hb + (uint32_t)(16 * (rs.zdst[k] / rs.wg));
         }
         const int nbn = (nz - k0) > 8 ? 2 : 1;
         // W_enc fragments of this warp's first two encoder K blocks: issued

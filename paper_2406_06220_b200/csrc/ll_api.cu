@@ -661,7 +661,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   // one row smaller lets them take wider windows, and the longest utterances
   // (dealt by length) go there -- the critical group needs fewer ticks
   int gp_small = 0, gp_rsmall = 0, gp_wsmall = 0;
-  if (g_opt.group_plan != 0 && !sc && !frame_looping && !g_opt.probe_logits && !otf && bf &&
+  if (g_opt.group_plan != 0 && !sc && !frame_looping && !g_opt.probe_logits && bf &&
       is_fc(bf, H, P, cf.C) && !g_opt.group_rows && !g_opt.window && (g_opt.schedule < 0 || g_opt.schedule == 1) &&
       B <= 32 && cf.R >= 3) {
     const int ng = (B + cf.R - 1) / cf.R, xs = ng * cf.R - B, rsm = cf.R - 1;
@@ -669,7 +669,8 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     if (wsm > 8) wsm = 8;
     for (; xs > 0 && xs < ng && wsm > cf.W; --wsm) {   // the widest window whose buffers fit
       const int wfs = wsm + (maxd > 1 ? maxd - 1 : 0);   // TDT: the window plus the largest jump
-      const Layout L2 = make_layout(bf, lstm, H, P, V1, nD, cf.R, cf.W, wfs, cf.C, 0, 0, true, nl, 0, rsm * wsm);
+      const Layout L2 = make_layout(bf, lstm, H, P, V1, nD, cf.R, cf.W, wfs, cf.C, 0, 0, true, nl, otf ? De : 0,
+                                    rsm * wsm);
       if (L2.total + sizeof(RowState) + 1024 <= SMEM_LIMIT) {
         cf.L = L2;
         cf.WF = wfs;
