@@ -297,11 +297,16 @@ ll_status ll_release(void *workspace);
  *  schedule       -1 default (per-row ticks), 0 the batched outer loop of
  *                 Alg. 3 as listed, 1 per-row ticks.
  *  spec_prefetch  -1 default (on), 0 off, 1 on: speculative next-window copies.
- *  group_plan     -1 default (on), 0 off, 1 on: length-sorted unequal groups for
+ *  group_plan     -1 default (on), 0 off, 1 on: which utterances share a group
+ *                 (hypotheses are the same either way).  On:
  *                 one-wave decodes of the FastConformer shape (B <= 32, RNN-T and
- *                 TDT, tick schedule, no scores / probe):
- *                 the groups with a spare slot hold the longest utterances and
- *                 take a wider window; hypotheses are the same.
+ *                 TDT, tick schedule, no scores / probe) use length-sorted
+ *                 unequal groups (the groups with a spare slot hold the longest
+ *                 utterances and take a wider window); every other decode with
+ *                 more than one group ranks the utterances by length on the
+ *                 device (one small kernel) and groups consecutive ranks, so a
+ *                 group's rows have similar lengths and the longest groups run
+ *                 first.  Off: groups of consecutive utterances.
  *  gemm_mma_sync  1: encoder projection on the mma.sync GEMM instead of tcgen05.
  *  timeline       DEVICE u64 buffer for the per-warp timeline (libll_timeline
  *                 builds only; ignored by libll.so).

@@ -265,6 +265,7 @@ struct DecodeParams {
   int frame_looping;             // 1: Alg. 2 baseline control flow (RNN-T, W = 1)
   int sched;                     // label-looping schedule: 0 = Alg. 3 batched outer loop, 1 = per-row ticks
   const int *lengths;
+  const int *perm;               // optional: group rows are perm[grp * R + slot] (length-ranked utterances)
   const void *f;                 // [B, T_max, H] bf16 (bf16 path) / f32
   const void *w_out, *b_out, *w_dur, *b_dur;
   const void *w_pred, *b_pred, *w_hh;
@@ -2981,6 +2982,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
       if (t0) s_cnt[SC_GROUPS]++;
       // ---- group init (warp 0: lane = row slot) -----------------------------
       int gb = grp * R + lane, gsize = R;   // this slot's utterance, the group's size
+      if (warp == 0 && p.perm != nullptr && gb < p.B) gb = p.perm[gb];
       if (warp == 0) {
         if (p.gp_small > 0) {
           // unequal groups: utterance i (lane i, B <= 32) ranked by (length desc, i)

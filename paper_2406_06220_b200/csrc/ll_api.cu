@@ -33,7 +33,7 @@ constexpr int RPREF_MANY_LSTM = 8, RPREF_MANY_STATELESS = 16;
 constexpr size_t SMEM_LIMIT = 232448;
 
 struct Ws {
-  size_t f, tab, h, g, wst, wih, total;
+  size_t f, tab, h, g, wst, wih, perm, total;
 };
 
 size_t esize(ll_dtype d) { return d == LL_BF16 ? 2 : 4; }
@@ -62,6 +62,8 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)nlayers(pr) * 2 * B * P * esize(dt), 256);
   w.g = o;
   if (pr->kind == LL_PRED_LSTM) o = align_up(o + (size_t)B * H * 4, 256);
+  w.perm = o;   // utterances ranked by length (groups of similar lengths, longest first)
+  o = align_up(o + (size_t)B * 4, 256);
   w.total = o;
   return w;
 }
@@ -492,6 +494,35 @@ ll_status build_tables(bool bf, const ll_predictor *pr, const ll_joint *jn, ll_d
   return LL_OK;
 }
 
+// Utterances ranked by (length desc, index): perm[rank] = b.  Groups of
+// consecutive ranks then hold utterances of similar lengths (a group runs as
+// long as its longest row) and the work counter hands out the longest groups
+// first (LPT).  O(B^2) comparisons through shared-memory tiles: ~µs at B = 512.
+__global__ void rank_lengths_kernel(const int *lengths, int B, int T_max, int *perm) {
+  __shared__ int tile[256];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int Li = 0;
+  if (i < B) {
+    Li = lengths[i];
+    if (Li < 0 || Li > T_max) Li = 0;
+  }
+  int rk = 0;
+  for (int j0 = 0; j0 < B; j0 += 256) {
+    __syncthreads();
+    if (j0 + threadIdx.x < B) {
+      int L = lengths[j0 + threadIdx.x];
+      tile[threadIdx.x] = (L < 0 || L > T_max) ? 0 : L;
+    }
+    __syncthreads();
+    const int n = min(256, B - j0);
+    for (int j = 0; j < n; ++j) {
+      const int Lj = tile[j];
+      rk += (Lj > Li || (Lj == Li && j0 + j < i)) ? 1 : 0;
+    }
+  }
+  if (i < B) perm[rk] = i;
+}
+
 // ---------------------------------------------------------------------------
 // LL_PREC_EXACT with bf16 inputs, and bf16 LSTM predictors of more than one
 // layer: the call runs the fp32 kernels on fp32 copies of the bf16 values.
@@ -736,6 +767,13 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.gp_small = gp_small;
   p.gp_rsmall = gp_rsmall;
   p.gp_wsmall = gp_wsmall;
+  // more than one group and no unequal plan: groups of length-ranked utterances
+  if (g_opt.group_plan != 0 && gp_small == 0 && p.n_groups > 1) {
+    int *perm = (int *)(ws + w.perm);
+    rank_lengths_kernel<<<(B + 255) / 256, 256, 0, st>>>(lengths, B, T_max, perm);
+    if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
+    p.perm = perm;
+  }
   p.frame_looping = frame_looping ? 1 : 0;
   p.sched = g_opt.schedule < 0 ? 1 : g_opt.schedule;
   p.lengths = lengths;

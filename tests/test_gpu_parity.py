@@ -655,16 +655,20 @@ def test_multilayer_lstm_f32(cfg, layers):
 
 
 @pytest.mark.parametrize("cfg,B", [("fc-rnnt", 32), ("fc-rnnt", 30), ("fc-rnnt", 29), ("fc-tdt", 32),
-                                   ("fc-tdt", 31)])
+                                   ("fc-tdt", 31), ("fc-rnnt", 64), ("fc-tdt", 45), ("tiny", 40),
+                                   ("tiny-tdt", 37)])
 def test_group_plan_equals_equal_groups(cfg, B):
     """Length-sorted unequal groups (ll_options.group_plan, default on for
-    one-wave FC decodes, RNN-T and TDT): hypotheses identical to equal groups of
-    consecutive utterances (utterances are independent), every
+    one-wave FC decodes, RNN-T and TDT) and length-ranked groups (every other
+    decode with more than one group, any kernel): hypotheses identical to
+    equal groups of consecutive utterances (utterances are independent,
+    SPEC.md:354), every
     output length written (buffers pre-filled with garbage), a zero-length
     utterance included; every row verified against float64."""
     c = synth.CONFIGS[cfg]
     spec = c["spec"]
-    w = synth.make_weights(spec, 91 + B, blank_bias=synth.random_family_blank_bias(spec))
+    fam = synth.random_family_blank_bias(spec) if spec.joint_dim >= 70 else 0.5
+    w = synth.make_weights(spec, 91 + B, blank_bias=fam)
     enc, lengths = synth.make_inputs(92 + B, B, c["T_max"], spec.enc_dim, c["len_lo"], c["len_hi"])
     lengths[B // 2] = 0
     model = gpu_model(spec, w)
