@@ -526,8 +526,9 @@ def main():
                 "mode": "serving loop: step i+1's H2D overlaps step i's decode (H2D / D2H streams, 2 workspaces)",
                 "single_call": {"ms": single_ms, "value": audio_s / (single_ms / 1e3), "unit": UNIT,
                                 "mode": "one call at a time: H2D, decode, D2H back to back on one stream (latency)"}},
-        # encoder projection GEMM + decode kernel (tables prepared once); on the fly: the decode kernel only
-        "gpu_launches": a.steps * (1 if a.projections == "on-the-fly" else 2),
+        # the library's own count of the call's kernels (ll_stats [12]): encoder projection GEMM (not on
+        # the fly), the length ranking (decodes of several groups), the decode kernel; tables prepared once
+        "gpu_launches": a.steps * stats["launches"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": "decode_kernel",
                      "kernel_ms": kern_mean, "kernel_share_of_step": kern_mean / (tot_ms_max / a.steps),
@@ -763,9 +764,10 @@ def run_sweep(a, rank, world, local, dev):
         "utterances_per_s": a.steps * n_utt / (tot_ms / 1e3),
         "e2e": {"value": a.steps * audio_s / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_tot / a.steps},
-        # per launch: projection GEMM + decode; per step: the two packing kernels of ll_gather_ragged
-        # (NCCL's own all-gather / send-recv kernels not counted); model tables prepared once before timing
-        "gpu_launches": a.steps * (len(chunks) * 2 + 2),
+        # per launch: the library's own count (ll_stats [12]: projection GEMM, length ranking, decode);
+        # per step: the two packing kernels of ll_gather_ragged (NCCL's own all-gather / send-recv
+        # kernels not counted); model tables prepared once before timing
+        "gpu_launches": a.steps * (sum(st["launches"] for st in per_launch) + 2),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None, "kernel": "decode_kernel (rank 0, every launch)",
                      "kernel_ms_sum": sum(kern_mean), "flops_per_step": sum(flops),

@@ -235,7 +235,7 @@ ll_status ll_sync(void *workspace, ll_stream stream);
 const char *ll_status_string(ll_status status);
 
 /* Decode statistics of the last call that used `workspace`, copied to HOST
- * `out[12]` after synchronising `stream`: [0] outer steps (label-loop
+ * `out[13]` after synchronising `stream`: [0] outer steps (label-loop
  * iterations, summed over groups), [1] joint rounds (W-frame windows),
  * [2] joint evaluations whose decision was used (the algorithmic count of
  * Alg. 1), [3] batched predictor steps, [4] predictor row evaluations,
@@ -243,7 +243,9 @@ const char *ll_status_string(ll_status status);
  * computed (including speculative window frames), [9] window W, [10] rows
  * per group R, [11] the longest per-cluster chain, packed (rounds + steps) << 40
  * | joint rounds << 20 | predictor steps of that cluster (each field saturates
- * at 2^20 - 1): the critical path of the launch (bench.py's chain floor). */
+ * at 2^20 - 1): the critical path of the launch (bench.py's chain floor),
+ * [12] kernels the call launched (projection GEMM, model tables if rebuilt,
+ * length ranking, widening, the decode kernel). */
 ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream);
 
 /*

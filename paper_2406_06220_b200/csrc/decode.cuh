@@ -296,6 +296,7 @@ struct DecodeParams {
   // groups g < gp_small hold gp_rsmall utterances with a gp_wsmall-frame
   // window, the others R with W; utterances dealt by (length desc, index)
   int gp_small, gp_rsmall, gp_wsmall;
+  int n_launch;                  // kernels launched by this call (host count; ll_stats [12])
   // OTF (LM = 4): p.f points at the ENCODER output [B, T_max, De] (bf16)
   int De;
   const void *w_enc, *b_enc;
@@ -3449,6 +3450,7 @@ __global__ void __launch_bounds__(MAX_NW * 32 + (sizeof(T) == 2 && HC == TJ_H &&
         p.stats[7] = (unsigned long long)C;
         p.stats[9] = (unsigned long long)p.W;
         p.stats[10] = (unsigned long long)p.R;
+        p.stats[12] = (unsigned long long)p.n_launch;
       }
     }
   }

@@ -69,6 +69,9 @@ Ws ws_layout(int B, int T, const ll_predictor *pr, const ll_joint *jn, ll_dtype 
 }
 
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+// kernels launched by the current public decode call of this thread (reported
+// by ll_stats [12]; every launch site counts itself)
+thread_local int g_nlaunch = 0;
 
 // Test / debug options of this host thread (ll_set_options; ll.h).  The
 // production path reads no environment variable.
@@ -379,6 +382,7 @@ bool linear_tc(const void *X, int64_t ldx, const void *W, int64_t ldw, const voi
   }
   const int ntiles = mt * ((N + bn - 1) / bn);
   dim3 grid(std::min(ntiles, nsm));
+  ++g_nlaunch;
   if (out_bf16) gemm_tc_kernel<bf16><<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, a);
   else gemm_tc_kernel<float><<<grid, TC_THREADS, TC_SMEM, st>>>(mx, mw, a);
   s = cudaPeekAtLastError() == cudaSuccess ? LL_OK : LL_ERR_CUDA;
@@ -395,6 +399,7 @@ ll_status linear(bool bf, const void *X, int64_t ldx, const void *W, int64_t ldw
     if (linear_tc(X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K, out_bf16, st, s, lengths, T)) return s;
   }
   LinearArgs a{X, ldx, W, ldw, bias, bias2, Y, ldy, M, N, K};
+  ++g_nlaunch;
   if (bf) {
     dim3 grid((N + LB_N - 1) / LB_N, (M + LB_M - 1) / LB_M);
     if (out_bf16)
@@ -469,6 +474,7 @@ ll_status build_tables(bool bf, const ll_predictor *pr, const ll_joint *jn, ll_d
     // row's slice with ONE bulk copy of 4*UPC floats
     bf16 *wih = (bf16 *)(ws + w.wih);
     bf16 *bih = wih + (size_t)4 * P * P, *bhh = bih + 4 * P;
+    ++g_nlaunch;
     permute_gate_rows<<<296, 256, 0, st>>>((const bf16 *)pr->w_ih, (const bf16 *)pr->b_ih, (const bf16 *)pr->b_hh,
                                            wih, bih, bhh, P, C, L.UPC);
     if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
@@ -487,6 +493,7 @@ ll_status build_tables(bool bf, const ll_predictor *pr, const ll_joint *jn, ll_d
   if (s != LL_OK) return s;
   if (ring) {
     // contiguous per-CTA tile stream of W_hh / W_pred
+    ++g_nlaunch;
     pack_lstm_stream<<<296, 256, 0, st>>>((const bf16 *)pr->w_hh, (const bf16 *)jn->w_pred,
                                           (bf16 *)(ws + w.wst), P, C, L.UPC, L.DPC);
     if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
@@ -610,6 +617,7 @@ float *widen_all(const void *enc, size_t enc_n, const ll_predictor *pr, const ll
   auto widen = [&](const void *src, float *dst, size_t n) {
     if (n == 0) return;
     const int blocks = (int)std::min<size_t>((n + 255) / 256, 4096);
+    ++g_nlaunch;
     widen_bf16_kernel<<<blocks, 256, 0, st>>>((const bf16 *)src, dst, n);
   };
   for (int i = 0; i < na; ++i) {
@@ -770,6 +778,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   // more than one group and no unequal plan: groups of length-ranked utterances
   if (g_opt.group_plan != 0 && gp_small == 0 && p.n_groups > 1) {
     int *perm = (int *)(ws + w.perm);
+    ++g_nlaunch;
     rank_lengths_kernel<<<(B + 255) / 256, 256, 0, st>>>(lengths, B, T_max, perm);
     if (cudaPeekAtLastError() != cudaSuccess) return LL_ERR_CUDA;
     p.perm = perm;
@@ -818,6 +827,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
     if (cudaMemsetAsync(p.probe_counts, 0, sizeof(int) * 2 * p.probe_regions, st) != cudaSuccess) return LL_ERR_CUDA;
   }
   int used = 0;
+  p.n_launch = g_nlaunch + 1;   // this call's kernels, the decode kernel included (ll_stats [12])
   if (g_ev_before && cudaEventRecord(g_ev_before, st) != cudaSuccess) return LL_ERR_CUDA;
   if (otf) {             // on-the-fly projections (Table 3's ablation arm)
     s = tdt ? launch_decode<bf16, 0, KREG, FC_H, FC_P, FC_C, 4, 2>(p, C, L, p.n_groups, st, used)
@@ -951,6 +961,7 @@ ll_status ll_decode_rnnt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t 
                          int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
                          int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
                          void *workspace, size_t workspace_bytes, ll_stream stream) {
+  g_nlaunch = 0;
   return decode_impl(false, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
                      workspace_bytes, stream);
@@ -961,6 +972,7 @@ ll_status ll_decode_rnnt_scores(const void *enc, ll_dtype dtype, ll_prec prec, i
                                 int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
                                 int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
                                 float *out_scores, void *workspace, size_t workspace_bytes, ll_stream stream) {
+  g_nlaunch = 0;
   if (B > 0 && !out_scores) return LL_ERR_INVALID_ARGUMENT;
   return decode_impl(false, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
@@ -973,6 +985,7 @@ ll_status ll_decode_tdt_scores(const void *enc, ll_dtype dtype, ll_prec prec, in
                                int32_t num_durations, int32_t *out_tokens, int32_t *out_timestamps,
                                int32_t *out_durations, int32_t *out_lengths, int32_t out_capacity,
                                float *out_scores, void *workspace, size_t workspace_bytes, ll_stream stream) {
+  g_nlaunch = 0;
   if (B > 0 && !out_scores) return LL_ERR_INVALID_ARGUMENT;
   return decode_impl(true, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      durations, num_durations, out_tokens, out_timestamps, out_durations, out_lengths,
@@ -984,6 +997,7 @@ ll_status ll_decode_rnnt_frame_looping(const void *enc, ll_dtype dtype, ll_prec 
                                        int32_t blank_id, int32_t max_symbols, int32_t *out_tokens,
                                        int32_t *out_timestamps, int32_t *out_lengths, int32_t out_capacity,
                                        void *workspace, size_t workspace_bytes, ll_stream stream) {
+  g_nlaunch = 0;
   return decode_impl(false, true, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      nullptr, 0, out_tokens, out_timestamps, nullptr, out_lengths, out_capacity, workspace,
                      workspace_bytes, stream);
@@ -995,6 +1009,7 @@ ll_status ll_decode_tdt(const void *enc, ll_dtype dtype, ll_prec prec, int32_t B
                         int32_t num_durations, int32_t *out_tokens, int32_t *out_timestamps,
                         int32_t *out_durations, int32_t *out_lengths, int32_t out_capacity,
                         void *workspace, size_t workspace_bytes, ll_stream stream) {
+  g_nlaunch = 0;
   return decode_impl(true, false, enc, dtype, prec, B, T_max, lengths, pred, joint, blank_id, max_symbols,
                      durations, num_durations, out_tokens, out_timestamps, out_durations, out_lengths,
                      out_capacity, workspace, workspace_bytes, stream);
@@ -1044,7 +1059,7 @@ ll_status ll_sync(void *workspace, ll_stream stream) {
 ll_status ll_stats(const void *workspace, uint64_t *out, ll_stream stream) {
   if (!workspace || !out) return LL_ERR_INVALID_ARGUMENT;
   if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return LL_ERR_CUDA;
-  if (cudaMemcpy(out, (const uint8_t *)workspace + 64, 12 * sizeof(uint64_t), cudaMemcpyDeviceToHost) !=
+  if (cudaMemcpy(out, (const uint8_t *)workspace + 64, 13 * sizeof(uint64_t), cudaMemcpyDeviceToHost) !=
       cudaSuccess)
     return LL_ERR_CUDA;
   return LL_OK;

@@ -197,7 +197,8 @@ class LabelLoopingDecoder:
         if s != ll.LL_OK:
             raise ll.LLError(s, "ll_stats")
         keys = ["outer_steps", "joint_rounds", "joint_evals", "predictor_steps", "predictor_rows",
-                "labels", "groups", "cluster_size", "joint_rows_computed", "window", "group_rows", "chain"]
+                "labels", "groups", "cluster_size", "joint_rows_computed", "window", "group_rows", "chain",
+                "launches"]
         d = dict(zip(keys, v))
         c = d.pop("chain")
         d["chain_rounds"], d["chain_pred_steps"] = (c >> 20) & 0xFFFFF, c & 0xFFFFF

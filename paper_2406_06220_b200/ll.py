@@ -208,7 +208,7 @@ def ll_sync(workspace, stream) -> int:
 
 
 def ll_stats(workspace, stream):
-    out = (c_uint64 * 12)()
+    out = (c_uint64 * 13)()
     st = int(load_library().ll_stats(workspace, out, stream))
     return st, list(out)
 

@@ -685,3 +685,29 @@ def test_group_plan_equals_equal_groups(cfg, B):
     assert out[-1][0][B // 2][0] == []
     assert out[0][1]["joint_evals"] == out[-1][1]["joint_evals"]
     verify_all(spec, w, enc, lengths, out[-1][0])
+
+
+def test_stats_count_kernel_launches():
+    """ll_stats [12]: the kernels a decode call launched, counted by the library
+    (bench.py's gpu_launches): with the model tables prepared, one-wave B = 32
+    runs the projection GEMM + the decode kernel; B = 64 adds the length ranking;
+    on the fly, the decode kernel alone; an unprepared LSTM decode also builds
+    its tables (gate permutation, E' GEMM, packed weights)."""
+    c = synth.CONFIGS["fc-rnnt"]
+    spec = c["spec"]
+    w = synth.make_weights(spec, 5, blank_bias=synth.random_family_blank_bias(spec))
+    model = gpu_model(spec, w)
+    for B, want in ((32, 2), (64, 3)):
+        enc, lengths = synth.make_inputs(6, B, 60, spec.enc_dim, 20, 60)
+        dec = LabelLoopingDecoder(model, spec.max_symbols, B, 60)
+        dec.prepare()
+        dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), torch.from_numpy(lengths).cuda())
+        assert dec.stats()["launches"] == want, (B, dec.stats())
+    enc, lengths = synth.make_inputs(6, 32, 60, spec.enc_dim, 20, 60)
+    dec = LabelLoopingDecoder(model, spec.max_symbols, 32, 60)
+    dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), torch.from_numpy(lengths).cuda())
+    assert dec.stats()["launches"] == 5, dec.stats()
+    dec.prepare()
+    with ll.options(projections=1):
+        dec.decode(torch.from_numpy(enc).to("cuda", torch.bfloat16), torch.from_numpy(lengths).cuda())
+    assert dec.stats()["launches"] == 1, dec.stats()
