@@ -776,7 +776,7 @@ ll_status decode_impl(bool tdt, bool frame_looping, const void *enc, ll_dtype dt
   p.gp_rsmall = gp_rsmall;
   p.gp_wsmall = gp_wsmall;
   // more than one group and no unequal plan: groups of length-ranked utterances
-  if (g_opt.group_plan != 0 && gp_small == 0 && p.n_groups > 1) {
+  if (g_opt.group_plan != 0 && gp_small == 0 && p.n_groups > 1 && B <= 65536) {   // O(B^2) ranking
     int *perm = (int *)(ws + w.perm);
     ++g_nlaunch;
     rank_lengths_kernel<<<(B + 255) / 256, 256, 0, st>>>(lengths, B, T_max, perm);
