@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-group-plan", action="store_true",
                     help="equal groups of consecutive utterances (ll_options.group_plan = 0) instead of the "
                          "length-sorted unequal groups")
+    ap.add_argument("--group-rows", type=int, default=0,
+                    help="force the rows per group R (ll_options.group_rows; tuning experiments)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="utterances in the oracle sample (0: auto)")
     return ap.parse_args()
@@ -318,10 +320,10 @@ def main():
     from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
 
     llbuild.build()
-    if a.schedule == "batched" or a.projections == "on-the-fly" or a.no_group_plan:   # ll_options of this thread
-        o = ll.options(schedule=0 if a.schedule == "batched" else -1,
+    if a.schedule == "batched" or a.projections == "on-the-fly" or a.no_group_plan or a.group_rows:
+        o = ll.options(schedule=0 if a.schedule == "batched" else -1,   # ll_options of this thread
                        projections=1 if a.projections == "on-the-fly" else 0,
-                       group_plan=0 if a.no_group_plan else -1).opts
+                       group_plan=0 if a.no_group_plan else -1, group_rows=a.group_rows).opts
         if ll.ll_set_options(o) != ll.LL_OK:
             raise RuntimeError("ll_set_options")
     torch.cuda.set_device(local)
