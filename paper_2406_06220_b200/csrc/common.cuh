@@ -372,6 +372,18 @@ __device__ __forceinline__ uint4 relu_add_bf16x8_2(uint4 f, uint4 g0, uint4 g1) 
   return o;
 }
 
+// dot product of two bf16x8 vectors in fp32 (each product exact in fp32), in element order
+__device__ __forceinline__ float dot_bf16x8(uint4 a, uint4 b) {
+  float d = bf16_lo(a.x) * bf16_lo(b.x);
+  d = fmaf(bf16_hi(a.x), bf16_hi(b.x), d);
+  d = fmaf(bf16_lo(a.y), bf16_lo(b.y), d);
+  d = fmaf(bf16_hi(a.y), bf16_hi(b.y), d);
+  d = fmaf(bf16_lo(a.z), bf16_lo(b.z), d);
+  d = fmaf(bf16_hi(a.z), bf16_hi(b.z), d);
+  d = fmaf(bf16_lo(a.w), bf16_lo(b.w), d);
+  return fmaf(bf16_hi(a.w), bf16_hi(b.w), d);
+}
+
 template <typename T> __device__ __forceinline__ float to_f32(T v);
 template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
 template <> __device__ __forceinline__ float to_f32<bf16>(bf16 v) { return __bfloat162float(v); }

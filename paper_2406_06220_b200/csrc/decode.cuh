@@ -350,6 +350,7 @@ struct Ctx {
   int C, rank, tid, warp, lane, NW, NCT, g, q;
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
   int vm0, nmain, vx0, nx;    // TJ: main rows [vm0, vm0 + nmain) (tensor core), extra rows [vx0, vx0 + nx) (CUDA cores)
+  bool xrep;                  // TJ: <= 2 extra rows in all, held by EVERY CTA (joint rows dealt by rank)
   int u0, d0;                 // LSTM units / W_pred output dims owned
   int iw;                     // issuing warp for bulk copies (a warp without a joint tile if any)
   // Barrier phase bookkeeping, replicated in every consumer thread and packed
@@ -388,7 +389,10 @@ struct Ctx {
       if (v >= -1) tl_stamp(area, idx, ph);
     }
   }
-  __device__ void tl_init() { tl = (p.prof != nullptr && blockIdx.x == 0) ? p.prof : nullptr; }
+  // one [2][TL_N][TL_PH][MAX_NW] record per block (the buffer holds gridDim.x of them)
+  __device__ void tl_init() {
+    tl = p.prof != nullptr ? p.prof + (size_t)blockIdx.x * 2 * TL_N * TL_PH * MAX_NW : nullptr;
+  }
   // warp 0's sub-phases of a round's finish (phase slot 14, "warp" column k)
   __device__ void tl_sub(int k) const {
     if (tl != nullptr && tl_round < TL_N && lane == 0) tl[((size_t)tl_round * TL_PH + 14) * MAX_NW + k] = clock64();
@@ -428,8 +432,15 @@ struct Ctx {
       const int NV = p.V1 + p.nD, nxr = NV > 64 * TJ_C ? (NV - 64 * TJ_C + TJ_C - 1) / TJ_C : 0;
       vm0 = 64 * rank;
       nmain = min(max(NV - vm0, 0), 64);
-      vx0 = 64 * TJ_C + nxr * rank;
-      nx = min(max(NV - vx0, 0), nxr);
+      // replicated for <= 2 extra rows (the FC RNN-T: 1); TDT's 6 measured faster spread (+2.6% replicated)
+      xrep = NV > 64 * TJ_C && NV - 64 * TJ_C <= 2;
+      if (xrep) {   // every CTA holds all extra rows; CTA r evaluates them for joint rows r, r + 16
+        vx0 = 64 * TJ_C;
+        nx = NV - 64 * TJ_C;
+      } else {      // more extra rows: spread over the CTAs (<= 8 each), every joint row
+        vx0 = 64 * TJ_C + nxr * rank;
+        nx = min(max(NV - vx0, 0), nxr);
+      }
     }
     u0 = rank * upc();
     d0 = rank * dpc();
@@ -1215,7 +1226,65 @@ struct Ctx {
     // shared memory are busy with them until then), warps 8 and 9 take joint
     // rows 0-15 / 16-31 on mma.sync: z rows as the m16 A operand (ldmatrix from
     // the swizzled z), the extra weight rows as the n8 B operand, 4 chains
-    if ((warp == 8 || (warp == 9 && rs.nz > 16)) && nx > 0) {
+    if (xrep) {
+      // the extra row(s) (1 for the FC RNN-T) on CUDA cores WHILE the
+      // MMAs run, for this CTA's joint rows only: warp 8 row k = rank, warp 9
+      // row k = rank + 16; every CTA evaluates 2 rows instead of one CTA all 32
+      // after the MMAs (that tail, ~1.5K cycles on rank 0, held every round of
+      // the cluster).  Lanes split the 80 z chunks; a fixed xor butterfly sums.
+      if (warp >= 8) {
+        const int hf = warp - 8;
+        for (int k = 16 * hf + lane; k < min(L.JR, 16 * hf + 16); k += 32) {   // neutral partials
+          if (k == rank + 16 * hf) continue;
+          uint64_t *dst = wk + ((size_t)4 * L.JR + k) * wks();
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
+          if constexpr (SC) {
+            const uint64_t e = lse_empty();
+            *reinterpret_cast<uint4 *>(dst + 2) = make_uint4((uint32_t)e, (uint32_t)(e >> 32), (uint32_t)e, (uint32_t)(e >> 32));
+          }
+        }
+        const uint32_t zb = smem_u32(zs()), wb = smem_u32(sm + L.off_wx);
+        {
+          const int k = rank + 16 * hf;
+          uint4 zc[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int c = lane + 32 * i;
+            zc[i] = c < TJ_H / 8 ? lds128_u32(zb + (uint32_t)zoff(k, c)) : make_uint4(0, 0, 0, 0);
+          }
+          uint64_t tk2 = 0, dk2 = 0;
+          [[maybe_unused]] uint64_t tl2 = lse_empty(), dl2 = lse_empty();
+#pragma unroll 1
+          for (int x = 0; x < nx; ++x) {
+            float d = 0.f;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              const int c = lane + 32 * i;
+              if (c < TJ_H / 8) d += dot_bf16x8(zc[i], lds128_u32(wb + (uint32_t)(x * TJ_XROW + c * 16)));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            const float val = d + bsl()[64 + x];
+            const int v2 = vx0 + x;
+            if (logits != nullptr && lane == 0 && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v2] = val;
+            if (v2 < V1) tk2 = umax64(tk2, pack_key(val, v2));
+            else dk2 = umax64(dk2, pack_key(val, v2 - V1));
+            if constexpr (SC) {
+              if (v2 < V1) tl2 = lse_combine(tl2, lse_pack(val, 1.f));
+              else dl2 = lse_combine(dl2, lse_pack(val, 1.f));
+            }
+          }
+          if (lane == 0 && k < L.JR) {
+            uint64_t *dst = wk + ((size_t)4 * L.JR + k) * wks();
+            *reinterpret_cast<uint4 *>(dst) =
+                make_uint4((uint32_t)tk2, (uint32_t)(tk2 >> 32), (uint32_t)dk2, (uint32_t)(dk2 >> 32));
+            if constexpr (SC)
+              *reinterpret_cast<uint4 *>(dst + 2) =
+                  make_uint4((uint32_t)tl2, (uint32_t)(tl2 >> 32), (uint32_t)dl2, (uint32_t)(dl2 >> 32));
+          }
+        }
+      }
+    } else if ((warp == 8 || (warp == 9 && rs.nz > 16)) && nx > 0) {
       const int m0 = 16 * (warp - 8);
       mbar_wait(bar(BAR_JOINT), jph());
       float acc[4][4];

@@ -15,7 +15,8 @@ from paper_2406_06220_b200 import ll
 _exp = [a[2:] for a in sys.argv if a.startswith("--exp")]   # --exp1 -> variant timeline_exp1 (-DLL_EXP1)
 ll.LIB_PATH = llbuild.build(variant="timeline" + "".join("_" + e for e in _exp))   # timeline hooks compiled in
 TL_N, TL_PH, NW = 128, 16, 10
-buf = torch.zeros(2 * TL_N * TL_PH * NW, dtype=torch.int64, device="cuda")
+NBLK = 160   # one record per block (the decode grid has <= 148 blocks)
+buf = torch.zeros(NBLK * 2 * TL_N * TL_PH * NW, dtype=torch.int64, device="cuda")
 ll.ll_set_options(ll.options(timeline=buf.data_ptr()).opts)   # this thread, for every decode below
 import bench
 from paper_2406_06220_b200.decoder import LabelLoopingDecoder, Model
@@ -39,7 +40,19 @@ for _ in range(3):
 print("decode ms (timeline build):", round(ev0.elapsed_time(ev1), 4))
 torch.cuda.synchronize()
 print(cfg, dec.stats())
-tl = buf.cpu().numpy().reshape(2, TL_N, TL_PH, NW).astype(np.float64)
+allb = buf.cpu().numpy().reshape(NBLK, 2, TL_N, TL_PH, NW).astype(np.float64)
+_blk = [int(a.split("=")[1]) for a in sys.argv if a.startswith("--block=")]
+tl = allb[_blk[0] if _blk else 0]
+if "--ranks" in sys.argv:   # per rank of cluster 0: own phase durations (clock64 is per SM: no cross-SM deltas)
+    print("\nper rank of cluster 0 (averages over rounds, cycles):  build_z  MMA  epilogue  send  wait(others)  decide")
+    for r in range(16):
+        x = allb[r][0]
+        ev = [i for i in range(TL_N) if all((x[i, ph] > 0).any() for ph in (1, 11, 12, 13, 4, 5, 6, 9))]
+        if not ev:
+            continue
+        def d(a, b):
+            return np.mean([x[i, b][x[i, b] > 0].max() - x[i, a][x[i, a] > 0].max() for i in ev])
+        print(f"  rank {r:2d}: {d(1, 11):7.0f} {d(3, 12):7.0f} {d(12, 4):8.0f} {d(4, 5):6.0f} {d(5, 6):9.0f} {d(8, 9):8.0f}   ({len(ev)} rounds)")
 
 def report(area, name, order, labels):
     x = tl[area]
