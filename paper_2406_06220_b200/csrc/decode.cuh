@@ -30,7 +30,9 @@
 //         z = ReLU(f[b, t..t+W-1] + g_b)            (bf16, the swizzled B operand)
 //         joint GEMM on tcgen05: this CTA's 64 vocabulary rows K-folded into an
 //           M = 128 A operand (shared memory), z rows as N, D' in TMEM; the
-//           <= 8 extra rows of the CTA on mma.sync
+//           extra rows (1024..): <= 2 held by every CTA and evaluated on CUDA
+//           cores for its own joint rows during the MMAs, else spread over the
+//           CTAs on mma.sync after them
 //         argmax fused in the TMEM epilogue (packed 64-bit keys, butterfly),
 //         per-CTA partial keys st.async'ed to every CTA of the cluster,
 //         mbarrier completion, every CTA reduces the C partials and applies the
@@ -118,8 +120,8 @@ __host__ __device__ inline bool tg_shape(bool bf, bool lstm, int H, int P, int C
 
 // ---------------------------------------------------------------------------
 // TJ: the FC joint (H = 640 in 16-CTA clusters, LSTM or stateless) on tcgen05.
-// Each CTA owns 64 vocabulary rows (8 n8 tiles) on the tensor core plus at
-// most one extra tile (rows 1024.. when V+1+|D| > 1024) on mma.sync.  The
+// Each CTA owns 64 vocabulary rows (8 n8 tiles) on the tensor core plus the
+// extra rows (1024.. when V+1+|D| > 1024; see joint_keys_tj).  The
 // 64 x 640 weight slice is the A operand in shared memory, K-folded into
 // M = 128: A row r = 32 (v / 16) + 16 a + v % 16 holds vocabulary row v's
 // K-half a (320 elements); the z rows are the B operand with both K-halves
