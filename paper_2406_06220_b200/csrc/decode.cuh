@@ -237,7 +237,11 @@ __host__ __device__ inline Layout make_layout(bool bf, bool lstm, int H, int P, 
   }
   L.off_c = o;    o = align_up(o + (size_t)R * (lstm ? L.UPC : 0) * layers * 4, 128);   // c of every layer
   L.off_part = o; o = align_up(o + (size_t)2 * C * L.JR * 8 * L.pks, 128);
-  L.off_wkey = o; o = align_up(o + (size_t)(L.tj ? TJ_NKW : L.NW) * L.JR * 8 * L.wks, 128);
+  {   // TJ: 3..8 extra rows -> 5 more per-warp-subset partials (xall, joint_keys_tj)
+    const int ext = V1 + nD - 64 * TJ_C;
+    const int nkw = L.tj ? (ext > 2 && ext <= 8 ? TJ_NKW + 4 : TJ_NKW) : L.NW;
+    L.off_wkey = o; o = align_up(o + (size_t)nkw * L.JR * 8 * L.wks, 128);
+  }
   L.off_hs = o;   o = align_up(o + (size_t)(L.tg ? TG_HBYTES : L.ring ? 2 * R * L.hstride : 0), 128);
   L.off_ring = o; o = align_up(o + (size_t)L.NS * 8 * P * 2, 128);
   // E' slices (bf16 LSTM); fp32 LSTM with layers > 1: the input-side gate partials of a layer
@@ -353,6 +357,7 @@ struct Ctx {
   int tile0, ntiles;          // vocab n8 tiles owned by this CTA
   int vm0, nmain, vx0, nx;    // TJ: main rows [vm0, vm0 + nmain) (tensor core), extra rows [vx0, vx0 + nx) (CUDA cores)
   bool xrep;                  // TJ: <= 2 extra rows in all, held by EVERY CTA (joint rows dealt by rank)
+  bool xall;                  // TJ: 3..8 extra rows, held by every CTA, dealt over all 10 warps during the MMAs
   int u0, d0;                 // LSTM units / W_pred output dims owned
   int iw;                     // issuing warp for bulk copies (a warp without a joint tile if any)
   // Barrier phase bookkeeping, replicated in every consumer thread and packed
@@ -434,9 +439,10 @@ struct Ctx {
       const int NV = p.V1 + p.nD, nxr = NV > 64 * TJ_C ? (NV - 64 * TJ_C + TJ_C - 1) / TJ_C : 0;
       vm0 = 64 * rank;
       nmain = min(max(NV - vm0, 0), 64);
-      // replicated for <= 2 extra rows (the FC RNN-T: 1); TDT's 6 measured faster spread (+2.6% replicated)
+      // <= 2 extra rows (the FC RNN-T: 1): warps 8-9; 3..8 (TDT: 6): all 10 warps
       xrep = NV > 64 * TJ_C && NV - 64 * TJ_C <= 2;
-      if (xrep) {   // every CTA holds all extra rows; CTA r evaluates them for joint rows r, r + 16
+      xall = NV - 64 * TJ_C > 2 && NV - 64 * TJ_C <= 8;
+      if (xrep || xall) {   // every CTA holds all extra rows; CTA r evaluates them for joint rows r, r + 16
         vx0 = 64 * TJ_C;
         nx = NV - 64 * TJ_C;
       } else {      // more extra rows: spread over the CTAs (<= 8 each), every joint row
@@ -1205,7 +1211,7 @@ struct Ctx {
     x[0] = (lane & 8) ? lse_combine(o, x[0]) : lse_combine(x[0], o);
   }
   __device__ __forceinline__ int nkw() const {
-    if constexpr (TJ) return nx > 0 ? TJ_NKW : TJ_NKW - 1;
+    if constexpr (TJ) return xall ? TJ_NKW + 4 : nx > 0 ? TJ_NKW : TJ_NKW - 1;
     else return NW;
   }
 
@@ -1228,7 +1234,66 @@ struct Ctx {
     // shared memory are busy with them until then), warps 8 and 9 take joint
     // rows 0-15 / 16-31 on mma.sync: z rows as the m16 A operand (ldmatrix from
     // the swizzled z), the extra weight rows as the n8 B operand, 4 chains
-    if (xrep) {
+    if (TM != 1 && xall) {   // (compiled out of the RNN-T kernels)
+      // 3..8 extra rows (TDT: token 1024 + 5 duration rows): every CTA, for its
+      // joint rows k = rank + 16 h only, dealt over the 10 consumer warps while
+      // the MMAs run (warps 0-7 idle until BAR_JOINT): warp w takes h = w & 1
+      // and the extra rows {w / 2, w / 2 + 5}, its keys are partial 4 + w / 2
+      // (the other joint rows of that partial: neutral), reduced with the rest
+      // in exchange_keys
+      const int hf = warp & 1, j = warp >> 1;
+      uint64_t *wkj = wk + (size_t)(4 + j) * L.JR * wks();
+      for (int k = 16 * hf + lane; k < min(L.JR, 16 * hf + 16); k += 32) {   // neutral partials
+        if (k == rank + 16 * hf) continue;
+        uint64_t *dst = wkj + (size_t)k * wks();
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
+        if constexpr (SC) {
+          const uint64_t e = lse_empty();
+          *reinterpret_cast<uint4 *>(dst + 2) = make_uint4((uint32_t)e, (uint32_t)(e >> 32), (uint32_t)e, (uint32_t)(e >> 32));
+        }
+      }
+      const int k = rank + 16 * hf;
+      const uint32_t zb = smem_u32(zs()), wb = smem_u32(sm + L.off_wx);
+      uint4 zc[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int c = lane + 32 * i;
+        zc[i] = c < TJ_H / 8 ? lds128_u32(zb + (uint32_t)zoff(k, c)) : make_uint4(0, 0, 0, 0);
+      }
+      uint64_t tk2 = 0, dk2 = 0;
+      [[maybe_unused]] uint64_t tl2 = lse_empty(), dl2 = lse_empty();
+#pragma unroll
+      for (int xx = 0; xx < 2; ++xx) {
+        const int x = j + 5 * xx;
+        if (x < nx) {
+          float d = 0.f;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int c = lane + 32 * i;
+            if (c < TJ_H / 8) d += dot_bf16x8(zc[i], lds128_u32(wb + (uint32_t)(x * TJ_XROW + c * 16)));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          const float val = d + bsl()[64 + x];
+          const int v2 = vx0 + x;
+          if (logits != nullptr && lane == 0 && k < nrows_valid) logits[(size_t)(row_base + k) * NV + v2] = val;
+          if (v2 < V1) tk2 = umax64(tk2, pack_key(val, v2));
+          else dk2 = umax64(dk2, pack_key(val, v2 - V1));
+          if constexpr (SC) {
+            if (v2 < V1) tl2 = lse_combine(tl2, lse_pack(val, 1.f));
+            else dl2 = lse_combine(dl2, lse_pack(val, 1.f));
+          }
+        }
+      }
+      if (lane == 0 && k < L.JR) {
+        uint64_t *dst = wkj + (size_t)k * wks();
+        *reinterpret_cast<uint4 *>(dst) =
+            make_uint4((uint32_t)tk2, (uint32_t)(tk2 >> 32), (uint32_t)dk2, (uint32_t)(dk2 >> 32));
+        if constexpr (SC)
+          *reinterpret_cast<uint4 *>(dst + 2) =
+              make_uint4((uint32_t)tl2, (uint32_t)(tl2 >> 32), (uint32_t)dl2, (uint32_t)(dl2 >> 32));
+      }
+    } else if (xrep) {
       // the extra row(s) (1 for the FC RNN-T) on CUDA cores WHILE the
       // MMAs run, for this CTA's joint rows only: warp 8 row k = rank, warp 9
       // row k = rank + 16; every CTA evaluates 2 rows instead of one CTA all 32
